@@ -1,0 +1,340 @@
+#!/usr/bin/env python
+"""Benchmark of the evaluate+stamp hot path (BASELINE.json metric:
+"MOSFET eval+stamp per sec (1 B200, FP64) and % of FP64/HBM roofline").
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config I] [--variant V]
+    python bench.py --impl reference ...        # the CPU oracle arm
+
+One step = one ees_eval_stamp call over the whole netlist (every §8(a) row:
+evaluation + stamping + rail side-reduction), inputs resident in HBM, L2
+flushed (256 MiB write) before every step, A and b cleared outside the timed
+region (the caller's clear).  Timing: CUDA events on the launching
+stream around each call, summed over exactly K steps, barrier + synchronize
+on both sides, max over ranks.  N>1 runs N independent replicas (DESIGN.md
+§6: "replicas only"), weak scaling.  Rank 0 prints ONE JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import netgen  # noqa: E402
+
+METRIC = "MOSFET eval+stamp per sec (1 B200, FP64) and % of FP64/HBM roofline"
+UNIT = "FET eval+stamp/s"
+L2_FLUSH_BYTES = 256 << 20
+DEFAULT_CONFIG = 1          # BASELINE.json configs[1] (ring oscillators, 202,000 FETs)
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def algorithmic_bytes(n_dev, n, nnz):
+    """SURVEY §8(d) compulsory bytes per call: 48 B device data per FET
+    (4 x int32 terminals, f64 beta, 3 x f64 v_prev) + x read once (8 B per
+    unknown) + A_vals read-modify-write (16 B per nonzero) + b RMW (16 B per
+    unknown).  Slot maps, scratch and sector amplification are overhead."""
+    return 48 * n_dev + 8 * n + 16 * nnz + 16 * n
+
+
+def load_traffic(cfg, variant):
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if not os.path.exists(p):
+        return None
+    d = json.load(open(p))
+    v = d.get(f"cfg{cfg}", {}).get(variant)
+    return v
+
+
+class ClockSampler:
+    """Samples SM clock and throttle reasons via NVML while running."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x100: "display_clock_setting"}
+
+    def __init__(self, index, period=0.005):
+        self.index, self.period = index, period
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+
+    def __enter__(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self._nv = None
+            return self
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def _run(self):
+        nv = self._nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+def cpu_baseline(nl, budget_s=10.0):
+    """The oracle's Table I kernels as they stand, on this host's
+    cores: ColorFused and loadomp with all cores, loadsingle with 1 thread.
+    Bounded sample: repeat full calls on the same netlist until budget_s."""
+    import oracle
+    cores = os.cpu_count() or 1
+    bl = oracle.Baseline(nl)
+    nnz = bl.nnz
+    A = np.zeros(nnz)
+    b = np.zeros(nl.n)
+    out = {}
+    for kind, threads, budget in (("colorfused", cores, budget_s), ("loadomp", cores, budget_s / 3),
+                                  ("loadsingle", 1, budget_s / 3)):
+        bl.run(kind, A, b, threads)      # warm-up
+        reps, t0 = 0, time.perf_counter()
+        while True:
+            bl.run(kind, A, b, threads)
+            reps += 1
+            el = time.perf_counter() - t0
+            if el >= budget:
+                break
+        out[kind] = dict(value=nl.n_dev * reps / el, threads=threads, calls=reps, seconds=el)
+    bl.close()
+    best = out["colorfused"]
+    return {"value": best["value"], "unit": UNIT, "cores": best["threads"], "kind": "oracle",
+            "sample": f"{nl.name}: {best['calls']} full ColorFused calls ({nl.n_dev} FETs each) "
+                      f"in {best['seconds']:.1f} s on {best['threads']} threads",
+            "loadsingle_1t": out["loadsingle"]["value"], "loadomp": out["loadomp"]["value"],
+            "colorfused": out["colorfused"]["value"], "cpu_model": cpu_model()}
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle (ColorFused, all host cores) on the same
+    config, metric and unit; rank 0 only."""
+    if int(os.environ.get("RANK", "0")) != 0:
+        return
+    nl = netgen.config(args.config)
+    import oracle
+    cores = os.cpu_count() or 1
+    bl = oracle.Baseline(nl)
+    A = np.zeros(bl.nnz)
+    b = np.zeros(nl.n)
+    for _ in range(args.warmup):
+        bl.run("colorfused", A, b, cores)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        A[:] = 0
+        b[:] = 0
+        bl.run("colorfused", A, b, cores)
+    el = time.perf_counter() - t0
+    bl.close()
+    value = nl.n_dev * args.steps / el
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 0,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": netgen.CONFIG_NAMES[args.config], "n_dev": nl.n_dev},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": f"{args.steps} full ColorFused calls of {nl.name}",
+                             "cpu_model": cpu_model()},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--config", type=int, default=DEFAULT_CONFIG)
+    ap.add_argument("--variant", default="auto", choices=["auto", "color", "atomic", "gather"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=10.0)
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+    from paper_2604_03079_b200 import Context
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.device("cuda", torch.cuda.current_device())
+
+    nl = netgen.config(args.config)
+    ctx = Context.from_netlist(nl, variant=args.variant)
+    st = ctx.stats()
+    stream = torch.cuda.Stream()
+    x = torch.from_numpy(nl.x).to(dev)
+    A = torch.zeros(ctx.nnz, dtype=torch.float64, device=dev)
+    b = torch.zeros(ctx.n, dtype=torch.float64, device=dev)
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
+    torch.cuda.synchronize()
+
+    def step_pre(k):
+        with torch.cuda.stream(stream):
+            flush.fill_(k & 0xFF)          # evict A, b, x, device data from L2
+            A.zero_()
+            b.zero_()
+
+    with torch.cuda.stream(stream):
+        for k in range(args.warmup):
+            step_pre(k)
+            ctx.eval_stamp(x, nl.h, A, b, stream=stream)
+    torch.cuda.synchronize()
+
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        with torch.cuda.stream(stream):
+            for k in range(args.steps):
+                step_pre(k)
+                evs[k][0].record(stream)
+                ctx.eval_stamp(x, nl.h, A, b, stream=stream)
+                evs[k][1].record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    per = [e0.elapsed_time(e1) for e0, e1 in evs]
+    total_ms = sum(per)
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    max_ms = float(t.item())
+    ms_per_step = max_ms / args.steps
+    value = world * nl.n_dev / (ms_per_step * 1e-3)
+    st = ctx.stats()
+    variant = st["variant_chosen"]
+
+    # roofline of the dominant kernel: single-launch variants time the kernel
+    # itself; multi-launch variants report the whole call (all their kernels)
+    hbm, peak_src = peaks()
+    alg = algorithmic_bytes(nl.n_dev, ctx.n, ctx.nnz)
+    achieved = alg / (ms_per_step * 1e-3) / 1e9
+    roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+            "frac": achieved / hbm, "traffic": load_traffic(args.config, variant),
+            "kernel": {"atomic": "k_atomic", "color": "k_color x C + k_rail_final",
+                       "gather": "k_gather_eval + k_gather_reduce (+k_gather_heavy)"}[variant],
+            "algorithmic_bytes_per_launch": alg, "peak_source": peak_src,
+            "per_unit": "48 B/FET + 8 B/unknown (x) + 16 B/nonzero (A RMW) + 16 B/unknown (b RMW)"}
+
+    # end to end through the host-buffer ABI call (pinned buffers)
+    e2e = None
+    if not args.no_e2e:
+        hx = torch.from_numpy(nl.x).pin_memory()
+        hA = torch.zeros(ctx.nnz, dtype=torch.float64).pin_memory()
+        hb = torch.zeros(ctx.n, dtype=torch.float64).pin_memory()
+        for _ in range(3):
+            ctx.eval_stamp_host(hx, nl.h, hA, hb, stream=stream)
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(args.steps)]
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        for k in range(args.steps):
+            ev[k][0].record(stream)
+            ctx.eval_stamp_host(hx, nl.h, hA, hb, stream=stream)
+            ev[k][1].record(stream)
+        torch.cuda.synchronize()
+        e_ms = sum(a.elapsed_time(bq) for a, bq in ev)
+        te = torch.tensor([e_ms], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e_ms = float(te.item()) / args.steps
+        e2e = {"value": world * nl.n_dev / (e_ms * 1e-3), "unit": UNIT,
+               "h2d_bytes_per_step": 8 * (2 * ctx.n + ctx.nnz),
+               "d2h_bytes_per_step": 8 * (ctx.n + ctx.nnz), "ms_per_step": e_ms,
+               "api": "ees_eval_stamp_host (pinned host x, A, b)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(nl, args.cpu_budget)
+
+    if rank == 0:
+        per_sorted = sorted(per)
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": netgen.CONFIG_NAMES[args.config], "config_index": args.config,
+                       "n_dev": nl.n_dev, "n": ctx.n, "nnz": ctx.nnz, "colors": st["n_colors"],
+                       "variant": variant, "tune_ms": st["tune_ms"],
+                       "l2": "flushed before every step (256 MiB write)",
+                       "parallelism": "replicas" if world > 1 else "single",
+                       "p10_ms": per_sorted[len(per) // 10], "p50_ms": per_sorted[len(per) // 2],
+                       "p90_ms": per_sorted[(9 * len(per)) // 10], "setup_s": st["setup_s"]},
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": st["launches_per_call"] * args.steps,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,180 @@
+/*
+ * ees.h -- C ABI of the B200 evaluate+stamp library (libees.so).
+ *
+ * One call, ees_eval_stamp(), performs the hot path of one Newton-Raphson
+ * iteration of EEspice (arxiv 2604.03079): every MOSFET instance is evaluated
+ * at the current node-voltage vector x ("Compute Phase") and
+ * its linearised contributions are stamped into the shared MNA matrix A (CSR
+ * values) and right-hand side b ("Stamp Phase") without write races
+ * (P:31).  The device model is SPEC.md's Level-1 MOSFET with gmin and three
+ * backward-Euler capacitor companions, read as in
+ * SURVEY.md §8(c) / DESIGN.md §2.
+ *
+ * Conventions
+ *  - All calls return ees_status (0 = EES_OK, < 0 = error).  No C++
+ *    exception crosses the ABI.  ees_strerror() names a status.
+ *  - Nodes are 0 .. n_nodes-1; ground is -1 and is eliminated.
+ *    Unknowns n = n_nodes + n_extra: source-branch unknowns follow the nodes
+ *    (S:158).  MOSFETs never reference branch unknowns; the caller's linear
+ *    devices may, through `extra_row/extra_col` pattern entries.
+ *  - Terminals are d, g, s, b = drain, gate, source, bulk.  The bulk
+ *    carries only the drain-bulk capacitor (no body effect).
+ *  - beta = (kp * W) / L, evaluated in that order in FP64.
+ *  - All floating point is IEEE FP64.  Results equal the serial reference
+ *    (S:339 loadsingle) up to summation order: per entry within
+ *    1e-12 * sum|elementary contributions| (BASELINE.json north_star).
+ *
+ * Thread-safety: different contexts are independent.  One context must not
+ * be used by two calls at once (it owns scratch buffers).
+ */
+#ifndef EES_H
+#define EES_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct ees_ctx ees_ctx;          /* opaque; owns all library device memory */
+typedef void *ees_stream;                /* a cudaStream_t; NULL = legacy default stream */
+
+typedef enum {
+    EES_OK = 0,
+    EES_EINVAL = -1,     /* bad argument (null pointer, id out of range, h <= 0 or NaN, ...) */
+    EES_ENOMEM = -2,     /* host or device allocation failed */
+    EES_ECUDA = -3,      /* a CUDA runtime call or kernel launch failed */
+    EES_ESTATE = -4      /* context not usable (e.g. a variant that was not built) */
+} ees_status;
+
+/* Stamping variants (north_star subsystem (3)); all fuse evaluation. */
+typedef enum {
+    EES_AUTO = 0,        /* setup times COLOR/ATOMIC/GATHER on this topology, keeps the fastest */
+    EES_COLOR = 1,       /* colour-phased: one phase per colour, plain read-modify-write */
+    EES_ATOMIC = 2,      /* one pass, FP64 atomicAdd (RED) into A and b */
+    EES_GATHER = 3       /* deterministic: contributions to scratch, per-entry segmented reduction */
+} ees_variant;
+
+/* Conflict relation for the colouring (P:60 and SURVEY A1). */
+typedef enum {
+    EES_CONFLICT_EXCLUDE_RAILS = 0, /* edge iff two FETs share a node that is neither ground nor a rail;
+                                       rail x rail entries of A and rail rows of b then take a
+                                       deterministic side reduction (DESIGN.md §2 reading R1) */
+    EES_CONFLICT_PAPER = 1          /* paper-literal: edge iff two FETs share any non-ground node */
+} ees_conflict_rule;
+
+enum { EES_MAX_MODELS = 16, EES_MAX_RAILS = 8 };
+
+typedef struct {
+    int32_t polarity;        /* +1 NMOS, -1 PMOS */
+    int32_t reserved;        /* must be 0 */
+    double vt0;              /* V; SPICE sign convention: PMOS vt0 < 0 */
+    double kp;               /* A/V^2, > 0 */
+    double lambda;           /* 1/V */
+    double cgs, cgd, cdb;    /* F, >= 0 */
+} ees_model;
+
+typedef struct {
+    int32_t n_nodes;         /* non-ground nodes, >= 0 */
+    int32_t n_extra;         /* branch unknowns after the nodes, >= 0 */
+    int64_t n_dev;           /* MOSFETs, >= 0 */
+    const int32_t *d, *g, *s, *b;   /* host [n_dev], each in [-1, n_nodes); -1 = ground */
+    const double *w, *l;            /* host [n_dev], metres, finite and > 0 */
+    const int32_t *model;           /* host [n_dev], in [0, n_models) */
+    const double *vprev;            /* host [3][n_dev] SoA: v_gs, v_gd, v_db at the last accepted
+                                       step (physical frame) */
+    int32_t n_models;               /* 1 .. EES_MAX_MODELS */
+    const ees_model *models;        /* host [n_models] */
+    int32_t n_rails;                /* 0 .. EES_MAX_RAILS */
+    const int32_t *rails;           /* host [n_rails]: distinct nodes held by ideal sources (VDD) */
+    int64_t n_extra_entries;        /* caller's linear-device pattern entries */
+    const int32_t *extra_row, *extra_col;  /* host [n_extra_entries], each in [0, n) */
+    double gmin;                    /* S, >= 0, added drain-source on every FET */
+    int32_t variant;                /* ees_variant */
+    int32_t conflict_rule;          /* ees_conflict_rule */
+    int32_t flags;                  /* 0, or EES_SETUP_HOST_ONLY */
+} ees_desc;
+
+/* ees_desc.flags: build only the host-side topology (pattern, slots,
+ * colouring, statistics) without touching a GPU; ees_eval_stamp and
+ * ees_race_probe then return EES_ESTATE.  For host-logic tests. */
+enum { EES_SETUP_HOST_ONLY = 1 };
+
+typedef struct {
+    int64_t n_dev, nnz, n_contributions;   /* contributions = live (entry, device) stamps */
+    int32_t n;                              /* unknowns */
+    int32_t n_colors;                       /* C under the context's conflict rule */
+    int32_t max_group, min_group;           /* colour-group sizes */
+    int32_t max_conflict_node_degree;       /* devices on the busiest conflict node */
+    int32_t variant_chosen;                 /* the variant ees_eval_stamp runs */
+    int32_t n_rail_entries;                 /* rail x rail A entries + rail b rows */
+    int32_t n_heavy_targets;                /* GATHER entries reduced by block-chunks */
+    int32_t launches_per_call;              /* kernels one ees_eval_stamp enqueues */
+    double setup_s;                         /* wall time of ees_setup */
+    double setup_pattern_s, setup_color_s;  /* parts of it */
+    double tune_ms[4];                      /* EES_AUTO: measured ms per call of [_, COLOR, ATOMIC, GATHER] */
+} ees_stats_t;
+
+/* Build everything that depends only on topology ("constructs the FET
+ * conflict graph during setup"): validate, CSR pattern of all ordered
+ * non-ground terminal pairs plus extra entries, per-device stamp
+ * slots, first-fit greedy colouring in netlist order, colour-
+ * major schedule, transposed contributor lists, rail side-reduction tables;
+ * upload to the current CUDA device.  Copies every host input: the caller may
+ * free them on return.  On error *out is NULL. */
+ees_status ees_setup(const ees_desc *desc, ees_ctx **out);
+
+/* Host CSR pattern, rows sorted by column, library-owned until ees_destroy.
+ * A_vals[k] of ees_eval_stamp is the entry (row r, col col_idx[k]) with
+ * row_ptr[r] <= k < row_ptr[r+1]. */
+ees_status ees_pattern(const ees_ctx *ctx, int32_t *n, int64_t *nnz,
+                       const int32_t **row_ptr, const int32_t **col_idx);
+
+/* CSR index of (row, col), or *slot = -1 if absent. */
+ees_status ees_find_slot(const ees_ctx *ctx, int32_t row, int32_t col, int64_t *slot);
+
+/* Host colour of every device (netlist order), library-owned. */
+ees_status ees_colors(const ees_ctx *ctx, const int32_t **color, int32_t *n_colors);
+
+/* Evaluate + stamp every MOSFET at x for time step h, ACCUMULATING
+ * into the caller's arrays (S:141 add semantics):
+ *   A_vals[k] += sum of device stamps on entry k,  b[r] += sum on row r.
+ * The caller clears them or pre-loads linear stamps first (S:426 order).
+ *   x       device pointer, [n] FP64 (branch entries are never read)
+ *   h       time step in seconds, > 0; +INFINITY = DC (capacitors open)
+ *   A_vals  device pointer, [nnz] FP64, in/out
+ *   b       device pointer, [n] FP64, in/out
+ *   stream  the caller's CUDA stream; the call only enqueues work, never
+ *           synchronises.  x, A_vals, b must stay valid until it completes.
+ * Errors: EES_EINVAL (null pointer, h <= 0 or NaN) before any work is
+ * enqueued; EES_ECUDA if a launch fails.  NaN in x propagates. */
+ees_status ees_eval_stamp(ees_ctx *ctx, const double *x, double h, double *A_vals, double *b,
+                          ees_stream stream);
+
+/* Same with HOST arrays (x [n] in; A_vals [nnz] and b [n] in/out, accumulate):
+ * copies x, A_vals, b to the device, runs ees_eval_stamp, copies A_vals and b
+ * back and synchronises `stream` before returning.  Page-locked host memory
+ * gives full copy bandwidth. */
+ees_status ees_eval_stamp_host(ees_ctx *ctx, const double *x, double h, double *A_vals,
+                               double *b, ees_stream stream);
+
+/* Choose the variant later calls run (EES_AUTO = the one setup measured fastest). */
+ees_status ees_set_variant(ees_ctx *ctx, int32_t variant);
+
+ees_status ees_stats(const ees_ctx *ctx, ees_stats_t *out);
+
+/* Race instrument: replays the COLOR schedule given by
+ * `color` (host [n_dev]; NULL = the context's own colouring) on the device,
+ * counting per colour how many devices write each A entry and b row that is
+ * not rail-reduced.  *n_conflicts = number of (colour, entry) pairs written by
+ * more than one device: 0 for a valid colouring.  Synchronous. */
+ees_status ees_race_probe(ees_ctx *ctx, const int32_t *color, int64_t *n_conflicts);
+
+ees_status ees_destroy(ees_ctx *ctx);
+
+const char *ees_strerror(ees_status status);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EES_H */

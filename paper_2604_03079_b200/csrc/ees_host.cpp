@@ -1,0 +1,867 @@
+// ees_host.cpp -- host side of libees: the C ABI (include/ees.h), topology
+// setup (pattern, stamp slots, colouring, schedules, contributor lists) and
+// per-call dispatch of the sm_100a kernels in ees_kernels.cu.
+//
+// Setup follows PAPER.md P:36 ("constructs the FET conflict graph during
+// setup, partitions instances into color groups") and SPEC.md's mna-core
+// reserve/finalize and coloring module.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#include "ees_internal.h"
+
+using namespace ees;
+
+namespace {
+
+double now_s()
+{
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+struct Layout {
+    int64_t N = 0;
+    int4 *term = nullptr;
+    double *beta = nullptr;
+    double *v0 = nullptr;
+    uint8_t *model = nullptr;
+    int32_t *slot = nullptr;
+    DevK k() const { return DevK{N, term, beta, v0, model, slot}; }
+};
+
+}  // namespace
+
+struct ees_ctx {
+    int32_t n_nodes = 0, n_extra = 0, n = 0;
+    int64_t n_dev = 0, nnz = 0;
+    std::vector<int32_t> row_ptr, col_idx;
+    std::vector<int32_t> color;
+    int32_t n_colors = 0;
+    std::vector<int64_t> color_ptr;
+    std::vector<ees_model> models;
+    std::vector<int32_t> rails;
+    double gmin = 0.0;
+    int32_t rule = 0;
+    int32_t n_rail_a = 0, n_rail_entries = 0;
+    int32_t rail_target[kMaxRailEntries] = {};
+    Layout L_atomic, L_color, L_gather;
+    GatherK gk{};
+    std::vector<int64_t> color_blk_off;   // [C+1] block offsets of colours into partials
+    double *partials = nullptr;
+    int atomic_grid = 1;
+    int32_t variant = EES_ATOMIC;
+    int32_t launches = 0;
+    bool host_only = false;
+    ees_stats_t st{};
+    double *hx = nullptr, *hA = nullptr, *hb = nullptr;   // ees_eval_stamp_host staging
+    std::vector<void *> allocs;
+};
+
+namespace {
+
+template <typename T>
+ees_status dalloc(ees_ctx *c, T **p, size_t count)
+{
+    *p = nullptr;
+    if (count == 0) count = 1;
+    void *q = nullptr;
+    const cudaError_t e = cudaMalloc(&q, count * sizeof(T));
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return e == cudaErrorMemoryAllocation ? EES_ENOMEM : EES_ECUDA;
+    }
+    c->allocs.push_back(q);
+    *p = static_cast<T *>(q);
+    return EES_OK;
+}
+
+template <typename T>
+ees_status upload(ees_ctx *c, T **p, const T *src, size_t count)
+{
+    ees_status s = dalloc(c, p, count);
+    if (s != EES_OK) return s;
+    if (count && cudaMemcpy(*p, src, count * sizeof(T), cudaMemcpyHostToDevice) != cudaSuccess)
+        return EES_ECUDA;
+    return EES_OK;
+}
+
+#define TRY(expr)                         \
+    do {                                  \
+        ees_status _s = (expr);           \
+        if (_s != EES_OK) return _s;      \
+    } while (0)
+
+ees_status validate(const ees_desc *d)
+{
+    if (!d) return EES_EINVAL;
+    if (d->n_nodes < 0 || d->n_extra < 0 || d->n_dev < 0) return EES_EINVAL;
+    if ((int64_t)d->n_nodes + d->n_extra > INT32_MAX - 1) return EES_EINVAL;
+    if (d->n_models < 1 || d->n_models > EES_MAX_MODELS || !d->models) return EES_EINVAL;
+    if (d->n_rails < 0 || d->n_rails > EES_MAX_RAILS || (d->n_rails && !d->rails)) return EES_EINVAL;
+    if (d->n_extra_entries < 0 || (d->n_extra_entries && (!d->extra_row || !d->extra_col)))
+        return EES_EINVAL;
+    if (!(d->gmin >= 0.0) || !std::isfinite(d->gmin)) return EES_EINVAL;
+    if (d->variant < EES_AUTO || d->variant > EES_GATHER) return EES_EINVAL;
+    if (d->conflict_rule != EES_CONFLICT_EXCLUDE_RAILS && d->conflict_rule != EES_CONFLICT_PAPER)
+        return EES_EINVAL;
+    if (d->flags & ~EES_SETUP_HOST_ONLY) return EES_EINVAL;
+    for (int k = 0; k < d->n_models; k++) {
+        const ees_model &m = d->models[k];
+        if ((m.polarity != 1 && m.polarity != -1) || m.reserved != 0) return EES_EINVAL;
+        if (!(m.kp > 0.0) || !std::isfinite(m.kp) || !std::isfinite(m.vt0) || !std::isfinite(m.lambda))
+            return EES_EINVAL;
+        if (!(m.cgs >= 0.0) || !(m.cgd >= 0.0) || !(m.cdb >= 0.0)) return EES_EINVAL;
+        if (!std::isfinite(m.cgs) || !std::isfinite(m.cgd) || !std::isfinite(m.cdb)) return EES_EINVAL;
+    }
+    if (d->n_dev) {
+        if (!d->d || !d->g || !d->s || !d->b || !d->w || !d->l || !d->model || !d->vprev)
+            return EES_EINVAL;
+        for (int64_t i = 0; i < d->n_dev; i++) {
+            const int32_t T[4] = {d->d[i], d->g[i], d->s[i], d->b[i]};
+            for (int a = 0; a < 4; a++)
+                if (T[a] < -1 || T[a] >= d->n_nodes) return EES_EINVAL;
+            if (d->model[i] < 0 || d->model[i] >= d->n_models) return EES_EINVAL;
+            if (!(d->w[i] > 0.0) || !(d->l[i] > 0.0) || !std::isfinite(d->w[i]) || !std::isfinite(d->l[i]))
+                return EES_EINVAL;
+        }
+    }
+    const int32_t n = d->n_nodes + d->n_extra;
+    for (int k = 0; k < d->n_rails; k++) {
+        if (d->rails[k] < 0 || d->rails[k] >= d->n_nodes) return EES_EINVAL;
+        for (int j = 0; j < k; j++)
+            if (d->rails[j] == d->rails[k]) return EES_EINVAL;
+    }
+    for (int64_t e = 0; e < d->n_extra_entries; e++)
+        if (d->extra_row[e] < 0 || d->extra_row[e] >= n || d->extra_col[e] < 0 || d->extra_col[e] >= n)
+            return EES_EINVAL;
+    return EES_OK;
+}
+
+// node -> devices incidence over all non-ground nodes (a device appears once
+// per distinct node), devices ascending.
+void build_incidence(const ees_desc *d, std::vector<int64_t> &ptr, std::vector<int32_t> &dev)
+{
+    const int64_t N = d->n_dev;
+    ptr.assign((size_t)d->n_nodes + 1, 0);
+    for (int64_t i = 0; i < N; i++) {
+        const int32_t T[4] = {d->d[i], d->g[i], d->s[i], d->b[i]};
+        for (int a = 0; a < 4; a++) {
+            bool dup = T[a] < 0;
+            for (int c = 0; c < a; c++) dup |= T[c] == T[a];
+            if (!dup) ptr[T[a] + 1]++;
+        }
+    }
+    for (int32_t v = 0; v < d->n_nodes; v++) ptr[v + 1] += ptr[v];
+    dev.resize((size_t)ptr[d->n_nodes]);
+    std::vector<int64_t> fill(ptr.begin(), ptr.end() - 1);
+    for (int64_t i = 0; i < N; i++) {
+        const int32_t T[4] = {d->d[i], d->g[i], d->s[i], d->b[i]};
+        for (int a = 0; a < 4; a++) {
+            bool dup = T[a] < 0;
+            for (int c = 0; c < a; c++) dup |= T[c] == T[a];
+            if (!dup) dev[fill[T[a]]++] = (int32_t)i;
+        }
+    }
+}
+
+// CSR pattern: row r holds every non-ground terminal of every device on r
+// (all ordered pairs) plus the extra entries of row r; sorted unique.
+ees_status build_pattern(const ees_desc *d, ees_ctx *c, const std::vector<int64_t> &iptr,
+                         const std::vector<int32_t> &idev)
+{
+    const int32_t n = c->n;
+    std::vector<int64_t> eptr((size_t)n + 1, 0);
+    for (int64_t e = 0; e < d->n_extra_entries; e++) eptr[d->extra_row[e] + 1]++;
+    for (int32_t r = 0; r < n; r++) eptr[r + 1] += eptr[r];
+    std::vector<int32_t> ecol((size_t)eptr[n]);
+    {
+        std::vector<int64_t> fill(eptr.begin(), eptr.end() - 1);
+        for (int64_t e = 0; e < d->n_extra_entries; e++) ecol[fill[d->extra_row[e]]++] = d->extra_col[e];
+    }
+    std::vector<int64_t> cnt((size_t)n + 1, 0);
+    const int32_t *TT[4] = {d->d, d->g, d->s, d->b};
+    auto collect = [&](int32_t r, std::vector<int32_t> &tmp) {
+        tmp.clear();
+        if (r < d->n_nodes)
+            for (int64_t k = iptr[r]; k < iptr[r + 1]; k++) {
+                const int32_t i = idev[k];
+                for (int a = 0; a < 4; a++)
+                    if (TT[a][i] >= 0) tmp.push_back(TT[a][i]);
+            }
+        for (int64_t k = eptr[r]; k < eptr[r + 1]; k++) tmp.push_back(ecol[k]);
+        std::sort(tmp.begin(), tmp.end());
+        tmp.erase(std::unique(tmp.begin(), tmp.end()), tmp.end());
+    };
+#pragma omp parallel
+    {
+        std::vector<int32_t> tmp;
+#pragma omp for schedule(dynamic, 4096)
+        for (int32_t r = 0; r < n; r++) {
+            collect(r, tmp);
+            cnt[r + 1] = (int64_t)tmp.size();
+        }
+    }
+    for (int32_t r = 0; r < n; r++) cnt[r + 1] += cnt[r];
+    if (cnt[n] > INT32_MAX) return EES_EINVAL;   // nnz must fit int32 (SURVEY §8(a) layout)
+    c->nnz = cnt[n];
+    c->row_ptr.resize((size_t)n + 1);
+    for (int32_t r = 0; r <= n; r++) c->row_ptr[r] = (int32_t)cnt[r];
+    c->col_idx.resize((size_t)c->nnz);
+#pragma omp parallel
+    {
+        std::vector<int32_t> tmp;
+#pragma omp for schedule(dynamic, 4096)
+        for (int32_t r = 0; r < n; r++) {
+            collect(r, tmp);
+            std::copy(tmp.begin(), tmp.end(), c->col_idx.begin() + cnt[r]);
+        }
+    }
+    return EES_OK;
+}
+
+int32_t find_slot(const ees_ctx *c, int32_t r, int32_t col)
+{
+    const int32_t *b = c->col_idx.data() + c->row_ptr[r];
+    const int32_t *e = c->col_idx.data() + c->row_ptr[r + 1];
+    const int32_t *p = std::lower_bound(b, e, col);
+    return (p != e && *p == col) ? (int32_t)(p - c->col_idx.data()) : -1;
+}
+
+// First-fit greedy colouring in netlist order over the
+// conflict nodes (non-ground; rails removed under EES_CONFLICT_EXCLUDE_RAILS).
+// Each node keeps the colours of its already-coloured devices: up to 4 inline,
+// then a bitset with a monotone "first non-full word" cursor, so a device on a
+// clique of size f costs O(1) amortised instead of O(f).
+struct NodeColors {
+    int32_t cnt = 0;       // inline colours, or -1 once converted to a bitset
+    int32_t inl[4];
+    int32_t big = -1;      // index into bitsets
+};
+
+int32_t greedy_color(const ees_desc *d, const std::vector<uint8_t> &excluded,
+                     std::vector<int32_t> &color, int32_t &max_node_deg)
+{
+    const int64_t N = d->n_dev;
+    color.assign((size_t)N, 0);
+    std::vector<NodeColors> nc((size_t)d->n_nodes);
+    std::vector<std::vector<uint64_t>> bits;
+    std::vector<int32_t> first_nonfull;
+    std::vector<int32_t> deg((size_t)d->n_nodes, 0);
+    int32_t C = 0;
+    for (int64_t i = 0; i < N; i++) {
+        int32_t U[4];
+        int nu = 0;
+        const int32_t T[4] = {d->d[i], d->g[i], d->s[i], d->b[i]};
+        for (int a = 0; a < 4; a++) {
+            if (T[a] < 0 || excluded[T[a]]) continue;
+            bool dup = false;
+            for (int k = 0; k < nu; k++) dup |= U[k] == T[a];
+            if (!dup) U[nu++] = T[a];
+        }
+        int64_t w = 0;
+        for (int k = 0; k < nu; k++) {
+            const NodeColors &s = nc[U[k]];
+            if (s.big >= 0) w = std::max<int64_t>(w, first_nonfull[s.big]);
+        }
+        int32_t col;
+        for (;; w++) {
+            uint64_t m = 0;
+            for (int k = 0; k < nu; k++) {
+                const NodeColors &s = nc[U[k]];
+                if (s.big >= 0) {
+                    const std::vector<uint64_t> &bv = bits[s.big];
+                    if (w < (int64_t)bv.size()) m |= bv[w];
+                } else {
+                    for (int q = 0; q < s.cnt; q++)
+                        if ((s.inl[q] >> 6) == w) m |= 1ull << (s.inl[q] & 63);
+                }
+            }
+            if (~m) {
+                col = (int32_t)(64 * w + __builtin_ctzll(~m));
+                break;
+            }
+        }
+        color[i] = col;
+        if (col + 1 > C) C = col + 1;
+        for (int k = 0; k < nu; k++) {
+            NodeColors &s = nc[U[k]];
+            deg[U[k]]++;
+            if (s.big < 0 && s.cnt < 4) {
+                s.inl[s.cnt++] = col;
+                continue;
+            }
+            if (s.big < 0) {
+                s.big = (int32_t)bits.size();
+                bits.emplace_back();
+                first_nonfull.push_back(0);
+                for (int q = 0; q < s.cnt; q++) {
+                    const int32_t cc = s.inl[q];
+                    if ((int64_t)bits[s.big].size() <= (cc >> 6)) bits[s.big].resize((cc >> 6) + 1, 0);
+                    bits[s.big][cc >> 6] |= 1ull << (cc & 63);
+                }
+                s.cnt = -1;
+            }
+            std::vector<uint64_t> &bv = bits[s.big];
+            if ((int64_t)bv.size() <= (col >> 6)) bv.resize((col >> 6) + 1, 0);
+            bv[col >> 6] |= 1ull << (col & 63);
+            int32_t &f = first_nonfull[s.big];
+            while (f < (int32_t)bv.size() && bv[f] == ~0ull) f++;
+        }
+    }
+    max_node_deg = 0;
+    for (int32_t v = 0; v < d->n_nodes; v++) max_node_deg = std::max(max_node_deg, deg[v]);
+    return N ? C : 0;
+}
+
+CallK make_call(const ees_ctx *c, const double *x, double h, double *A, double *b)
+{
+    CallK k;
+    std::memset(&k, 0, sizeof(k));
+    for (size_t m = 0; m < c->models.size(); m++) {
+        const ees_model &md = c->models[m];
+        CardK &cd = k.cards[m];
+        cd.p = (double)md.polarity;
+        cd.vt = cd.p * md.vt0;
+        cd.lam = md.lambda;
+        cd.gcgs = md.cgs / h;      // S:196 Geq = C/dt (IEEE division; h = +inf -> 0)
+        cd.gcgd = md.cgd / h;
+        cd.gcdb = md.cdb / h;
+    }
+    k.x = x;
+    k.A = A;
+    k.b = b;
+    k.gmin = c->gmin;
+    k.n_models = (int32_t)c->models.size();
+    k.n_rail_nodes = (int32_t)c->rails.size();
+    for (size_t r = 0; r < c->rails.size(); r++) k.rail_node[r] = c->rails[r];
+    k.n_rail_a = c->n_rail_a;
+    k.n_rail_entries = c->n_rail_entries;
+    std::memcpy(k.rail_target, c->rail_target, sizeof(k.rail_target));
+    return k;
+}
+
+ees_status enqueue(ees_ctx *c, int32_t variant, const double *x, double h, double *A, double *b,
+                   cudaStream_t st, int32_t *launches)
+{
+    const CallK call = make_call(c, x, h, A, b);
+    int nl = 0;
+    cudaError_t e = cudaSuccess;
+    if (variant == EES_ATOMIC) {
+        e = launch_atomic(c->L_atomic.k(), call, c->atomic_grid, st);
+        nl = c->n_dev ? 1 : 0;
+    } else if (variant == EES_COLOR) {
+        const DevK dv = c->L_color.k();
+        for (int32_t col = 0; col < c->n_colors && e == cudaSuccess; col++) {
+            e = launch_color(dv, call, c->color_ptr[col], c->color_ptr[col + 1] - c->color_ptr[col],
+                             c->partials + c->color_blk_off[col] * c->n_rail_entries, st);
+            nl++;
+        }
+        if (e == cudaSuccess && c->n_rail_entries && c->n_dev) {
+            e = launch_rail_finalize(call, c->partials, c->color_blk_off[c->n_colors], st);
+            nl++;
+        }
+    } else if (variant == EES_GATHER) {
+        e = launch_gather(c->L_gather.k(), c->gk, call, st, &nl);
+    } else {
+        return EES_ESTATE;
+    }
+    if (launches) *launches = nl;
+    return e == cudaSuccess ? EES_OK : EES_ECUDA;
+}
+
+ees_status build_layouts(const ees_desc *d, ees_ctx *c, const std::vector<int32_t> &raw_slot,
+                         const std::vector<int32_t> &rail_ord)
+{
+    const int64_t N = c->n_dev;
+    // netlist-order SoA shared by ATOMIC and GATHER
+    std::vector<double> beta((size_t)N), v0((size_t)(3 * N));
+    std::vector<uint8_t> model((size_t)N);
+    std::vector<int4> term_plain((size_t)N), term_rail((size_t)N);
+    std::vector<int32_t> slot_rail((size_t)(NPAIR * N));
+    auto railcode = [&](int32_t t) { return (t >= 0 && rail_ord[t] >= 0) ? -2 - rail_ord[t] : t; };
+    // map raw A slot -> rail entry
+    auto slotcode = [&](int32_t k) {
+        if (k < 0) return k;
+        for (int e = 0; e < c->n_rail_a; e++)
+            if (c->rail_target[e] == k) return -2 - e;
+        return k;
+    };
+    std::vector<uint8_t> is_rail_slot;
+    if (c->n_rail_a) {
+        is_rail_slot.assign((size_t)c->nnz, 0);
+        for (int e = 0; e < c->n_rail_a; e++) is_rail_slot[c->rail_target[e]] = 1;
+    }
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < N; i++) {
+        const ees_model &m = c->models[d->model[i]];
+        beta[i] = (m.kp * d->w[i]) / d->l[i];
+        for (int t = 0; t < 3; t++) v0[t * N + i] = d->vprev[t * N + i];
+        model[i] = (uint8_t)d->model[i];
+        term_plain[i] = make_int4(d->d[i], d->g[i], d->s[i], d->b[i]);
+        term_rail[i] = make_int4(railcode(d->d[i]), railcode(d->g[i]), railcode(d->s[i]), railcode(d->b[i]));
+        for (int p = 0; p < NPAIR; p++) {
+            const int32_t k = raw_slot[p * N + i];
+            slot_rail[p * N + i] = (k >= 0 && c->n_rail_a && is_rail_slot[k]) ? slotcode(k) : k;
+        }
+    }
+    Layout &La = c->L_atomic;
+    La.N = N;
+    TRY(upload(c, &La.term, term_rail.data(), N));
+    TRY(upload(c, &La.beta, beta.data(), N));
+    TRY(upload(c, &La.v0, v0.data(), 3 * N));
+    TRY(upload(c, &La.model, model.data(), N));
+    TRY(upload(c, &La.slot, slot_rail.data(), NPAIR * N));
+    Layout &Lg = c->L_gather;
+    Lg = La;
+    Lg.slot = nullptr;
+    TRY(upload(c, &Lg.term, term_plain.data(), N));
+    // colour-major copy
+    {
+        std::vector<int32_t> perm((size_t)N);
+        std::vector<int64_t> fill(c->color_ptr.begin(), c->color_ptr.end() - 1);
+        for (int64_t i = 0; i < N; i++) perm[fill[c->color[i]]++] = (int32_t)i;
+        std::vector<double> beta_c((size_t)N), v0_c((size_t)(3 * N));
+        std::vector<uint8_t> model_c((size_t)N);
+        std::vector<int4> term_c((size_t)N);
+        std::vector<int32_t> slot_c((size_t)(NPAIR * N));
+#pragma omp parallel for schedule(static)
+        for (int64_t q = 0; q < N; q++) {
+            const int64_t i = perm[q];
+            beta_c[q] = beta[i];
+            for (int t = 0; t < 3; t++) v0_c[t * N + q] = v0[t * N + i];
+            model_c[q] = model[i];
+            term_c[q] = term_rail[i];
+            for (int p = 0; p < NPAIR; p++) slot_c[p * N + q] = slot_rail[p * N + i];
+        }
+        Layout &Lc = c->L_color;
+        Lc.N = N;
+        TRY(upload(c, &Lc.term, term_c.data(), N));
+        TRY(upload(c, &Lc.beta, beta_c.data(), N));
+        TRY(upload(c, &Lc.v0, v0_c.data(), 3 * N));
+        TRY(upload(c, &Lc.model, model_c.data(), N));
+        TRY(upload(c, &Lc.slot, slot_c.data(), NPAIR * N));
+    }
+    // colour block offsets + rail partials
+    c->color_blk_off.assign((size_t)c->n_colors + 1, 0);
+    for (int32_t col = 0; col < c->n_colors; col++) {
+        const int64_t cnt = c->color_ptr[col + 1] - c->color_ptr[col];
+        c->color_blk_off[col + 1] = c->color_blk_off[col] + (cnt + kBlock - 1) / kBlock;
+    }
+    TRY(dalloc(c, &c->partials, (size_t)(c->color_blk_off[c->n_colors] * std::max(1, c->n_rail_entries))));
+    return EES_OK;
+}
+
+// GATHER: compact contribution buffer + transposed per-target lists.
+ees_status build_gather(const ees_desc *d, ees_ctx *c, const std::vector<int32_t> &raw_slot)
+{
+    const int64_t N = c->n_dev, nnz = c->nnz;
+    const int64_t NT = nnz + c->n;
+    const int32_t *TT[4] = {d->d, d->g, d->s, d->b};
+    std::vector<int32_t> off((size_t)N + 1, 0);
+    std::vector<int64_t> tcnt((size_t)NT + 1, 0);
+    for (int64_t i = 0; i < N; i++) {
+        int q = 0;
+        for (int p = 0; p < NPAIR; p++) {
+            const int32_t k = raw_slot[p * N + i];
+            if (k >= 0) { q++; tcnt[k]++; }
+        }
+        for (int a = 0; a < 4; a++)
+            if (TT[a][i] >= 0) { q++; tcnt[nnz + TT[a][i]]++; }
+        if ((int64_t)off[i] + q > INT32_MAX) return EES_EINVAL;
+        off[i + 1] = off[i] + q;
+    }
+    const int64_t ncontrib = off[N];
+    c->st.n_contributions = ncontrib;
+    // light / heavy split
+    std::vector<int32_t> tptr((size_t)NT + 1, 0);
+    std::vector<int32_t> heavy_target;
+    std::vector<int32_t> hpos((size_t)NT, -1);
+    int64_t hl = 0;
+    for (int64_t t = 0; t < NT; t++) {
+        const bool heavy = tcnt[t] > kHeavyLen;
+        if (heavy) {
+            hpos[t] = (int32_t)heavy_target.size();
+            heavy_target.push_back((int32_t)t);
+            hl += tcnt[t];
+        }
+        tptr[t + 1] = tptr[t] + (heavy ? 0 : (int32_t)tcnt[t]);
+    }
+    const int32_t nh = (int32_t)heavy_target.size();
+    std::vector<int64_t> hptr((size_t)nh + 1, 0);
+    for (int32_t h = 0; h < nh; h++) hptr[h + 1] = hptr[h] + tcnt[heavy_target[h]];
+    std::vector<int32_t> tidx((size_t)tptr[NT]), hidx((size_t)hl);
+    {
+        std::vector<int32_t> fill(tptr.begin(), tptr.end() - 1);
+        std::vector<int64_t> hfill(hptr.begin(), hptr.end() - 1);
+        for (int64_t i = 0; i < N; i++) {     // device order -> lists sorted by device
+            int32_t q = off[i];
+            auto put = [&](int64_t t) {
+                if (hpos[t] >= 0) hidx[hfill[hpos[t]]++] = q;
+                else tidx[fill[t]++] = q;
+                q++;
+            };
+            for (int p = 0; p < NPAIR; p++) {
+                const int32_t k = raw_slot[p * N + i];
+                if (k >= 0) put(k);
+            }
+            for (int a = 0; a < 4; a++)
+                if (TT[a][i] >= 0) put(nnz + TT[a][i]);
+        }
+    }
+    // heavy lists are cut into chunks of kChunk; chunks of one target are
+    // consecutive, so chunk c spans [chunk_beg[c], chunk_beg[c+1]).
+    std::vector<int32_t> chunk_beg, heavy_chunk((size_t)nh + 1, 0);
+    for (int32_t h = 0; h < nh; h++) {
+        heavy_chunk[h] = (int32_t)chunk_beg.size();
+        for (int64_t b0 = hptr[h]; b0 < hptr[h + 1]; b0 += kChunk) chunk_beg.push_back((int32_t)b0);
+    }
+    heavy_chunk[nh] = (int32_t)chunk_beg.size();
+    const int32_t nchunks = (int32_t)chunk_beg.size();
+    chunk_beg.push_back((int32_t)hl);
+    GatherK &g = c->gk;
+    g.n_targets = NT;
+    g.nnz = nnz;
+    g.n_chunks = nchunks;
+    g.n_heavy = nh;
+    TRY(upload(c, const_cast<int32_t **>(&g.off), off.data(), N + 1));
+    TRY(dalloc(c, &g.buf, (size_t)ncontrib));
+    TRY(upload(c, const_cast<int32_t **>(&g.tptr), tptr.data(), NT + 1));
+    TRY(upload(c, const_cast<int32_t **>(&g.tidx), tidx.data(), tidx.size()));
+    TRY(upload(c, const_cast<int32_t **>(&g.chunk_beg), chunk_beg.data(), chunk_beg.size()));
+    TRY(upload(c, const_cast<int32_t **>(&g.hidx), hidx.data(), hidx.size()));
+    TRY(dalloc(c, &g.chunk_part, (size_t)nchunks));
+    TRY(upload(c, const_cast<int32_t **>(&g.heavy_target), heavy_target.data(), heavy_target.size()));
+    TRY(upload(c, const_cast<int32_t **>(&g.heavy_chunk), heavy_chunk.data(), heavy_chunk.size()));
+    c->st.n_heavy_targets = nh;
+    return EES_OK;
+}
+
+ees_status autotune(ees_ctx *c)
+{
+    double *x, *A, *b;
+    TRY(dalloc(c, &x, (size_t)c->n));
+    TRY(dalloc(c, &A, (size_t)c->nnz));
+    TRY(dalloc(c, &b, (size_t)c->n));
+    cudaStream_t st;
+    if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) return EES_ECUDA;
+    cudaMemsetAsync(x, 0, sizeof(double) * std::max(1, c->n), st);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    double best = 1e300;
+    int32_t bestv = EES_ATOMIC;
+    ees_status rc = EES_OK;
+    for (int32_t v = EES_COLOR; v <= EES_GATHER && rc == EES_OK; v++) {
+        // skip hopeless colour phasing: more than 512 colours is launch-bound by construction
+        if (v == EES_COLOR && c->n_colors > 512) { c->st.tune_ms[v] = -1; continue; }
+        for (int it = 0; it < 2 && rc == EES_OK; it++) rc = enqueue(c, v, x, 1e-12, A, b, st, nullptr);
+        cudaEventRecord(e0, st);
+        const int reps = 5;
+        for (int it = 0; it < reps && rc == EES_OK; it++) rc = enqueue(c, v, x, 1e-12, A, b, st, nullptr);
+        cudaEventRecord(e1, st);
+        if (cudaEventSynchronize(e1) != cudaSuccess) rc = EES_ECUDA;
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e0, e1);
+        c->st.tune_ms[v] = ms / reps;
+        if (ms / reps < best) { best = ms / reps; bestv = v; }
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaStreamDestroy(st);
+    c->variant = bestv;
+    return rc;
+}
+
+ees_status setup_impl(const ees_desc *d, ees_ctx *c)
+{
+    const double t0 = now_s();
+    TRY(validate(d));
+    c->n_nodes = d->n_nodes;
+    c->n_extra = d->n_extra;
+    c->n = d->n_nodes + d->n_extra;
+    c->n_dev = d->n_dev;
+    c->models.assign(d->models, d->models + d->n_models);
+    c->rails.assign(d->rails, d->rails + d->n_rails);
+    c->gmin = d->gmin;
+    c->rule = d->conflict_rule;
+    const int64_t N = d->n_dev;
+
+    std::vector<int64_t> iptr;
+    std::vector<int32_t> idev;
+    build_incidence(d, iptr, idev);
+    TRY(build_pattern(d, c, iptr, idev));
+    // stamp slots (raw CSR indices) per device and live pair
+    std::vector<int32_t> raw_slot((size_t)(NPAIR * N));
+    {
+        const int32_t *TT[4] = {d->d, d->g, d->s, d->b};
+#pragma omp parallel for schedule(static)
+        for (int64_t i = 0; i < N; i++)
+            for (int p = 0; p < NPAIR; p++) {
+                const int32_t r = TT[kPairRow[p]][i], col = TT[kPairCol[p]][i];
+                raw_slot[p * N + i] = (r >= 0 && col >= 0) ? find_slot(c, r, col) : -1;
+            }
+    }
+    c->st.setup_pattern_s = now_s() - t0;
+    // rails: ordinals, rail x rail A entries, rail b rows
+    std::vector<int32_t> rail_ord((size_t)std::max(1, c->n_nodes), -1);
+    for (size_t r = 0; r < c->rails.size(); r++) rail_ord[c->rails[r]] = (int32_t)r;
+    int32_t ne = 0;
+    for (size_t r = 0; r < c->rails.size(); r++)
+        for (size_t r2 = 0; r2 < c->rails.size(); r2++) {
+            const int32_t k = find_slot(c, c->rails[r], c->rails[r2]);
+            if (k >= 0) c->rail_target[ne++] = k;
+        }
+    c->n_rail_a = ne;
+    for (size_t r = 0; r < c->rails.size(); r++) c->rail_target[ne++] = c->rails[r];
+    c->n_rail_entries = ne;
+    // colouring
+    const double tc = now_s();
+    std::vector<uint8_t> excluded((size_t)std::max(1, c->n_nodes), 0);
+    if (d->conflict_rule == EES_CONFLICT_EXCLUDE_RAILS)
+        for (int32_t r : c->rails) excluded[r] = 1;
+    int32_t maxdeg = 0;
+    c->n_colors = greedy_color(d, excluded, c->color, maxdeg);
+    c->color_ptr.assign((size_t)c->n_colors + 1, 0);
+    for (int64_t i = 0; i < N; i++) c->color_ptr[c->color[i] + 1]++;
+    int64_t gmax = 0, gmin = N;
+    for (int32_t col = 0; col < c->n_colors; col++) {
+        gmax = std::max(gmax, c->color_ptr[col + 1]);
+        gmin = std::min(gmin, c->color_ptr[col + 1]);
+    }
+    for (int32_t col = 0; col < c->n_colors; col++) c->color_ptr[col + 1] += c->color_ptr[col];
+    c->st.setup_color_s = now_s() - tc;
+    c->st.max_group = (int32_t)gmax;
+    c->st.min_group = c->n_colors ? (int32_t)gmin : 0;
+    c->st.max_conflict_node_degree = maxdeg;
+
+    c->host_only = (d->flags & EES_SETUP_HOST_ONLY) != 0;
+    if (c->host_only) {
+        int64_t nc = 0;
+        for (int64_t k = 0; k < NPAIR * N; k++) nc += raw_slot[k] >= 0;
+        for (int64_t i = 0; i < N; i++)
+            nc += (d->d[i] >= 0) + (d->g[i] >= 0) + (d->s[i] >= 0) + (d->b[i] >= 0);
+        c->st.n_contributions = nc;
+        c->variant = d->variant == EES_AUTO ? EES_ATOMIC : d->variant;
+        c->st.setup_s = now_s() - t0;
+        return EES_OK;
+    }
+    TRY(build_layouts(d, c, raw_slot, rail_ord));
+    TRY(build_gather(d, c, raw_slot));
+    int sms = 148;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t want = (N + kBlock - 1) / kBlock;
+    c->atomic_grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sms * atomic_blocks_per_sm()));
+    if (cudaDeviceSynchronize() != cudaSuccess) return EES_ECUDA;
+    if (d->variant == EES_AUTO) {
+        TRY(autotune(c));
+    } else {
+        c->variant = d->variant;
+    }
+    c->st.setup_s = now_s() - t0;
+    return EES_OK;
+}
+
+void free_ctx(ees_ctx *c)
+{
+    if (!c) return;
+    for (void *p : c->allocs) cudaFree(p);
+    delete c;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" {
+
+ees_status ees_setup(const ees_desc *desc, ees_ctx **out)
+{
+    if (!out) return EES_EINVAL;
+    *out = nullptr;
+    ees_ctx *c = new (std::nothrow) ees_ctx();
+    if (!c) return EES_ENOMEM;
+    ees_status s;
+    try {
+        s = setup_impl(desc, c);
+    } catch (const std::bad_alloc &) {
+        s = EES_ENOMEM;
+    } catch (...) {
+        s = EES_EINVAL;
+    }
+    if (s != EES_OK) {
+        free_ctx(c);
+        return s;
+    }
+    *out = c;
+    return EES_OK;
+}
+
+ees_status ees_pattern(const ees_ctx *c, int32_t *n, int64_t *nnz, const int32_t **row_ptr,
+                       const int32_t **col_idx)
+{
+    if (!c) return EES_EINVAL;
+    if (n) *n = c->n;
+    if (nnz) *nnz = c->nnz;
+    if (row_ptr) *row_ptr = c->row_ptr.data();
+    if (col_idx) *col_idx = c->col_idx.data();
+    return EES_OK;
+}
+
+ees_status ees_find_slot(const ees_ctx *c, int32_t row, int32_t col, int64_t *slot)
+{
+    if (!c || !slot || row < 0 || row >= c->n || col < 0 || col >= c->n) return EES_EINVAL;
+    *slot = find_slot(c, row, col);
+    return EES_OK;
+}
+
+ees_status ees_colors(const ees_ctx *c, const int32_t **color, int32_t *n_colors)
+{
+    if (!c) return EES_EINVAL;
+    if (color) *color = c->color.data();
+    if (n_colors) *n_colors = c->n_colors;
+    return EES_OK;
+}
+
+ees_status ees_eval_stamp(ees_ctx *c, const double *x, double h, double *A, double *b, ees_stream stream)
+{
+    if (!c) return EES_EINVAL;
+    if (!(h > 0.0)) return EES_EINVAL;           // rejects h <= 0 and NaN; +inf = DC
+    if (c->host_only) return EES_ESTATE;
+    if (c->n_dev == 0) return EES_OK;
+    if (!x || !A || !b) return EES_EINVAL;
+    int32_t nl = 0;
+    ees_status s = enqueue(c, c->variant, x, h, A, b, (cudaStream_t)stream, &nl);
+    c->launches = nl;
+    return s;
+}
+
+ees_status ees_eval_stamp_host(ees_ctx *c, const double *x, double h, double *A, double *b,
+                               ees_stream stream)
+{
+    if (!c) return EES_EINVAL;
+    if (!(h > 0.0)) return EES_EINVAL;
+    if (c->host_only) return EES_ESTATE;
+    if (!x || !A || !b) return EES_EINVAL;
+    if (!c->hx) {
+        TRY(dalloc(c, &c->hx, (size_t)c->n));
+        TRY(dalloc(c, &c->hA, (size_t)c->nnz));
+        TRY(dalloc(c, &c->hb, (size_t)c->n));
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t bn = sizeof(double) * (size_t)c->n, ba = sizeof(double) * (size_t)c->nnz;
+    if (cudaMemcpyAsync(c->hx, x, bn, cudaMemcpyHostToDevice, st) != cudaSuccess) return EES_ECUDA;
+    if (cudaMemcpyAsync(c->hA, A, ba, cudaMemcpyHostToDevice, st) != cudaSuccess) return EES_ECUDA;
+    if (cudaMemcpyAsync(c->hb, b, bn, cudaMemcpyHostToDevice, st) != cudaSuccess) return EES_ECUDA;
+    ees_status s = ees_eval_stamp(c, c->hx, h, c->hA, c->hb, stream);
+    if (s != EES_OK) return s;
+    if (cudaMemcpyAsync(A, c->hA, ba, cudaMemcpyDeviceToHost, st) != cudaSuccess) return EES_ECUDA;
+    if (cudaMemcpyAsync(b, c->hb, bn, cudaMemcpyDeviceToHost, st) != cudaSuccess) return EES_ECUDA;
+    return cudaStreamSynchronize(st) == cudaSuccess ? EES_OK : EES_ECUDA;
+}
+
+ees_status ees_set_variant(ees_ctx *c, int32_t variant)
+{
+    if (!c || variant < EES_AUTO || variant > EES_GATHER) return EES_EINVAL;
+    if (variant == EES_AUTO) {
+        double best = 1e300;
+        int32_t bv = c->variant;
+        for (int v = EES_COLOR; v <= EES_GATHER; v++)
+            if (c->st.tune_ms[v] > 0 && c->st.tune_ms[v] < best) { best = c->st.tune_ms[v]; bv = v; }
+        c->variant = bv;
+    } else {
+        c->variant = variant;
+    }
+    return EES_OK;
+}
+
+ees_status ees_stats(const ees_ctx *c, ees_stats_t *out)
+{
+    if (!c || !out) return EES_EINVAL;
+    *out = c->st;
+    out->n_dev = c->n_dev;
+    out->nnz = c->nnz;
+    out->n = c->n;
+    out->n_colors = c->n_colors;
+    out->variant_chosen = c->variant;
+    out->n_rail_entries = c->n_rail_entries;
+    out->launches_per_call = c->launches;
+    return EES_OK;
+}
+
+ees_status ees_race_probe(ees_ctx *c, const int32_t *color, int64_t *n_conflicts)
+{
+    if (!c || !n_conflicts) return EES_EINVAL;
+    if (c->host_only) return EES_ESTATE;
+    const int64_t N = c->n_dev;
+    const int32_t *col = color ? color : c->color.data();
+    int32_t C = 0;
+    for (int64_t i = 0; i < N; i++) {
+        if (col[i] < 0) return EES_EINVAL;
+        C = std::max(C, col[i] + 1);
+    }
+    std::vector<int64_t> ptr((size_t)C + 1, 0);
+    for (int64_t i = 0; i < N; i++) ptr[col[i] + 1]++;
+    for (int32_t k = 0; k < C; k++) ptr[k + 1] += ptr[k];
+    std::vector<int32_t> perm((size_t)std::max<int64_t>(1, N));
+    {
+        std::vector<int64_t> fill(ptr.begin(), ptr.end() - 1);
+        for (int64_t i = 0; i < N; i++) perm[fill[col[i]]++] = (int32_t)i;
+    }
+    int32_t *dperm = nullptr, *cnt_a = nullptr, *cnt_b = nullptr;
+    unsigned long long *dout = nullptr;
+    cudaError_t e = cudaMalloc(&dperm, sizeof(int32_t) * perm.size());
+    e = e == cudaSuccess ? cudaMalloc(&cnt_a, sizeof(int32_t) * std::max<int64_t>(1, c->nnz)) : e;
+    e = e == cudaSuccess ? cudaMalloc(&cnt_b, sizeof(int32_t) * std::max(1, c->n)) : e;
+    e = e == cudaSuccess ? cudaMalloc(&dout, sizeof(unsigned long long)) : e;
+    if (e == cudaSuccess) e = cudaMemcpy(dperm, perm.data(), sizeof(int32_t) * perm.size(), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemset(dout, 0, sizeof(unsigned long long));
+    for (int32_t k = 0; k < C && e == cudaSuccess; k++) {
+        cudaMemsetAsync(cnt_a, 0, sizeof(int32_t) * c->nnz, 0);
+        cudaMemsetAsync(cnt_b, 0, sizeof(int32_t) * c->n, 0);
+        e = launch_race_probe(c->L_atomic.k(), dperm, ptr[k], ptr[k + 1] - ptr[k], cnt_a, cnt_b, 0);
+        if (e == cudaSuccess) e = launch_count_conflicts(cnt_a, c->nnz, dout, 0);
+        if (e == cudaSuccess) e = launch_count_conflicts(cnt_b, c->n, dout, 0);
+    }
+    unsigned long long hout = 0;
+    if (e == cudaSuccess) e = cudaMemcpy(&hout, dout, sizeof(hout), cudaMemcpyDeviceToHost);
+    cudaFree(dperm);
+    cudaFree(cnt_a);
+    cudaFree(cnt_b);
+    cudaFree(dout);
+    if (e != cudaSuccess) return EES_ECUDA;
+    *n_conflicts = (int64_t)hout;
+    return EES_OK;
+}
+
+ees_status ees_destroy(ees_ctx *c)
+{
+    if (!c) return EES_EINVAL;
+    free_ctx(c);
+    return EES_OK;
+}
+
+const char *ees_strerror(ees_status s)
+{
+    switch (s) {
+    case EES_OK: return "ok";
+    case EES_EINVAL: return "invalid argument";
+    case EES_ENOMEM: return "out of memory";
+    case EES_ECUDA: return "CUDA error";
+    case EES_ESTATE: return "invalid context state";
+    default: return "unknown status";
+    }
+}
+
+}  // extern "C"

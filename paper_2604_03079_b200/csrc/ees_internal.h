@@ -1,0 +1,96 @@
+// ees_internal.h -- shared between the host setup (ees_host.cpp) and the
+// sm_100a kernels (ees_kernels.cu).  Product code; never includes oracle/.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/ees.h"
+
+namespace ees {
+
+// Live stamp pairs of the 4-terminal FET (SURVEY §8(a) "12 of 16"; GB, BG,
+// SB, BS are structurally zero because the bulk carries only C_db, S:77,
+// S:230).  Terminal index D=0 G=1 S=2 B=3.
+enum Pair { DD = 0, DG, DS, DB, GD, GG, GS, SD, SG, SS, BD, BB, NPAIR };
+constexpr int kPairRow[NPAIR] = {0, 0, 0, 0, 1, 1, 1, 2, 2, 2, 3, 3};
+constexpr int kPairCol[NPAIR] = {0, 1, 2, 3, 0, 1, 2, 0, 1, 2, 0, 3};
+__host__ __device__ constexpr int pair_row(int p) { return p < 4 ? 0 : p < 7 ? 1 : p < 10 ? 2 : 3; }
+__host__ __device__ constexpr int pair_col(int p)
+{
+    return p < 4 ? p : p < 7 ? p - 4 : p < 10 ? p - 7 : (p == 10 ? 0 : 3);
+}
+
+constexpr int kMaxRailEntries = EES_MAX_RAILS * EES_MAX_RAILS + EES_MAX_RAILS;
+constexpr int kBlock = 256;          // threads per block of the per-device kernels
+constexpr int kHeavyLen = 128;       // GATHER: lists longer than this are chunk-reduced
+constexpr int kChunk = 4096;         // GATHER: contributions per heavy chunk (one block)
+
+// Per-call model card: everything h-dependent is folded in on the host
+// (Gc = C/h, correctly rounded FP64 division, "Geq = C/dt").
+struct CardK {
+    double vt;        // p * vt0
+    double lam;
+    double gcgs, gcgd, gcdb;
+    double p;         // +1 / -1
+};
+
+struct CallK {
+    CardK cards[EES_MAX_MODELS];
+    const double *x;
+    double *A;
+    double *b;
+    double gmin;
+    int32_t n_models;
+    int32_t n_rail_nodes;
+    int32_t n_rail_a;                 // rail entries [0, n_rail_a) are A slots, the rest b rows
+    int32_t n_rail_entries;
+    int32_t rail_node[EES_MAX_RAILS];
+    int32_t rail_target[kMaxRailEntries];
+};
+
+// SoA device arrays of one execution order.
+//  term : (d, g, s, b); >= 0 node, -1 ground, <= -2 rail ordinal r = -2 - code
+//         (rail-coded layouts only; the GATHER layout holds plain node ids)
+//  slot : [NPAIR][N]; >= 0 A index, -1 no entry, <= -2 rail entry e = -2 - code
+struct DevK {
+    int64_t N;
+    const int4 *term;
+    const double *beta;
+    const double *v0;      // [3][N]: v_gs, v_gd, v_db at the last accepted step
+    const uint8_t *model;
+    const int32_t *slot;   // [NPAIR][N] (null in the GATHER layout)
+};
+
+// GATHER layout extras
+struct GatherK {
+    const int32_t *off;        // [N+1] first compact contribution of each device
+    double *buf;               // [n_contrib] contribution values
+    const int32_t *tptr;       // [nnz+n+1] light contributor lists per target
+    const int32_t *tidx;       // compact contribution indices
+    int64_t n_targets;         // nnz + n
+    int64_t nnz;
+    // heavy targets, chunk-reduced
+    int32_t n_chunks;
+    const int32_t *chunk_beg;  // [n_chunks+1] into hidx
+    const int32_t *hidx;       // compact indices of heavy lists, concatenated
+    double *chunk_part;        // [n_chunks]
+    int32_t n_heavy;
+    const int32_t *heavy_target;   // [n_heavy]
+    const int32_t *heavy_chunk;    // [n_heavy+1]
+};
+
+// ---- launchers (ees_kernels.cu); all asynchronous on `st` ----
+cudaError_t launch_atomic(const DevK &dv, const CallK &call, int grid, cudaStream_t st);
+cudaError_t launch_color(const DevK &dv, const CallK &call, int64_t begin, int64_t count,
+                         double *partials, cudaStream_t st);
+cudaError_t launch_rail_finalize(const CallK &call, const double *partials, int64_t n_blocks,
+                                 cudaStream_t st);
+cudaError_t launch_gather(const DevK &dv, const GatherK &gk, const CallK &call, cudaStream_t st,
+                          int *n_launches);
+cudaError_t launch_race_probe(const DevK &dv, const int32_t *perm, int64_t begin, int64_t count,
+                              int32_t *cnt_a, int32_t *cnt_b, cudaStream_t st);
+cudaError_t launch_count_conflicts(const int32_t *cnt, int64_t n, unsigned long long *out,
+                                   cudaStream_t st);
+int atomic_blocks_per_sm();
+
+}  // namespace ees

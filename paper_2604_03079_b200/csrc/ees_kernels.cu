@@ -1,0 +1,459 @@
+// ees_kernels.cu -- sm_100a kernels of the evaluate+stamp hot path.
+//
+// Evaluation ("Compute Phase") is SPEC.md's Level-1 MOSFET
+// with gmin and backward-Euler capacitor companions, read
+// as SURVEY.md §8(c) / DESIGN.md §2: FP64, one thread per device, all
+// intermediates in registers, SoA loads in the variant's device order.  It is
+// fused into each stamping variant ("Stamp Phase"):
+//
+//   k_color        colour-phased, no atomics (P:36, P:62, P:80 ColorFused)
+//   k_atomic       one pass, FP64 RED into A_vals / b
+//   k_gather_*     contributions to scratch, then a deterministic per-entry
+//                  segmented reduction (north_star "gather")
+//   k_rail_final   deterministic fixed-order sum of per-block rail partials
+//
+// The path is HBM-bound (~46 FP64 flops vs ~100-155 compulsory bytes per
+// device); there is no dense contraction, so no tensor cores.
+#include <cuda_runtime.h>
+
+#include "ees_internal.h"
+
+namespace ees {
+
+// ---------------------------------------------------------------------------
+// Device evaluation: Y (12 live pairs) and J (4 rows) of one FET.
+// S:196 Level-1 + D/S swap + PMOS reflection; SURVEY §8(c) steps 1-8.
+// ---------------------------------------------------------------------------
+struct Stamp {
+    double y[NPAIR];
+    double j[4];
+};
+
+__device__ __forceinline__ void eval_fet(const CardK &cd, double beta, double gmin, double VD,
+                                         double VG, double VS, double v0gs, double v0gd,
+                                         double v0db, Stamp &st)
+{
+    const double p = cd.p;
+    const double vgs = p * (VG - VS);               // reflected frame
+    const double vds = p * (VD - VS);
+    const bool fwd = vds >= 0.0;                    // mode (A8: vds = 0 -> forward)
+    const double u = fwd ? vgs : vgs - vds;         // D/S swap in reverse mode
+    const double v = fwd ? vds : -vds;
+    const double uov = u - cd.vt;
+    const double op = 1.0 + cd.lam * v;
+    const bool on = uov > 0.0;                      // uov = 0 -> cutoff
+    const bool sat = v >= uov;                      // v = uov -> saturation
+    // q = f / (beta*op): saturation uov^2/2, triode uov*v - v^2/2
+    const double q = sat ? 0.5 * uov * uov : uov * v - 0.5 * v * v;
+    const double bop = beta * op;
+    double f = bop * q;
+    double fu = bop * (sat ? uov : v);
+    double fv = (sat ? 0.0 : bop * (uov - v)) + beta * q * cd.lam;
+    if (!on) { f = 0.0; fu = 0.0; fv = 0.0; }
+    const double F = fwd ? f : -f;
+    const double gm = fwd ? fu : -fu;               // terminal frame (A9)
+    const double gds = fwd ? fv : fu + fv;
+    const double I = p * F;
+    const double ieq = I - gm * (VG - VS) - gds * (VD - VS);   // Norton
+    const double g1 = cd.gcgs, g2 = cd.gcgd, g3 = cd.gcdb;     // C/h
+    const double gmgds = gm + gds;
+    st.y[DD] = gds + gmin + g2 + g3;
+    st.y[DG] = gm - g2;
+    st.y[DS] = -gmgds - gmin;
+    st.y[DB] = -g3;
+    st.y[GD] = -g2;
+    st.y[GG] = g1 + g2;
+    st.y[GS] = -g1;
+    st.y[SD] = -gds - gmin;
+    st.y[SG] = -gm - g1;
+    st.y[SS] = gmgds + gmin + g1;
+    st.y[BD] = -g3;
+    st.y[BB] = g3;
+    const double qgs = g1 * v0gs, qgd = g2 * v0gd, qdb = g3 * v0db;   // BE companions
+    st.j[0] = -ieq - qgd + qdb;
+    st.j[1] = qgs + qgd;
+    st.j[2] = ieq - qgs;
+    st.j[3] = -qdb;
+}
+
+__device__ __forceinline__ double volt(int t, const double *__restrict__ x, const double *s_railx)
+{
+    return t >= 0 ? __ldg(x + t) : (t == -1 ? 0.0 : s_railx[-2 - t]);
+}
+
+// Load + evaluate device i of layout dv.  Returns terminal codes in T.
+__device__ __forceinline__ void load_eval(const DevK &dv, const CallK &P, const CardK *s_cards,
+                                          const double *s_railx, int64_t i, int4 &T, Stamp &st)
+{
+    T = __ldg(dv.term + i);
+    const double beta = __ldg(dv.beta + i);
+    const double a0 = __ldg(dv.v0 + i);
+    const double a1 = __ldg(dv.v0 + dv.N + i);
+    const double a2 = __ldg(dv.v0 + 2 * dv.N + i);
+    const int m = __ldg(dv.model + i);
+    const double VD = volt(T.x, P.x, s_railx);
+    const double VG = volt(T.y, P.x, s_railx);
+    const double VS = volt(T.z, P.x, s_railx);
+    eval_fet(s_cards[m], beta, P.gmin, VD, VG, VS, a0, a1, a2, st);
+}
+
+__device__ __forceinline__ void load_call_smem(const CallK &P, CardK *s_cards, double *s_railx)
+{
+    for (int k = threadIdx.x; k < P.n_models; k += blockDim.x) s_cards[k] = P.cards[k];
+    for (int k = threadIdx.x; k < P.n_rail_nodes; k += blockDim.x) s_railx[k] = P.x[P.rail_node[k]];
+}
+
+__device__ __forceinline__ double warp_sum(double v)
+{
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Rail side reduction, per warp: for every rail entry e, the warp's sum of
+// this iteration's contributions is added (fixed order) to s_acc[warp][e].
+__device__ __forceinline__ void rail_accumulate(const CallK &P, const int32_t *slot, const int4 &T,
+                                                const Stamp &st, bool valid, double *s_acc)
+{
+    const int tc[4] = {T.x, T.y, T.z, T.w};
+    bool mine = false;
+    if (valid) {
+#pragma unroll
+        for (int p = 0; p < NPAIR; p++) mine |= slot[p] <= -2;
+#pragma unroll
+        for (int a = 0; a < 4; a++) mine |= tc[a] <= -2;
+    }
+    if (!__any_sync(0xffffffffu, mine)) return;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int e = 0; e < P.n_rail_entries; e++) {
+        double v = 0.0;
+        if (mine) {
+            if (e < P.n_rail_a) {
+                const int code = -2 - e;
+#pragma unroll
+                for (int p = 0; p < NPAIR; p++) v += slot[p] == code ? st.y[p] : 0.0;
+            } else {
+                const int code = -2 - (e - P.n_rail_a);
+#pragma unroll
+                for (int a = 0; a < 4; a++) v += tc[a] == code ? st.j[a] : 0.0;
+            }
+        }
+        v = warp_sum(v);
+        if (lane == 0) s_acc[warp * P.n_rail_entries + e] += v;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// ATOMIC: grid-stride over devices (netlist order), RED.F64 into A and b;
+// rail entries reduced per block, one atomic per block and entry at the end.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kBlock) k_atomic(DevK dv, CallK P)
+{
+    __shared__ CardK s_cards[EES_MAX_MODELS];
+    __shared__ double s_railx[EES_MAX_RAILS];
+    extern __shared__ double s_acc[];   // [warps][n_rail_entries]
+    load_call_smem(P, s_cards, s_railx);
+    const int nw = blockDim.x >> 5;
+    for (int k = threadIdx.x; k < nw * P.n_rail_entries; k += blockDim.x) s_acc[k] = 0.0;
+    __syncthreads();
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    // iterate with warp-uniform trip count so rail_accumulate's shuffles are full-warp
+    const int64_t base0 = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31);
+    for (int64_t base = base0; base < dv.N; base += stride) {
+        const int64_t i = base + (threadIdx.x & 31);
+        const bool valid = i < dv.N;
+        int4 T = make_int4(-1, -1, -1, -1);
+        Stamp st;
+        int32_t slot[NPAIR];
+        if (valid) {
+            load_eval(dv, P, s_cards, s_railx, i, T, st);
+#pragma unroll
+            for (int p = 0; p < NPAIR; p++) slot[p] = __ldg(dv.slot + (int64_t)p * dv.N + i);
+#pragma unroll
+            for (int p = 0; p < NPAIR; p++)
+                if (slot[p] >= 0) atomicAdd(P.A + slot[p], st.y[p]);
+            const int tc[4] = {T.x, T.y, T.z, T.w};
+#pragma unroll
+            for (int a = 0; a < 4; a++)
+                if (tc[a] >= 0) atomicAdd(P.b + tc[a], st.j[a]);
+        } else {
+#pragma unroll
+            for (int p = 0; p < NPAIR; p++) slot[p] = -1;
+        }
+        if (P.n_rail_entries) rail_accumulate(P, slot, T, st, valid, s_acc);
+    }
+    if (P.n_rail_entries) {
+        __syncthreads();
+        for (int e = threadIdx.x; e < P.n_rail_entries; e += blockDim.x) {
+            double v = 0.0;
+            for (int w = 0; w < nw; w++) v += s_acc[w * P.n_rail_entries + e];
+            double *dst = e < P.n_rail_a ? P.A + P.rail_target[e] : P.b + P.rail_target[e];
+            atomicAdd(dst, v);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// COLOR: one launch per colour; devices of a colour share no non-rail node,
+// so plain read-modify-write is race-free.  Rail entries go to a
+// per-block partial (deterministic), summed by k_rail_final.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kBlock) k_color(DevK dv, CallK P, int64_t begin, int64_t count,
+                                                  double *partials)
+{
+    __shared__ CardK s_cards[EES_MAX_MODELS];
+    __shared__ double s_railx[EES_MAX_RAILS];
+    extern __shared__ double s_acc[];
+    load_call_smem(P, s_cards, s_railx);
+    const int nw = blockDim.x >> 5;
+    for (int k = threadIdx.x; k < nw * P.n_rail_entries; k += blockDim.x) s_acc[k] = 0.0;
+    __syncthreads();
+    const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool valid = q < count;
+    const int64_t i = begin + q;
+    int4 T = make_int4(-1, -1, -1, -1);
+    Stamp st;
+    int32_t slot[NPAIR];
+    if (valid) {
+        load_eval(dv, P, s_cards, s_railx, i, T, st);
+#pragma unroll
+        for (int p = 0; p < NPAIR; p++) slot[p] = __ldg(dv.slot + (int64_t)p * dv.N + i);
+#pragma unroll
+        for (int p = 0; p < NPAIR; p++)
+            if (slot[p] >= 0) P.A[slot[p]] += st.y[p];
+        const int tc[4] = {T.x, T.y, T.z, T.w};
+#pragma unroll
+        for (int a = 0; a < 4; a++)
+            if (tc[a] >= 0) P.b[tc[a]] += st.j[a];
+    } else {
+#pragma unroll
+        for (int p = 0; p < NPAIR; p++) slot[p] = -1;
+    }
+    if (P.n_rail_entries) {
+        rail_accumulate(P, slot, T, st, valid, s_acc);
+        __syncthreads();
+        for (int e = threadIdx.x; e < P.n_rail_entries; e += blockDim.x) {
+            double v = 0.0;
+            for (int w = 0; w < nw; w++) v += s_acc[w * P.n_rail_entries + e];
+            partials[(int64_t)blockIdx.x * P.n_rail_entries + e] = v;
+        }
+    }
+}
+
+// Fixed-order reduction of the rail partials: one block per rail entry; each
+// thread sums a fixed strided subset, then a fixed shuffle/smem tree.
+__global__ void __launch_bounds__(kBlock) k_rail_final(CallK P, const double *partials,
+                                                       int64_t n_blocks)
+{
+    __shared__ double s_w[kBlock / 32];
+    const int e = blockIdx.x;
+    double v = 0.0;
+    for (int64_t k = threadIdx.x; k < n_blocks; k += blockDim.x)
+        v += partials[k * P.n_rail_entries + e];
+    v = warp_sum(v);
+    if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); w++) t += s_w[w];
+        double *dst = e < P.n_rail_a ? P.A + P.rail_target[e] : P.b + P.rail_target[e];
+        *dst += t;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// GATHER (deterministic): K3a evaluates and writes each device's live
+// contributions contiguously (pairs in order, then b rows), staged through
+// shared memory so the global store is coalesced; K3b reduces every target
+// (A entry, then b row) over its contributor list in list order; heavy lists
+// are split into fixed chunks reduced by whole blocks (K3b tail blocks) and
+// summed in chunk order by K3c.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kBlock) k_gather_eval(DevK dv, GatherK gk, CallK P)
+{
+    __shared__ CardK s_cards[EES_MAX_MODELS];
+    __shared__ double s_railx[EES_MAX_RAILS];
+    __shared__ double s_buf[kBlock * (NPAIR + 4)];
+    load_call_smem(P, s_cards, s_railx);
+    __syncthreads();
+    const int64_t i0 = (int64_t)blockIdx.x * blockDim.x;
+    const int64_t i = i0 + threadIdx.x;
+    const int64_t iend = min((int64_t)dv.N, i0 + blockDim.x);
+    const int32_t base = gk.off[i0];
+    const int32_t total = gk.off[iend] - base;
+    if (i < dv.N) {
+        int4 T;
+        Stamp st;
+        load_eval(dv, P, s_cards, s_railx, i, T, st);
+        const int tc[4] = {T.x, T.y, T.z, T.w};
+        int o = gk.off[i] - base;
+#pragma unroll
+        for (int p = 0; p < NPAIR; p++)
+            if (tc[pair_row(p)] >= 0 && tc[pair_col(p)] >= 0) s_buf[o++] = st.y[p];
+#pragma unroll
+        for (int a = 0; a < 4; a++)
+            if (tc[a] >= 0) s_buf[o++] = st.j[a];
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < total; k += blockDim.x) gk.buf[base + k] = s_buf[k];
+}
+
+__global__ void __launch_bounds__(kBlock) k_gather_reduce(GatherK gk, CallK P, int64_t n_light_blocks)
+{
+    if (blockIdx.x < n_light_blocks) {
+        const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+        if (t >= gk.n_targets) return;
+        const int32_t b0 = gk.tptr[t], b1 = gk.tptr[t + 1];
+        if (b0 == b1) return;
+        double s = 0.0;
+        for (int32_t k = b0; k < b1; k++) s += gk.buf[__ldg(gk.tidx + k)];
+        if (t < gk.nnz) P.A[t] += s;
+        else P.b[t - gk.nnz] += s;
+        return;
+    }
+    // heavy chunk: fixed-shape block reduction
+    __shared__ double s_w[kBlock / 32];
+    const int64_t c = blockIdx.x - n_light_blocks;
+    const int32_t b0 = gk.chunk_beg[c], b1 = gk.chunk_beg[c + 1];
+    double v = 0.0;
+    for (int32_t k = b0 + threadIdx.x; k < b1; k += blockDim.x) v += gk.buf[__ldg(gk.hidx + k)];
+    v = warp_sum(v);
+    if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); w++) t += s_w[w];
+        gk.chunk_part[c] = t;
+    }
+}
+
+__global__ void k_gather_heavy(GatherK gk, CallK P)
+{
+    const int h = blockIdx.x * blockDim.x + threadIdx.x;
+    if (h >= gk.n_heavy) return;
+    double s = 0.0;
+    for (int32_t c = gk.heavy_chunk[h]; c < gk.heavy_chunk[h + 1]; c++) s += gk.chunk_part[c];
+    const int64_t t = gk.heavy_target[h];
+    if (t < gk.nnz) P.A[t] += s;
+    else P.b[t - gk.nnz] += s;
+}
+
+// ---------------------------------------------------------------------------
+// Race instrument: per colour, count distinct-device writers
+// of every non-rail A entry and b row.
+// ---------------------------------------------------------------------------
+__global__ void k_race_probe(DevK dv, const int32_t *perm, int64_t begin, int64_t count,
+                             int32_t *cnt_a, int32_t *cnt_b)
+{
+    const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= count) return;
+    const int64_t i = perm[begin + q];
+    int32_t slot[NPAIR];
+#pragma unroll
+    for (int p = 0; p < NPAIR; p++) slot[p] = dv.slot[(int64_t)p * dv.N + i];
+#pragma unroll
+    for (int p = 0; p < NPAIR; p++) {
+        bool dup = false;
+#pragma unroll
+        for (int r = 0; r < p; r++) dup |= slot[r] == slot[p];
+        if (slot[p] >= 0 && !dup) atomicAdd(cnt_a + slot[p], 1);
+    }
+    const int4 T = dv.term[i];
+    const int tc[4] = {T.x, T.y, T.z, T.w};
+#pragma unroll
+    for (int a = 0; a < 4; a++) {
+        bool dup = false;
+#pragma unroll
+        for (int r = 0; r < a; r++) dup |= tc[r] == tc[a];
+        if (tc[a] >= 0 && !dup) atomicAdd(cnt_b + tc[a], 1);
+    }
+}
+
+__global__ void k_count_conflicts(const int32_t *cnt, int64_t n, unsigned long long *out)
+{
+    unsigned long long local = 0;
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
+         k += (int64_t)gridDim.x * blockDim.x)
+        local += cnt[k] > 1;
+    if (local) atomicAdd(out, local);
+}
+
+// ---------------------------------------------------------------------------
+// launchers
+// ---------------------------------------------------------------------------
+static size_t rail_smem(const CallK &P) { return sizeof(double) * (kBlock / 32) * P.n_rail_entries; }
+
+int atomic_blocks_per_sm()
+{
+    int nb = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_atomic, kBlock,
+                                                  sizeof(double) * (kBlock / 32) * kMaxRailEntries);
+    return nb > 0 ? nb : 1;
+}
+
+cudaError_t launch_atomic(const DevK &dv, const CallK &call, int grid, cudaStream_t st)
+{
+    if (dv.N == 0) return cudaSuccess;
+    k_atomic<<<grid, kBlock, rail_smem(call), st>>>(dv, call);
+    return cudaPeekAtLastError();
+}
+
+cudaError_t launch_color(const DevK &dv, const CallK &call, int64_t begin, int64_t count,
+                         double *partials, cudaStream_t st)
+{
+    if (count == 0) return cudaSuccess;
+    const int64_t grid = (count + kBlock - 1) / kBlock;
+    k_color<<<(unsigned)grid, kBlock, rail_smem(call), st>>>(dv, call, begin, count, partials);
+    return cudaPeekAtLastError();
+}
+
+cudaError_t launch_rail_finalize(const CallK &call, const double *partials, int64_t n_blocks,
+                                 cudaStream_t st)
+{
+    if (call.n_rail_entries == 0 || n_blocks == 0) return cudaSuccess;
+    k_rail_final<<<call.n_rail_entries, kBlock, 0, st>>>(call, partials, n_blocks);
+    return cudaPeekAtLastError();
+}
+
+cudaError_t launch_gather(const DevK &dv, const GatherK &gk, const CallK &call, cudaStream_t st,
+                          int *n_launches)
+{
+    int nl = 0;
+    if (dv.N > 0) {
+        const int64_t grid = (dv.N + kBlock - 1) / kBlock;
+        k_gather_eval<<<(unsigned)grid, kBlock, 0, st>>>(dv, gk, call);
+        nl++;
+        cudaError_t e = cudaPeekAtLastError();
+        if (e != cudaSuccess) return e;
+        const int64_t light = (gk.n_targets + kBlock - 1) / kBlock;
+        k_gather_reduce<<<(unsigned)(light + gk.n_chunks), kBlock, 0, st>>>(gk, call, light);
+        nl++;
+        e = cudaPeekAtLastError();
+        if (e != cudaSuccess) return e;
+        if (gk.n_heavy) {
+            k_gather_heavy<<<(gk.n_heavy + 127) / 128, 128, 0, st>>>(gk, call);
+            nl++;
+        }
+    }
+    if (n_launches) *n_launches = nl;
+    return cudaPeekAtLastError();
+}
+
+cudaError_t launch_race_probe(const DevK &dv, const int32_t *perm, int64_t begin, int64_t count,
+                              int32_t *cnt_a, int32_t *cnt_b, cudaStream_t st)
+{
+    if (count == 0) return cudaSuccess;
+    k_race_probe<<<(unsigned)((count + kBlock - 1) / kBlock), kBlock, 0, st>>>(dv, perm, begin,
+                                                                               count, cnt_a, cnt_b);
+    return cudaPeekAtLastError();
+}
+
+cudaError_t launch_count_conflicts(const int32_t *cnt, int64_t n, unsigned long long *out,
+                                   cudaStream_t st)
+{
+    if (n == 0) return cudaSuccess;
+    k_count_conflicts<<<296, kBlock, 0, st>>>(cnt, n, out);
+    return cudaPeekAtLastError();
+}
+
+}  // namespace ees

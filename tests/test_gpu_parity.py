@@ -1,0 +1,237 @@
+"""Parity of the CUDA path (through the C ABI) against the independent CPU
+oracle: per entry |A_gpu - A_ref| <= 1e-12 * sum|c| (BASELINE.json
+north_star), pattern set-equality, colouring bit-exact and
+conflict-free, determinism, race instrument, edge cases."""
+import math
+
+import numpy as np
+import pytest
+
+import netgen
+import oracle
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-12
+VARIANTS = ["color", "atomic", "gather"]
+
+_ref_cache = {}
+
+
+def ctx_for(nl, **kw):
+    from paper_2604_03079_b200 import Context
+    return Context.from_netlist(nl, **kw)
+
+
+def reference(nl, key=None, A0=None, b0=None):
+    if key is not None and key in _ref_cache:
+        return _ref_cache[key]
+    r = oracle.reference(nl, A0=A0, b0=b0)
+    if key is not None:
+        _ref_cache.clear()          # keep at most one full-size reference alive
+        _ref_cache[key] = r
+    return r
+
+
+def gpu_run(ctx, nl, variant=None, h=None, A0=None, b0=None, x=None):
+    import torch
+    if variant is not None:
+        ctx.set_variant(variant)
+    dev = torch.device("cuda")
+    xt = torch.from_numpy(nl.x if x is None else x).to(dev)
+    A = (torch.zeros(ctx.nnz, dtype=torch.float64, device=dev) if A0 is None
+         else torch.from_numpy(np.array(A0, float)).to(dev))
+    b = (torch.zeros(ctx.n, dtype=torch.float64, device=dev) if b0 is None
+         else torch.from_numpy(np.array(b0, float)).to(dev))
+    ctx.eval_stamp(xt, nl.h if h is None else h, A, b)
+    torch.cuda.synchronize()
+    return A.cpu().numpy(), b.cpu().numpy()
+
+
+def assert_parity(ref, A, b, what=""):
+    for got, want, mag, name in ((A, ref["A"], ref["A_abs"], "A"), (b, ref["b"], ref["b_abs"], "b")):
+        err = np.abs(got - want)
+        bad = ~(err <= TOL * mag)          # NaN-safe: NaN counts as bad
+        if bad.any():
+            k = int(np.argmax(np.where(bad, err / np.maximum(mag, 1e-300), 0)))
+            raise AssertionError(f"{what} {name}: {int(bad.sum())} entries out of tolerance; worst k={k} "
+                                 f"got={got[k]!r} want={want[k]!r} sum|c|={mag[k]!r}")
+
+
+def assert_pattern(ctx, ref):
+    rp, ci = ctx.pattern()
+    assert np.array_equal(rp, ref["row_ptr"]) and np.array_equal(ci, ref["col_idx"])
+
+
+# ---------------------------------------------------------------- reduced configs
+@pytest.mark.parametrize("cfg", [0, 1, 2, 3, 4])
+@pytest.mark.parametrize("rule", ["exclude_rails", "paper"])
+def test_parity_reduced(cuda_ok, cfg, rule):
+    nl = netgen.config(cfg, 0.01 if cfg else 1.0)
+    if rule == "paper" and cfg in (2, 4):
+        nl = netgen.config(cfg, 0.001)
+    ref = reference(nl)
+    ctx = ctx_for(nl, rule=rule)
+    assert_pattern(ctx, ref)
+    col, C = ctx.colors()
+    assert np.array_equal(col, oracle.greedy_color(nl, rule)[0])
+    assert oracle.color_violations(nl, col, C, rule) == 0
+    assert ctx.race_probe() == 0
+    for v in VARIANTS:
+        A, b = gpu_run(ctx, nl, v)
+        assert_parity(ref, A, b, f"cfg{cfg} {rule} {v}")
+    ctx.close()
+
+
+# ---------------------------------------------------------------- full size
+@pytest.mark.parametrize("cfg", [0, 1, 2, 3, 4])
+def test_parity_full_size(cuda_ok, cfg):
+    """BASELINE.json configs at full size, every variant, in the launch
+    configuration bench.py times; all entries compared."""
+    nl = netgen.config(cfg)
+    ref = reference(nl, key=("full", cfg))
+    ctx = ctx_for(nl, variant="auto")
+    assert_pattern(ctx, ref)
+    st = ctx.stats()
+    col, C = ctx.colors()
+    ocol, oC = oracle.greedy_color(nl)
+    assert C == oC and np.array_equal(col, ocol)
+    assert oracle.color_violations(nl, col, C) == 0
+    for v in VARIANTS:
+        if v == "color" and st["n_colors"] > 600:
+            continue        # thousands of launches; covered on reduced instances
+        A, b = gpu_run(ctx, nl, v)
+        assert_parity(ref, A, b, f"cfg{cfg} full {v}")
+    ctx.set_variant("auto")
+    A, b = gpu_run(ctx, nl)
+    assert_parity(ref, A, b, f"cfg{cfg} full auto={st['variant_chosen']}")
+    ctx.close()
+
+
+# ---------------------------------------------------------------- colour sweep (B5)
+@pytest.mark.parametrize("ct", [1, 2, 7, 64, 333])
+def test_parity_synth(cuda_ok, ct):
+    nl = netgen.gen_synth(20000 + 37, ct)
+    ref = reference(nl)
+    ctx = ctx_for(nl)
+    assert ctx.stats()["n_colors"] == ct
+    for v in VARIANTS:
+        assert_parity(ref, *gpu_run(ctx, nl, v), f"synth C={ct} {v}")
+
+
+# ---------------------------------------------------------------- edge cases
+def _tiny():
+    ms = netgen.bench_models()
+    yield netgen.custom("nmos", 3, [(0, 1, 2, -1)], 0, ms, seed=1)
+    yield netgen.custom("allground", 2, [(-1, -1, -1, -1), (0, -1, -1, -1), (-1, 1, -1, -1)], 0, ms)
+    yield netgen.custom("coincident", 3, [(0, 0, 0, 0), (1, 2, 1, -1), (2, 1, 2, 2)], [0, 1, 1], ms)
+    yield netgen.ota_5t()
+    yield netgen.inverter_chain(1)
+    yield netgen.ring_oscillators(3, 101, fanout=4)
+    yield netgen.custom("rails3", 6, [(0, 3, 4, 5), (3, 4, 5, 5), (1, 4, 3, 3), (2, 5, 0, 4)],
+                        [1, 0, 1, 0], ms, rails=[3, 4, 5])
+
+
+@pytest.mark.parametrize("nl", list(_tiny()), ids=lambda n: n.name)
+def test_parity_tiny(cuda_ok, nl):
+    ref = reference(nl)
+    ctx = ctx_for(nl)
+    assert_pattern(ctx, ref)
+    for v in VARIANTS:
+        assert_parity(ref, *gpu_run(ctx, nl, v), f"{nl.name} {v}")
+
+
+def test_empty(cuda_ok):
+    nl = netgen.custom("empty", 3, np.zeros((0, 4), np.int64), 0, netgen.bench_models())
+    ctx = ctx_for(nl)
+    for v in VARIANTS:
+        A, b = gpu_run(ctx, nl, v, b0=np.arange(3.0))
+        assert A.shape == (0,) and np.array_equal(b, np.arange(3.0))
+
+
+def test_dc_and_accumulate(cuda_ok):
+    """h = +inf (DC: caps open) and accumulate semantics with random
+    initial A, b (included in sum|c|)."""
+    nl = netgen.config(1, 0.02)
+    rng = np.random.Generator(np.random.PCG64(3))
+    ctx = ctx_for(nl)
+    A0 = rng.uniform(-1, 1, ctx.nnz)
+    b0 = rng.uniform(-1, 1, ctx.n)
+    for h in (nl.h, math.inf):
+        nl2 = netgen.Netlist(**{**nl.__dict__, "h": h})
+        ref = oracle.reference(nl2, A0=A0, b0=b0)
+        for v in VARIANTS:
+            assert_parity(ref, *gpu_run(ctx, nl2, v, h=h, A0=A0, b0=b0), f"h={h} {v}")
+
+
+def test_spec_card_all_cutoff(cuda_ok):
+    nl = netgen.inverter_chain(300, models=netgen.spec_models())
+    ref = reference(nl)
+    ctx = ctx_for(nl)
+    for v in VARIANTS:
+        assert_parity(ref, *gpu_run(ctx, nl, v), f"spec card {v}")
+
+
+def test_determinism(cuda_ok):
+    """COLOR and GATHER are bitwise reproducible run to run (fixed summation
+    order); ATOMIC within tolerance."""
+    nl = netgen.config(2, 0.02)
+    ref = reference(nl)
+    ctx = ctx_for(nl)
+    for v in ("color", "gather"):
+        A1, b1 = gpu_run(ctx, nl, v)
+        for _ in range(3):
+            A2, b2 = gpu_run(ctx, nl, v)
+            assert np.array_equal(A1, A2) and np.array_equal(b1, b2)
+    A, b = gpu_run(ctx, nl, "atomic")
+    assert_parity(ref, A, b, "atomic")
+
+
+def test_race_probe_detects_corrupted_schedule(cuda_ok):
+    """S:362 negative test: two adjacent devices forced into one colour."""
+    nl = netgen.ring_oscillators(4, 101)
+    ctx = ctx_for(nl)
+    col, C = ctx.colors()
+    assert ctx.race_probe() == 0
+    bad = col.copy()
+    bad[1] = bad[0]
+    assert ctx.race_probe(bad) > 0
+    assert ctx.race_probe(np.zeros_like(col)) > 0
+
+
+def test_nan_propagates(cuda_ok):
+    nl = netgen.inverter_chain(10)
+    ctx = ctx_for(nl)
+    x = nl.x.copy()
+    x[3] = np.nan
+    for v in VARIANTS:
+        A, b = gpu_run(ctx, nl, v, x=x)
+        assert np.isnan(A).any() and np.isnan(b).any()
+
+
+def test_host_buffer_call_matches(cuda_ok):
+    nl = netgen.config(1, 0.05)
+    ref = reference(nl)
+    ctx = ctx_for(nl)
+    for v in VARIANTS:
+        ctx.set_variant(v)
+        A = np.zeros(ctx.nnz)
+        b = np.zeros(ctx.n)
+        ctx.eval_stamp_host(nl.x, nl.h, A, b)
+        assert_parity(ref, A, b, f"host {v}")
+
+
+def test_abi_errors(cuda_ok):
+    import torch
+    from paper_2604_03079_b200 import EESError
+    nl = netgen.inverter_chain(5)
+    ctx = ctx_for(nl)
+    x = torch.zeros(ctx.n, dtype=torch.float64, device="cuda")
+    A = torch.zeros(ctx.nnz, dtype=torch.float64, device="cuda")
+    b = torch.zeros(ctx.n, dtype=torch.float64, device="cuda")
+    for h in (0.0, -1e-12, float("nan")):
+        with pytest.raises(EESError):
+            ctx.eval_stamp(x, h, A, b)
+    with pytest.raises(ValueError):
+        ctx.eval_stamp(x[:-1], 1e-12, A, b)
+    with pytest.raises(ValueError):
+        ctx.eval_stamp(x.float(), 1e-12, A, b)

@@ -1,0 +1,122 @@
+"""Host logic of the C-ABI library, no GPU: the exported symbols, argument
+validation, and that the library's setup (pattern, colouring) equals the
+independent oracle bit for bit.  CPU only."""
+import ctypes as C
+import os
+import re
+
+import numpy as np
+import pytest
+
+import netgen
+import oracle
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_2604_03079_b200 import _lib
+    hdr = open(os.path.join(ROOT, "include", "ees.h")).read()
+    declared = set(re.findall(r"^(?:ees_status|const char \*)\s*(ees_\w+)\s*\(", hdr, re.M))
+    assert declared == set(_lib.EXPORTS)
+    for name in declared:
+        assert getattr(_lib.lib, name) is not None
+
+
+def _ctx(nl, **kw):
+    from paper_2604_03079_b200 import Context
+    return Context.from_netlist(nl, host_only=True, **kw)
+
+
+@pytest.mark.parametrize("cfg", [0, 1, 2, 3, 4])
+def test_pattern_equals_oracle(cfg):
+    nl = netgen.config(cfg, 0.01)
+    c = _ctx(nl)
+    rp, ci = c.pattern()
+    orp, oci, _ = oracle.pattern(nl)
+    assert np.array_equal(rp, orp) and np.array_equal(ci, oci)
+    for k in range(0, len(ci), max(1, len(ci) // 50)):
+        r = int(np.searchsorted(rp, k, side="right") - 1)
+        assert c.find_slot(r, int(ci[k])) == k
+
+
+@pytest.mark.parametrize("rule", ["exclude_rails", "paper"])
+@pytest.mark.parametrize("cfg", [0, 1, 2, 3, 4])
+def test_colouring_equals_oracle(cfg, rule):
+    nl = netgen.config(cfg, 0.01)
+    c = _ctx(nl, rule=rule)
+    col, C_ = c.colors()
+    ocol, oC = oracle.greedy_color(nl, rule)
+    assert C_ == oC
+    assert np.array_equal(col, ocol)
+    assert oracle.color_violations(nl, col, C_, rule) == 0
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_colouring_random_small(seed):
+    rng = np.random.Generator(np.random.PCG64(1000 + seed))
+    N = int(rng.integers(1, 400)); nn = int(rng.integers(2, N + 3))
+    T = rng.integers(-1, nn, size=(N, 4))
+    rails = sorted(set(int(v) for v in rng.integers(0, nn, int(rng.integers(0, 3)))))
+    nl = netgen.custom("r", nn, [tuple(t) for t in T], 0, netgen.bench_models(), rails=rails)
+    for rule in ("exclude_rails", "paper"):
+        col, C_ = _ctx(nl, rule=rule).colors()
+        ocol, oC = oracle.greedy_color(nl, rule)
+        assert C_ == oC and np.array_equal(col, ocol)
+
+
+def test_full_size_colour_counts():
+    """C(cfg0..cfg2) = 4, 6, 2052 (rails excluded); the
+    library's incidence/bitset first-fit equals the plain oracle at full size."""
+    for cfg, want in ((0, 4), (1, 6), (2, 2052)):
+        nl = netgen.config(cfg)
+        col, C_ = _ctx(nl).colors()
+        assert C_ == want
+        if cfg < 2:
+            assert np.array_equal(col, oracle.greedy_color(nl)[0])
+
+
+def test_invalid_descriptors():
+    from paper_2604_03079_b200 import Context, EESError
+    nl = netgen.inverter_chain(4)
+    bad = []
+    d2 = nl.d.copy(); d2[0] = nl.n_nodes          # node id out of range
+    bad.append(dict(d=d2))
+    w2 = nl.w.copy(); w2[1] = 0.0                 # W must be > 0
+    bad.append(dict(w=w2))
+    m2 = nl.model.copy(); m2[0] = 5               # model index out of range
+    bad.append(dict(model=m2))
+    bad.append(dict(rails=[nl.rails[0], nl.rails[0]]))     # duplicate rail
+    bad.append(dict(extra_row=[nl.n], extra_col=[0]))       # extra entry out of range
+    bad.append(dict(gmin=-1.0))
+    bad.append(dict(models=[dict(polarity=2, vt0=0.3, kp=2e-5, lam=0, cgs=0, cgd=0, cdb=0)]))
+    bad.append(dict(models=[dict(polarity=1, vt0=0.3, kp=0.0, lam=0, cgs=0, cgd=0, cdb=0)]))
+    base = dict(n_nodes=nl.n_nodes, n_extra=nl.n_extra, d=nl.d, g=nl.g, s=nl.s, b=nl.b, w=nl.w,
+                l=nl.l, model=nl.model, vprev=nl.vprev, models=nl.models, rails=nl.rails,
+                extra_row=nl.extra_row, extra_col=nl.extra_col, host_only=True)
+    Context(**base).close()
+    for over in bad:
+        kw = dict(base); kw.update(over)
+        if "extra_row" in over:
+            kw["extra_col"] = over["extra_col"]
+        with pytest.raises(EESError) as e:
+            Context(**kw)
+        assert e.value.status == -1
+
+
+def test_host_only_refuses_eval():
+    from paper_2604_03079_b200 import _lib
+    c = _ctx(netgen.inverter_chain(4))
+    buf = (C.c_double * 64)()
+    st = _lib.lib.ees_eval_stamp(c._h, buf, 1e-12, buf, buf, None)
+    assert st == _lib.EES_ESTATE
+    assert _lib.lib.ees_eval_stamp(c._h, buf, 0.0, buf, buf, None) == _lib.EES_EINVAL
+    assert _lib.lib.ees_eval_stamp(c._h, buf, float("nan"), buf, buf, None) == _lib.EES_EINVAL
+    assert _lib.lib.ees_eval_stamp(None, buf, 1e-12, buf, buf, None) == _lib.EES_EINVAL
+
+
+def test_empty_netlist():
+    nl = netgen.custom("empty", 3, np.zeros((0, 4), np.int64), 0, netgen.bench_models())
+    c = _ctx(nl)
+    st = c.stats()
+    assert st["n_dev"] == 0 and st["nnz"] == 0 and st["n_colors"] == 0
