@@ -163,6 +163,18 @@ ees_status ees_set_variant(ees_ctx *ctx, int32_t variant);
 
 ees_status ees_stats(const ees_ctx *ctx, ees_stats_t *out);
 
+/* Per-phase device timing (S:326 PhaseTimings).  When enabled, every
+ * ees_eval_stamp records CUDA events on the call's stream around each kernel
+ * group ("phase"):  COLOR {0: colour kernels, 1: rail finalise},
+ * ATOMIC {0: k_atomic},  GATHER {0: evaluate to scratch, 1: segmented
+ * reduction, 2: heavy-target finalise}. */
+ees_status ees_set_timing(ees_ctx *ctx, int32_t enable);
+
+/* Sum of device milliseconds per phase over the calls recorded since the
+ * last read; synchronises on those events, then resets.  ms[4] out;
+ * *n_calls = number of calls summed. */
+ees_status ees_phase_times(ees_ctx *ctx, double ms[4], int32_t *n_calls);
+
 /* Race instrument: replays the COLOR schedule given by
  * `color` (host [n_dev]; NULL = the context's own colouring) on the device,
  * counting per colour how many devices write each A entry and b row that is

@@ -110,6 +110,16 @@ class Context:
         v = VARIANTS[variant] if isinstance(variant, str) else int(variant)
         _check(L.lib.ees_set_variant(self._h, v), "ees_set_variant")
 
+    def set_timing(self, enable=True):
+        _check(L.lib.ees_set_timing(self._h, 1 if enable else 0), "ees_set_timing")
+
+    def phase_times(self):
+        """(per-phase device ms summed over calls since the last read, calls)."""
+        ms = (C.c_double * 4)()
+        n = L.i32()
+        _check(L.lib.ees_phase_times(self._h, ms, C.byref(n)), "ees_phase_times")
+        return list(ms), n.value
+
     # ------------------------------------------------------------ hot path
     def eval_stamp(self, x, h, A, b, stream=None):
         """A += stamps, b += stamps for node voltages x at step h (device

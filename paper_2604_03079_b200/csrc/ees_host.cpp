@@ -61,6 +61,12 @@ struct ees_ctx {
     int32_t variant = EES_ATOMIC;
     int32_t launches = 0;
     bool host_only = false;
+    // phase timing
+    bool timing = false;
+    struct Mark { int phase; cudaEvent_t a, b; };
+    std::vector<Mark> marks;
+    std::vector<cudaEvent_t> ev_free;
+    int32_t timed_calls = 0;
     ees_stats_t st{};
     double *hx = nullptr, *hA = nullptr, *hb = nullptr;   // ees_eval_stamp_host staging
     std::vector<void *> allocs;
@@ -349,28 +355,77 @@ CallK make_call(const ees_ctx *c, const double *x, double h, double *A, double *
     return k;
 }
 
+cudaEvent_t take_event(ees_ctx *c)
+{
+    if (!c->ev_free.empty()) {
+        cudaEvent_t e = c->ev_free.back();
+        c->ev_free.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+
+// Records an event pair around one phase when timing is enabled.
+struct PhaseMark {
+    ees_ctx *c;
+    cudaStream_t st;
+    int phase;
+    cudaEvent_t a = nullptr;
+    PhaseMark(ees_ctx *c_, cudaStream_t s_, int p_, bool on) : c(c_), st(s_), phase(p_)
+    {
+        if (on) {
+            a = take_event(c);
+            cudaEventRecord(a, st);
+        }
+    }
+    ~PhaseMark()
+    {
+        if (a) {
+            cudaEvent_t b = take_event(c);
+            cudaEventRecord(b, st);
+            c->marks.push_back({phase, a, b});
+        }
+    }
+};
+
 ees_status enqueue(ees_ctx *c, int32_t variant, const double *x, double h, double *A, double *b,
-                   cudaStream_t st, int32_t *launches)
+                   cudaStream_t st, int32_t *launches, bool timed = false)
 {
     const CallK call = make_call(c, x, h, A, b);
     int nl = 0;
     cudaError_t e = cudaSuccess;
     if (variant == EES_ATOMIC) {
+        PhaseMark m(c, st, 0, timed);
         e = launch_atomic(c->L_atomic.k(), call, c->atomic_grid, st);
         nl = c->n_dev ? 1 : 0;
     } else if (variant == EES_COLOR) {
         const DevK dv = c->L_color.k();
-        for (int32_t col = 0; col < c->n_colors && e == cudaSuccess; col++) {
-            e = launch_color(dv, call, c->color_ptr[col], c->color_ptr[col + 1] - c->color_ptr[col],
-                             c->partials + c->color_blk_off[col] * c->n_rail_entries, st);
-            nl++;
+        {
+            PhaseMark m(c, st, 0, timed);
+            for (int32_t col = 0; col < c->n_colors && e == cudaSuccess; col++) {
+                e = launch_color(dv, call, c->color_ptr[col], c->color_ptr[col + 1] - c->color_ptr[col],
+                                 c->partials + c->color_blk_off[col] * c->n_rail_entries, st);
+                nl++;
+            }
         }
         if (e == cudaSuccess && c->n_rail_entries && c->n_dev) {
+            PhaseMark m(c, st, 1, timed);
             e = launch_rail_finalize(call, c->partials, c->color_blk_off[c->n_colors], st);
             nl++;
         }
     } else if (variant == EES_GATHER) {
-        e = launch_gather(c->L_gather.k(), c->gk, call, st, &nl);
+        if (timed) {
+            for (int ph = 0; ph < 3 && e == cudaSuccess; ph++) {
+                PhaseMark m(c, st, ph, true);
+                int k = 0;
+                e = launch_gather_phase(c->L_gather.k(), c->gk, call, st, ph, &k);
+                nl += k;
+            }
+        } else {
+            e = launch_gather(c->L_gather.k(), c->gk, call, st, &nl);
+        }
     } else {
         return EES_ESTATE;
     }
@@ -675,6 +730,11 @@ ees_status setup_impl(const ees_desc *d, ees_ctx *c)
 void free_ctx(ees_ctx *c)
 {
     if (!c) return;
+    for (auto &m : c->marks) {
+        cudaEventDestroy(m.a);
+        cudaEventDestroy(m.b);
+    }
+    for (cudaEvent_t e : c->ev_free) cudaEventDestroy(e);
     for (void *p : c->allocs) cudaFree(p);
     delete c;
 }
@@ -742,7 +802,8 @@ ees_status ees_eval_stamp(ees_ctx *c, const double *x, double h, double *A, doub
     if (c->n_dev == 0) return EES_OK;
     if (!x || !A || !b) return EES_EINVAL;
     int32_t nl = 0;
-    ees_status s = enqueue(c, c->variant, x, h, A, b, (cudaStream_t)stream, &nl);
+    ees_status s = enqueue(c, c->variant, x, h, A, b, (cudaStream_t)stream, &nl, c->timing);
+    if (c->timing) c->timed_calls++;
     c->launches = nl;
     return s;
 }
@@ -798,6 +859,31 @@ ees_status ees_stats(const ees_ctx *c, ees_stats_t *out)
     out->n_rail_entries = c->n_rail_entries;
     out->launches_per_call = c->launches;
     return EES_OK;
+}
+
+ees_status ees_set_timing(ees_ctx *c, int32_t enable)
+{
+    if (!c) return EES_EINVAL;
+    c->timing = enable != 0;
+    return EES_OK;
+}
+
+ees_status ees_phase_times(ees_ctx *c, double ms[4], int32_t *n_calls)
+{
+    if (!c || !ms) return EES_EINVAL;
+    for (int k = 0; k < 4; k++) ms[k] = 0.0;
+    cudaError_t err = cudaSuccess;
+    for (auto &m : c->marks) {
+        if (err == cudaSuccess) err = cudaEventSynchronize(m.b);
+        float t = 0.f;
+        if (err == cudaSuccess && cudaEventElapsedTime(&t, m.a, m.b) == cudaSuccess) ms[m.phase] += t;
+        c->ev_free.push_back(m.a);
+        c->ev_free.push_back(m.b);
+    }
+    c->marks.clear();
+    if (n_calls) *n_calls = c->timed_calls;
+    c->timed_calls = 0;
+    return err == cudaSuccess ? EES_OK : EES_ECUDA;
 }
 
 ees_status ees_race_probe(ees_ctx *c, const int32_t *color, int64_t *n_conflicts)

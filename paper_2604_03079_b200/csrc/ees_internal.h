@@ -87,6 +87,9 @@ cudaError_t launch_rail_finalize(const CallK &call, const double *partials, int6
                                  cudaStream_t st);
 cudaError_t launch_gather(const DevK &dv, const GatherK &gk, const CallK &call, cudaStream_t st,
                           int *n_launches);
+// one GATHER phase: 0 evaluate, 1 reduce, 2 heavy finalise (for phase timing)
+cudaError_t launch_gather_phase(const DevK &dv, const GatherK &gk, const CallK &call, cudaStream_t st,
+                                int phase, int *n_launches);
 cudaError_t launch_race_probe(const DevK &dv, const int32_t *perm, int64_t begin, int64_t count,
                               int32_t *cnt_a, int32_t *cnt_b, cudaStream_t st);
 cudaError_t launch_count_conflicts(const int32_t *cnt, int64_t n, unsigned long long *out,

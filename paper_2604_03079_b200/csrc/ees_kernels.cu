@@ -415,28 +415,38 @@ cudaError_t launch_rail_finalize(const CallK &call, const double *partials, int6
     return cudaPeekAtLastError();
 }
 
+cudaError_t launch_gather_phase(const DevK &dv, const GatherK &gk, const CallK &call, cudaStream_t st,
+                                int phase, int *n_launches)
+{
+    *n_launches = 0;
+    if (dv.N == 0) return cudaSuccess;
+    if (phase == 0) {
+        const int64_t grid = (dv.N + kBlock - 1) / kBlock;
+        k_gather_eval<<<(unsigned)grid, kBlock, 0, st>>>(dv, gk, call);
+        *n_launches = 1;
+    } else if (phase == 1) {
+        const int64_t light = (gk.n_targets + kBlock - 1) / kBlock;
+        k_gather_reduce<<<(unsigned)(light + gk.n_chunks), kBlock, 0, st>>>(gk, call, light);
+        *n_launches = 1;
+    } else if (gk.n_heavy) {
+        k_gather_heavy<<<(gk.n_heavy + 127) / 128, 128, 0, st>>>(gk, call);
+        *n_launches = 1;
+    }
+    return cudaPeekAtLastError();
+}
+
 cudaError_t launch_gather(const DevK &dv, const GatherK &gk, const CallK &call, cudaStream_t st,
                           int *n_launches)
 {
-    int nl = 0;
-    if (dv.N > 0) {
-        const int64_t grid = (dv.N + kBlock - 1) / kBlock;
-        k_gather_eval<<<(unsigned)grid, kBlock, 0, st>>>(dv, gk, call);
-        nl++;
-        cudaError_t e = cudaPeekAtLastError();
+    int total = 0;
+    for (int ph = 0; ph < 3; ph++) {
+        int k = 0;
+        cudaError_t e = launch_gather_phase(dv, gk, call, st, ph, &k);
+        total += k;
         if (e != cudaSuccess) return e;
-        const int64_t light = (gk.n_targets + kBlock - 1) / kBlock;
-        k_gather_reduce<<<(unsigned)(light + gk.n_chunks), kBlock, 0, st>>>(gk, call, light);
-        nl++;
-        e = cudaPeekAtLastError();
-        if (e != cudaSuccess) return e;
-        if (gk.n_heavy) {
-            k_gather_heavy<<<(gk.n_heavy + 127) / 128, 128, 0, st>>>(gk, call);
-            nl++;
-        }
     }
-    if (n_launches) *n_launches = nl;
-    return cudaPeekAtLastError();
+    if (n_launches) *n_launches = total;
+    return cudaSuccess;
 }
 
 cudaError_t launch_race_probe(const DevK &dv, const int32_t *perm, int64_t begin, int64_t count,
