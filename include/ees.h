@@ -52,7 +52,10 @@ typedef enum {
     EES_AUTO = 0,        /* setup times COLOR/ATOMIC/GATHER on this topology, keeps the fastest */
     EES_COLOR = 1,       /* colour-phased: one phase per colour, plain read-modify-write */
     EES_ATOMIC = 2,      /* one pass, FP64 atomicAdd (RED) into A and b */
-    EES_GATHER = 3       /* deterministic: contributions to scratch, per-entry segmented reduction */
+    EES_GATHER = 3,      /* deterministic: contributions to scratch, per-entry segmented reduction */
+    EES_TILE = 4         /* deterministic, one launch: per-CTA row tiles; contributions staged in
+                            shared memory and gathered per owned entry; entries shared by tiles
+                            (heavy x heavy: rails, hubs) reduced from per-tile partials */
 } ees_variant;
 
 /* Conflict relation for the colouring (P:60 and SURVEY A1). */
@@ -112,7 +115,10 @@ typedef struct {
     int32_t launches_per_call;              /* kernels one ees_eval_stamp enqueues */
     double setup_s;                         /* wall time of ees_setup */
     double setup_pattern_s, setup_color_s;  /* parts of it */
-    double tune_ms[4];                      /* EES_AUTO: measured ms per call of [_, COLOR, ATOMIC, GATHER] */
+    int32_t n_tiles, n_heavy_nodes, n_side_targets;   /* EES_TILE structure */
+    int32_t reserved0;
+    int64_t n_tile_items;                   /* device copies over all tiles (>= n_dev) */
+    double tune_ms[5];                      /* EES_AUTO: measured ms per call of [_, COLOR, ATOMIC, GATHER, TILE] */
 } ees_stats_t;
 
 /* Build everything that depends only on topology ("constructs the FET
@@ -167,7 +173,7 @@ ees_status ees_stats(const ees_ctx *ctx, ees_stats_t *out);
  * ees_eval_stamp records CUDA events on the call's stream around each kernel
  * group ("phase"):  COLOR {0: colour kernels, 1: rail finalise},
  * ATOMIC {0: k_atomic},  GATHER {0: evaluate to scratch, 1: segmented
- * reduction, 2: heavy-target finalise}. */
+ * reduction, 2: heavy-target finalise},  TILE {0: k_tile}. */
 ees_status ees_set_timing(ees_ctx *ctx, int32_t enable);
 
 /* Sum of device milliseconds per phase over the calls recorded since the

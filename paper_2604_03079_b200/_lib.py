@@ -16,7 +16,7 @@ if not os.path.exists(LIB_PATH):
                       " -- the CUDA path has no CPU fallback")
 
 EES_OK, EES_EINVAL, EES_ENOMEM, EES_ECUDA, EES_ESTATE = 0, -1, -2, -3, -4
-EES_AUTO, EES_COLOR, EES_ATOMIC, EES_GATHER = 0, 1, 2, 3
+EES_AUTO, EES_COLOR, EES_ATOMIC, EES_GATHER, EES_TILE = 0, 1, 2, 3, 4
 EES_CONFLICT_EXCLUDE_RAILS, EES_CONFLICT_PAPER = 0, 1
 EES_MAX_MODELS, EES_MAX_RAILS = 16, 8
 EES_SETUP_HOST_ONLY = 1
@@ -44,7 +44,8 @@ class ees_stats_t(C.Structure):
                 ("max_conflict_node_degree", i32), ("variant_chosen", i32),
                 ("n_rail_entries", i32), ("n_heavy_targets", i32), ("launches_per_call", i32),
                 ("setup_s", f64), ("setup_pattern_s", f64), ("setup_color_s", f64),
-                ("tune_ms", f64 * 4)]
+                ("n_tiles", i32), ("n_heavy_nodes", i32), ("n_side_targets", i32),
+                ("reserved0", i32), ("n_tile_items", i64), ("tune_ms", f64 * 5)]
 
 
 lib = C.CDLL(LIB_PATH)

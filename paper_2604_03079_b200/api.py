@@ -10,7 +10,7 @@ import numpy as np
 from . import _lib as L
 
 VARIANTS = {"auto": L.EES_AUTO, "color": L.EES_COLOR, "atomic": L.EES_ATOMIC,
-            "gather": L.EES_GATHER}
+            "gather": L.EES_GATHER, "tile": L.EES_TILE}
 VARIANT_NAMES = {v: k for k, v in VARIANTS.items()}
 RULES = {"exclude_rails": L.EES_CONFLICT_EXCLUDE_RAILS, "paper": L.EES_CONFLICT_PAPER}
 
@@ -101,8 +101,8 @@ class Context:
     def stats(self):
         st = L.ees_stats_t()
         _check(L.lib.ees_stats(self._h, C.byref(st)), "ees_stats")
-        out = {f: getattr(st, f) for f, _ in L.ees_stats_t._fields_ if f != "tune_ms"}
-        out["tune_ms"] = {VARIANT_NAMES[v]: st.tune_ms[v] for v in (1, 2, 3)}
+        out = {f: getattr(st, f) for f, _ in L.ees_stats_t._fields_ if f not in ("tune_ms", "reserved0")}
+        out["tune_ms"] = {VARIANT_NAMES[v]: st.tune_ms[v] for v in (1, 2, 3, 4)}
         out["variant_chosen"] = VARIANT_NAMES[st.variant_chosen]
         return out
 

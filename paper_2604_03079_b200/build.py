@@ -18,7 +18,7 @@ INCLUDE = os.path.join(ROOT, "include")
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-SOURCES = ["ees_kernels.cu", "ees_host.cpp"]
+SOURCES = ["ees_kernels.cu", "ees_host.cpp", "ees_tile.cpp"]
 HEADERS = ["ees_internal.h"]
 
 

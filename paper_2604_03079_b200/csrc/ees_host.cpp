@@ -11,6 +11,7 @@
 #include <cstdio>
 #include <cstring>
 #include <new>
+#include <type_traits>
 #include <vector>
 
 #ifdef _OPENMP
@@ -55,6 +56,7 @@ struct ees_ctx {
     int32_t rail_target[kMaxRailEntries] = {};
     Layout L_atomic, L_color, L_gather;
     GatherK gk{};
+    TileK tk{};
     std::vector<int64_t> color_blk_off;   // [C+1] block offsets of colours into partials
     double *partials = nullptr;
     int atomic_grid = 1;
@@ -116,7 +118,7 @@ ees_status validate(const ees_desc *d)
     if (d->n_extra_entries < 0 || (d->n_extra_entries && (!d->extra_row || !d->extra_col)))
         return EES_EINVAL;
     if (!(d->gmin >= 0.0) || !std::isfinite(d->gmin)) return EES_EINVAL;
-    if (d->variant < EES_AUTO || d->variant > EES_GATHER) return EES_EINVAL;
+    if (d->variant < EES_AUTO || d->variant > EES_TILE) return EES_EINVAL;
     if (d->conflict_rule != EES_CONFLICT_EXCLUDE_RAILS && d->conflict_rule != EES_CONFLICT_PAPER)
         return EES_EINVAL;
     if (d->flags & ~EES_SETUP_HOST_ONLY) return EES_EINVAL;
@@ -415,6 +417,10 @@ ees_status enqueue(ees_ctx *c, int32_t variant, const double *x, double h, doubl
             e = launch_rail_finalize(call, c->partials, c->color_blk_off[c->n_colors], st);
             nl++;
         }
+    } else if (variant == EES_TILE) {
+        PhaseMark m(c, st, 0, timed);
+        e = launch_tile(c->tk, call, st);
+        nl = c->tk.n_tiles ? 1 : 0;
     } else if (variant == EES_GATHER) {
         if (timed) {
             for (int ph = 0; ph < 3 && e == cudaSuccess; ph++) {
@@ -600,6 +606,61 @@ ees_status build_gather(const ees_desc *d, ees_ctx *c, const std::vector<int32_t
     return EES_OK;
 }
 
+ees_status build_tile(const ees_desc *d, ees_ctx *c, const std::vector<int32_t> &raw_slot,
+                      const std::vector<int64_t> &iptr, const std::vector<int32_t> &idev)
+{
+    const int32_t *TT[4] = {d->d, d->g, d->s, d->b};
+    TileHost th;
+    if (!build_tile_host(c->n_dev, c->n_nodes, c->n, c->nnz, TT, raw_slot.data(), iptr, idev, c->rails, th))
+        return EES_EINVAL;
+    const int64_t NI = (int64_t)th.item_dev.size();
+    std::vector<int4> term((size_t)NI);
+    std::vector<double> beta((size_t)NI), v0((size_t)(3 * NI));
+    std::vector<uint8_t> model((size_t)NI);
+    const int64_t N = c->n_dev;
+#pragma omp parallel for schedule(static)
+    for (int64_t q = 0; q < NI; q++) {
+        const int32_t i = th.item_dev[q];
+        const ees_model &m = c->models[d->model[i]];
+        term[q] = make_int4(d->d[i], d->g[i], d->s[i], d->b[i]);
+        beta[q] = (m.kp * d->w[i]) / d->l[i];
+        for (int k = 0; k < 3; k++) v0[k * NI + q] = d->vprev[k * N + i];
+        model[q] = (uint8_t)d->model[i];
+    }
+    TileK &k = c->tk;
+    k.n_tiles = th.n_tiles;
+    k.nnz = c->nnz;
+    k.n_items = NI;
+    auto up = [&](auto **dst, const auto &vec) {
+        using T = typename std::remove_reference<decltype(vec)>::type::value_type;
+        return upload(c, const_cast<T **>(dst), vec.data(), vec.size());
+    };
+    TRY(up(&k.item_ptr, th.item_ptr));
+    TRY(up(&k.term, term));
+    TRY(up(&k.beta, beta));
+    TRY(up(&k.v0, v0));
+    TRY(up(&k.model, model));
+    TRY(up(&k.own_ptr, th.own_ptr));
+    TRY(up(&k.own_gid, th.own_gid));
+    TRY(up(&k.own_lst, th.own_lst));
+    TRY(up(&k.lst, th.lst));
+    TRY(up(&k.slst, th.slst));
+    TRY(up(&k.side_ptr, th.side_ptr));
+    TRY(up(&k.side_sid, th.side_sid));
+    TRY(up(&k.side_lst, th.side_lst));
+    TRY(up(&k.side_slot, th.side_slot));
+    TRY(up(&k.sd_gid, th.sd_gid));
+    TRY(up(&k.sd_part, th.sd_part));
+    TRY(dalloc(c, &k.sd_cnt, (size_t)th.n_side));
+    if (cudaMemset(k.sd_cnt, 0, sizeof(int32_t) * std::max(1, th.n_side)) != cudaSuccess) return EES_ECUDA;
+    TRY(dalloc(c, &k.part, th.side_sid.size()));
+    c->st.n_tiles = th.n_tiles;
+    c->st.n_heavy_nodes = th.n_heavy;
+    c->st.n_side_targets = th.n_side;
+    c->st.n_tile_items = NI;
+    return EES_OK;
+}
+
 ees_status autotune(ees_ctx *c)
 {
     double *x, *A, *b;
@@ -615,7 +676,7 @@ ees_status autotune(ees_ctx *c)
     double best = 1e300;
     int32_t bestv = EES_ATOMIC;
     ees_status rc = EES_OK;
-    for (int32_t v = EES_COLOR; v <= EES_GATHER && rc == EES_OK; v++) {
+    for (int32_t v = EES_COLOR; v <= EES_TILE && rc == EES_OK; v++) {
         // skip hopeless colour phasing: more than 512 colours is launch-bound by construction
         if (v == EES_COLOR && c->n_colors > 512) { c->st.tune_ms[v] = -1; continue; }
         for (int it = 0; it < 2 && rc == EES_OK; it++) rc = enqueue(c, v, x, 1e-12, A, b, st, nullptr);
@@ -705,12 +766,23 @@ ees_status setup_impl(const ees_desc *d, ees_ctx *c)
         for (int64_t i = 0; i < N; i++)
             nc += (d->d[i] >= 0) + (d->g[i] >= 0) + (d->s[i] >= 0) + (d->b[i] >= 0);
         c->st.n_contributions = nc;
+        {
+            const int32_t *TT[4] = {d->d, d->g, d->s, d->b};
+            TileHost th;
+            if (!build_tile_host(N, c->n_nodes, c->n, c->nnz, TT, raw_slot.data(), iptr, idev, c->rails, th))
+                return EES_EINVAL;
+            c->st.n_tiles = th.n_tiles;
+            c->st.n_heavy_nodes = th.n_heavy;
+            c->st.n_side_targets = th.n_side;
+            c->st.n_tile_items = (int64_t)th.item_dev.size();
+        }
         c->variant = d->variant == EES_AUTO ? EES_ATOMIC : d->variant;
         c->st.setup_s = now_s() - t0;
         return EES_OK;
     }
     TRY(build_layouts(d, c, raw_slot, rail_ord));
     TRY(build_gather(d, c, raw_slot));
+    TRY(build_tile(d, c, raw_slot, iptr, idev));
     int sms = 148;
     int dev = 0;
     cudaGetDevice(&dev);
@@ -834,11 +906,11 @@ ees_status ees_eval_stamp_host(ees_ctx *c, const double *x, double h, double *A,
 
 ees_status ees_set_variant(ees_ctx *c, int32_t variant)
 {
-    if (!c || variant < EES_AUTO || variant > EES_GATHER) return EES_EINVAL;
+    if (!c || variant < EES_AUTO || variant > EES_TILE) return EES_EINVAL;
     if (variant == EES_AUTO) {
         double best = 1e300;
         int32_t bv = c->variant;
-        for (int v = EES_COLOR; v <= EES_GATHER; v++)
+        for (int v = EES_COLOR; v <= EES_TILE; v++)
             if (c->st.tune_ms[v] > 0 && c->st.tune_ms[v] < best) { best = c->st.tune_ms[v]; bv = v; }
         c->variant = bv;
     } else {

@@ -79,7 +79,59 @@ struct GatherK {
     const int32_t *heavy_chunk;    // [n_heavy+1]
 };
 
+// TILE layout (ees_tile.cpp builds it; k_tile consumes it).  Rows are cut
+// into tiles; a tile's items are the FETs incident on its rows (boundary FETs
+// are copied into every tile they touch).  Each item's 16 contributions
+// (12 A pairs, 4 b rows) land in shared memory at slot p*kTileItems + item;
+// every owned target sums its slot list (u16) in a fixed order.
+constexpr int kTileItems = 512;      // max items (FET copies) per tile
+constexpr int kTileThreads = 256;
+constexpr int kHeavyDeg = 64;        // nodes with more incident FETs are heavy
+
+struct TileK {
+    int32_t n_tiles;
+    int64_t nnz;
+    const int32_t *item_ptr;       // [T+1]
+    const int4 *term;              // [n_items] plain node ids
+    const double *beta;            // [n_items]
+    const double *v0;              // [3][n_items]
+    const uint8_t *model;          // [n_items]
+    int64_t n_items;
+    const int32_t *own_ptr;        // [T+1] owned targets of each tile
+    const int32_t *own_gid;        // [n_own] A index, or nnz + b row
+    const int32_t *own_lst;        // [n_own+1] list ranges into lst
+    const uint16_t *lst;           // slot lists of owned targets
+    const uint16_t *slst;          // slot lists of side entries
+    const int32_t *side_ptr;       // [T+1] side entries of each tile
+    const int32_t *side_sid;       // [n_side_entries] side target
+    const int32_t *side_lst;       // [n_side_entries+1] list ranges into slst
+    const int32_t *side_slot;      // [n_side_entries] slot in `part`
+    const int32_t *sd_gid;         // [n_side] global target
+    const int32_t *sd_part;        // [n_side+1] partial ranges
+    int32_t *sd_cnt;               // [n_side] arrival counters, self-resetting
+    double *part;                  // [n_side_entries]
+};
+
+#ifndef __CUDACC__
+}  // namespace ees
+#include <vector>
+namespace ees {
+struct TileHost {
+    int32_t n_tiles = 0, n_heavy = 0, n_side = 0;
+    std::vector<int32_t> item_ptr, item_dev;
+    std::vector<int32_t> own_ptr, own_gid, own_lst;
+    std::vector<uint16_t> lst, slst;
+    std::vector<int32_t> side_ptr, side_sid, side_lst, side_slot;
+    std::vector<int32_t> sd_gid, sd_part;
+};
+// ees_tile.cpp
+bool build_tile_host(int64_t N, int32_t n_nodes, int32_t n, int64_t nnz, const int32_t *const TT[4],
+                     const int32_t *raw_slot, const std::vector<int64_t> &iptr,
+                     const std::vector<int32_t> &idev, const std::vector<int32_t> &rails, TileHost &out);
+#endif
+
 // ---- launchers (ees_kernels.cu); all asynchronous on `st` ----
+cudaError_t launch_tile(const TileK &tk, const CallK &call, cudaStream_t st);
 cudaError_t launch_atomic(const DevK &dv, const CallK &call, int grid, cudaStream_t st);
 cudaError_t launch_color(const DevK &dv, const CallK &call, int64_t begin, int64_t count,
                          double *partials, cudaStream_t st);

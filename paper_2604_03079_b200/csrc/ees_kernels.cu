@@ -41,7 +41,7 @@ __device__ __forceinline__ void eval_fet(const CardK &cd, double beta, double gm
     const double v = fwd ? vds : -vds;
     const double uov = u - cd.vt;
     const double op = 1.0 + cd.lam * v;
-    const bool on = uov > 0.0;                      // uov = 0 -> cutoff
+    const bool on = !(uov <= 0.0);                  // uov = 0 -> cutoff; NaN propagates (as the oracle)
     const bool sat = v >= uov;                      // v = uov -> saturation
     // q = f / (beta*op): saturation uov^2/2, triode uov*v - v^2/2
     const double q = sat ? 0.5 * uov * uov : uov * v - 0.5 * v * v;
@@ -112,10 +112,10 @@ __device__ __forceinline__ double warp_sum(double v)
 
 // Rail side reduction, per warp: for every rail entry e, the warp's sum of
 // this iteration's contributions is added (fixed order) to s_acc[warp][e].
-__device__ __forceinline__ void rail_accumulate(const CallK &P, const int32_t *slot, const int4 &T,
+// tc = (d, g, s, b) codes of the b rows (after any merge).
+__device__ __forceinline__ void rail_accumulate(const CallK &P, const int32_t *slot, const int *tc,
                                                 const Stamp &st, bool valid, double *s_acc)
 {
-    const int tc[4] = {T.x, T.y, T.z, T.w};
     bool mine = false;
     if (valid) {
 #pragma unroll
@@ -143,11 +143,29 @@ __device__ __forceinline__ void rail_accumulate(const CallK &P, const int32_t *s
     }
 }
 
+// Source tied to bulk (every PMOS of the inverter configs): DS/DB, SD/BD and
+// SS/BB address the same entry and J[S]/J[B] the same row -- fold them so one
+// RMW carries both (the sum is exact up to one rounding, inside 1e-12 sum|c|).
+__device__ __forceinline__ void merge_source_bulk(const int4 &T, Stamp &st, int32_t *slot, int *tc)
+{
+    if (T.z == T.w && T.z != -1) {
+        st.y[DS] += st.y[DB];
+        st.y[SD] += st.y[BD];
+        st.y[SS] += st.y[BB];
+        st.j[2] += st.j[3];
+        slot[DB] = -1;
+        slot[BD] = -1;
+        slot[BB] = -1;
+        tc[3] = -1;
+    }
+}
+
 // ---------------------------------------------------------------------------
 // ATOMIC: grid-stride over devices (netlist order), RED.F64 into A and b;
 // rail entries reduced per block, one atomic per block and entry at the end.
+// All per-device loads (data + 12 slots) are issued before the x gather.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kBlock) k_atomic(DevK dv, CallK P)
+__global__ void __launch_bounds__(kBlock, 4) k_atomic(DevK dv, CallK P)
 {
     __shared__ CardK s_cards[EES_MAX_MODELS];
     __shared__ double s_railx[EES_MAX_RAILS];
@@ -157,7 +175,7 @@ __global__ void __launch_bounds__(kBlock) k_atomic(DevK dv, CallK P)
     for (int k = threadIdx.x; k < nw * P.n_rail_entries; k += blockDim.x) s_acc[k] = 0.0;
     __syncthreads();
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    // iterate with warp-uniform trip count so rail_accumulate's shuffles are full-warp
+    // warp-uniform trip count so rail_accumulate's shuffles are full-warp
     const int64_t base0 = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31);
     for (int64_t base = base0; base < dv.N; base += stride) {
         const int64_t i = base + (threadIdx.x & 31);
@@ -165,14 +183,25 @@ __global__ void __launch_bounds__(kBlock) k_atomic(DevK dv, CallK P)
         int4 T = make_int4(-1, -1, -1, -1);
         Stamp st;
         int32_t slot[NPAIR];
+        int tc[4] = {-1, -1, -1, -1};
         if (valid) {
-            load_eval(dv, P, s_cards, s_railx, i, T, st);
+            T = __ldg(dv.term + i);
+            const double beta = __ldg(dv.beta + i);
+            const double a0 = __ldg(dv.v0 + i);
+            const double a1 = __ldg(dv.v0 + dv.N + i);
+            const double a2 = __ldg(dv.v0 + 2 * dv.N + i);
+            const int m = __ldg(dv.model + i);
 #pragma unroll
             for (int p = 0; p < NPAIR; p++) slot[p] = __ldg(dv.slot + (int64_t)p * dv.N + i);
+            const double VD = volt(T.x, P.x, s_railx);
+            const double VG = volt(T.y, P.x, s_railx);
+            const double VS = volt(T.z, P.x, s_railx);
+            eval_fet(s_cards[m], beta, P.gmin, VD, VG, VS, a0, a1, a2, st);
+            tc[0] = T.x; tc[1] = T.y; tc[2] = T.z; tc[3] = T.w;
+            merge_source_bulk(T, st, slot, tc);
 #pragma unroll
             for (int p = 0; p < NPAIR; p++)
                 if (slot[p] >= 0) atomicAdd(P.A + slot[p], st.y[p]);
-            const int tc[4] = {T.x, T.y, T.z, T.w};
 #pragma unroll
             for (int a = 0; a < 4; a++)
                 if (tc[a] >= 0) atomicAdd(P.b + tc[a], st.j[a]);
@@ -180,7 +209,7 @@ __global__ void __launch_bounds__(kBlock) k_atomic(DevK dv, CallK P)
 #pragma unroll
             for (int p = 0; p < NPAIR; p++) slot[p] = -1;
         }
-        if (P.n_rail_entries) rail_accumulate(P, slot, T, st, valid, s_acc);
+        if (P.n_rail_entries) rail_accumulate(P, slot, tc, st, valid, s_acc);
     }
     if (P.n_rail_entries) {
         __syncthreads();
@@ -214,14 +243,16 @@ __global__ void __launch_bounds__(kBlock) k_color(DevK dv, CallK P, int64_t begi
     int4 T = make_int4(-1, -1, -1, -1);
     Stamp st;
     int32_t slot[NPAIR];
+    int tc[4] = {-1, -1, -1, -1};
     if (valid) {
-        load_eval(dv, P, s_cards, s_railx, i, T, st);
 #pragma unroll
         for (int p = 0; p < NPAIR; p++) slot[p] = __ldg(dv.slot + (int64_t)p * dv.N + i);
+        load_eval(dv, P, s_cards, s_railx, i, T, st);
+        tc[0] = T.x; tc[1] = T.y; tc[2] = T.z; tc[3] = T.w;
+        merge_source_bulk(T, st, slot, tc);
 #pragma unroll
         for (int p = 0; p < NPAIR; p++)
             if (slot[p] >= 0) P.A[slot[p]] += st.y[p];
-        const int tc[4] = {T.x, T.y, T.z, T.w};
 #pragma unroll
         for (int a = 0; a < 4; a++)
             if (tc[a] >= 0) P.b[tc[a]] += st.j[a];
@@ -230,7 +261,7 @@ __global__ void __launch_bounds__(kBlock) k_color(DevK dv, CallK P, int64_t begi
         for (int p = 0; p < NPAIR; p++) slot[p] = -1;
     }
     if (P.n_rail_entries) {
-        rail_accumulate(P, slot, T, st, valid, s_acc);
+        rail_accumulate(P, slot, tc, st, valid, s_acc);
         __syncthreads();
         for (int e = threadIdx.x; e < P.n_rail_entries; e += blockDim.x) {
             double v = 0.0;
@@ -463,6 +494,97 @@ cudaError_t launch_count_conflicts(const int32_t *cnt, int64_t n, unsigned long 
 {
     if (n == 0) return cudaSuccess;
     k_count_conflicts<<<296, kBlock, 0, st>>>(cnt, n, out);
+    return cudaPeekAtLastError();
+}
+
+// ---------------------------------------------------------------------------
+// TILE (deterministic, one launch): one CTA per row tile.  Phase 1: every
+// item (FET copy) is evaluated and its 16 contributions are staged in shared
+// memory.  Phase 2: each owned target (A entry or b row whose contributors all
+// belong to this tile) sums its slot list in list order and does a plain RMW
+// -- no other CTA touches it.  Phase 3: targets shared by several tiles
+// (heavy x heavy entries: rails, hubs) -- one warp per (tile, target) sums the
+// tile's part (fixed lane stride + shuffle tree), stores it, and the warp that
+// brings the target's arrival counter to its part count sums all parts in
+// part order and applies the result.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kTileThreads) k_tile(TileK tk, CallK P)
+{
+    extern __shared__ double s_c[];   // [16][kTileItems]
+    __shared__ CardK s_cards[EES_MAX_MODELS];
+    for (int k = threadIdx.x; k < P.n_models; k += blockDim.x) s_cards[k] = P.cards[k];
+    __syncthreads();
+    const int t = blockIdx.x;
+    const int32_t i0 = tk.item_ptr[t], ni = tk.item_ptr[t + 1] - i0;
+    for (int it = threadIdx.x; it < ni; it += blockDim.x) {
+        const int64_t i = i0 + it;
+        const int4 T = __ldg(tk.term + i);
+        const double beta = __ldg(tk.beta + i);
+        const double a0 = __ldg(tk.v0 + i);
+        const double a1 = __ldg(tk.v0 + tk.n_items + i);
+        const double a2 = __ldg(tk.v0 + 2 * tk.n_items + i);
+        const int m = __ldg(tk.model + i);
+        const double VD = T.x >= 0 ? __ldg(P.x + T.x) : 0.0;
+        const double VG = T.y >= 0 ? __ldg(P.x + T.y) : 0.0;
+        const double VS = T.z >= 0 ? __ldg(P.x + T.z) : 0.0;
+        Stamp st;
+        eval_fet(s_cards[m], beta, P.gmin, VD, VG, VS, a0, a1, a2, st);
+#pragma unroll
+        for (int p = 0; p < NPAIR; p++) s_c[p * kTileItems + it] = st.y[p];
+#pragma unroll
+        for (int a = 0; a < 4; a++) s_c[(NPAIR + a) * kTileItems + it] = st.j[a];
+    }
+    __syncthreads();
+    const int32_t o1 = tk.own_ptr[t + 1];
+    for (int32_t j = tk.own_ptr[t] + threadIdx.x; j < o1; j += blockDim.x) {
+        const int32_t g = __ldg(tk.own_gid + j);
+        const int32_t l0 = __ldg(tk.own_lst + j), l1 = __ldg(tk.own_lst + j + 1);
+        double s = 0.0;
+        for (int32_t l = l0; l < l1; l++) s += s_c[__ldg(tk.lst + l)];
+        if (g < tk.nnz) P.A[g] += s;
+        else P.b[g - tk.nnz] += s;
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int32_t e1 = tk.side_ptr[t + 1];
+    for (int32_t e = tk.side_ptr[t] + warp; e < e1; e += nw) {
+        const int32_t l0 = __ldg(tk.side_lst + e), l1 = __ldg(tk.side_lst + e + 1);
+        double v = 0.0;
+        for (int32_t l = l0 + lane; l < l1; l += 32) v += s_c[__ldg(tk.slst + l)];
+        v = warp_sum(v);
+        const int32_t sid = __ldg(tk.side_sid + e);
+        const int32_t p0 = __ldg(tk.sd_part + sid), p1 = __ldg(tk.sd_part + sid + 1);
+        int last = 0;
+        if (lane == 0) {
+            tk.part[__ldg(tk.side_slot + e)] = v;
+            __threadfence();
+            last = atomicAdd(tk.sd_cnt + sid, 1) == (p1 - p0) - 1;
+        }
+        last = __shfl_sync(0xffffffffu, last, 0);
+        if (last) {
+            __threadfence();
+            double u = 0.0;
+            for (int32_t q = p0 + lane; q < p1; q += 32) u += __ldcg(tk.part + q);
+            u = warp_sum(u);
+            if (lane == 0) {
+                const int32_t g = __ldg(tk.sd_gid + sid);
+                if (g < tk.nnz) P.A[g] += u;
+                else P.b[g - tk.nnz] += u;
+                tk.sd_cnt[sid] = 0;
+            }
+        }
+    }
+}
+
+cudaError_t launch_tile(const TileK &tk, const CallK &call, cudaStream_t st)
+{
+    if (tk.n_tiles == 0) return cudaSuccess;
+    static bool attr = false;
+    const size_t smem = sizeof(double) * 16 * kTileItems;
+    if (!attr) {
+        cudaFuncSetAttribute(k_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = true;
+    }
+    k_tile<<<tk.n_tiles, kTileThreads, smem, st>>>(tk, call);
     return cudaPeekAtLastError();
 }
 

@@ -12,7 +12,7 @@ import oracle
 
 pytestmark = pytest.mark.gpu
 TOL = 1e-12
-VARIANTS = ["color", "atomic", "gather"]
+VARIANTS = ["color", "atomic", "gather", "tile"]
 
 _ref_cache = {}
 
@@ -172,12 +172,12 @@ def test_spec_card_all_cutoff(cuda_ok):
 
 
 def test_determinism(cuda_ok):
-    """COLOR and GATHER are bitwise reproducible run to run (fixed summation
-    order); ATOMIC within tolerance."""
+    """COLOR, GATHER and TILE are bitwise reproducible run to run (fixed
+    summation order); ATOMIC within tolerance."""
     nl = netgen.config(2, 0.02)
     ref = reference(nl)
     ctx = ctx_for(nl)
-    for v in ("color", "gather"):
+    for v in ("color", "gather", "tile"):
         A1, b1 = gpu_run(ctx, nl, v)
         for _ in range(3):
             A2, b2 = gpu_run(ctx, nl, v)

@@ -120,3 +120,32 @@ def test_empty_netlist():
     c = _ctx(nl)
     st = c.stats()
     assert st["n_dev"] == 0 and st["nnz"] == 0 and st["n_colors"] == 0
+
+
+@pytest.mark.parametrize("cfg", [0, 1, 2, 3, 4])
+def test_tile_structure(cfg):
+    """EES_TILE setup: every live contribution is listed exactly once (checked
+    inside ees_setup, which fails otherwise); heavy nodes and side targets as
+    expected from the topology."""
+    nl = netgen.config(cfg, 0.01)
+    st = _ctx(nl).stats()
+    assert st["n_tiles"] >= 1
+    assert st["n_tile_items"] >= st["n_dev"]
+    if cfg in (0, 1):
+        # VDD is the only heavy node; A[VDD,VDD] and b[VDD] are side targets
+        # once the FETs span more than one tile
+        assert st["n_heavy_nodes"] == 1
+        assert st["n_side_targets"] == (2 if st["n_tiles"] > 1 else 0)
+
+
+@pytest.mark.parametrize("seed", range(30))
+def test_tile_structure_random(seed):
+    rng = np.random.Generator(np.random.PCG64(77 + seed))
+    N = int(rng.integers(1, 3000)); nn = int(rng.integers(2, 200))
+    T = rng.integers(-1, nn, size=(N, 4))
+    hubs = rng.integers(0, nn, 3)
+    T[rng.random(N) < 0.3, 1] = hubs[0]          # a few high-fanout gates -> heavy nodes
+    rails = [int(hubs[1])] if seed % 2 else []
+    nl = netgen.custom("r", nn, [tuple(t) for t in T], 0, netgen.bench_models(), rails=rails)
+    st = _ctx(nl).stats()
+    assert st["n_tile_items"] >= N
