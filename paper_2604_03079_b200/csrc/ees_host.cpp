@@ -9,6 +9,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <type_traits>
@@ -59,6 +60,10 @@ struct ees_ctx {
     TileK tk{};
     std::vector<int64_t> color_blk_off;   // [C+1] block offsets of colours into partials
     double *partials = nullptr;
+    int color_coop = 0;                   // 1: persistent cooperative COLOR kernel
+    int coop_grid = 0;
+    int64_t *d_color_ptr = nullptr;
+    double *coop_partials = nullptr;
     int atomic_grid = 1;
     int32_t variant = EES_ATOMIC;
     int32_t launches = 0;
@@ -402,6 +407,11 @@ ees_status enqueue(ees_ctx *c, int32_t variant, const double *x, double h, doubl
         PhaseMark m(c, st, 0, timed);
         e = launch_atomic(c->L_atomic.k(), call, c->atomic_grid, st);
         nl = c->n_dev ? 1 : 0;
+    } else if (variant == EES_COLOR && c->color_coop) {
+        PhaseMark m(c, st, 0, timed);
+        e = launch_color_coop(c->L_color.k(), call, c->d_color_ptr, c->n_colors, c->coop_partials,
+                              c->coop_grid, st);
+        nl = c->n_dev ? 1 : 0;
     } else if (variant == EES_COLOR) {
         const DevK dv = c->L_color.k();
         {
@@ -518,6 +528,18 @@ ees_status build_layouts(const ees_desc *d, ees_ctx *c, const std::vector<int32_
         c->color_blk_off[col + 1] = c->color_blk_off[col] + (cnt + kBlock - 1) / kBlock;
     }
     TRY(dalloc(c, &c->partials, (size_t)(c->color_blk_off[c->n_colors] * std::max(1, c->n_rail_entries))));
+    // persistent cooperative form: one CTA set resident on every SM
+    {
+        int sms = 148, dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        int coop = 0;
+        cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+        const int bps = coop ? color_coop_blocks_per_sm() : 0;
+        c->coop_grid = bps * sms;
+        TRY(upload(c, &c->d_color_ptr, c->color_ptr.data(), c->color_ptr.size()));
+        TRY(dalloc(c, &c->coop_partials, (size_t)std::max(1, c->coop_grid) * std::max(1, c->n_rail_entries)));
+    }
     return EES_OK;
 }
 
@@ -661,7 +683,7 @@ ees_status build_tile(const ees_desc *d, ees_ctx *c, const std::vector<int32_t> 
     return EES_OK;
 }
 
-ees_status autotune(ees_ctx *c)
+ees_status autotune(ees_ctx *c, bool full)
 {
     double *x, *A, *b;
     TRY(dalloc(c, &x, (size_t)c->n));
@@ -676,9 +698,7 @@ ees_status autotune(ees_ctx *c)
     double best = 1e300;
     int32_t bestv = EES_ATOMIC;
     ees_status rc = EES_OK;
-    for (int32_t v = EES_COLOR; v <= EES_TILE && rc == EES_OK; v++) {
-        // skip hopeless colour phasing: more than 512 colours is launch-bound by construction
-        if (v == EES_COLOR && c->n_colors > 512) { c->st.tune_ms[v] = -1; continue; }
+    auto time_variant = [&](int32_t v) -> double {
         for (int it = 0; it < 2 && rc == EES_OK; it++) rc = enqueue(c, v, x, 1e-12, A, b, st, nullptr);
         cudaEventRecord(e0, st);
         const int reps = 5;
@@ -687,13 +707,36 @@ ees_status autotune(ees_ctx *c)
         if (cudaEventSynchronize(e1) != cudaSuccess) rc = EES_ECUDA;
         float ms = 0;
         cudaEventElapsedTime(&ms, e0, e1);
-        c->st.tune_ms[v] = ms / reps;
-        if (ms / reps < best) { best = ms / reps; bestv = v; }
+        return ms / reps;
+    };
+    const char *mode = std::getenv("EES_COLOR_MODE");   // debug knob: "launch" | "coop"
+    for (int32_t v = EES_COLOR; v <= (full ? EES_TILE : EES_COLOR) && rc == EES_OK; v++) {
+        double ms;
+        if (v == EES_COLOR && mode && (!std::strcmp(mode, "launch") || !std::strcmp(mode, "coop"))) {
+            c->color_coop = !std::strcmp(mode, "coop") && c->coop_grid > 0;
+            ms = time_variant(v);
+        } else if (v == EES_COLOR) {
+            // colour phasing pays one barrier per colour: past 512 colours it is
+            // launch/barrier-bound by construction, not worth timing
+            if (c->n_colors > 512) { c->st.tune_ms[v] = -1; continue; }
+            c->color_coop = 0;
+            ms = time_variant(v);
+            if (c->coop_grid > 0 && rc == EES_OK) {
+                c->color_coop = 1;
+                const double ms2 = time_variant(v);
+                if (ms2 < ms) ms = ms2;
+                else c->color_coop = 0;
+            }
+        } else {
+            ms = time_variant(v);
+        }
+        c->st.tune_ms[v] = ms;
+        if (ms < best) { best = ms; bestv = v; }
     }
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     cudaStreamDestroy(st);
-    c->variant = bestv;
+    if (full) c->variant = bestv;
     return rc;
 }
 
@@ -791,9 +834,10 @@ ees_status setup_impl(const ees_desc *d, ees_ctx *c)
     c->atomic_grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sms * atomic_blocks_per_sm()));
     if (cudaDeviceSynchronize() != cudaSuccess) return EES_ECUDA;
     if (d->variant == EES_AUTO) {
-        TRY(autotune(c));
+        TRY(autotune(c, true));
     } else {
         c->variant = d->variant;
+        if (d->variant == EES_COLOR) TRY(autotune(c, false));   // pick the COLOR form
     }
     c->st.setup_s = now_s() - t0;
     return EES_OK;

@@ -135,6 +135,9 @@ cudaError_t launch_tile(const TileK &tk, const CallK &call, cudaStream_t st);
 cudaError_t launch_atomic(const DevK &dv, const CallK &call, int grid, cudaStream_t st);
 cudaError_t launch_color(const DevK &dv, const CallK &call, int64_t begin, int64_t count,
                          double *partials, cudaStream_t st);
+int color_coop_blocks_per_sm();
+cudaError_t launch_color_coop(const DevK &dv, const CallK &call, const int64_t *cptr_dev, int32_t C,
+                              double *partials, int grid, cudaStream_t st);
 cudaError_t launch_rail_finalize(const CallK &call, const double *partials, int64_t n_blocks,
                                  cudaStream_t st);
 cudaError_t launch_gather(const DevK &dv, const GatherK &gk, const CallK &call, cudaStream_t st,

@@ -14,9 +14,12 @@
 //
 // The path is HBM-bound (~46 FP64 flops vs ~100-155 compulsory bytes per
 // device); there is no dense contraction, so no tensor cores.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include "ees_internal.h"
+
+namespace cg = cooperative_groups;
 
 namespace ees {
 
@@ -427,6 +430,140 @@ cudaError_t launch_atomic(const DevK &dv, const CallK &call, int grid, cudaStrea
     if (dv.N == 0) return cudaSuccess;
     k_atomic<<<grid, kBlock, rail_smem(call), st>>>(dv, call);
     return cudaPeekAtLastError();
+}
+
+// ---------------------------------------------------------------------------
+// COLOR, persistent form (Table I "Color": one parallel region with a barrier
+// between colours): one cooperative launch, grid.sync()
+// between colours.  A FET's data, slots and x gather do not depend on earlier
+// colours, so the first FET of colour c+1 is fetched before the barrier and
+// only the A/b read-modify-write stays behind it.  Rail entries accumulate
+// per warp across colours; block 0 sums the block parts in block order.
+// ---------------------------------------------------------------------------
+struct Fetched {
+    int4 T;
+    double beta, a0, a1, a2, VD, VG, VS;
+    int m;
+    int32_t slot[NPAIR];
+};
+
+__device__ __forceinline__ void fetch_dev(const DevK &dv, const CallK &P, const double *s_railx,
+                                          int64_t i, bool valid, Fetched &f)
+{
+    if (!valid) {
+        f.T = make_int4(-1, -1, -1, -1);
+        return;
+    }
+    f.T = __ldg(dv.term + i);
+    f.beta = __ldg(dv.beta + i);
+    f.a0 = __ldg(dv.v0 + i);
+    f.a1 = __ldg(dv.v0 + dv.N + i);
+    f.a2 = __ldg(dv.v0 + 2 * dv.N + i);
+    f.m = __ldg(dv.model + i);
+#pragma unroll
+    for (int p = 0; p < NPAIR; p++) f.slot[p] = __ldg(dv.slot + (int64_t)p * dv.N + i);
+    f.VD = volt(f.T.x, P.x, s_railx);
+    f.VG = volt(f.T.y, P.x, s_railx);
+    f.VS = volt(f.T.z, P.x, s_railx);
+}
+
+__global__ void __launch_bounds__(kBlock, 2) k_color_coop(DevK dv, CallK P, const int64_t *cptr,
+                                                          int32_t C, double *partials)
+{
+    cg::grid_group grid = cg::this_grid();
+    __shared__ CardK s_cards[EES_MAX_MODELS];
+    __shared__ double s_railx[EES_MAX_RAILS];
+    extern __shared__ double s_acc[];
+    load_call_smem(P, s_cards, s_railx);
+    const int nw = blockDim.x >> 5;
+    for (int k = threadIdx.x; k < nw * P.n_rail_entries; k += blockDim.x) s_acc[k] = 0.0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int64_t G = (int64_t)gridDim.x * blockDim.x;
+    const int64_t wbase = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31);
+    Fetched cur;
+    {
+        const int64_t i = cptr[0] + wbase + lane;
+        fetch_dev(dv, P, s_railx, i, C > 0 && i < cptr[1], cur);
+    }
+    for (int32_t c = 0; c < C; c++) {
+        const int64_t end = cptr[c + 1];
+        bool first = true;
+        for (int64_t base = cptr[c] + wbase; base < end; base += G) {
+            const int64_t i = base + lane;
+            const bool valid = i < end;
+            Fetched f;
+            if (first) f = cur;
+            else fetch_dev(dv, P, s_railx, i, valid, f);
+            first = false;
+            Stamp st;
+            int tc[4] = {-1, -1, -1, -1};
+            if (valid) {
+                eval_fet(s_cards[f.m], f.beta, P.gmin, f.VD, f.VG, f.VS, f.a0, f.a1, f.a2, st);
+                tc[0] = f.T.x; tc[1] = f.T.y; tc[2] = f.T.z; tc[3] = f.T.w;
+                merge_source_bulk(f.T, st, f.slot, tc);
+#pragma unroll
+                for (int p = 0; p < NPAIR; p++)
+                    if (f.slot[p] >= 0) P.A[f.slot[p]] += st.y[p];
+#pragma unroll
+                for (int a = 0; a < 4; a++)
+                    if (tc[a] >= 0) P.b[tc[a]] += st.j[a];
+            } else {
+#pragma unroll
+                for (int p = 0; p < NPAIR; p++) f.slot[p] = -1;
+            }
+            if (P.n_rail_entries) rail_accumulate(P, f.slot, tc, st, valid, s_acc);
+        }
+        if (c + 1 < C) {
+            const int64_t i = cptr[c + 1] + wbase + lane;
+            fetch_dev(dv, P, s_railx, i, i < cptr[c + 2], cur);
+        }
+        grid.sync();
+    }
+    if (P.n_rail_entries) {
+        __syncthreads();
+        for (int e = threadIdx.x; e < P.n_rail_entries; e += blockDim.x) {
+            double v = 0.0;
+            for (int w = 0; w < nw; w++) v += s_acc[w * P.n_rail_entries + e];
+            partials[(int64_t)blockIdx.x * P.n_rail_entries + e] = v;
+        }
+        __threadfence();
+        grid.sync();
+        if (blockIdx.x == 0) {
+            const int warp = threadIdx.x >> 5;
+            for (int e = warp; e < P.n_rail_entries; e += nw) {
+                double v = 0.0;
+                for (int64_t k = lane; k < gridDim.x; k += 32) v += __ldcg(partials + k * P.n_rail_entries + e);
+                v = warp_sum(v);
+                if (lane == 0) {
+                    double *dst = e < P.n_rail_a ? P.A + P.rail_target[e] : P.b + P.rail_target[e];
+                    *dst += v;
+                }
+            }
+        }
+    }
+}
+
+int color_coop_blocks_per_sm()
+{
+    int nb = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_color_coop, kBlock,
+                                                  sizeof(double) * (kBlock / 32) * kMaxRailEntries);
+    return nb;
+}
+
+cudaError_t launch_color_coop(const DevK &dv, const CallK &call, const int64_t *cptr_dev, int32_t C,
+                              double *partials, int grid, cudaStream_t st)
+{
+    if (dv.N == 0 || C == 0) return cudaSuccess;
+    DevK a0 = dv;
+    CallK a1 = call;
+    const int64_t *a2 = cptr_dev;
+    int32_t a3 = C;
+    double *a4 = partials;
+    void *args[] = {&a0, &a1, &a2, &a3, &a4};
+    return cudaLaunchCooperativeKernel((const void *)k_color_coop, dim3(grid), dim3(kBlock), args,
+                                       rail_smem(call), st);
 }
 
 cudaError_t launch_color(const DevK &dv, const CallK &call, int64_t begin, int64_t count,

@@ -200,8 +200,8 @@ def test_race_probe_detects_corrupted_schedule(cuda_ok):
 
 def test_nan_propagates(cuda_ok):
     """NaN in x is not checked (ees.h): it propagates exactly where the
-    oracle's arithmetic propagates it (NaN comparisons select cutoff, so A
-    stays finite; the Norton terms 0*NaN make b NaN)."""
+    oracle's arithmetic propagates it (a NaN bias fails the cutoff test and
+    poisons that FET's conductances and Norton terms)."""
     nl = netgen.inverter_chain(10)
     ctx = ctx_for(nl)
     nl.x[3] = np.nan
@@ -211,9 +211,9 @@ def test_nan_propagates(cuda_ok):
         A, b = gpu_run(ctx, nl, v)
         for got, want in ((A, ref["A"]), (b, ref["b"])):
             assert np.array_equal(np.isnan(got), np.isnan(want))
-        ok = ~np.isnan(ref["b"])
-        assert np.all(np.abs(b[ok] - ref["b"][ok]) <= 1e-12 * ref["b_abs"][ok])
-        assert np.all(np.abs(A - ref["A"]) <= 1e-12 * ref["A_abs"])
+        for got, want, mag in ((A, ref["A"], ref["A_abs"]), (b, ref["b"], ref["b_abs"])):
+            ok = ~np.isnan(want)
+            assert np.all(np.abs(got[ok] - want[ok]) <= 1e-12 * mag[ok])
 
 
 def test_host_buffer_call_matches(cuda_ok):
@@ -243,3 +243,20 @@ def test_abi_errors(cuda_ok):
         ctx.eval_stamp(x[:-1], 1e-12, A, b)
     with pytest.raises(ValueError):
         ctx.eval_stamp(x.float(), 1e-12, A, b)
+
+
+@pytest.mark.parametrize("mode", ["launch", "coop"])
+def test_color_forms(cuda_ok, mode, monkeypatch):
+    """Both COLOR forms: one launch per colour (Table I ColorFused) and
+    the persistent cooperative kernel with a grid barrier per colour (Table I
+    Color "single parallel region", P:79)."""
+    monkeypatch.setenv("EES_COLOR_MODE", mode)
+    for nl in (netgen.config(0), netgen.config(1, 0.05), netgen.gen_synth(5000, 40),
+               netgen.ota_5t()):
+        ref = reference(nl)
+        ctx = ctx_for(nl, variant="color")
+        A1, b1 = gpu_run(ctx, nl)
+        assert_parity(ref, A1, b1, f"{nl.name} color/{mode}")
+        A2, b2 = gpu_run(ctx, nl)
+        assert np.array_equal(A1, A2) and np.array_equal(b1, b2)
+        ctx.close()
