@@ -633,7 +633,8 @@ ees_status build_tile(const ees_desc *d, ees_ctx *c, const std::vector<int32_t> 
 {
     const int32_t *TT[4] = {d->d, d->g, d->s, d->b};
     TileHost th;
-    if (!build_tile_host(c->n_dev, c->n_nodes, c->n, c->nnz, TT, raw_slot.data(), iptr, idev, c->rails, th))
+    if (!build_tile_host(c->n_dev, c->n_nodes, c->n, c->nnz, TT, raw_slot.data(), iptr, idev, c->rails,
+                         c->row_ptr, c->col_idx, th))
         return EES_EINVAL;
     const int64_t NI = (int64_t)th.item_dev.size();
     std::vector<int4> term((size_t)NI);
@@ -662,14 +663,12 @@ ees_status build_tile(const ees_desc *d, ees_ctx *c, const std::vector<int32_t> 
     TRY(up(&k.beta, beta));
     TRY(up(&k.v0, v0));
     TRY(up(&k.model, model));
-    TRY(up(&k.own_ptr, th.own_ptr));
-    TRY(up(&k.own_gid, th.own_gid));
-    TRY(up(&k.own_lst, th.own_lst));
-    TRY(up(&k.lst, th.lst));
-    TRY(up(&k.slst, th.slst));
+    TRY(up(&k.blob_off, th.blob_off));
+    TRY(up(&k.blob, th.blob));
     TRY(up(&k.side_ptr, th.side_ptr));
     TRY(up(&k.side_sid, th.side_sid));
     TRY(up(&k.side_lst, th.side_lst));
+    TRY(up(&k.slst, th.slst));
     TRY(up(&k.side_slot, th.side_slot));
     TRY(up(&k.sd_gid, th.sd_gid));
     TRY(up(&k.sd_part, th.sd_part));
@@ -812,7 +811,8 @@ ees_status setup_impl(const ees_desc *d, ees_ctx *c)
         {
             const int32_t *TT[4] = {d->d, d->g, d->s, d->b};
             TileHost th;
-            if (!build_tile_host(N, c->n_nodes, c->n, c->nnz, TT, raw_slot.data(), iptr, idev, c->rails, th))
+            if (!build_tile_host(N, c->n_nodes, c->n, c->nnz, TT, raw_slot.data(), iptr, idev, c->rails,
+                                 c->row_ptr, c->col_idx, th))
                 return EES_EINVAL;
             c->st.n_tiles = th.n_tiles;
             c->st.n_heavy_nodes = th.n_heavy;

@@ -83,10 +83,24 @@ struct GatherK {
 // into tiles; a tile's items are the FETs incident on its rows (boundary FETs
 // are copied into every tile they touch).  Each item's 16 contributions
 // (12 A pairs, 4 b rows) land in shared memory at slot p*kTileItems + item;
-// every owned target sums its slot list (u16) in a fixed order.
-constexpr int kTileItems = 512;      // max items (FET copies) per tile
+// every owned target sums its slot list (u16) in a fixed order.  A tile's
+// owned-target program is one 16-byte-aligned blob, bulk-copied (TMA,
+// cp.async.bulk) into shared memory while the items are evaluated:
+//   TileHdr | runs[n_runs] (int2: global start, length) |
+//   lstart[n_own+1] (u16) | lst[n_lst] (u16) | pad to 16 B
+// Local target j maps to global target (A index, or nnz + b row) through the
+// runs; its contributions are lst[lstart[j] .. lstart[j+1]).
+constexpr int kTileItems = 256;      // max items (FET copies) per tile = threads per CTA
 constexpr int kTileThreads = 256;
 constexpr int kHeavyDeg = 64;        // nodes with more incident FETs are heavy
+constexpr int kBlobMax = 20480;      // bytes of shared memory for a tile's program
+constexpr int kTilePrefetch = 8;     // owned targets whose A/b value a thread prefetches
+
+struct TileHdr {
+    uint16_t n_items, n_own, n_runs, n_lst;
+    uint32_t bytes;                  // blob size, multiple of 16
+    uint32_t pad;
+};
 
 struct TileK {
     int32_t n_tiles;
@@ -97,14 +111,12 @@ struct TileK {
     const double *v0;              // [3][n_items]
     const uint8_t *model;          // [n_items]
     int64_t n_items;
-    const int32_t *own_ptr;        // [T+1] owned targets of each tile
-    const int32_t *own_gid;        // [n_own] A index, or nnz + b row
-    const int32_t *own_lst;        // [n_own+1] list ranges into lst
-    const uint16_t *lst;           // slot lists of owned targets
-    const uint16_t *slst;          // slot lists of side entries
+    const int64_t *blob_off;       // [T+1] byte offsets into blob
+    const uint8_t *blob;
     const int32_t *side_ptr;       // [T+1] side entries of each tile
     const int32_t *side_sid;       // [n_side_entries] side target
     const int32_t *side_lst;       // [n_side_entries+1] list ranges into slst
+    const uint16_t *slst;          // slot lists of side entries
     const int32_t *side_slot;      // [n_side_entries] slot in `part`
     const int32_t *sd_gid;         // [n_side] global target
     const int32_t *sd_part;        // [n_side+1] partial ranges
@@ -119,15 +131,19 @@ namespace ees {
 struct TileHost {
     int32_t n_tiles = 0, n_heavy = 0, n_side = 0;
     std::vector<int32_t> item_ptr, item_dev;
-    std::vector<int32_t> own_ptr, own_gid, own_lst;
-    std::vector<uint16_t> lst, slst;
+    std::vector<int64_t> blob_off;
+    std::vector<uint8_t> blob;
+    std::vector<uint16_t> slst;
     std::vector<int32_t> side_ptr, side_sid, side_lst, side_slot;
     std::vector<int32_t> sd_gid, sd_part;
+    int64_t n_owned = 0;
 };
 // ees_tile.cpp
 bool build_tile_host(int64_t N, int32_t n_nodes, int32_t n, int64_t nnz, const int32_t *const TT[4],
                      const int32_t *raw_slot, const std::vector<int64_t> &iptr,
-                     const std::vector<int32_t> &idev, const std::vector<int32_t> &rails, TileHost &out);
+                     const std::vector<int32_t> &idev, const std::vector<int32_t> &rails,
+                     const std::vector<int32_t> &row_ptr, const std::vector<int32_t> &col_idx,
+                     TileHost &out);
 #endif
 
 // ---- launchers (ees_kernels.cu); all asynchronous on `st` ----

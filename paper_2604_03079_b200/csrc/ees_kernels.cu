@@ -635,78 +635,186 @@ cudaError_t launch_count_conflicts(const int32_t *cnt, int64_t n, unsigned long 
 }
 
 // ---------------------------------------------------------------------------
-// TILE (deterministic, one launch): one CTA per row tile.  Phase 1: every
-// item (FET copy) is evaluated and its 16 contributions are staged in shared
-// memory.  Phase 2: each owned target (A entry or b row whose contributors all
-// belong to this tile) sums its slot list in list order and does a plain RMW
-// -- no other CTA touches it.  Phase 3: targets shared by several tiles
-// (heavy x heavy entries: rails, hubs) -- one warp per (tile, target) sums the
-// tile's part (fixed lane stride + shuffle tree), stores it, and the warp that
-// brings the target's arrival counter to its part count sums all parts in
-// part order and applies the result.
+// TILE (deterministic, one launch): one CTA per row tile.
+//  0. thread 0 starts a TMA bulk copy (cp.async.bulk + mbarrier) of the tile's
+//     owned-target program (runs, list starts, slot lists) into shared memory;
+//  1. every thread evaluates one item (FET copy) and stages its 16
+//     contributions in shared memory; meanwhile, once the program has landed,
+//     each thread prefetches the current A/b values of the targets it owns;
+//  2. each owned target (all contributors in this tile) sums its slot list in
+//     list order and stores value + sum -- a plain store, no other CTA writes it;
+//  3. targets shared by several tiles (heavy x heavy entries: rails, hubs):
+//     one thread per (tile, target) sums the tile's part and stores it; the
+//     thread that brings the target's arrival counter to its part count has
+//     its warp sum all parts in part order (fixed lane stride + shuffle tree)
+//     and apply the result, then resets the counter.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kTileThreads) k_tile(TileK tk, CallK P)
+__device__ __forceinline__ uint32_t smem_u32(const void *p)
 {
-    extern __shared__ double s_c[];   // [16][kTileItems]
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void tma_bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar)
+{
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase)
+{
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "EES_WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra EES_WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+
+constexpr size_t kTileSmem = sizeof(double) * 16 * kTileItems + kBlobMax;
+
+__global__ void __launch_bounds__(kTileThreads, 4) k_tile(TileK tk, CallK P)
+{
+    extern __shared__ __align__(16) unsigned char smem[];
+    double *s_c = reinterpret_cast<double *>(smem);                 // [16][kTileItems]
+    unsigned char *s_blob = smem + sizeof(double) * 16 * kTileItems;
     __shared__ CardK s_cards[EES_MAX_MODELS];
-    for (int k = threadIdx.x; k < P.n_models; k += blockDim.x) s_cards[k] = P.cards[k];
-    __syncthreads();
+    __shared__ __align__(8) uint64_t s_bar;
     const int t = blockIdx.x;
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        const int64_t off = tk.blob_off[t];
+        const uint32_t bytes = (uint32_t)(tk.blob_off[t + 1] - off);
+        mbar_init(&s_bar, 1);
+        mbar_expect_tx(&s_bar, bytes);
+        tma_bulk_g2s(s_blob, tk.blob + off, bytes, &s_bar);
+    }
+    for (int k = tid; k < P.n_models; k += blockDim.x) s_cards[k] = P.cards[k];
+    // phase 1 loads (item = thread)
     const int32_t i0 = tk.item_ptr[t], ni = tk.item_ptr[t + 1] - i0;
-    for (int it = threadIdx.x; it < ni; it += blockDim.x) {
-        const int64_t i = i0 + it;
-        const int4 T = __ldg(tk.term + i);
-        const double beta = __ldg(tk.beta + i);
-        const double a0 = __ldg(tk.v0 + i);
-        const double a1 = __ldg(tk.v0 + tk.n_items + i);
-        const double a2 = __ldg(tk.v0 + 2 * tk.n_items + i);
-        const int m = __ldg(tk.model + i);
+    const bool has_item = tid < ni;
+    int4 T = make_int4(-1, -1, -1, -1);
+    double beta = 0, a0 = 0, a1 = 0, a2 = 0;
+    int m = 0;
+    if (has_item) {
+        const int64_t i = i0 + tid;
+        T = __ldg(tk.term + i);
+        beta = __ldg(tk.beta + i);
+        a0 = __ldg(tk.v0 + i);
+        a1 = __ldg(tk.v0 + tk.n_items + i);
+        a2 = __ldg(tk.v0 + 2 * tk.n_items + i);
+        m = __ldg(tk.model + i);
+    }
+    __syncthreads();                       // mbarrier init + cards visible
+    // program landed -> prefetch the A/b values this thread owns
+    mbar_wait(&s_bar, 0);
+    const TileHdr hdr = *reinterpret_cast<const TileHdr *>(s_blob);
+    const int2 *runs = reinterpret_cast<const int2 *>(s_blob + sizeof(TileHdr));
+    const uint16_t *lstart = reinterpret_cast<const uint16_t *>(runs + hdr.n_runs);
+    const uint16_t *lst = lstart + hdr.n_own + 1;
+    int32_t gid[kTilePrefetch];
+    double pre[kTilePrefetch];
+    {
+        int r = 0, rbase = 0;
+#pragma unroll
+        for (int k = 0; k < kTilePrefetch; k++) {
+            const int j = tid + k * kTileThreads;
+            gid[k] = -1;
+            pre[k] = 0.0;
+            if (j < hdr.n_own) {
+                while (j >= rbase + runs[r].y) { rbase += runs[r].y; r++; }
+                const int32_t g = runs[r].x + (j - rbase);
+                gid[k] = g;
+                pre[k] = g < tk.nnz ? P.A[g] : P.b[g - tk.nnz];
+            }
+        }
+    }
+    if (has_item) {
         const double VD = T.x >= 0 ? __ldg(P.x + T.x) : 0.0;
         const double VG = T.y >= 0 ? __ldg(P.x + T.y) : 0.0;
         const double VS = T.z >= 0 ? __ldg(P.x + T.z) : 0.0;
         Stamp st;
         eval_fet(s_cards[m], beta, P.gmin, VD, VG, VS, a0, a1, a2, st);
 #pragma unroll
-        for (int p = 0; p < NPAIR; p++) s_c[p * kTileItems + it] = st.y[p];
+        for (int p = 0; p < NPAIR; p++) s_c[p * kTileItems + tid] = st.y[p];
 #pragma unroll
-        for (int a = 0; a < 4; a++) s_c[(NPAIR + a) * kTileItems + it] = st.j[a];
+        for (int a = 0; a < 4; a++) s_c[(NPAIR + a) * kTileItems + tid] = st.j[a];
     }
     __syncthreads();
-    const int32_t o1 = tk.own_ptr[t + 1];
-    for (int32_t j = tk.own_ptr[t] + threadIdx.x; j < o1; j += blockDim.x) {
-        const int32_t g = __ldg(tk.own_gid + j);
-        const int32_t l0 = __ldg(tk.own_lst + j), l1 = __ldg(tk.own_lst + j + 1);
-        double s = 0.0;
-        for (int32_t l = l0; l < l1; l++) s += s_c[__ldg(tk.lst + l)];
-        if (g < tk.nnz) P.A[g] += s;
-        else P.b[g - tk.nnz] += s;
+    // phase 2: owned targets
+#pragma unroll
+    for (int k = 0; k < kTilePrefetch; k++) {
+        const int j = tid + k * kTileThreads;
+        if (j < hdr.n_own) {
+            double s = 0.0;
+            for (int l = lstart[j]; l < lstart[j + 1]; l++) s += s_c[lst[l]];
+            const int32_t g = gid[k];
+            if (g < tk.nnz) P.A[g] = pre[k] + s;
+            else P.b[g - tk.nnz] = pre[k] + s;
+        }
     }
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    const int32_t e1 = tk.side_ptr[t + 1];
-    for (int32_t e = tk.side_ptr[t] + warp; e < e1; e += nw) {
-        const int32_t l0 = __ldg(tk.side_lst + e), l1 = __ldg(tk.side_lst + e + 1);
-        double v = 0.0;
-        for (int32_t l = l0 + lane; l < l1; l += 32) v += s_c[__ldg(tk.slst + l)];
-        v = warp_sum(v);
-        const int32_t sid = __ldg(tk.side_sid + e);
-        const int32_t p0 = __ldg(tk.sd_part + sid), p1 = __ldg(tk.sd_part + sid + 1);
-        int last = 0;
-        if (lane == 0) {
+    if (hdr.n_own > kTilePrefetch * kTileThreads) {
+        int r = 0, rbase = 0;
+        for (int j = tid + kTilePrefetch * kTileThreads; j < hdr.n_own; j += kTileThreads) {
+            while (j >= rbase + runs[r].y) { rbase += runs[r].y; r++; }
+            const int32_t g = runs[r].x + (j - rbase);
+            double s = 0.0;
+            for (int l = lstart[j]; l < lstart[j + 1]; l++) s += s_c[lst[l]];
+            if (g < tk.nnz) P.A[g] += s;
+            else P.b[g - tk.nnz] += s;
+        }
+    }
+    // phase 3: side entries, one thread each; warp-cooperative finish
+    const int lane = tid & 31;
+    const int32_t e0 = tk.side_ptr[t], e1 = tk.side_ptr[t + 1];
+    for (int32_t eb = e0 + (tid & ~31); eb < e1; eb += kTileThreads) {
+        const int32_t e = eb + lane;
+        const bool valid = e < e1;
+        int32_t sid = 0, p0 = 0, p1 = 0;
+        bool last = false;
+        if (valid) {
+            const int32_t l0 = __ldg(tk.side_lst + e), l1 = __ldg(tk.side_lst + e + 1);
+            double v = 0.0;
+            for (int32_t l = l0; l < l1; l++) v += s_c[__ldg(tk.slst + l)];
+            sid = __ldg(tk.side_sid + e);
+            p0 = __ldg(tk.sd_part + sid);
+            p1 = __ldg(tk.sd_part + sid + 1);
             tk.part[__ldg(tk.side_slot + e)] = v;
             __threadfence();
             last = atomicAdd(tk.sd_cnt + sid, 1) == (p1 - p0) - 1;
         }
-        last = __shfl_sync(0xffffffffu, last, 0);
-        if (last) {
-            __threadfence();
+        unsigned mask = __ballot_sync(0xffffffffu, last);
+        if (mask) __threadfence();
+        while (mask) {
+            const int src = __ffs(mask) - 1;
+            mask &= mask - 1;
+            const int32_t s_sid = __shfl_sync(0xffffffffu, sid, src);
+            const int32_t q0 = __shfl_sync(0xffffffffu, p0, src);
+            const int32_t q1 = __shfl_sync(0xffffffffu, p1, src);
             double u = 0.0;
-            for (int32_t q = p0 + lane; q < p1; q += 32) u += __ldcg(tk.part + q);
+            for (int32_t q = q0 + lane; q < q1; q += 32) u += __ldcg(tk.part + q);
             u = warp_sum(u);
             if (lane == 0) {
-                const int32_t g = __ldg(tk.sd_gid + sid);
+                const int32_t g = __ldg(tk.sd_gid + s_sid);
                 if (g < tk.nnz) P.A[g] += u;
                 else P.b[g - tk.nnz] += u;
-                tk.sd_cnt[sid] = 0;
+                tk.sd_cnt[s_sid] = 0;
             }
         }
     }
@@ -716,12 +824,11 @@ cudaError_t launch_tile(const TileK &tk, const CallK &call, cudaStream_t st)
 {
     if (tk.n_tiles == 0) return cudaSuccess;
     static bool attr = false;
-    const size_t smem = sizeof(double) * 16 * kTileItems;
     if (!attr) {
-        cudaFuncSetAttribute(k_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmem);
         attr = true;
     }
-    k_tile<<<tk.n_tiles, kTileThreads, smem, st>>>(tk, call);
+    k_tile<<<tk.n_tiles, kTileThreads, kTileSmem, st>>>(tk, call);
     return cudaPeekAtLastError();
 }
 

@@ -12,6 +12,7 @@
 // writers collide only through shared nodes) applied per SM instead of per
 // colour.
 #include <algorithm>
+#include <cstring>
 #include <numeric>
 #include <vector>
 
@@ -22,65 +23,120 @@ namespace ees {
 namespace {
 constexpr int32_t kUnset = -1;
 constexpr int32_t kSide = -2;
+// owned targets per tile such that the blob fits kBlobMax even with one run
+// per target: 16 + 8*R + 2*(own+1) + 2*16*kTileItems <= kBlobMax, R <= own
+constexpr int64_t kOwnMax = (kBlobMax - 16 - 2 - 2 * 16 * kTileItems) / 10;
 }  // namespace
 
 bool build_tile_host(int64_t N, int32_t n_nodes, int32_t n, int64_t nnz, const int32_t *const TT[4],
                      const int32_t *raw_slot, const std::vector<int64_t> &iptr,
-                     const std::vector<int32_t> &idev, const std::vector<int32_t> &rails, TileHost &out)
+                     const std::vector<int32_t> &idev, const std::vector<int32_t> &rails,
+                     const std::vector<int32_t> &row_ptr, const std::vector<int32_t> &col_idx,
+                     TileHost &out)
 {
+    static_assert(kOwnMax > 64, "tile budget too small");
     out = TileHost();
-    std::vector<uint8_t> heavy((size_t)std::max(1, n_nodes), 0);
+    const int32_t NN = std::max(1, n_nodes);
+    std::vector<uint8_t> heavy((size_t)NN, 0);
     for (int32_t v = 0; v < n_nodes; v++) heavy[v] = (iptr[v + 1] - iptr[v]) > kHeavyDeg;
     for (int32_t r : rails) heavy[r] = 1;
-    out.n_heavy = 0;
     for (int32_t v = 0; v < n_nodes; v++) out.n_heavy += heavy[v];
 
-    // ---- tiles of consecutive light rows, <= kTileItems incident FETs each
-    std::vector<int32_t> tile_of_row((size_t)std::max(1, n_nodes), -1);
+    // heavy-row entries (h, c) with c a light node belong to c's tile
+    std::vector<int32_t> hs_ptr((size_t)NN + 1, 0), hs_k;
+    for (int32_t h = 0; h < n_nodes; h++)
+        if (heavy[h])
+            for (int32_t k = row_ptr[h]; k < row_ptr[h + 1]; k++) {
+                const int32_t c = col_idx[k];
+                if (c < n_nodes && !heavy[c]) hs_ptr[c + 1]++;
+            }
+    for (int32_t v = 0; v < n_nodes; v++) hs_ptr[v + 1] += hs_ptr[v];
+    hs_k.resize((size_t)hs_ptr[n_nodes]);
+    {
+        std::vector<int32_t> fill(hs_ptr.begin(), hs_ptr.end() - 1);
+        for (int32_t h = 0; h < n_nodes; h++)
+            if (heavy[h])
+                for (int32_t k = row_ptr[h]; k < row_ptr[h + 1]; k++) {
+                    const int32_t c = col_idx[k];
+                    if (c < n_nodes && !heavy[c]) hs_k[fill[c]++] = k;
+                }
+    }
+    // heavy x heavy contributions of a FET (owned by its home tile or side)
+    auto hh_count = [&](int64_t i) {
+        int32_t k = 0;
+        for (int p = 0; p < NPAIR; p++)
+            if (raw_slot[p * N + i] >= 0 && heavy[TT[pair_row(p)][i]] && heavy[TT[pair_col(p)][i]]) k++;
+        for (int a = 0; a < 4; a++)
+            if (TT[a][i] >= 0 && heavy[TT[a][i]]) k++;
+        return k;
+    };
+
+    // ---- tiles of consecutive light rows: <= kTileItems FETs, <= kOwnMax targets
+    std::vector<int32_t> tile_of_row((size_t)NN, -1);
     std::vector<int32_t> mark((size_t)std::max<int64_t>(1, N), -1);
-    std::vector<int32_t> cur;
+    std::vector<int32_t> home((size_t)std::max<int64_t>(1, N), -1);
+    std::vector<int32_t> cur, tile_rows_ptr{0}, tile_rows;
     out.item_ptr.push_back(0);
     int32_t t = 0;
+    int64_t own = 0;
     auto close_tile = [&]() {
         std::sort(cur.begin(), cur.end());
         out.item_dev.insert(out.item_dev.end(), cur.begin(), cur.end());
         out.item_ptr.push_back((int32_t)out.item_dev.size());
+        tile_rows_ptr.push_back((int32_t)tile_rows.size());
         cur.clear();
+        own = 0;
         t++;
     };
     for (int32_t v = 0; v < n_nodes; v++) {
         if (heavy[v]) continue;
-        int32_t fresh = 0;
-        for (int64_t k = iptr[v]; k < iptr[v + 1]; k++) fresh += mark[idev[k]] != t;
-        if (!cur.empty() && (int64_t)cur.size() + fresh > kTileItems) close_tile();
-        tile_of_row[v] = t;
-        for (int64_t k = iptr[v]; k < iptr[v + 1]; k++)
-            if (mark[idev[k]] != t) {
-                mark[idev[k]] = t;
-                cur.push_back(idev[k]);
+        for (int pass = 0; pass < 2; pass++) {
+            int32_t fresh = 0;
+            int64_t add = (row_ptr[v + 1] - row_ptr[v]) + 1 + (hs_ptr[v + 1] - hs_ptr[v]);
+            for (int64_t k = iptr[v]; k < iptr[v + 1]; k++) {
+                const int32_t i = idev[k];
+                if (mark[i] != t) fresh++;
+                if (home[i] < 0) add += hh_count(i);
             }
+            const bool over = (int64_t)cur.size() + fresh > kTileItems || own + add > kOwnMax;
+            if (over && pass == 0 && !cur.empty()) {
+                close_tile();
+                continue;
+            }
+            if (over) return false;        // a single light row exceeds a tile
+            own += add;
+            break;
+        }
+        tile_of_row[v] = t;
+        tile_rows.push_back(v);
+        for (int64_t k = iptr[v]; k < iptr[v + 1]; k++) {
+            const int32_t i = idev[k];
+            if (mark[i] != t) {
+                mark[i] = t;
+                cur.push_back(i);
+            }
+            if (home[i] < 0) home[i] = t;
+        }
     }
     if (!cur.empty()) close_tile();
     // FETs with no light terminal (all heavy or ground): orphan tiles
     for (int64_t i = 0; i < N; i++)
-        if (mark[i] < 0) {
+        if (home[i] < 0) {
+            const int32_t add = hh_count(i);
+            if (!cur.empty() && ((int64_t)cur.size() + 1 > kTileItems || own + add > kOwnMax)) close_tile();
+            home[i] = t;
+            own += add;
             cur.push_back((int32_t)i);
-            if ((int64_t)cur.size() == kTileItems) close_tile();
         }
     if (!cur.empty()) close_tile();
     const int32_t T = t;
     out.n_tiles = T;
     if ((int64_t)out.item_dev.size() > INT32_MAX) return false;
 
-    // home tile of each FET = first tile holding it (side contributions come from there)
-    std::vector<int32_t> home((size_t)std::max<int64_t>(1, N), -1);
-    for (int32_t tt = 0; tt < T; tt++)
-        for (int32_t q = out.item_ptr[tt]; q < out.item_ptr[tt + 1]; q++)
-            if (home[out.item_dev[q]] < 0) home[out.item_dev[q]] = tt;
-
     // heavy x heavy targets: owned by the common home tile of all contributors, else side
     const int64_t NT = nnz + n;
     std::vector<int32_t> hh_owner((size_t)NT, kUnset);
+    std::vector<std::vector<int32_t>> hh_of_tile((size_t)T);
     auto note_hh = [&](int64_t g, int32_t h) {
         int32_t &o = hh_owner[g];
         if (o == kUnset) o = h;
@@ -89,24 +145,40 @@ bool build_tile_host(int64_t N, int32_t n_nodes, int32_t n, int64_t nnz, const i
     for (int64_t i = 0; i < N; i++) {
         for (int p = 0; p < NPAIR; p++) {
             const int32_t k = raw_slot[p * N + i];
-            if (k < 0) continue;
-            if (heavy[TT[pair_row(p)][i]] && heavy[TT[pair_col(p)][i]]) note_hh(k, home[i]);
+            if (k >= 0 && heavy[TT[pair_row(p)][i]] && heavy[TT[pair_col(p)][i]]) note_hh(k, home[i]);
         }
         for (int a = 0; a < 4; a++) {
             const int32_t r = TT[a][i];
             if (r >= 0 && heavy[r]) note_hh(nnz + r, home[i]);
         }
     }
+    for (int64_t g = 0; g < NT; g++)
+        if (hh_owner[g] >= 0) hh_of_tile[hh_owner[g]].push_back((int32_t)g);
 
-    // ---- per tile: owned lists and side entries
+    // ---- per tile: blob (owned program) and side entries
     std::vector<int32_t> sid_of((size_t)NT, -1);
-    std::vector<std::pair<int32_t, uint16_t>> own, side;
-    out.own_ptr.push_back(0);
-    out.own_lst.push_back(0);
+    std::vector<std::pair<int32_t, uint16_t>> con, side;
+    std::vector<int32_t> gids;
+    std::vector<std::pair<int32_t, int32_t>> runs;
+    std::vector<uint16_t> lstart, lst;
+    out.blob_off.push_back(0);
     out.side_ptr.push_back(0);
     out.side_lst.push_back(0);
+    int64_t listed = 0;
     for (int32_t tt = 0; tt < T; tt++) {
-        own.clear();
+        // owned targets, ascending
+        gids.clear();
+        for (int32_t q = tile_rows_ptr[tt]; q < tile_rows_ptr[tt + 1]; q++) {
+            const int32_t r = tile_rows[q];
+            for (int32_t k = row_ptr[r]; k < row_ptr[r + 1]; k++) gids.push_back(k);
+            gids.push_back((int32_t)(nnz + r));
+            for (int32_t k = hs_ptr[r]; k < hs_ptr[r + 1]; k++) gids.push_back(hs_k[k]);
+        }
+        gids.insert(gids.end(), hh_of_tile[tt].begin(), hh_of_tile[tt].end());
+        std::sort(gids.begin(), gids.end());
+        if ((int64_t)gids.size() > kOwnMax) return false;
+        // contributions of this tile's items
+        con.clear();
         side.clear();
         const int32_t q0 = out.item_ptr[tt];
         for (int32_t q = q0; q < out.item_ptr[tt + 1]; q++) {
@@ -130,9 +202,9 @@ bool build_tile_host(int64_t N, int32_t n_nodes, int32_t n, int64_t nnz, const i
                 const uint16_t slot = (uint16_t)(p * kTileItems + loc);
                 if (!heavy[r] || !heavy[c]) {
                     const int32_t owner = !heavy[r] ? tile_of_row[r] : tile_of_row[c];
-                    if (owner == tt) own.emplace_back((int32_t)g, slot);
+                    if (owner == tt) con.emplace_back((int32_t)g, slot);
                 } else if (home[i] == tt) {
-                    if (hh_owner[g] == tt) own.emplace_back((int32_t)g, slot);
+                    if (hh_owner[g] == tt) con.emplace_back((int32_t)g, slot);
                     else side.emplace_back((int32_t)g, slot);
                 }
             }
@@ -140,17 +212,49 @@ bool build_tile_host(int64_t N, int32_t n_nodes, int32_t n, int64_t nnz, const i
         auto by_target = [](const std::pair<int32_t, uint16_t> &a, const std::pair<int32_t, uint16_t> &b) {
             return a.first < b.first;
         };
-        std::stable_sort(own.begin(), own.end(), by_target);
+        std::stable_sort(con.begin(), con.end(), by_target);
         std::stable_sort(side.begin(), side.end(), by_target);
-        for (size_t k = 0; k < own.size(); k++) {
-            if (k == 0 || own[k].first != own[k - 1].first) {
-                if (k) out.own_lst.push_back((int32_t)out.lst.size());
-                out.own_gid.push_back(own[k].first);
-            }
-            out.lst.push_back(own[k].second);
+        // lists in owned-target order; runs of consecutive global ids
+        lstart.assign(1, 0);
+        lst.clear();
+        runs.clear();
+        size_t ci = 0;
+        for (size_t j = 0; j < gids.size(); j++) {
+            const int32_t g = gids[j];
+            if (ci < con.size() && con[ci].first < g) return false;   // contribution without an owned slot
+            while (ci < con.size() && con[ci].first == g) lst.push_back(con[ci++].second);
+            lstart.push_back((uint16_t)lst.size());
+            if (!runs.empty() && runs.back().first + runs.back().second == g) runs.back().second++;
+            else runs.emplace_back(g, 1);
         }
-        if (!own.empty()) out.own_lst.push_back((int32_t)out.lst.size());
-        out.own_ptr.push_back((int32_t)out.own_gid.size());
+        if (ci != con.size()) return false;
+        listed += (int64_t)lst.size();
+        TileHdr hdr;
+        hdr.n_items = (uint16_t)(out.item_ptr[tt + 1] - q0);
+        hdr.n_own = (uint16_t)gids.size();
+        hdr.n_runs = (uint16_t)runs.size();
+        hdr.n_lst = (uint16_t)lst.size();
+        size_t bytes = sizeof(TileHdr) + 8 * runs.size() + 2 * lstart.size() + 2 * lst.size();
+        bytes = (bytes + 15) & ~(size_t)15;
+        if (bytes > (size_t)kBlobMax) return false;
+        hdr.bytes = (uint32_t)bytes;
+        hdr.pad = 0;
+        const size_t base = out.blob.size();
+        out.blob.resize(base + bytes, 0);
+        uint8_t *bp = out.blob.data() + base;
+        std::memcpy(bp, &hdr, sizeof(hdr));
+        bp += sizeof(hdr);
+        for (auto &rn : runs) {
+            const int32_t v2[2] = {rn.first, rn.second};
+            std::memcpy(bp, v2, 8);
+            bp += 8;
+        }
+        std::memcpy(bp, lstart.data(), 2 * lstart.size());
+        bp += 2 * lstart.size();
+        if (!lst.empty()) std::memcpy(bp, lst.data(), 2 * lst.size());
+        out.blob_off.push_back((int64_t)out.blob.size());
+        out.n_owned += (int64_t)gids.size();
+        // side entries
         for (size_t k = 0; k < side.size(); k++) {
             if (k == 0 || side[k].first != side[k - 1].first) {
                 if (k) out.side_lst.push_back((int32_t)out.slst.size());
@@ -165,7 +269,7 @@ bool build_tile_host(int64_t N, int32_t n_nodes, int32_t n, int64_t nnz, const i
         }
         if (!side.empty()) out.side_lst.push_back((int32_t)out.slst.size());
         out.side_ptr.push_back((int32_t)out.side_sid.size());
-        if (out.lst.size() > (size_t)INT32_MAX || out.slst.size() > (size_t)INT32_MAX) return false;
+        if (out.slst.size() > (size_t)INT32_MAX) return false;
     }
     // every live contribution is listed exactly once (owned or side)
     {
@@ -173,7 +277,7 @@ bool build_tile_host(int64_t N, int32_t n_nodes, int32_t n, int64_t nnz, const i
         for (int64_t k = 0; k < NPAIR * N; k++) live += raw_slot[k] >= 0;
         for (int64_t i = 0; i < N; i++)
             for (int a = 0; a < 4; a++) live += TT[a][i] >= 0;
-        if ((int64_t)(out.lst.size() + out.slst.size()) != live) return false;
+        if (listed + (int64_t)out.slst.size() != live) return false;
     }
     // partial slots: per side target, its entries in tile order
     out.n_side = (int32_t)out.sd_gid.size();
