@@ -157,12 +157,16 @@ ees_status ees_colors(const ees_ctx *ctx, const int32_t **color, int32_t *n_colo
 ees_status ees_eval_stamp(ees_ctx *ctx, const double *x, double h, double *A_vals, double *b,
                           ees_stream stream);
 
-/* Same with HOST arrays (x [n] in; A_vals [nnz] and b [n] in/out, accumulate):
- * copies x, A_vals, b to the device, runs ees_eval_stamp, copies A_vals and b
- * back and synchronises `stream` before returning.  Page-locked host memory
- * gives full copy bandwidth. */
+/* Same with HOST arrays: copies x (and, unless EES_HOST_ASSIGN, A_vals and b)
+ * to the device, runs ees_eval_stamp, copies A_vals and b back and
+ * synchronises `stream` before returning.
+ *   flags = 0                accumulate: A_vals [nnz], b [n] in/out (+=)
+ *   flags = EES_HOST_ASSIGN  assign: A_vals = stamps, b = stamps (outputs only;
+ *                            the device copies are cleared instead of uploaded)
+ * Page-locked host memory gives full copy bandwidth. */
+enum { EES_HOST_ASSIGN = 1 };
 ees_status ees_eval_stamp_host(ees_ctx *ctx, const double *x, double h, double *A_vals,
-                               double *b, ees_stream stream);
+                               double *b, ees_stream stream, int32_t flags);
 
 /* Choose the variant later calls run (EES_AUTO = the one setup measured fastest). */
 ees_status ees_set_variant(ees_ctx *ctx, int32_t variant);

@@ -20,6 +20,7 @@ EES_AUTO, EES_COLOR, EES_ATOMIC, EES_GATHER, EES_TILE = 0, 1, 2, 3, 4
 EES_CONFLICT_EXCLUDE_RAILS, EES_CONFLICT_PAPER = 0, 1
 EES_MAX_MODELS, EES_MAX_RAILS = 16, 8
 EES_SETUP_HOST_ONLY = 1
+EES_HOST_ASSIGN = 1
 
 P = C.c_void_p
 i32, i64, f64 = C.c_int32, C.c_int64, C.c_double
@@ -54,7 +55,7 @@ lib.ees_pattern.argtypes = [P, C.POINTER(i32), C.POINTER(i64), C.POINTER(P), C.P
 lib.ees_find_slot.argtypes = [P, i32, i32, C.POINTER(i64)]
 lib.ees_colors.argtypes = [P, C.POINTER(P), C.POINTER(i32)]
 lib.ees_eval_stamp.argtypes = [P, P, f64, P, P, P]
-lib.ees_eval_stamp_host.argtypes = [P, P, f64, P, P, P]
+lib.ees_eval_stamp_host.argtypes = [P, P, f64, P, P, P, i32]
 lib.ees_set_variant.argtypes = [P, i32]
 lib.ees_stats.argtypes = [P, C.POINTER(ees_stats_t)]
 lib.ees_set_timing.argtypes = [P, i32]

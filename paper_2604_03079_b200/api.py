@@ -136,8 +136,9 @@ class Context:
                                     C.c_void_p(A.data_ptr()), C.c_void_p(b.data_ptr()),
                                     C.c_void_p(sh)), "ees_eval_stamp")
 
-    def eval_stamp_host(self, x, h, A, b, stream=None):
-        """Host-buffer form (numpy float64 or pinned CPU tensors); blocking."""
+    def eval_stamp_host(self, x, h, A, b, stream=None, assign=False):
+        """Host-buffer form (numpy float64 or pinned CPU tensors); blocking.
+        assign=True: A, b are outputs only (A = stamps, no upload)."""
         def ptr(t, n, name):
             if isinstance(t, np.ndarray):
                 if t.dtype != np.float64 or not t.flags.c_contiguous or t.size != n:
@@ -152,7 +153,8 @@ class Context:
             sh = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
         _check(L.lib.ees_eval_stamp_host(self._h, ptr(x, self.n, "x"), float(h),
                                          ptr(A, self.nnz, "A"), ptr(b, self.n, "b"),
-                                         C.c_void_p(sh)), "ees_eval_stamp_host")
+                                         C.c_void_p(sh), L.EES_HOST_ASSIGN if assign else 0),
+               "ees_eval_stamp_host")
 
     def race_probe(self, color=None):
         cp = None

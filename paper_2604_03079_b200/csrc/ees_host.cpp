@@ -925,8 +925,9 @@ ees_status ees_eval_stamp(ees_ctx *c, const double *x, double h, double *A, doub
 }
 
 ees_status ees_eval_stamp_host(ees_ctx *c, const double *x, double h, double *A, double *b,
-                               ees_stream stream)
+                               ees_stream stream, int32_t flags)
 {
+    if (flags & ~EES_HOST_ASSIGN) return EES_EINVAL;
     if (!c) return EES_EINVAL;
     if (!(h > 0.0)) return EES_EINVAL;
     if (c->host_only) return EES_ESTATE;
@@ -939,8 +940,13 @@ ees_status ees_eval_stamp_host(ees_ctx *c, const double *x, double h, double *A,
     cudaStream_t st = (cudaStream_t)stream;
     const size_t bn = sizeof(double) * (size_t)c->n, ba = sizeof(double) * (size_t)c->nnz;
     if (cudaMemcpyAsync(c->hx, x, bn, cudaMemcpyHostToDevice, st) != cudaSuccess) return EES_ECUDA;
-    if (cudaMemcpyAsync(c->hA, A, ba, cudaMemcpyHostToDevice, st) != cudaSuccess) return EES_ECUDA;
-    if (cudaMemcpyAsync(c->hb, b, bn, cudaMemcpyHostToDevice, st) != cudaSuccess) return EES_ECUDA;
+    if (flags & EES_HOST_ASSIGN) {
+        if (cudaMemsetAsync(c->hA, 0, ba, st) != cudaSuccess) return EES_ECUDA;
+        if (cudaMemsetAsync(c->hb, 0, bn, st) != cudaSuccess) return EES_ECUDA;
+    } else {
+        if (cudaMemcpyAsync(c->hA, A, ba, cudaMemcpyHostToDevice, st) != cudaSuccess) return EES_ECUDA;
+        if (cudaMemcpyAsync(c->hb, b, bn, cudaMemcpyHostToDevice, st) != cudaSuccess) return EES_ECUDA;
+    }
     ees_status s = ees_eval_stamp(c, c->hx, h, c->hA, c->hb, stream);
     if (s != EES_OK) return s;
     if (cudaMemcpyAsync(A, c->hA, ba, cudaMemcpyDeviceToHost, st) != cudaSuccess) return EES_ECUDA;

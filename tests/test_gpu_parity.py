@@ -226,6 +226,10 @@ def test_host_buffer_call_matches(cuda_ok):
         b = np.zeros(ctx.n)
         ctx.eval_stamp_host(nl.x, nl.h, A, b)
         assert_parity(ref, A, b, f"host {v}")
+        A[:] = 7.0                                  # assign form ignores the inputs
+        b[:] = -3.0
+        ctx.eval_stamp_host(nl.x, nl.h, A, b, assign=True)
+        assert_parity(ref, A, b, f"host assign {v}")
 
 
 def test_abi_errors(cuda_ok):
