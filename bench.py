@@ -205,6 +205,62 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def time_calls(ctx, nl, x, A, b, stream, steps, warmup, flush):
+    """Per-call device ms (CUDA events on `stream`), L2 flushed before each."""
+    import torch
+    for k in range(warmup):
+        with torch.cuda.stream(stream):
+            flush.fill_(k & 0xFF)
+            A.zero_(); b.zero_()
+        ctx.eval_stamp(x, nl.h, A, b, stream=stream)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(steps)]
+    torch.cuda.synchronize()
+    for k in range(steps):
+        with torch.cuda.stream(stream):
+            flush.fill_(k & 0xFF)
+            A.zero_(); b.zero_()
+        evs[k][0].record(stream)
+        ctx.eval_stamp(x, nl.h, A, b, stream=stream)
+        evs[k][1].record(stream)
+    torch.cuda.synchronize()
+    return sorted(e0.elapsed_time(e1) for e0, e1 in evs)
+
+
+def run_sweep(args):
+    """B5: gen_synth N FETs as N/C cliques, C = 1..4096; every
+    variant timed per C -> the stamping-variant crossover against the colour
+    count (the GPU analogue of the paper's Fig. 5(c-d))."""
+    import torch
+    from paper_2604_03079_b200 import Context
+    torch.cuda.set_device(0)
+    dev = torch.device("cuda", 0)
+    stream = torch.cuda.Stream()
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
+    out = open(args.sweep_out, "w") if args.sweep_out else None
+    for C in [int(c) for c in args.sweep_c.split(",")]:
+        nl = netgen.gen_synth(args.sweep_n, C)
+        ctx = Context.from_netlist(nl, variant="auto")
+        st = ctx.stats()
+        x = torch.from_numpy(nl.x).to(dev)
+        A = torch.zeros(ctx.nnz, dtype=torch.float64, device=dev)
+        b = torch.zeros(ctx.n, dtype=torch.float64, device=dev)
+        rec = {"C": st["n_colors"], "n_dev": nl.n_dev, "nnz": ctx.nnz, "auto": st["variant_chosen"],
+               "ms": {}}
+        for v in ("color", "atomic", "gather", "tile"):
+            ctx.set_variant(v)
+            steps = args.steps if (v != "color" or C <= 512) else max(3, args.steps // 10)
+            per = time_calls(ctx, nl, x, A, b, stream, steps, 3, flush)
+            rec["ms"][v] = per[len(per) // 2]
+        rec["fet_per_s"] = {v: nl.n_dev / (ms * 1e-3) for v, ms in rec["ms"].items()}
+        line = json.dumps(rec)
+        print(line, flush=True)
+        if out:
+            out.write(line + "\n")
+            out.flush()
+        ctx.close()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -216,10 +272,16 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=10.0)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--sweep", action="store_true", help="B5 colour-count crossover sweep")
+    ap.add_argument("--sweep-n", type=int, default=4_000_000)
+    ap.add_argument("--sweep-c", default="1,2,4,8,16,32,64,128,256,512,1024,2048,4096")
+    ap.add_argument("--sweep-out", default=None)
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     if args.impl == "reference":
         return run_reference(args)
+    if args.sweep:
+        return run_sweep(args)
 
     import torch
     import torch.distributed as dist

@@ -61,6 +61,7 @@ struct ees_ctx {
     std::vector<int64_t> color_blk_off;   // [C+1] block offsets of colours into partials
     double *partials = nullptr;
     int color_coop = 0;                   // 1: persistent cooperative COLOR kernel
+    int tile_grid = 1;                    // persistent TILE CTAs
     int coop_grid = 0;
     int64_t *d_color_ptr = nullptr;
     double *coop_partials = nullptr;
@@ -429,7 +430,7 @@ ees_status enqueue(ees_ctx *c, int32_t variant, const double *x, double h, doubl
         }
     } else if (variant == EES_TILE) {
         PhaseMark m(c, st, 0, timed);
-        e = launch_tile(c->tk, call, st);
+        e = launch_tile(c->tk, call, c->tile_grid, st);
         nl = c->tk.n_tiles ? 1 : 0;
     } else if (variant == EES_GATHER) {
         if (timed) {
@@ -632,53 +633,39 @@ ees_status build_tile(const ees_desc *d, ees_ctx *c, const std::vector<int32_t> 
                       const std::vector<int64_t> &iptr, const std::vector<int32_t> &idev)
 {
     const int32_t *TT[4] = {d->d, d->g, d->s, d->b};
-    TileHost th;
-    if (!build_tile_host(c->n_dev, c->n_nodes, c->n, c->nnz, TT, raw_slot.data(), iptr, idev, c->rails,
-                         c->row_ptr, c->col_idx, th))
-        return EES_EINVAL;
-    const int64_t NI = (int64_t)th.item_dev.size();
-    std::vector<int4> term((size_t)NI);
-    std::vector<double> beta((size_t)NI), v0((size_t)(3 * NI));
-    std::vector<uint8_t> model((size_t)NI);
     const int64_t N = c->n_dev;
-#pragma omp parallel for schedule(static)
-    for (int64_t q = 0; q < NI; q++) {
-        const int32_t i = th.item_dev[q];
+    std::vector<double> beta((size_t)std::max<int64_t>(1, N));
+    for (int64_t i = 0; i < N; i++) {
         const ees_model &m = c->models[d->model[i]];
-        term[q] = make_int4(d->d[i], d->g[i], d->s[i], d->b[i]);
-        beta[q] = (m.kp * d->w[i]) / d->l[i];
-        for (int k = 0; k < 3; k++) v0[k * NI + q] = d->vprev[k * N + i];
-        model[q] = (uint8_t)d->model[i];
+        beta[i] = (m.kp * d->w[i]) / d->l[i];
     }
+    TileHost th;
+    if (!build_tile_host(N, c->n_nodes, c->n, c->nnz, TT, raw_slot.data(), iptr, idev, c->rails,
+                         c->row_ptr, c->col_idx, beta.data(), d->vprev, d->model, th))
+        return EES_EINVAL;
+    c->st.n_tiles = th.n_tiles;
+    c->st.n_heavy_nodes = th.n_heavy;
+    c->st.n_side_targets = th.n_side;
+    c->st.n_tile_items = th.n_items;
+    if (c->host_only) return EES_OK;
     TileK &k = c->tk;
     k.n_tiles = th.n_tiles;
     k.nnz = c->nnz;
-    k.n_items = NI;
     auto up = [&](auto **dst, const auto &vec) {
         using T = typename std::remove_reference<decltype(vec)>::type::value_type;
         return upload(c, const_cast<T **>(dst), vec.data(), vec.size());
     };
-    TRY(up(&k.item_ptr, th.item_ptr));
-    TRY(up(&k.term, term));
-    TRY(up(&k.beta, beta));
-    TRY(up(&k.v0, v0));
-    TRY(up(&k.model, model));
     TRY(up(&k.blob_off, th.blob_off));
     TRY(up(&k.blob, th.blob));
-    TRY(up(&k.side_ptr, th.side_ptr));
-    TRY(up(&k.side_sid, th.side_sid));
-    TRY(up(&k.side_lst, th.side_lst));
-    TRY(up(&k.slst, th.slst));
-    TRY(up(&k.side_slot, th.side_slot));
     TRY(up(&k.sd_gid, th.sd_gid));
     TRY(up(&k.sd_part, th.sd_part));
     TRY(dalloc(c, &k.sd_cnt, (size_t)th.n_side));
     if (cudaMemset(k.sd_cnt, 0, sizeof(int32_t) * std::max(1, th.n_side)) != cudaSuccess) return EES_ECUDA;
-    TRY(dalloc(c, &k.part, th.side_sid.size()));
-    c->st.n_tiles = th.n_tiles;
-    c->st.n_heavy_nodes = th.n_heavy;
-    c->st.n_side_targets = th.n_side;
-    c->st.n_tile_items = NI;
+    TRY(dalloc(c, &k.part, (size_t)th.n_side_entries));
+    int sms = 148, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    c->tile_grid = std::max(1, std::min(th.n_tiles, sms * tile_blocks_per_sm()));
     return EES_OK;
 }
 
@@ -808,17 +795,7 @@ ees_status setup_impl(const ees_desc *d, ees_ctx *c)
         for (int64_t i = 0; i < N; i++)
             nc += (d->d[i] >= 0) + (d->g[i] >= 0) + (d->s[i] >= 0) + (d->b[i] >= 0);
         c->st.n_contributions = nc;
-        {
-            const int32_t *TT[4] = {d->d, d->g, d->s, d->b};
-            TileHost th;
-            if (!build_tile_host(N, c->n_nodes, c->n, c->nnz, TT, raw_slot.data(), iptr, idev, c->rails,
-                                 c->row_ptr, c->col_idx, th))
-                return EES_EINVAL;
-            c->st.n_tiles = th.n_tiles;
-            c->st.n_heavy_nodes = th.n_heavy;
-            c->st.n_side_targets = th.n_side;
-            c->st.n_tile_items = (int64_t)th.item_dev.size();
-        }
+        TRY(build_tile(d, c, raw_slot, iptr, idev));
         c->variant = d->variant == EES_AUTO ? EES_ATOMIC : d->variant;
         c->st.setup_s = now_s() - t0;
         return EES_OK;

@@ -83,41 +83,43 @@ struct GatherK {
 // into tiles; a tile's items are the FETs incident on its rows (boundary FETs
 // are copied into every tile they touch).  Each item's 16 contributions
 // (12 A pairs, 4 b rows) land in shared memory at slot p*kTileItems + item;
-// every owned target sums its slot list (u16) in a fixed order.  A tile's
-// owned-target program is one 16-byte-aligned blob, bulk-copied (TMA,
-// cp.async.bulk) into shared memory while the items are evaluated:
-//   TileHdr | runs[n_runs] (int2: global start, length) |
-//   lstart[n_own+1] (u16) | lst[n_lst] (u16) | pad to 16 B
+// every owned target sums its slot list (u16) in a fixed order.  Everything a
+// tile needs except x and the A/b values is one 16-byte-aligned blob that a
+// TMA bulk copy (cp.async.bulk + mbarrier) brings into shared memory, double
+// buffered across the tiles a persistent CTA processes:
+//   TileHdr
+//   items:   term int4[ni] | beta f64[ni] | v0 f64[3][ni] | model u8[ni] (pad 16)
+//   program: runs int2[n_runs] (global start, length) | lstart u16[n_own+1] |
+//            lst u16[n_lst] (pad 16)
+//   side:    SideEnt[n_sent] | slst u16[n_slst] (pad 16)
 // Local target j maps to global target (A index, or nnz + b row) through the
 // runs; its contributions are lst[lstart[j] .. lstart[j+1]).
 constexpr int kTileItems = 256;      // max items (FET copies) per tile = threads per CTA
 constexpr int kTileThreads = 256;
 constexpr int kHeavyDeg = 64;        // nodes with more incident FETs are heavy
-constexpr int kBlobMax = 20480;      // bytes of shared memory for a tile's program
+constexpr int kStageMax = 36864;     // bytes of one pipeline stage (a tile blob)
 constexpr int kTilePrefetch = 8;     // owned targets whose A/b value a thread prefetches
 
 struct TileHdr {
     uint16_t n_items, n_own, n_runs, n_lst;
+    uint16_t n_sent, n_slst;
     uint32_t bytes;                  // blob size, multiple of 16
+    uint32_t off_prog, off_side;     // byte offsets of the program and side sections
     uint32_t pad;
+};
+static_assert(sizeof(TileHdr) == 28 || sizeof(TileHdr) == 32, "TileHdr layout");
+
+struct SideEnt {
+    int32_t sid;                     // side target
+    int32_t slot;                    // this tile's part slot in `part`
+    uint16_t lbeg, lcnt;             // range in slst
 };
 
 struct TileK {
     int32_t n_tiles;
     int64_t nnz;
-    const int32_t *item_ptr;       // [T+1]
-    const int4 *term;              // [n_items] plain node ids
-    const double *beta;            // [n_items]
-    const double *v0;              // [3][n_items]
-    const uint8_t *model;          // [n_items]
-    int64_t n_items;
     const int64_t *blob_off;       // [T+1] byte offsets into blob
     const uint8_t *blob;
-    const int32_t *side_ptr;       // [T+1] side entries of each tile
-    const int32_t *side_sid;       // [n_side_entries] side target
-    const int32_t *side_lst;       // [n_side_entries+1] list ranges into slst
-    const uint16_t *slst;          // slot lists of side entries
-    const int32_t *side_slot;      // [n_side_entries] slot in `part`
     const int32_t *sd_gid;         // [n_side] global target
     const int32_t *sd_part;        // [n_side+1] partial ranges
     int32_t *sd_cnt;               // [n_side] arrival counters, self-resetting
@@ -130,24 +132,23 @@ struct TileK {
 namespace ees {
 struct TileHost {
     int32_t n_tiles = 0, n_heavy = 0, n_side = 0;
-    std::vector<int32_t> item_ptr, item_dev;
+    int64_t n_items = 0, n_owned = 0, n_side_entries = 0;
     std::vector<int64_t> blob_off;
     std::vector<uint8_t> blob;
-    std::vector<uint16_t> slst;
-    std::vector<int32_t> side_ptr, side_sid, side_lst, side_slot;
     std::vector<int32_t> sd_gid, sd_part;
-    int64_t n_owned = 0;
 };
-// ees_tile.cpp
+// ees_tile.cpp.  Per-FET data for the item sections: beta (computed by the
+// caller exactly as for the other layouts), vprev [3][N], model.
 bool build_tile_host(int64_t N, int32_t n_nodes, int32_t n, int64_t nnz, const int32_t *const TT[4],
                      const int32_t *raw_slot, const std::vector<int64_t> &iptr,
                      const std::vector<int32_t> &idev, const std::vector<int32_t> &rails,
                      const std::vector<int32_t> &row_ptr, const std::vector<int32_t> &col_idx,
-                     TileHost &out);
+                     const double *beta, const double *vprev, const int32_t *model, TileHost &out);
 #endif
 
 // ---- launchers (ees_kernels.cu); all asynchronous on `st` ----
-cudaError_t launch_tile(const TileK &tk, const CallK &call, cudaStream_t st);
+int tile_blocks_per_sm();
+cudaError_t launch_tile(const TileK &tk, const CallK &call, int grid, cudaStream_t st);
 cudaError_t launch_atomic(const DevK &dv, const CallK &call, int grid, cudaStream_t st);
 cudaError_t launch_color(const DevK &dv, const CallK &call, int64_t begin, int64_t count,
                          double *partials, cudaStream_t st);

@@ -687,148 +687,181 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase)
         : "memory");
 }
 
-constexpr size_t kTileSmem = sizeof(double) * 16 * kTileItems + kBlobMax;
+constexpr size_t kTileSmem = sizeof(double) * 16 * kTileItems + 2 * (size_t)kStageMax;
 
-__global__ void __launch_bounds__(kTileThreads, 4) k_tile(TileK tk, CallK P)
+// ---------------------------------------------------------------------------
+// TILE (deterministic, one launch): persistent CTAs walk the tiles
+// blockIdx.x, +gridDim.x, ...  Thread 0 keeps the next tile's blob in flight
+// (TMA bulk copy into the other pipeline stage) while the current one is
+// processed:
+//  1. every thread evaluates one item (FET copy) from shared memory and
+//     stages its 16 contributions in shared memory; in the same window it
+//     prefetches the current A/b values of the targets it owns;
+//  2. each owned target (all contributors in this tile) sums its slot list in
+//     list order and stores value + sum -- no other CTA writes it;
+//  3. side targets (heavy x heavy entries and heavy b rows shared by several
+//     tiles: rails, hubs): one thread per entry stores the tile's part; after
+//     a fence and a barrier each entry bumps its target's arrival counter;
+//     the warp of the last arrival sums all parts in part order (fixed lane
+//     stride + shuffle tree), applies the result and resets the counter.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kTileThreads, 2) k_tile(TileK tk, CallK P)
 {
     extern __shared__ __align__(16) unsigned char smem[];
-    double *s_c = reinterpret_cast<double *>(smem);                 // [16][kTileItems]
-    unsigned char *s_blob = smem + sizeof(double) * 16 * kTileItems;
+    double *s_c = reinterpret_cast<double *>(smem);                       // [16][kTileItems]
+    unsigned char *s_stage = smem + sizeof(double) * 16 * kTileItems;      // [2][kStageMax]
     __shared__ CardK s_cards[EES_MAX_MODELS];
-    __shared__ __align__(8) uint64_t s_bar;
-    const int t = blockIdx.x;
-    const int tid = threadIdx.x;
+    __shared__ __align__(8) uint64_t s_bar[2];
+    const int tid = threadIdx.x, lane = tid & 31;
+    auto issue = [&](int32_t tile, int stage) {
+        const int64_t off = tk.blob_off[tile];
+        const uint32_t bytes = (uint32_t)(tk.blob_off[tile + 1] - off);
+        mbar_expect_tx(&s_bar[stage], bytes);
+        tma_bulk_g2s(s_stage + (size_t)stage * kStageMax, tk.blob + off, bytes, &s_bar[stage]);
+    };
     if (tid == 0) {
-        const int64_t off = tk.blob_off[t];
-        const uint32_t bytes = (uint32_t)(tk.blob_off[t + 1] - off);
-        mbar_init(&s_bar, 1);
-        mbar_expect_tx(&s_bar, bytes);
-        tma_bulk_g2s(s_blob, tk.blob + off, bytes, &s_bar);
+        mbar_init(&s_bar[0], 1);
+        mbar_init(&s_bar[1], 1);
+        if ((int32_t)blockIdx.x < tk.n_tiles) issue(blockIdx.x, 0);
     }
     for (int k = tid; k < P.n_models; k += blockDim.x) s_cards[k] = P.cards[k];
-    // phase 1 loads (item = thread)
-    const int32_t i0 = tk.item_ptr[t], ni = tk.item_ptr[t + 1] - i0;
-    const bool has_item = tid < ni;
-    int4 T = make_int4(-1, -1, -1, -1);
-    double beta = 0, a0 = 0, a1 = 0, a2 = 0;
-    int m = 0;
-    if (has_item) {
-        const int64_t i = i0 + tid;
-        T = __ldg(tk.term + i);
-        beta = __ldg(tk.beta + i);
-        a0 = __ldg(tk.v0 + i);
-        a1 = __ldg(tk.v0 + tk.n_items + i);
-        a2 = __ldg(tk.v0 + 2 * tk.n_items + i);
-        m = __ldg(tk.model + i);
-    }
-    __syncthreads();                       // mbarrier init + cards visible
-    // program landed -> prefetch the A/b values this thread owns
-    mbar_wait(&s_bar, 0);
-    const TileHdr hdr = *reinterpret_cast<const TileHdr *>(s_blob);
-    const int2 *runs = reinterpret_cast<const int2 *>(s_blob + sizeof(TileHdr));
-    const uint16_t *lstart = reinterpret_cast<const uint16_t *>(runs + hdr.n_runs);
-    const uint16_t *lst = lstart + hdr.n_own + 1;
-    int32_t gid[kTilePrefetch];
-    double pre[kTilePrefetch];
-    {
-        int r = 0, rbase = 0;
+    __syncthreads();
+    uint32_t parity[2] = {0, 0};
+    int stage = 0;
+    for (int32_t t = blockIdx.x; t < tk.n_tiles; t += gridDim.x) {
+        const int32_t tn = t + gridDim.x;
+        if (tid == 0 && tn < tk.n_tiles) issue(tn, stage ^ 1);   // freed by the previous iteration's barrier
+        mbar_wait(&s_bar[stage], parity[stage]);
+        parity[stage] ^= 1;
+        const unsigned char *blob = s_stage + (size_t)stage * kStageMax;
+        const TileHdr hdr = *reinterpret_cast<const TileHdr *>(blob);
+        const int ni = hdr.n_items;
+        const unsigned char *items = blob + ((sizeof(TileHdr) + 15) & ~(size_t)15);
+        const int4 *term = reinterpret_cast<const int4 *>(items);
+        const double *beta = reinterpret_cast<const double *>(items + 16 * (size_t)ni);
+        const double *v0 = beta + ni;
+        const uint8_t *model = reinterpret_cast<const uint8_t *>(v0 + 3 * (size_t)ni);
+        const int2 *runs = reinterpret_cast<const int2 *>(blob + hdr.off_prog);
+        const uint16_t *lstart = reinterpret_cast<const uint16_t *>(runs + hdr.n_runs);
+        const uint16_t *lst = lstart + hdr.n_own + 1;
+        // x gather first (longest latency), then the owned A/b values
+        int4 T = make_int4(-1, -1, -1, -1);
+        double VD = 0.0, VG = 0.0, VS = 0.0;
+        if (tid < ni) {
+            T = term[tid];
+            VD = T.x >= 0 ? __ldg(P.x + T.x) : 0.0;
+            VG = T.y >= 0 ? __ldg(P.x + T.y) : 0.0;
+            VS = T.z >= 0 ? __ldg(P.x + T.z) : 0.0;
+        }
+        int32_t gid[kTilePrefetch];
+        double pre[kTilePrefetch];
+        {
+            int r = 0, rbase = 0;
+#pragma unroll
+            for (int k = 0; k < kTilePrefetch; k++) {
+                const int j = tid + k * kTileThreads;
+                gid[k] = -1;
+                pre[k] = 0.0;
+                if (j < hdr.n_own) {
+                    while (j >= rbase + runs[r].y) { rbase += runs[r].y; r++; }
+                    const int32_t g = runs[r].x + (j - rbase);
+                    gid[k] = g;
+                    pre[k] = g < tk.nnz ? P.A[g] : P.b[g - tk.nnz];
+                }
+            }
+        }
+        if (tid < ni) {
+            Stamp st;
+            eval_fet(s_cards[model[tid]], beta[tid], P.gmin, VD, VG, VS, v0[tid], v0[ni + tid],
+                     v0[2 * ni + tid], st);
+#pragma unroll
+            for (int p = 0; p < NPAIR; p++) s_c[p * kTileItems + tid] = st.y[p];
+#pragma unroll
+            for (int a = 0; a < 4; a++) s_c[(NPAIR + a) * kTileItems + tid] = st.j[a];
+        }
+        __syncthreads();
+        // owned targets
 #pragma unroll
         for (int k = 0; k < kTilePrefetch; k++) {
             const int j = tid + k * kTileThreads;
-            gid[k] = -1;
-            pre[k] = 0.0;
             if (j < hdr.n_own) {
+                double s = 0.0;
+                for (int l = lstart[j]; l < lstart[j + 1]; l++) s += s_c[lst[l]];
+                const int32_t g = gid[k];
+                if (g < tk.nnz) P.A[g] = pre[k] + s;
+                else P.b[g - tk.nnz] = pre[k] + s;
+            }
+        }
+        if (hdr.n_own > kTilePrefetch * kTileThreads) {
+            int r = 0, rbase = 0;
+            for (int j = tid + kTilePrefetch * kTileThreads; j < hdr.n_own; j += kTileThreads) {
                 while (j >= rbase + runs[r].y) { rbase += runs[r].y; r++; }
                 const int32_t g = runs[r].x + (j - rbase);
-                gid[k] = g;
-                pre[k] = g < tk.nnz ? P.A[g] : P.b[g - tk.nnz];
+                double s = 0.0;
+                for (int l = lstart[j]; l < lstart[j + 1]; l++) s += s_c[lst[l]];
+                if (g < tk.nnz) P.A[g] += s;
+                else P.b[g - tk.nnz] += s;
             }
         }
-    }
-    if (has_item) {
-        const double VD = T.x >= 0 ? __ldg(P.x + T.x) : 0.0;
-        const double VG = T.y >= 0 ? __ldg(P.x + T.y) : 0.0;
-        const double VS = T.z >= 0 ? __ldg(P.x + T.z) : 0.0;
-        Stamp st;
-        eval_fet(s_cards[m], beta, P.gmin, VD, VG, VS, a0, a1, a2, st);
-#pragma unroll
-        for (int p = 0; p < NPAIR; p++) s_c[p * kTileItems + tid] = st.y[p];
-#pragma unroll
-        for (int a = 0; a < 4; a++) s_c[(NPAIR + a) * kTileItems + tid] = st.j[a];
-    }
-    __syncthreads();
-    // phase 2: owned targets
-#pragma unroll
-    for (int k = 0; k < kTilePrefetch; k++) {
-        const int j = tid + k * kTileThreads;
-        if (j < hdr.n_own) {
-            double s = 0.0;
-            for (int l = lstart[j]; l < lstart[j + 1]; l++) s += s_c[lst[l]];
-            const int32_t g = gid[k];
-            if (g < tk.nnz) P.A[g] = pre[k] + s;
-            else P.b[g - tk.nnz] = pre[k] + s;
-        }
-    }
-    if (hdr.n_own > kTilePrefetch * kTileThreads) {
-        int r = 0, rbase = 0;
-        for (int j = tid + kTilePrefetch * kTileThreads; j < hdr.n_own; j += kTileThreads) {
-            while (j >= rbase + runs[r].y) { rbase += runs[r].y; r++; }
-            const int32_t g = runs[r].x + (j - rbase);
-            double s = 0.0;
-            for (int l = lstart[j]; l < lstart[j + 1]; l++) s += s_c[lst[l]];
-            if (g < tk.nnz) P.A[g] += s;
-            else P.b[g - tk.nnz] += s;
-        }
-    }
-    // phase 3: side entries, one thread each; warp-cooperative finish
-    const int lane = tid & 31;
-    const int32_t e0 = tk.side_ptr[t], e1 = tk.side_ptr[t + 1];
-    for (int32_t eb = e0 + (tid & ~31); eb < e1; eb += kTileThreads) {
-        const int32_t e = eb + lane;
-        const bool valid = e < e1;
-        int32_t sid = 0, p0 = 0, p1 = 0;
-        bool last = false;
-        if (valid) {
-            const int32_t l0 = __ldg(tk.side_lst + e), l1 = __ldg(tk.side_lst + e + 1);
-            double v = 0.0;
-            for (int32_t l = l0; l < l1; l++) v += s_c[__ldg(tk.slst + l)];
-            sid = __ldg(tk.side_sid + e);
-            p0 = __ldg(tk.sd_part + sid);
-            p1 = __ldg(tk.sd_part + sid + 1);
-            tk.part[__ldg(tk.side_slot + e)] = v;
+        // side targets
+        if (hdr.n_sent) {
+            const SideEnt *sents = reinterpret_cast<const SideEnt *>(blob + hdr.off_side);
+            const uint16_t *slst = reinterpret_cast<const uint16_t *>(sents + hdr.n_sent);
+            for (int e = tid; e < hdr.n_sent; e += kTileThreads) {
+                const SideEnt se = sents[e];
+                double v = 0.0;
+                for (int l = se.lbeg; l < se.lbeg + se.lcnt; l++) v += s_c[slst[l]];
+                tk.part[se.slot] = v;
+            }
             __threadfence();
-            last = atomicAdd(tk.sd_cnt + sid, 1) == (p1 - p0) - 1;
-        }
-        unsigned mask = __ballot_sync(0xffffffffu, last);
-        if (mask) __threadfence();
-        while (mask) {
-            const int src = __ffs(mask) - 1;
-            mask &= mask - 1;
-            const int32_t s_sid = __shfl_sync(0xffffffffu, sid, src);
-            const int32_t q0 = __shfl_sync(0xffffffffu, p0, src);
-            const int32_t q1 = __shfl_sync(0xffffffffu, p1, src);
-            double u = 0.0;
-            for (int32_t q = q0 + lane; q < q1; q += 32) u += __ldcg(tk.part + q);
-            u = warp_sum(u);
-            if (lane == 0) {
-                const int32_t g = __ldg(tk.sd_gid + s_sid);
-                if (g < tk.nnz) P.A[g] += u;
-                else P.b[g - tk.nnz] += u;
-                tk.sd_cnt[s_sid] = 0;
+            __syncthreads();
+            for (int eb = tid & ~31; eb < hdr.n_sent; eb += kTileThreads) {
+                const int e = eb + lane;
+                int32_t sid = 0, p0 = 0, p1 = 0;
+                bool last = false;
+                if (e < hdr.n_sent) {
+                    sid = sents[e].sid;
+                    p0 = __ldg(tk.sd_part + sid);
+                    p1 = __ldg(tk.sd_part + sid + 1);
+                    last = atomicAdd(tk.sd_cnt + sid, 1) == (p1 - p0) - 1;
+                }
+                unsigned mask = __ballot_sync(0xffffffffu, last);
+                if (mask) __threadfence();
+                while (mask) {
+                    const int src = __ffs(mask) - 1;
+                    mask &= mask - 1;
+                    const int32_t s_sid = __shfl_sync(0xffffffffu, sid, src);
+                    const int32_t q0 = __shfl_sync(0xffffffffu, p0, src);
+                    const int32_t q1 = __shfl_sync(0xffffffffu, p1, src);
+                    double u = 0.0;
+                    for (int32_t q = q0 + lane; q < q1; q += 32) u += __ldcg(tk.part + q);
+                    u = warp_sum(u);
+                    if (lane == 0) {
+                        const int32_t g = __ldg(tk.sd_gid + s_sid);
+                        if (g < tk.nnz) P.A[g] += u;
+                        else P.b[g - tk.nnz] += u;
+                        tk.sd_cnt[s_sid] = 0;
+                    }
+                }
             }
         }
+        __syncthreads();          // s_c and this stage are reused
+        stage ^= 1;
     }
 }
 
-cudaError_t launch_tile(const TileK &tk, const CallK &call, cudaStream_t st)
+int tile_blocks_per_sm()
+{
+    cudaFuncSetAttribute(k_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmem);
+    int nb = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_tile, kTileThreads, kTileSmem);
+    return nb > 0 ? nb : 1;
+}
+
+cudaError_t launch_tile(const TileK &tk, const CallK &call, int grid, cudaStream_t st)
 {
     if (tk.n_tiles == 0) return cudaSuccess;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmem);
-        attr = true;
-    }
-    k_tile<<<tk.n_tiles, kTileThreads, kTileSmem, st>>>(tk, call);
+    k_tile<<<grid, kTileThreads, kTileSmem, st>>>(tk, call);
     return cudaPeekAtLastError();
 }
 

@@ -23,16 +23,20 @@ namespace ees {
 namespace {
 constexpr int32_t kUnset = -1;
 constexpr int32_t kSide = -2;
-// owned targets per tile such that the blob fits kBlobMax even with one run
-// per target: 16 + 8*R + 2*(own+1) + 2*16*kTileItems <= kBlobMax, R <= own
-constexpr int64_t kOwnMax = (kBlobMax - 16 - 2 - 2 * 16 * kTileItems) / 10;
+// targets per tile (owned + side entries) such that the blob fits one stage
+// even with one run per owned target: header + items (49 B each) + runs (8 B)
+// + list starts (2 B) + side entries (12 B) + lists (<= 16 u16 per item)
+constexpr int64_t kOwnMax =
+    (kStageMax - (int64_t)sizeof(TileHdr) - 48 - 49 * kTileItems - 2 * 16 * kTileItems - 2) / 12;
+
+size_t pad16(size_t x) { return (x + 15) & ~(size_t)15; }
 }  // namespace
 
 bool build_tile_host(int64_t N, int32_t n_nodes, int32_t n, int64_t nnz, const int32_t *const TT[4],
                      const int32_t *raw_slot, const std::vector<int64_t> &iptr,
                      const std::vector<int32_t> &idev, const std::vector<int32_t> &rails,
                      const std::vector<int32_t> &row_ptr, const std::vector<int32_t> &col_idx,
-                     TileHost &out)
+                     const double *beta, const double *vprev, const int32_t *model, TileHost &out)
 {
     static_assert(kOwnMax > 64, "tile budget too small");
     out = TileHost();
@@ -76,13 +80,13 @@ bool build_tile_host(int64_t N, int32_t n_nodes, int32_t n, int64_t nnz, const i
     std::vector<int32_t> mark((size_t)std::max<int64_t>(1, N), -1);
     std::vector<int32_t> home((size_t)std::max<int64_t>(1, N), -1);
     std::vector<int32_t> cur, tile_rows_ptr{0}, tile_rows;
-    out.item_ptr.push_back(0);
+    std::vector<int32_t> out_item_ptr{0}, item_dev;
     int32_t t = 0;
     int64_t own = 0;
     auto close_tile = [&]() {
         std::sort(cur.begin(), cur.end());
-        out.item_dev.insert(out.item_dev.end(), cur.begin(), cur.end());
-        out.item_ptr.push_back((int32_t)out.item_dev.size());
+        item_dev.insert(item_dev.end(), cur.begin(), cur.end());
+        out_item_ptr.push_back((int32_t)item_dev.size());
         tile_rows_ptr.push_back((int32_t)tile_rows.size());
         cur.clear();
         own = 0;
@@ -131,7 +135,7 @@ bool build_tile_host(int64_t N, int32_t n_nodes, int32_t n, int64_t nnz, const i
     if (!cur.empty()) close_tile();
     const int32_t T = t;
     out.n_tiles = T;
-    if ((int64_t)out.item_dev.size() > INT32_MAX) return false;
+    if ((int64_t)item_dev.size() > INT32_MAX) return false;
 
     // heavy x heavy targets: owned by the common home tile of all contributors, else side
     const int64_t NT = nnz + n;
@@ -155,15 +159,15 @@ bool build_tile_host(int64_t N, int32_t n_nodes, int32_t n, int64_t nnz, const i
     for (int64_t g = 0; g < NT; g++)
         if (hh_owner[g] >= 0) hh_of_tile[hh_owner[g]].push_back((int32_t)g);
 
-    // ---- per tile: blob (owned program) and side entries
+    // ---- per tile: blob = header | items | owned program | side entries
     std::vector<int32_t> sid_of((size_t)NT, -1);
     std::vector<std::pair<int32_t, uint16_t>> con, side;
     std::vector<int32_t> gids;
     std::vector<std::pair<int32_t, int32_t>> runs;
-    std::vector<uint16_t> lstart, lst;
+    std::vector<uint16_t> lstart, lst, slst;
+    std::vector<SideEnt> sents;
+    std::vector<int32_t> sent_tile_sid;     // side id of each entry, in emission order
     out.blob_off.push_back(0);
-    out.side_ptr.push_back(0);
-    out.side_lst.push_back(0);
     int64_t listed = 0;
     for (int32_t tt = 0; tt < T; tt++) {
         // owned targets, ascending
@@ -176,13 +180,13 @@ bool build_tile_host(int64_t N, int32_t n_nodes, int32_t n, int64_t nnz, const i
         }
         gids.insert(gids.end(), hh_of_tile[tt].begin(), hh_of_tile[tt].end());
         std::sort(gids.begin(), gids.end());
-        if ((int64_t)gids.size() > kOwnMax) return false;
         // contributions of this tile's items
         con.clear();
         side.clear();
-        const int32_t q0 = out.item_ptr[tt];
-        for (int32_t q = q0; q < out.item_ptr[tt + 1]; q++) {
-            const int32_t i = out.item_dev[q];
+        const int32_t q0 = out_item_ptr[tt];
+        const int32_t ni = out_item_ptr[tt + 1] - q0;
+        for (int32_t q = q0; q < out_item_ptr[tt + 1]; q++) {
+            const int32_t i = item_dev[q];
             const int32_t loc = q - q0;
             for (int p = 0; p < NPAIR + 4; p++) {
                 int64_t g;
@@ -214,7 +218,7 @@ bool build_tile_host(int64_t N, int32_t n_nodes, int32_t n, int64_t nnz, const i
         };
         std::stable_sort(con.begin(), con.end(), by_target);
         std::stable_sort(side.begin(), side.end(), by_target);
-        // lists in owned-target order; runs of consecutive global ids
+        // owned lists in target order; runs of consecutive global ids
         lstart.assign(1, 0);
         lst.clear();
         runs.clear();
@@ -229,47 +233,79 @@ bool build_tile_host(int64_t N, int32_t n_nodes, int32_t n, int64_t nnz, const i
         }
         if (ci != con.size()) return false;
         listed += (int64_t)lst.size();
-        TileHdr hdr;
-        hdr.n_items = (uint16_t)(out.item_ptr[tt + 1] - q0);
-        hdr.n_own = (uint16_t)gids.size();
-        hdr.n_runs = (uint16_t)runs.size();
-        hdr.n_lst = (uint16_t)lst.size();
-        size_t bytes = sizeof(TileHdr) + 8 * runs.size() + 2 * lstart.size() + 2 * lst.size();
-        bytes = (bytes + 15) & ~(size_t)15;
-        if (bytes > (size_t)kBlobMax) return false;
-        hdr.bytes = (uint32_t)bytes;
-        hdr.pad = 0;
-        const size_t base = out.blob.size();
-        out.blob.resize(base + bytes, 0);
-        uint8_t *bp = out.blob.data() + base;
-        std::memcpy(bp, &hdr, sizeof(hdr));
-        bp += sizeof(hdr);
-        for (auto &rn : runs) {
-            const int32_t v2[2] = {rn.first, rn.second};
-            std::memcpy(bp, v2, 8);
-            bp += 8;
-        }
-        std::memcpy(bp, lstart.data(), 2 * lstart.size());
-        bp += 2 * lstart.size();
-        if (!lst.empty()) std::memcpy(bp, lst.data(), 2 * lst.size());
-        out.blob_off.push_back((int64_t)out.blob.size());
-        out.n_owned += (int64_t)gids.size();
-        // side entries
+        // side entries (slot filled below, once every side target's entry count is known)
+        sents.clear();
+        slst.clear();
         for (size_t k = 0; k < side.size(); k++) {
             if (k == 0 || side[k].first != side[k - 1].first) {
-                if (k) out.side_lst.push_back((int32_t)out.slst.size());
                 int32_t &sid = sid_of[side[k].first];
                 if (sid < 0) {
                     sid = (int32_t)out.sd_gid.size();
                     out.sd_gid.push_back(side[k].first);
                 }
-                out.side_sid.push_back(sid);
+                SideEnt se;
+                se.sid = sid;
+                se.slot = -1;
+                se.lbeg = (uint16_t)slst.size();
+                se.lcnt = 0;
+                sents.push_back(se);
+                sent_tile_sid.push_back(sid);
             }
-            out.slst.push_back(side[k].second);
+            slst.push_back(side[k].second);
+            sents.back().lcnt++;
         }
-        if (!side.empty()) out.side_lst.push_back((int32_t)out.slst.size());
-        out.side_ptr.push_back((int32_t)out.side_sid.size());
-        if (out.slst.size() > (size_t)INT32_MAX) return false;
+        // emit the blob
+        TileHdr hdr;
+        std::memset(&hdr, 0, sizeof(hdr));
+        hdr.n_items = (uint16_t)ni;
+        hdr.n_own = (uint16_t)gids.size();
+        hdr.n_runs = (uint16_t)runs.size();
+        hdr.n_lst = (uint16_t)lst.size();
+        hdr.n_sent = (uint16_t)sents.size();
+        hdr.n_slst = (uint16_t)slst.size();
+        const size_t items_bytes = pad16((size_t)ni * 49);
+        hdr.off_prog = (uint32_t)(pad16(sizeof(TileHdr)) + items_bytes);
+        const size_t prog_bytes = pad16(8 * runs.size() + 2 * lstart.size() + 2 * lst.size());
+        hdr.off_side = (uint32_t)(hdr.off_prog + prog_bytes);
+        const size_t side_bytes = pad16(sizeof(SideEnt) * sents.size() + 2 * slst.size());
+        const size_t bytes = hdr.off_side + side_bytes;
+        if (bytes > (size_t)kStageMax || gids.size() > 65535 || lst.size() > 65535) return false;
+        hdr.bytes = (uint32_t)bytes;
+        const size_t base = out.blob.size();
+        out.blob.resize(base + bytes, 0);
+        uint8_t *bp = out.blob.data() + base;
+        std::memcpy(bp, &hdr, sizeof(hdr));
+        uint8_t *it = bp + pad16(sizeof(TileHdr));
+        int4 *term = reinterpret_cast<int4 *>(it);
+        double *bt = reinterpret_cast<double *>(it + 16 * (size_t)ni);
+        double *v0 = bt + ni;
+        uint8_t *md = reinterpret_cast<uint8_t *>(v0 + 3 * (size_t)ni);
+        for (int32_t q = 0; q < ni; q++) {
+            const int32_t i = item_dev[q0 + q];
+            int4 tv;
+            tv.x = TT[0][i]; tv.y = TT[1][i]; tv.z = TT[2][i]; tv.w = TT[3][i];
+            std::memcpy(term + q, &tv, sizeof(tv));
+            bt[q] = beta[i];
+            for (int k = 0; k < 3; k++) v0[k * ni + q] = vprev[k * N + i];
+            md[q] = (uint8_t)model[i];
+        }
+        uint8_t *pp = bp + hdr.off_prog;
+        for (auto &rn : runs) {
+            const int32_t v2[2] = {rn.first, rn.second};
+            std::memcpy(pp, v2, 8);
+            pp += 8;
+        }
+        std::memcpy(pp, lstart.data(), 2 * lstart.size());
+        pp += 2 * lstart.size();
+        if (!lst.empty()) std::memcpy(pp, lst.data(), 2 * lst.size());
+        uint8_t *sp = bp + hdr.off_side;
+        if (!sents.empty()) std::memcpy(sp, sents.data(), sizeof(SideEnt) * sents.size());
+        sp += sizeof(SideEnt) * sents.size();
+        if (!slst.empty()) std::memcpy(sp, slst.data(), 2 * slst.size());
+        out.blob_off.push_back((int64_t)out.blob.size());
+        out.n_owned += (int64_t)gids.size();
+        out.n_side_entries += (int64_t)sents.size();
+        listed += (int64_t)slst.size();
     }
     // every live contribution is listed exactly once (owned or side)
     {
@@ -277,16 +313,29 @@ bool build_tile_host(int64_t N, int32_t n_nodes, int32_t n, int64_t nnz, const i
         for (int64_t k = 0; k < NPAIR * N; k++) live += raw_slot[k] >= 0;
         for (int64_t i = 0; i < N; i++)
             for (int a = 0; a < 4; a++) live += TT[a][i] >= 0;
-        if (listed + (int64_t)out.slst.size() != live) return false;
+        if (listed != live) return false;
     }
-    // partial slots: per side target, its entries in tile order
+    // partial slots: per side target, its entries in tile order; patch the blobs
     out.n_side = (int32_t)out.sd_gid.size();
     out.sd_part.assign((size_t)out.n_side + 1, 0);
-    for (int32_t sid : out.side_sid) out.sd_part[sid + 1]++;
-    for (int32_t s = 0; s < out.n_side; s++) out.sd_part[s + 1] += out.sd_part[s];
-    std::vector<int32_t> fill(out.sd_part.begin(), out.sd_part.end() - 1);
-    out.side_slot.resize(out.side_sid.size());
-    for (size_t e = 0; e < out.side_sid.size(); e++) out.side_slot[e] = fill[out.side_sid[e]]++;
+    for (int32_t sid : sent_tile_sid) out.sd_part[sid + 1]++;
+    for (int32_t s2 = 0; s2 < out.n_side; s2++) out.sd_part[s2 + 1] += out.sd_part[s2];
+    {
+        std::vector<int32_t> fill(out.sd_part.begin(), out.sd_part.end() - 1);
+        for (int32_t tt = 0; tt < T; tt++) {
+            uint8_t *bp = out.blob.data() + out.blob_off[tt];
+            TileHdr hdr;
+            std::memcpy(&hdr, bp, sizeof(hdr));
+            SideEnt *se = reinterpret_cast<SideEnt *>(bp + hdr.off_side);
+            for (int e = 0; e < hdr.n_sent; e++) {
+                SideEnt v;
+                std::memcpy(&v, se + e, sizeof(v));
+                v.slot = fill[v.sid]++;
+                std::memcpy(se + e, &v, sizeof(v));
+            }
+        }
+    }
+    out.n_items = (int64_t)item_dev.size();
     return true;
 }
 
