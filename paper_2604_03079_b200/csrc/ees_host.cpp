@@ -430,8 +430,7 @@ ees_status enqueue(ees_ctx *c, int32_t variant, const double *x, double h, doubl
         }
     } else if (variant == EES_TILE) {
         PhaseMark m(c, st, 0, timed);
-        e = launch_tile(c->tk, call, c->tile_grid, st);
-        nl = c->tk.n_tiles ? 1 : 0;
+        e = launch_tile(c->tk, call, c->tile_grid, st, &nl);
     } else if (variant == EES_GATHER) {
         if (timed) {
             for (int ph = 0; ph < 3 && e == cudaSuccess; ph++) {
@@ -659,8 +658,10 @@ ees_status build_tile(const ees_desc *d, ees_ctx *c, const std::vector<int32_t> 
     TRY(up(&k.blob, th.blob));
     TRY(up(&k.sd_gid, th.sd_gid));
     TRY(up(&k.sd_part, th.sd_part));
-    TRY(dalloc(c, &k.sd_cnt, (size_t)th.n_side));
-    if (cudaMemset(k.sd_cnt, 0, sizeof(int32_t) * std::max(1, th.n_side)) != cudaSuccess) return EES_ECUDA;
+    k.n_side = th.n_side;
+    k.side_inline = th.n_side_entries <= kSideInlineParts;
+    TRY(dalloc(c, &k.done, 1));
+    if (cudaMemset(k.done, 0, sizeof(uint32_t)) != cudaSuccess) return EES_ECUDA;
     TRY(dalloc(c, &k.part, (size_t)th.n_side_entries));
     int sms = 148, dev = 0;
     cudaGetDevice(&dev);

@@ -94,11 +94,12 @@ struct GatherK {
 //   side:    SideEnt[n_sent] | slst u16[n_slst] (pad 16)
 // Local target j maps to global target (A index, or nnz + b row) through the
 // runs; its contributions are lst[lstart[j] .. lstart[j+1]).
-constexpr int kTileItems = 256;      // max items (FET copies) per tile = threads per CTA
-constexpr int kTileThreads = 256;
+constexpr int kTileItems = 128;      // max items (FET copies) per tile = threads per CTA
+constexpr int kTileThreads = 128;
 constexpr int kHeavyDeg = 64;        // nodes with more incident FETs are heavy
-constexpr int kStageMax = 36864;     // bytes of one pipeline stage (a tile blob)
-constexpr int kTilePrefetch = 8;     // owned targets whose A/b value a thread prefetches
+constexpr int kStageMax = 18432;     // bytes of one pipeline stage (a tile blob)
+constexpr int kTilePrefetch = 6;     // owned targets whose A/b value a thread prefetches
+constexpr int64_t kSideInlineParts = 8192;   // up to this many parts: last CTA finalises
 
 struct TileHdr {
     uint16_t n_items, n_own, n_runs, n_lst;
@@ -120,9 +121,11 @@ struct TileK {
     int64_t nnz;
     const int64_t *blob_off;       // [T+1] byte offsets into blob
     const uint8_t *blob;
+    int32_t n_side;
+    int32_t side_inline;           // 1: the last CTA finalises side targets; 0: k_side_final
     const int32_t *sd_gid;         // [n_side] global target
     const int32_t *sd_part;        // [n_side+1] partial ranges
-    int32_t *sd_cnt;               // [n_side] arrival counters, self-resetting
+    uint32_t *done;                // CTA completion ticket, self-resetting
     double *part;                  // [n_side_entries]
 };
 
@@ -148,7 +151,7 @@ bool build_tile_host(int64_t N, int32_t n_nodes, int32_t n, int64_t nnz, const i
 
 // ---- launchers (ees_kernels.cu); all asynchronous on `st` ----
 int tile_blocks_per_sm();
-cudaError_t launch_tile(const TileK &tk, const CallK &call, int grid, cudaStream_t st);
+cudaError_t launch_tile(const TileK &tk, const CallK &call, int grid, cudaStream_t st, int *n_launches);
 cudaError_t launch_atomic(const DevK &dv, const CallK &call, int grid, cudaStream_t st);
 cudaError_t launch_color(const DevK &dv, const CallK &call, int64_t begin, int64_t count,
                          double *partials, cudaStream_t st);

@@ -689,29 +689,124 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase)
 
 constexpr size_t kTileSmem = sizeof(double) * 16 * kTileItems + 2 * (size_t)kStageMax;
 
+// Views into one staged tile blob (layout in ees_internal.h).
+struct TileView {
+    TileHdr hdr;
+    const int4 *term;
+    const double *beta, *v0;
+    const uint8_t *model;
+    const int2 *runs;
+    const uint16_t *lstart, *lst;
+    const SideEnt *sents;
+    const uint16_t *slst;
+};
+
+__device__ __forceinline__ TileView tile_view(const unsigned char *blob)
+{
+    TileView v;
+    v.hdr = *reinterpret_cast<const TileHdr *>(blob);
+    const int ni = v.hdr.n_items;
+    const unsigned char *items = blob + ((sizeof(TileHdr) + 15) & ~(size_t)15);
+    v.term = reinterpret_cast<const int4 *>(items);
+    v.beta = reinterpret_cast<const double *>(items + 16 * (size_t)ni);
+    v.v0 = v.beta + ni;
+    v.model = reinterpret_cast<const uint8_t *>(v.v0 + 3 * (size_t)ni);
+    v.runs = reinterpret_cast<const int2 *>(blob + v.hdr.off_prog);
+    v.lstart = reinterpret_cast<const uint16_t *>(v.runs + v.hdr.n_runs);
+    v.lst = v.lstart + v.hdr.n_own + 1;
+    v.sents = reinterpret_cast<const SideEnt *>(blob + v.hdr.off_side);
+    v.slst = reinterpret_cast<const uint16_t *>(v.sents + v.hdr.n_sent);
+    return v;
+}
+
+// What a thread gathers from global memory for one tile: its item's node
+// voltages and the current values of the targets it owns.
+struct TileRegs {
+    double VD, VG, VS;
+    int32_t gid[kTilePrefetch];
+    double pre[kTilePrefetch];
+};
+
+__device__ __forceinline__ void tile_gather(const TileView &v, const TileK &tk, const CallK &P,
+                                            TileRegs &R)
+{
+    const int tid = threadIdx.x;
+    R.VD = R.VG = R.VS = 0.0;
+    if (tid < v.hdr.n_items) {
+        const int4 T = v.term[tid];
+        R.VD = T.x >= 0 ? __ldg(P.x + T.x) : 0.0;
+        R.VG = T.y >= 0 ? __ldg(P.x + T.y) : 0.0;
+        R.VS = T.z >= 0 ? __ldg(P.x + T.z) : 0.0;
+    }
+    int r = 0, rbase = 0;
+#pragma unroll
+    for (int k = 0; k < kTilePrefetch; k++) {
+        const int j = tid + k * kTileThreads;
+        R.gid[k] = -1;
+        R.pre[k] = 0.0;
+        if (j < v.hdr.n_own) {
+            while (j >= rbase + v.runs[r].y) { rbase += v.runs[r].y; r++; }
+            const int32_t g = v.runs[r].x + (j - rbase);
+            R.gid[k] = g;
+            R.pre[k] = g < tk.nnz ? P.A[g] : P.b[g - tk.nnz];
+        }
+    }
+}
+
+__device__ __forceinline__ double sum_list(const double *s_c, const uint16_t *lst, int l0, int l1)
+{
+    double s = 0.0;
+    int l = l0;
+    for (; l + 4 <= l1; l += 4) {            // four independent loads, summed in list order
+        const double a = s_c[lst[l]], b = s_c[lst[l + 1]], c = s_c[lst[l + 2]], d = s_c[lst[l + 3]];
+        s += a;
+        s += b;
+        s += c;
+        s += d;
+    }
+    for (; l < l1; l++) s += s_c[lst[l]];
+    return s;
+}
+
+// Fixed-order sum of one side target's parts by a whole warp.
+__device__ __forceinline__ void side_finish(const TileK &tk, const CallK &P, int32_t sid, int lane)
+{
+    const int32_t q0 = __ldg(tk.sd_part + sid), q1 = __ldg(tk.sd_part + sid + 1);
+    double u = 0.0;
+    for (int32_t q = q0 + lane; q < q1; q += 32) u += __ldcg(tk.part + q);
+    u = warp_sum(u);
+    if (lane == 0) {
+        const int32_t g = __ldg(tk.sd_gid + sid);
+        if (g < tk.nnz) P.A[g] += u;
+        else P.b[g - tk.nnz] += u;
+    }
+}
+
 // ---------------------------------------------------------------------------
-// TILE (deterministic, one launch): persistent CTAs walk the tiles
-// blockIdx.x, +gridDim.x, ...  Thread 0 keeps the next tile's blob in flight
-// (TMA bulk copy into the other pipeline stage) while the current one is
-// processed:
-//  1. every thread evaluates one item (FET copy) from shared memory and
-//     stages its 16 contributions in shared memory; in the same window it
-//     prefetches the current A/b values of the targets it owns;
-//  2. each owned target (all contributors in this tile) sums its slot list in
-//     list order and stores value + sum -- no other CTA writes it;
-//  3. side targets (heavy x heavy entries and heavy b rows shared by several
-//     tiles: rails, hubs): one thread per entry stores the tile's part; after
-//     a fence and a barrier each entry bumps its target's arrival counter;
-//     the warp of the last arrival sums all parts in part order (fixed lane
-//     stride + shuffle tree), applies the result and resets the counter.
+// TILE (deterministic, one launch, +1 for many side targets): persistent CTAs
+// walk the tiles blockIdx.x, +gridDim.x, ...  Pipeline per CTA:
+//   * thread 0 keeps the next tile's blob in flight (TMA bulk copy into the
+//     other stage of a double buffer);
+//   * each thread holds in registers the x values of its item and the current
+//     A/b values of the targets it owns for the current tile, and gathers
+//     those of the next tile while the current tile's sums run;
+//   1. evaluate one item (FET copy) from shared memory, stage its 16
+//      contributions in shared memory;
+//   2. each owned target (all contributors in this tile) sums its slot list in
+//      list order and stores value + sum -- no other CTA writes it;
+//   3. side targets (heavy x heavy entries, heavy b rows shared by tiles):
+//      store this tile's part; after every tile, a fence + a ticket: the last
+//      CTA sums the parts of every side target in part order (few parts), or
+//      k_side_final does it (many).
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kTileThreads, 2) k_tile(TileK tk, CallK P)
+__global__ void __launch_bounds__(kTileThreads, 4) k_tile(TileK tk, CallK P)
 {
     extern __shared__ __align__(16) unsigned char smem[];
     double *s_c = reinterpret_cast<double *>(smem);                       // [16][kTileItems]
     unsigned char *s_stage = smem + sizeof(double) * 16 * kTileItems;      // [2][kStageMax]
     __shared__ CardK s_cards[EES_MAX_MODELS];
     __shared__ __align__(8) uint64_t s_bar[2];
+    __shared__ int s_last;
     const int tid = threadIdx.x, lane = tid & 31;
     auto issue = [&](int32_t tile, int stage) {
         const int64_t off = tk.blob_off[tile];
@@ -719,135 +814,95 @@ __global__ void __launch_bounds__(kTileThreads, 2) k_tile(TileK tk, CallK P)
         mbar_expect_tx(&s_bar[stage], bytes);
         tma_bulk_g2s(s_stage + (size_t)stage * kStageMax, tk.blob + off, bytes, &s_bar[stage]);
     };
+    const int32_t t0 = blockIdx.x;
     if (tid == 0) {
         mbar_init(&s_bar[0], 1);
         mbar_init(&s_bar[1], 1);
-        if ((int32_t)blockIdx.x < tk.n_tiles) issue(blockIdx.x, 0);
+        if (t0 < tk.n_tiles) issue(t0, 0);
+        if (t0 + (int32_t)gridDim.x < tk.n_tiles) issue(t0 + gridDim.x, 1);
     }
     for (int k = tid; k < P.n_models; k += blockDim.x) s_cards[k] = P.cards[k];
     __syncthreads();
     uint32_t parity[2] = {0, 0};
     int stage = 0;
-    for (int32_t t = blockIdx.x; t < tk.n_tiles; t += gridDim.x) {
+    TileRegs cur, nxt;
+    TileView v;
+    if (t0 < tk.n_tiles) {
+        mbar_wait(&s_bar[0], 0);
+        parity[0] = 1;
+        v = tile_view(s_stage);
+        tile_gather(v, tk, P, cur);
+    }
+    for (int32_t t = t0; t < tk.n_tiles; t += gridDim.x) {
         const int32_t tn = t + gridDim.x;
-        if (tid == 0 && tn < tk.n_tiles) issue(tn, stage ^ 1);   // freed by the previous iteration's barrier
-        mbar_wait(&s_bar[stage], parity[stage]);
-        parity[stage] ^= 1;
-        const unsigned char *blob = s_stage + (size_t)stage * kStageMax;
-        const TileHdr hdr = *reinterpret_cast<const TileHdr *>(blob);
-        const int ni = hdr.n_items;
-        const unsigned char *items = blob + ((sizeof(TileHdr) + 15) & ~(size_t)15);
-        const int4 *term = reinterpret_cast<const int4 *>(items);
-        const double *beta = reinterpret_cast<const double *>(items + 16 * (size_t)ni);
-        const double *v0 = beta + ni;
-        const uint8_t *model = reinterpret_cast<const uint8_t *>(v0 + 3 * (size_t)ni);
-        const int2 *runs = reinterpret_cast<const int2 *>(blob + hdr.off_prog);
-        const uint16_t *lstart = reinterpret_cast<const uint16_t *>(runs + hdr.n_runs);
-        const uint16_t *lst = lstart + hdr.n_own + 1;
-        // x gather first (longest latency), then the owned A/b values
-        int4 T = make_int4(-1, -1, -1, -1);
-        double VD = 0.0, VG = 0.0, VS = 0.0;
-        if (tid < ni) {
-            T = term[tid];
-            VD = T.x >= 0 ? __ldg(P.x + T.x) : 0.0;
-            VG = T.y >= 0 ? __ldg(P.x + T.y) : 0.0;
-            VS = T.z >= 0 ? __ldg(P.x + T.z) : 0.0;
-        }
-        int32_t gid[kTilePrefetch];
-        double pre[kTilePrefetch];
-        {
-            int r = 0, rbase = 0;
-#pragma unroll
-            for (int k = 0; k < kTilePrefetch; k++) {
-                const int j = tid + k * kTileThreads;
-                gid[k] = -1;
-                pre[k] = 0.0;
-                if (j < hdr.n_own) {
-                    while (j >= rbase + runs[r].y) { rbase += runs[r].y; r++; }
-                    const int32_t g = runs[r].x + (j - rbase);
-                    gid[k] = g;
-                    pre[k] = g < tk.nnz ? P.A[g] : P.b[g - tk.nnz];
-                }
-            }
-        }
+        const int ni = v.hdr.n_items;
         if (tid < ni) {
             Stamp st;
-            eval_fet(s_cards[model[tid]], beta[tid], P.gmin, VD, VG, VS, v0[tid], v0[ni + tid],
-                     v0[2 * ni + tid], st);
+            eval_fet(s_cards[v.model[tid]], v.beta[tid], P.gmin, cur.VD, cur.VG, cur.VS, v.v0[tid],
+                     v.v0[ni + tid], v.v0[2 * ni + tid], st);
 #pragma unroll
             for (int p = 0; p < NPAIR; p++) s_c[p * kTileItems + tid] = st.y[p];
 #pragma unroll
             for (int a = 0; a < 4; a++) s_c[(NPAIR + a) * kTileItems + tid] = st.j[a];
+        }
+        // next tile: its blob was issued one iteration ago; start its gathers now
+        TileView vn;
+        if (tn < tk.n_tiles) {
+            mbar_wait(&s_bar[stage ^ 1], parity[stage ^ 1]);
+            parity[stage ^ 1] ^= 1;
+            vn = tile_view(s_stage + (size_t)(stage ^ 1) * kStageMax);
+            tile_gather(vn, tk, P, nxt);
         }
         __syncthreads();
         // owned targets
 #pragma unroll
         for (int k = 0; k < kTilePrefetch; k++) {
             const int j = tid + k * kTileThreads;
-            if (j < hdr.n_own) {
-                double s = 0.0;
-                for (int l = lstart[j]; l < lstart[j + 1]; l++) s += s_c[lst[l]];
-                const int32_t g = gid[k];
-                if (g < tk.nnz) P.A[g] = pre[k] + s;
-                else P.b[g - tk.nnz] = pre[k] + s;
+            if (j < v.hdr.n_own) {
+                const double s = sum_list(s_c, v.lst, v.lstart[j], v.lstart[j + 1]);
+                const int32_t g = cur.gid[k];
+                if (g < tk.nnz) P.A[g] = cur.pre[k] + s;
+                else P.b[g - tk.nnz] = cur.pre[k] + s;
             }
         }
-        if (hdr.n_own > kTilePrefetch * kTileThreads) {
+        if (v.hdr.n_own > kTilePrefetch * kTileThreads) {
             int r = 0, rbase = 0;
-            for (int j = tid + kTilePrefetch * kTileThreads; j < hdr.n_own; j += kTileThreads) {
-                while (j >= rbase + runs[r].y) { rbase += runs[r].y; r++; }
-                const int32_t g = runs[r].x + (j - rbase);
-                double s = 0.0;
-                for (int l = lstart[j]; l < lstart[j + 1]; l++) s += s_c[lst[l]];
+            for (int j = tid + kTilePrefetch * kTileThreads; j < v.hdr.n_own; j += kTileThreads) {
+                while (j >= rbase + v.runs[r].y) { rbase += v.runs[r].y; r++; }
+                const int32_t g = v.runs[r].x + (j - rbase);
+                const double s = sum_list(s_c, v.lst, v.lstart[j], v.lstart[j + 1]);
                 if (g < tk.nnz) P.A[g] += s;
                 else P.b[g - tk.nnz] += s;
             }
         }
-        // side targets
-        if (hdr.n_sent) {
-            const SideEnt *sents = reinterpret_cast<const SideEnt *>(blob + hdr.off_side);
-            const uint16_t *slst = reinterpret_cast<const uint16_t *>(sents + hdr.n_sent);
-            for (int e = tid; e < hdr.n_sent; e += kTileThreads) {
-                const SideEnt se = sents[e];
-                double v = 0.0;
-                for (int l = se.lbeg; l < se.lbeg + se.lcnt; l++) v += s_c[slst[l]];
-                tk.part[se.slot] = v;
-            }
-            __threadfence();
-            __syncthreads();
-            for (int eb = tid & ~31; eb < hdr.n_sent; eb += kTileThreads) {
-                const int e = eb + lane;
-                int32_t sid = 0, p0 = 0, p1 = 0;
-                bool last = false;
-                if (e < hdr.n_sent) {
-                    sid = sents[e].sid;
-                    p0 = __ldg(tk.sd_part + sid);
-                    p1 = __ldg(tk.sd_part + sid + 1);
-                    last = atomicAdd(tk.sd_cnt + sid, 1) == (p1 - p0) - 1;
-                }
-                unsigned mask = __ballot_sync(0xffffffffu, last);
-                if (mask) __threadfence();
-                while (mask) {
-                    const int src = __ffs(mask) - 1;
-                    mask &= mask - 1;
-                    const int32_t s_sid = __shfl_sync(0xffffffffu, sid, src);
-                    const int32_t q0 = __shfl_sync(0xffffffffu, p0, src);
-                    const int32_t q1 = __shfl_sync(0xffffffffu, p1, src);
-                    double u = 0.0;
-                    for (int32_t q = q0 + lane; q < q1; q += 32) u += __ldcg(tk.part + q);
-                    u = warp_sum(u);
-                    if (lane == 0) {
-                        const int32_t g = __ldg(tk.sd_gid + s_sid);
-                        if (g < tk.nnz) P.A[g] += u;
-                        else P.b[g - tk.nnz] += u;
-                        tk.sd_cnt[s_sid] = 0;
-                    }
-                }
-            }
+        // side parts (plain stores; ordered by the fence + ticket below)
+        for (int e = tid; e < v.hdr.n_sent; e += kTileThreads) {
+            const SideEnt se = v.sents[e];
+            tk.part[se.slot] = sum_list(s_c, v.slst, se.lbeg, se.lbeg + se.lcnt);
         }
-        __syncthreads();          // s_c and this stage are reused
+        __syncthreads();          // s_c and this stage are free again
+        if (tid == 0 && tn + (int32_t)gridDim.x < tk.n_tiles) issue(tn + gridDim.x, stage);
         stage ^= 1;
+        v = vn;
+        cur = nxt;
     }
+    if (tk.n_side && tk.side_inline) {
+        __threadfence();
+        __syncthreads();
+        if (tid == 0) s_last = atomicAdd(tk.done, 1u) == gridDim.x - 1;
+        __syncthreads();
+        if (s_last) {
+            __threadfence();
+            for (int32_t sid = tid >> 5; sid < tk.n_side; sid += kTileThreads >> 5) side_finish(tk, P, sid, lane);
+            if (tid == 0) *tk.done = 0;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) k_side_final(TileK tk, CallK P)
+{
+    const int32_t sid = (int32_t)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+    if (sid < tk.n_side) side_finish(tk, P, sid, threadIdx.x & 31);
 }
 
 int tile_blocks_per_sm()
@@ -858,10 +913,16 @@ int tile_blocks_per_sm()
     return nb > 0 ? nb : 1;
 }
 
-cudaError_t launch_tile(const TileK &tk, const CallK &call, int grid, cudaStream_t st)
+cudaError_t launch_tile(const TileK &tk, const CallK &call, int grid, cudaStream_t st, int *n_launches)
 {
+    *n_launches = 0;
     if (tk.n_tiles == 0) return cudaSuccess;
     k_tile<<<grid, kTileThreads, kTileSmem, st>>>(tk, call);
+    *n_launches = 1;
+    if (tk.n_side && !tk.side_inline) {
+        k_side_final<<<(unsigned)((tk.n_side * 32 + 255) / 256), 256, 0, st>>>(tk, call);
+        *n_launches = 2;
+    }
     return cudaPeekAtLastError();
 }
 
