@@ -39,15 +39,45 @@ bool build_tile_host(int64_t N, int32_t n_nodes, int32_t n, int64_t nnz, const i
                      const double *beta, const double *vprev, const int32_t *model, TileHost &out)
 {
     static_assert(kOwnMax > 64, "tile budget too small");
-    out = TileHost();
     const int32_t NN = std::max(1, n_nodes);
-    std::vector<uint8_t> heavy((size_t)NN, 0);
-    for (int32_t v = 0; v < n_nodes; v++) heavy[v] = (iptr[v + 1] - iptr[v]) > kHeavyDeg;
+    // A light row whose FETs alone overflow a tile (pathological: many heavy x
+    // heavy entries on few FETs) is promoted to heavy and the partition redone.
+    std::vector<uint8_t> promoted((size_t)NN, 0);
+    std::vector<uint8_t> heavy;
+    std::vector<int32_t> hs_ptr, hs_k;
+    std::vector<int32_t> tile_of_row, mark, home, cur, tile_rows_ptr, tile_rows, out_item_ptr, item_dev;
+    int32_t t = 0;
+    int64_t own = 0;
+    // heavy x heavy contributions of a FET (owned by its home tile or side)
+    auto hh_count = [&](int64_t i) {
+        int32_t k = 0;
+        for (int p = 0; p < NPAIR; p++)
+            if (raw_slot[p * N + i] >= 0 && heavy[TT[pair_row(p)][i]] && heavy[TT[pair_col(p)][i]]) k++;
+        for (int a = 0; a < 4; a++)
+            if (TT[a][i] >= 0 && heavy[TT[a][i]]) k++;
+        return k;
+    };
+
+    auto close_tile = [&]() {
+        std::sort(cur.begin(), cur.end());
+        item_dev.insert(item_dev.end(), cur.begin(), cur.end());
+        out_item_ptr.push_back((int32_t)item_dev.size());
+        tile_rows_ptr.push_back((int32_t)tile_rows.size());
+        cur.clear();
+        own = 0;
+        t++;
+    };
+    for (bool done = false; !done;) {
+    done = true;
+    out = TileHost();
+    heavy.assign((size_t)NN, 0);
+    for (int32_t v = 0; v < n_nodes; v++) heavy[v] = (iptr[v + 1] - iptr[v]) > kHeavyDeg || promoted[v];
     for (int32_t r : rails) heavy[r] = 1;
     for (int32_t v = 0; v < n_nodes; v++) out.n_heavy += heavy[v];
 
     // heavy-row entries (h, c) with c a light node belong to c's tile
-    std::vector<int32_t> hs_ptr((size_t)NN + 1, 0), hs_k;
+    hs_ptr.assign((size_t)NN + 1, 0);
+    hs_k.clear();
     for (int32_t h = 0; h < n_nodes; h++)
         if (heavy[h])
             for (int32_t k = row_ptr[h]; k < row_ptr[h + 1]; k++) {
@@ -65,33 +95,17 @@ bool build_tile_host(int64_t N, int32_t n_nodes, int32_t n, int64_t nnz, const i
                     if (c < n_nodes && !heavy[c]) hs_k[fill[c]++] = k;
                 }
     }
-    // heavy x heavy contributions of a FET (owned by its home tile or side)
-    auto hh_count = [&](int64_t i) {
-        int32_t k = 0;
-        for (int p = 0; p < NPAIR; p++)
-            if (raw_slot[p * N + i] >= 0 && heavy[TT[pair_row(p)][i]] && heavy[TT[pair_col(p)][i]]) k++;
-        for (int a = 0; a < 4; a++)
-            if (TT[a][i] >= 0 && heavy[TT[a][i]]) k++;
-        return k;
-    };
-
     // ---- tiles of consecutive light rows: <= kTileItems FETs, <= kOwnMax targets
-    std::vector<int32_t> tile_of_row((size_t)NN, -1);
-    std::vector<int32_t> mark((size_t)std::max<int64_t>(1, N), -1);
-    std::vector<int32_t> home((size_t)std::max<int64_t>(1, N), -1);
-    std::vector<int32_t> cur, tile_rows_ptr{0}, tile_rows;
-    std::vector<int32_t> out_item_ptr{0}, item_dev;
-    int32_t t = 0;
-    int64_t own = 0;
-    auto close_tile = [&]() {
-        std::sort(cur.begin(), cur.end());
-        item_dev.insert(item_dev.end(), cur.begin(), cur.end());
-        out_item_ptr.push_back((int32_t)item_dev.size());
-        tile_rows_ptr.push_back((int32_t)tile_rows.size());
-        cur.clear();
-        own = 0;
-        t++;
-    };
+    tile_of_row.assign((size_t)NN, -1);
+    mark.assign((size_t)std::max<int64_t>(1, N), -1);
+    home.assign((size_t)std::max<int64_t>(1, N), -1);
+    cur.clear();
+    tile_rows_ptr.assign(1, 0);
+    tile_rows.clear();
+    out_item_ptr.assign(1, 0);
+    item_dev.clear();
+    t = 0;
+    own = 0;
     for (int32_t v = 0; v < n_nodes; v++) {
         if (heavy[v]) continue;
         for (int pass = 0; pass < 2; pass++) {
@@ -107,10 +121,14 @@ bool build_tile_host(int64_t N, int32_t n_nodes, int32_t n, int64_t nnz, const i
                 close_tile();
                 continue;
             }
-            if (over) return false;        // a single light row exceeds a tile
+            if (over) {                    // a single light row exceeds a tile
+                promoted[v] = 1;
+                done = false;
+            }
             own += add;
             break;
         }
+        if (!done) break;
         tile_of_row[v] = t;
         tile_rows.push_back(v);
         for (int64_t k = iptr[v]; k < iptr[v + 1]; k++) {
@@ -122,6 +140,7 @@ bool build_tile_host(int64_t N, int32_t n_nodes, int32_t n, int64_t nnz, const i
             if (home[i] < 0) home[i] = t;
         }
     }
+    }   // partition attempt
     if (!cur.empty()) close_tile();
     // FETs with no light terminal (all heavy or ground): orphan tiles
     for (int64_t i = 0; i < N; i++)
