@@ -116,7 +116,7 @@ typedef struct {
     double setup_s;                         /* wall time of ees_setup */
     double setup_pattern_s, setup_color_s;  /* parts of it */
     int32_t n_tiles, n_heavy_nodes, n_side_targets;   /* EES_TILE structure */
-    int32_t reserved0;
+    int32_t tile_blob_max;                  /* largest per-tile blob (bytes) */
     int64_t n_tile_items;                   /* device copies over all tiles (>= n_dev) */
     double tune_ms[5];                      /* EES_AUTO: measured ms per call of [_, COLOR, ATOMIC, GATHER, TILE] */
 } ees_stats_t;

@@ -46,7 +46,7 @@ class ees_stats_t(C.Structure):
                 ("n_rail_entries", i32), ("n_heavy_targets", i32), ("launches_per_call", i32),
                 ("setup_s", f64), ("setup_pattern_s", f64), ("setup_color_s", f64),
                 ("n_tiles", i32), ("n_heavy_nodes", i32), ("n_side_targets", i32),
-                ("reserved0", i32), ("n_tile_items", i64), ("tune_ms", f64 * 5)]
+                ("tile_blob_max", i32), ("n_tile_items", i64), ("tune_ms", f64 * 5)]
 
 
 lib = C.CDLL(LIB_PATH)

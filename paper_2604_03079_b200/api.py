@@ -101,7 +101,7 @@ class Context:
     def stats(self):
         st = L.ees_stats_t()
         _check(L.lib.ees_stats(self._h, C.byref(st)), "ees_stats")
-        out = {f: getattr(st, f) for f, _ in L.ees_stats_t._fields_ if f not in ("tune_ms", "reserved0")}
+        out = {f: getattr(st, f) for f, _ in L.ees_stats_t._fields_ if f != "tune_ms"}
         out["tune_ms"] = {VARIANT_NAMES[v]: st.tune_ms[v] for v in (1, 2, 3, 4)}
         out["variant_chosen"] = VARIANT_NAMES[st.variant_chosen]
         return out

@@ -638,14 +638,22 @@ ees_status build_tile(const ees_desc *d, ees_ctx *c, const std::vector<int32_t> 
         const ees_model &m = c->models[d->model[i]];
         beta[i] = (m.kp * d->w[i]) / d->l[i];
     }
+    int sms = 148, dev = 0;
+    int grid = sms * 4;
+    if (!c->host_only) {
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        grid = sms * tile_blocks_per_sm();
+    }
     TileHost th;
     if (!build_tile_host(N, c->n_nodes, c->n, c->nnz, TT, raw_slot.data(), iptr, idev, c->rails,
-                         c->row_ptr, c->col_idx, beta.data(), d->vprev, d->model, th))
+                         c->row_ptr, c->col_idx, beta.data(), d->vprev, d->model, grid, th))
         return EES_EINVAL;
     c->st.n_tiles = th.n_tiles;
     c->st.n_heavy_nodes = th.n_heavy;
     c->st.n_side_targets = th.n_side;
     c->st.n_tile_items = th.n_items;
+    c->st.tile_blob_max = th.blob_max;
     if (c->host_only) return EES_OK;
     TileK &k = c->tk;
     k.n_tiles = th.n_tiles;
@@ -659,14 +667,14 @@ ees_status build_tile(const ees_desc *d, ees_ctx *c, const std::vector<int32_t> 
     TRY(up(&k.sd_gid, th.sd_gid));
     TRY(up(&k.sd_part, th.sd_part));
     k.n_side = th.n_side;
-    k.side_inline = th.n_side_entries <= kSideInlineParts;
+    k.side_inline = th.n_parts <= kSideInlineParts;
+    k.n_hot = th.n_hot;
+    k.hot_base = th.hot_base;
     TRY(dalloc(c, &k.done, 1));
     if (cudaMemset(k.done, 0, sizeof(uint32_t)) != cudaSuccess) return EES_ECUDA;
-    TRY(dalloc(c, &k.part, (size_t)th.n_side_entries));
-    int sms = 148, dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    c->tile_grid = std::max(1, std::min(th.n_tiles, sms * tile_blocks_per_sm()));
+    TRY(dalloc(c, &k.part, (size_t)th.n_parts));
+    // the grid the hot parts were laid out for (every CTA stores its hot parts)
+    c->tile_grid = grid;
     return EES_OK;
 }
 

@@ -97,9 +97,11 @@ struct GatherK {
 constexpr int kTileItems = 128;      // max items (FET copies) per tile = threads per CTA
 constexpr int kTileThreads = 128;
 constexpr int kHeavyDeg = 64;        // nodes with more incident FETs are heavy
-constexpr int kStageMax = 18432;     // bytes of one pipeline stage (a tile blob)
+constexpr int kStageMax = 12288;     // bytes of one pipeline stage (a tile blob)
+constexpr int kStages = 3;           // TMA pipeline depth (blobs in flight per CTA)
 constexpr int kTilePrefetch = 6;     // owned targets whose A/b value a thread prefetches
 constexpr int64_t kSideInlineParts = 8192;   // up to this many parts: last CTA finalises
+constexpr int kMaxHot = 16;          // side targets pre-reduced per CTA (rails): parts = CTAs, not tiles
 
 struct TileHdr {
     uint16_t n_items, n_own, n_runs, n_lst;
@@ -112,7 +114,7 @@ static_assert(sizeof(TileHdr) == 28 || sizeof(TileHdr) == 32, "TileHdr layout");
 
 struct SideEnt {
     int32_t sid;                     // side target
-    int32_t slot;                    // this tile's part slot in `part`
+    int32_t slot;                    // this tile's part slot in `part`, or -1-h for hot target h
     uint16_t lbeg, lcnt;             // range in slst
 };
 
@@ -123,6 +125,8 @@ struct TileK {
     const uint8_t *blob;
     int32_t n_side;
     int32_t side_inline;           // 1: the last CTA finalises side targets; 0: k_side_final
+    int32_t n_hot;                 // hot side targets: CTA b's part at part[hot_base + h*grid + b]
+    int64_t hot_base;
     const int32_t *sd_gid;         // [n_side] global target
     const int32_t *sd_part;        // [n_side+1] partial ranges
     uint32_t *done;                // CTA completion ticket, self-resetting
@@ -136,6 +140,8 @@ namespace ees {
 struct TileHost {
     int32_t n_tiles = 0, n_heavy = 0, n_side = 0;
     int64_t n_items = 0, n_owned = 0, n_side_entries = 0;
+    int64_t n_parts = 0, hot_base = 0;
+    int32_t blob_max = 0, n_hot = 0;
     std::vector<int64_t> blob_off;
     std::vector<uint8_t> blob;
     std::vector<int32_t> sd_gid, sd_part;
@@ -146,7 +152,8 @@ bool build_tile_host(int64_t N, int32_t n_nodes, int32_t n, int64_t nnz, const i
                      const int32_t *raw_slot, const std::vector<int64_t> &iptr,
                      const std::vector<int32_t> &idev, const std::vector<int32_t> &rails,
                      const std::vector<int32_t> &row_ptr, const std::vector<int32_t> &col_idx,
-                     const double *beta, const double *vprev, const int32_t *model, TileHost &out);
+                     const double *beta, const double *vprev, const int32_t *model, int32_t grid,
+                     TileHost &out);
 #endif
 
 // ---- launchers (ees_kernels.cu); all asynchronous on `st` ----

@@ -687,7 +687,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase)
         : "memory");
 }
 
-constexpr size_t kTileSmem = sizeof(double) * 16 * kTileItems + 2 * (size_t)kStageMax;
+constexpr size_t kTileSmem = sizeof(double) * 16 * kTileItems + kStages * (size_t)kStageMax;
 
 // Views into one staged tile blob (layout in ees_internal.h).
 struct TileView {
@@ -768,12 +768,22 @@ __device__ __forceinline__ double sum_list(const double *s_c, const uint16_t *ls
     return s;
 }
 
-// Fixed-order sum of one side target's parts by a whole warp.
+// Fixed-order sum of one side target's parts by a whole warp (fixed lane
+// stride, four loads in flight per lane, shuffle tree).
 __device__ __forceinline__ void side_finish(const TileK &tk, const CallK &P, int32_t sid, int lane)
 {
-    const int32_t q0 = __ldg(tk.sd_part + sid), q1 = __ldg(tk.sd_part + sid + 1);
+    const int32_t q0 = __ldg(tk.sd_part + 2 * sid), q1 = __ldg(tk.sd_part + 2 * sid + 1);
     double u = 0.0;
-    for (int32_t q = q0 + lane; q < q1; q += 32) u += __ldcg(tk.part + q);
+    int32_t q = q0 + lane;
+    for (; q + 96 < q1; q += 128) {
+        const double a = __ldcg(tk.part + q), b = __ldcg(tk.part + q + 32);
+        const double c = __ldcg(tk.part + q + 64), d = __ldcg(tk.part + q + 96);
+        u += a;
+        u += b;
+        u += c;
+        u += d;
+    }
+    for (; q < q1; q += 32) u += __ldcg(tk.part + q);
     u = warp_sum(u);
     if (lane == 0) {
         const int32_t g = __ldg(tk.sd_gid + sid);
@@ -803,11 +813,14 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_tile(TileK tk, CallK P)
 {
     extern __shared__ __align__(16) unsigned char smem[];
     double *s_c = reinterpret_cast<double *>(smem);                       // [16][kTileItems]
-    unsigned char *s_stage = smem + sizeof(double) * 16 * kTileItems;      // [2][kStageMax]
+    unsigned char *s_stage = smem + sizeof(double) * 16 * kTileItems;      // [kStages][kStageMax]
     __shared__ CardK s_cards[EES_MAX_MODELS];
-    __shared__ __align__(8) uint64_t s_bar[2];
+    __shared__ __align__(8) uint64_t s_bar[kStages];
+    __shared__ double s_hot[kMaxHot];
     __shared__ int s_last;
     const int tid = threadIdx.x, lane = tid & 31;
+    const int32_t G = gridDim.x;
+    if (tid < kMaxHot) s_hot[tid] = 0.0;
     auto issue = [&](int32_t tile, int stage) {
         const int64_t off = tk.blob_off[tile];
         const uint32_t bytes = (uint32_t)(tk.blob_off[tile + 1] - off);
@@ -816,25 +829,25 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_tile(TileK tk, CallK P)
     };
     const int32_t t0 = blockIdx.x;
     if (tid == 0) {
-        mbar_init(&s_bar[0], 1);
-        mbar_init(&s_bar[1], 1);
-        if (t0 < tk.n_tiles) issue(t0, 0);
-        if (t0 + (int32_t)gridDim.x < tk.n_tiles) issue(t0 + gridDim.x, 1);
+        for (int k = 0; k < kStages; k++) mbar_init(&s_bar[k], 1);
+        for (int k = 0; k < kStages; k++)
+            if (t0 + k * G < tk.n_tiles) issue(t0 + k * G, k);
     }
     for (int k = tid; k < P.n_models; k += blockDim.x) s_cards[k] = P.cards[k];
     __syncthreads();
-    uint32_t parity[2] = {0, 0};
+    uint32_t parity = 0;                 // bit k: phase of s_bar[k]
     int stage = 0;
     TileRegs cur, nxt;
     TileView v;
     if (t0 < tk.n_tiles) {
         mbar_wait(&s_bar[0], 0);
-        parity[0] = 1;
+        parity ^= 1u;
         v = tile_view(s_stage);
         tile_gather(v, tk, P, cur);
     }
-    for (int32_t t = t0; t < tk.n_tiles; t += gridDim.x) {
-        const int32_t tn = t + gridDim.x;
+    for (int32_t t = t0; t < tk.n_tiles; t += G) {
+        const int32_t tn = t + G;
+        const int sn = stage + 1 == kStages ? 0 : stage + 1;
         const int ni = v.hdr.n_items;
         if (tid < ni) {
             Stamp st;
@@ -845,12 +858,12 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_tile(TileK tk, CallK P)
 #pragma unroll
             for (int a = 0; a < 4; a++) s_c[(NPAIR + a) * kTileItems + tid] = st.j[a];
         }
-        // next tile: its blob was issued one iteration ago; start its gathers now
+        // next tile: its blob was issued >= one iteration ago; start its gathers now
         TileView vn;
         if (tn < tk.n_tiles) {
-            mbar_wait(&s_bar[stage ^ 1], parity[stage ^ 1]);
-            parity[stage ^ 1] ^= 1;
-            vn = tile_view(s_stage + (size_t)(stage ^ 1) * kStageMax);
+            mbar_wait(&s_bar[sn], (parity >> sn) & 1u);
+            parity ^= 1u << sn;
+            vn = tile_view(s_stage + (size_t)sn * kStageMax);
             tile_gather(vn, tk, P, nxt);
         }
         __syncthreads();
@@ -875,26 +888,32 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_tile(TileK tk, CallK P)
                 else P.b[g - tk.nnz] += s;
             }
         }
-        // side parts (plain stores; ordered by the fence + ticket below)
+        // side parts (plain stores; ordered by the fence + ticket below); a hot
+        // target appears at most once per tile, so one thread owns s_hot[h] here
         for (int e = tid; e < v.hdr.n_sent; e += kTileThreads) {
             const SideEnt se = v.sents[e];
-            tk.part[se.slot] = sum_list(s_c, v.slst, se.lbeg, se.lbeg + se.lcnt);
+            const double part = sum_list(s_c, v.slst, se.lbeg, se.lbeg + se.lcnt);
+            if (se.slot >= 0) tk.part[se.slot] = part;
+            else s_hot[-1 - se.slot] += part;
         }
         __syncthreads();          // s_c and this stage are free again
-        if (tid == 0 && tn + (int32_t)gridDim.x < tk.n_tiles) issue(tn + gridDim.x, stage);
-        stage ^= 1;
+        if (tid == 0 && t + kStages * G < tk.n_tiles) issue(t + kStages * G, stage);
+        stage = sn;
         v = vn;
         cur = nxt;
     }
-    if (tk.n_side && tk.side_inline) {
-        __threadfence();
-        __syncthreads();
-        if (tid == 0) s_last = atomicAdd(tk.done, 1u) == gridDim.x - 1;
-        __syncthreads();
-        if (s_last) {
+    if (tk.n_side) {
+        for (int h = tid; h < tk.n_hot; h += kTileThreads) tk.part[tk.hot_base + (int64_t)h * G + blockIdx.x] = s_hot[h];
+        if (tk.side_inline) {
             __threadfence();
-            for (int32_t sid = tid >> 5; sid < tk.n_side; sid += kTileThreads >> 5) side_finish(tk, P, sid, lane);
-            if (tid == 0) *tk.done = 0;
+            __syncthreads();
+            if (tid == 0) s_last = atomicAdd(tk.done, 1u) == (unsigned)G - 1;
+            __syncthreads();
+            if (s_last) {
+                __threadfence();
+                for (int32_t sid = tid >> 5; sid < tk.n_side; sid += kTileThreads >> 5) side_finish(tk, P, sid, lane);
+                if (tid == 0) *tk.done = 0;
+            }
         }
     }
 }

@@ -23,11 +23,13 @@ namespace ees {
 namespace {
 constexpr int32_t kUnset = -1;
 constexpr int32_t kSide = -2;
-// targets per tile (owned + side entries) such that the blob fits one stage
-// even with one run per owned target: header + items (49 B each) + runs (8 B)
-// + list starts (2 B) + side entries (12 B) + lists (<= 16 u16 per item)
-constexpr int64_t kOwnMax =
-    (kStageMax - (int64_t)sizeof(TileHdr) - 48 - 49 * kTileItems - 2 * 16 * kTileItems - 2) / 12;
+// Upper bound of a tile's blob while it is being formed: header, items (49 B),
+// owned targets (2 B list start each), runs (8 B; one per row-range break,
+// heavy slice entry and heavy x heavy target), list entries (2 B per live
+// contribution of the items), heavy x heavy contributions as side entries
+// (12 B) -- plus padding of the three sections.
+constexpr int64_t kBlobFixed = 32 + 48 + 2;
+constexpr int64_t kOwnMax = 4096;      // u16 list starts also bound the owned count
 
 size_t pad16(size_t x) { return (x + 15) & ~(size_t)15; }
 }  // namespace
@@ -36,7 +38,8 @@ bool build_tile_host(int64_t N, int32_t n_nodes, int32_t n, int64_t nnz, const i
                      const int32_t *raw_slot, const std::vector<int64_t> &iptr,
                      const std::vector<int32_t> &idev, const std::vector<int32_t> &rails,
                      const std::vector<int32_t> &row_ptr, const std::vector<int32_t> &col_idx,
-                     const double *beta, const double *vprev, const int32_t *model, TileHost &out)
+                     const double *beta, const double *vprev, const int32_t *model, int32_t grid,
+                     TileHost &out)
 {
     static_assert(kOwnMax > 64, "tile budget too small");
     const int32_t NN = std::max(1, n_nodes);
@@ -47,7 +50,35 @@ bool build_tile_host(int64_t N, int32_t n_nodes, int32_t n, int64_t nnz, const i
     std::vector<int32_t> hs_ptr, hs_k;
     std::vector<int32_t> tile_of_row, mark, home, cur, tile_rows_ptr, tile_rows, out_item_ptr, item_dev;
     int32_t t = 0;
-    int64_t own = 0;
+    int64_t own = 0, bytes = kBlobFixed;
+    int32_t last_row = -2;
+    // distinct heavy x heavy targets a FET brings to tile t (each costs at most
+    // one side entry + one run + one list start); marks them
+    std::vector<int32_t> hh_seen((size_t)(nnz + n), -1);
+    auto hh_new = [&](int64_t i, int32_t tile) {
+        int32_t k = 0;
+        for (int p = 0; p < NPAIR; p++) {
+            const int32_t s2 = raw_slot[p * N + i];
+            if (s2 >= 0 && heavy[TT[pair_row(p)][i]] && heavy[TT[pair_col(p)][i]] && hh_seen[s2] != tile) {
+                hh_seen[s2] = tile;
+                k++;
+            }
+        }
+        for (int a = 0; a < 4; a++) {
+            const int32_t r = TT[a][i];
+            if (r >= 0 && heavy[r] && hh_seen[nnz + r] != tile) {
+                hh_seen[nnz + r] = tile;
+                k++;
+            }
+        }
+        return k;
+    };
+    auto live_count = [&](int64_t i) {
+        int32_t k = 0;
+        for (int p = 0; p < NPAIR; p++) k += raw_slot[p * N + i] >= 0;
+        for (int a = 0; a < 4; a++) k += TT[a][i] >= 0;
+        return k;
+    };
     // heavy x heavy contributions of a FET (owned by its home tile or side)
     auto hh_count = [&](int64_t i) {
         int32_t k = 0;
@@ -65,6 +96,7 @@ bool build_tile_host(int64_t N, int32_t n_nodes, int32_t n, int64_t nnz, const i
         tile_rows_ptr.push_back((int32_t)tile_rows.size());
         cur.clear();
         own = 0;
+        bytes = kBlobFixed;
         t++;
     };
     for (bool done = false; !done;) {
@@ -106,17 +138,30 @@ bool build_tile_host(int64_t N, int32_t n_nodes, int32_t n, int64_t nnz, const i
     item_dev.clear();
     t = 0;
     own = 0;
+    bytes = kBlobFixed;
+    last_row = -2;
+    std::fill(hh_seen.begin(), hh_seen.end(), -1);
     for (int32_t v = 0; v < n_nodes; v++) {
         if (heavy[v]) continue;
         for (int pass = 0; pass < 2; pass++) {
             int32_t fresh = 0;
-            int64_t add = (row_ptr[v + 1] - row_ptr[v]) + 1 + (hs_ptr[v + 1] - hs_ptr[v]);
+            const int64_t hs = hs_ptr[v + 1] - hs_ptr[v];
+            int64_t add_own = (row_ptr[v + 1] - row_ptr[v]) + 1 + hs;
+            int64_t add_bytes = 2 * add_own + 8 * (hs + ((!cur.empty() && last_row == v - 1) ? 0 : 2));
             for (int64_t k = iptr[v]; k < iptr[v + 1]; k++) {
                 const int32_t i = idev[k];
-                if (mark[i] != t) fresh++;
-                if (home[i] < 0) add += hh_count(i);
+                if (mark[i] != t) {
+                    fresh++;
+                    add_bytes += 49 + 2 * live_count(i);
+                }
+                if (home[i] < 0) {
+                    const int32_t hh = hh_new(i, t);
+                    add_own += hh;
+                    add_bytes += 22 * hh;
+                }
             }
-            const bool over = (int64_t)cur.size() + fresh > kTileItems || own + add > kOwnMax;
+            const bool over = (int64_t)cur.size() + fresh > kTileItems || own + add_own > kOwnMax ||
+                              bytes + add_bytes > kStageMax;
             if (over && pass == 0 && !cur.empty()) {
                 close_tile();
                 continue;
@@ -125,10 +170,12 @@ bool build_tile_host(int64_t N, int32_t n_nodes, int32_t n, int64_t nnz, const i
                 promoted[v] = 1;
                 done = false;
             }
-            own += add;
+            own += add_own;
+            bytes += add_bytes;
             break;
         }
         if (!done) break;
+        last_row = v;
         tile_of_row[v] = t;
         tile_rows.push_back(v);
         for (int64_t k = iptr[v]; k < iptr[v + 1]; k++) {
@@ -146,9 +193,13 @@ bool build_tile_host(int64_t N, int32_t n_nodes, int32_t n, int64_t nnz, const i
     for (int64_t i = 0; i < N; i++)
         if (home[i] < 0) {
             const int32_t add = hh_count(i);
-            if (!cur.empty() && ((int64_t)cur.size() + 1 > kTileItems || own + add > kOwnMax)) close_tile();
+            const int64_t add_bytes = 49 + 2 * live_count(i) + 22 * add;
+            if (!cur.empty() && ((int64_t)cur.size() + 1 > kTileItems || own + add > kOwnMax ||
+                                 bytes + add_bytes > kStageMax))
+                close_tile();
             home[i] = t;
             own += add;
+            bytes += add_bytes;
             cur.push_back((int32_t)i);
         }
     if (!cur.empty()) close_tile();
@@ -322,6 +373,7 @@ bool build_tile_host(int64_t N, int32_t n_nodes, int32_t n, int64_t nnz, const i
         sp += sizeof(SideEnt) * sents.size();
         if (!slst.empty()) std::memcpy(sp, slst.data(), 2 * slst.size());
         out.blob_off.push_back((int64_t)out.blob.size());
+        out.blob_max = std::max(out.blob_max, (int32_t)bytes);
         out.n_owned += (int64_t)gids.size();
         out.n_side_entries += (int64_t)sents.size();
         listed += (int64_t)slst.size();
@@ -334,13 +386,45 @@ bool build_tile_host(int64_t N, int32_t n_nodes, int32_t n, int64_t nnz, const i
             for (int a = 0; a < 4; a++) live += TT[a][i] >= 0;
         if (listed != live) return false;
     }
-    // partial slots: per side target, its entries in tile order; patch the blobs
+    // partial slots.  Side targets with parts in far more tiles than there are
+    // CTAs (rails) are "hot": each CTA pre-sums its tiles' parts in tile order
+    // and stores one part (CTA order), so the final sum has `grid` terms.
+    // Every other side target gets one part per contributing tile, in tile order.
     out.n_side = (int32_t)out.sd_gid.size();
+    std::vector<int64_t> cnt((size_t)out.n_side, 0);
+    for (int32_t sid : sent_tile_sid) cnt[sid]++;
+    std::vector<int32_t> order((size_t)out.n_side);
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return cnt[a] > cnt[b]; });
+    std::vector<int32_t> hot_of((size_t)out.n_side, -1);
+    for (int32_t k = 0; k < out.n_side && k < kMaxHot; k++)
+        if (cnt[order[k]] > 4 * (int64_t)grid) hot_of[order[k]] = out.n_hot++;
     out.sd_part.assign((size_t)out.n_side + 1, 0);
-    for (int32_t sid : sent_tile_sid) out.sd_part[sid + 1]++;
-    for (int32_t s2 = 0; s2 < out.n_side; s2++) out.sd_part[s2 + 1] += out.sd_part[s2];
+    std::vector<int64_t> base((size_t)out.n_side, 0);
+    int64_t cold = 0;
+    for (int32_t s2 = 0; s2 < out.n_side; s2++)
+        if (hot_of[s2] < 0) { base[s2] = cold; cold += cnt[s2]; }
+    out.hot_base = cold;
+    out.n_parts = cold + (int64_t)out.n_hot * grid;
+    if (out.n_parts > INT32_MAX) return false;
+    std::vector<int32_t> part_lo((size_t)out.n_side), part_hi((size_t)out.n_side);
+    for (int32_t s2 = 0; s2 < out.n_side; s2++) {
+        if (hot_of[s2] >= 0) {
+            part_lo[s2] = (int32_t)(out.hot_base + (int64_t)hot_of[s2] * grid);
+            part_hi[s2] = part_lo[s2] + grid;
+        } else {
+            part_lo[s2] = (int32_t)base[s2];
+            part_hi[s2] = (int32_t)(base[s2] + cnt[s2]);
+        }
+    }
+    // sd_part as (lo, hi) pairs flattened: sd_part[2*sid], sd_part[2*sid+1]
+    out.sd_part.resize(2 * (size_t)out.n_side);
+    for (int32_t s2 = 0; s2 < out.n_side; s2++) {
+        out.sd_part[2 * s2] = part_lo[s2];
+        out.sd_part[2 * s2 + 1] = part_hi[s2];
+    }
     {
-        std::vector<int32_t> fill(out.sd_part.begin(), out.sd_part.end() - 1);
+        std::vector<int64_t> fill(base);
         for (int32_t tt = 0; tt < T; tt++) {
             uint8_t *bp = out.blob.data() + out.blob_off[tt];
             TileHdr hdr;
@@ -349,7 +433,7 @@ bool build_tile_host(int64_t N, int32_t n_nodes, int32_t n, int64_t nnz, const i
             for (int e = 0; e < hdr.n_sent; e++) {
                 SideEnt v;
                 std::memcpy(&v, se + e, sizeof(v));
-                v.slot = fill[v.sid]++;
+                v.slot = hot_of[v.sid] >= 0 ? -1 - hot_of[v.sid] : (int32_t)fill[v.sid]++;
                 std::memcpy(se + e, &v, sizeof(v));
             }
         }
