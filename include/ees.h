@@ -192,6 +192,13 @@ ees_status ees_phase_times(ees_ctx *ctx, double ms[4], int32_t *n_calls);
  * more than one device: 0 for a valid colouring.  Synchronous. */
 ees_status ees_race_probe(ees_ctx *ctx, const int32_t *color, int64_t *n_conflicts);
 
+/* Debug: one EES_TILE call that also records %globaltimer stamps (ns) per
+ * CTA into trace [n_ctas][64] (host, cap entries): slot 0 start, 1 first tile
+ * staged, per tile i: 2+4i evaluated, 3+4i after the barrier, 4+4i sums
+ * stored, 5+4i end; 62 ticket taken, 63 end.  Synchronous. */
+ees_status ees_tile_trace(ees_ctx *ctx, const double *x, double h, double *A_vals, double *b,
+                          ees_stream stream, uint64_t *trace, int64_t cap, int32_t *n_ctas);
+
 ees_status ees_destroy(ees_ctx *ctx);
 
 const char *ees_strerror(ees_status status);

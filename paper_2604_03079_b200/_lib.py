@@ -60,15 +60,16 @@ lib.ees_set_variant.argtypes = [P, i32]
 lib.ees_stats.argtypes = [P, C.POINTER(ees_stats_t)]
 lib.ees_set_timing.argtypes = [P, i32]
 lib.ees_phase_times.argtypes = [P, P, C.POINTER(i32)]
+lib.ees_tile_trace.argtypes = [P, P, f64, P, P, P, P, i64, C.POINTER(i32)]
 lib.ees_race_probe.argtypes = [P, P, C.POINTER(i64)]
 lib.ees_destroy.argtypes = [P]
 lib.ees_strerror.argtypes = [i32]
 lib.ees_strerror.restype = C.c_char_p
 for _f in ("ees_setup", "ees_pattern", "ees_find_slot", "ees_colors", "ees_eval_stamp",
            "ees_eval_stamp_host", "ees_set_variant", "ees_stats", "ees_race_probe", "ees_destroy",
-           "ees_set_timing", "ees_phase_times"):
+           "ees_set_timing", "ees_phase_times", "ees_tile_trace"):
     getattr(lib, _f).restype = i32
 
 EXPORTS = ["ees_setup", "ees_pattern", "ees_find_slot", "ees_colors", "ees_eval_stamp",
            "ees_eval_stamp_host", "ees_set_variant", "ees_stats", "ees_set_timing",
-           "ees_phase_times", "ees_race_probe", "ees_destroy", "ees_strerror"]
+           "ees_phase_times", "ees_tile_trace", "ees_race_probe", "ees_destroy", "ees_strerror"]

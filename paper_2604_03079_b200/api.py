@@ -156,6 +156,21 @@ class Context:
                                          C.c_void_p(sh), L.EES_HOST_ASSIGN if assign else 0),
                "ees_eval_stamp_host")
 
+    def tile_trace(self, x, h, A, b, stream=None):
+        """Debug: one traced EES_TILE call -> uint64 array [n_ctas, 64] of
+        %globaltimer stamps (see ees.h)."""
+        import torch
+        if stream is None:
+            stream = torch.cuda.current_stream()
+        sh = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+        cap = 1 << 20
+        buf = np.zeros(cap, np.uint64)
+        n = L.i32()
+        _check(L.lib.ees_tile_trace(self._h, C.c_void_p(x.data_ptr()), float(h), C.c_void_p(A.data_ptr()),
+                                    C.c_void_p(b.data_ptr()), C.c_void_p(sh), C.c_void_p(buf.ctypes.data),
+                                    cap, C.byref(n)), "ees_tile_trace")
+        return buf[: n.value * 64].reshape(n.value, 64)
+
     def race_probe(self, color=None):
         cp = None
         if color is not None:

@@ -994,6 +994,29 @@ ees_status ees_phase_times(ees_ctx *c, double ms[4], int32_t *n_calls)
     return err == cudaSuccess ? EES_OK : EES_ECUDA;
 }
 
+ees_status ees_tile_trace(ees_ctx *c, const double *x, double h, double *A, double *b, ees_stream stream,
+                          uint64_t *trace, int64_t cap, int32_t *n_ctas)
+{
+    if (!c || !trace || !n_ctas || !x || !A || !b || !(h > 0.0)) return EES_EINVAL;
+    if (c->host_only || c->tk.n_tiles == 0) return EES_ESTATE;
+    const int64_t need = (int64_t)c->tile_grid * kTraceSlots;
+    if (cap < need) return EES_EINVAL;
+    unsigned long long *d = nullptr;
+    if (cudaMalloc(&d, sizeof(uint64_t) * need) != cudaSuccess) return EES_ENOMEM;
+    cudaStream_t st = (cudaStream_t)stream;
+    cudaMemsetAsync(d, 0, sizeof(uint64_t) * need, st);
+    TileK k = c->tk;
+    k.trace = d;
+    const CallK call = make_call(c, x, h, A, b);
+    int nl = 0;
+    cudaError_t e = launch_tile(k, call, c->tile_grid, st, &nl);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(trace, d, sizeof(uint64_t) * need, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    cudaFree(d);
+    *n_ctas = c->tile_grid;
+    return e == cudaSuccess ? EES_OK : EES_ECUDA;
+}
+
 ees_status ees_race_probe(ees_ctx *c, const int32_t *color, int64_t *n_conflicts)
 {
     if (!c || !n_conflicts) return EES_EINVAL;

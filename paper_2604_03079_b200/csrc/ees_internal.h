@@ -131,7 +131,9 @@ struct TileK {
     const int32_t *sd_part;        // [n_side+1] partial ranges
     uint32_t *done;                // CTA completion ticket, self-resetting
     double *part;                  // [n_side_entries]
+    unsigned long long *trace;     // debug: [grid][kTraceSlots] %globaltimer stamps, or null
 };
+constexpr int kTraceSlots = 64;
 
 #ifndef __CUDACC__
 }  // namespace ees

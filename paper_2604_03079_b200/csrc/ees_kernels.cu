@@ -809,6 +809,18 @@ __device__ __forceinline__ void side_finish(const TileK &tk, const CallK &P, int
 //      CTA sums the parts of every side target in part order (few parts), or
 //      k_side_final does it (many).
 // ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned long long globaltimer()
+{
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define TILE_TRACE(slot)                                                            \
+    do {                                                                            \
+        if (tk.trace && tid == 0 && (slot) < kTraceSlots)                           \
+            tk.trace[(size_t)blockIdx.x * kTraceSlots + (slot)] = globaltimer();    \
+    } while (0)
+
 __global__ void __launch_bounds__(kTileThreads, 4) k_tile(TileK tk, CallK P)
 {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -835,7 +847,9 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_tile(TileK tk, CallK P)
     }
     for (int k = tid; k < P.n_models; k += blockDim.x) s_cards[k] = P.cards[k];
     __syncthreads();
+    TILE_TRACE(0);
     uint32_t parity = 0;                 // bit k: phase of s_bar[k]
+    int it = 0;
     int stage = 0;
     TileRegs cur, nxt;
     TileView v;
@@ -845,7 +859,8 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_tile(TileK tk, CallK P)
         v = tile_view(s_stage);
         tile_gather(v, tk, P, cur);
     }
-    for (int32_t t = t0; t < tk.n_tiles; t += G) {
+    TILE_TRACE(1);
+    for (int32_t t = t0; t < tk.n_tiles; t += G, it++) {
         const int32_t tn = t + G;
         const int sn = stage + 1 == kStages ? 0 : stage + 1;
         const int ni = v.hdr.n_items;
@@ -866,7 +881,9 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_tile(TileK tk, CallK P)
             vn = tile_view(s_stage + (size_t)sn * kStageMax);
             tile_gather(vn, tk, P, nxt);
         }
+        TILE_TRACE(2 + 4 * it);
         __syncthreads();
+        TILE_TRACE(3 + 4 * it);
         // owned targets
 #pragma unroll
         for (int k = 0; k < kTilePrefetch; k++) {
@@ -896,7 +913,9 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_tile(TileK tk, CallK P)
             if (se.slot >= 0) tk.part[se.slot] = part;
             else s_hot[-1 - se.slot] += part;
         }
+        TILE_TRACE(4 + 4 * it);
         __syncthreads();          // s_c and this stage are free again
+        TILE_TRACE(5 + 4 * it);
         if (tid == 0 && t + kStages * G < tk.n_tiles) issue(t + kStages * G, stage);
         stage = sn;
         v = vn;
@@ -909,6 +928,7 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_tile(TileK tk, CallK P)
             __syncthreads();
             if (tid == 0) s_last = atomicAdd(tk.done, 1u) == (unsigned)G - 1;
             __syncthreads();
+            TILE_TRACE(kTraceSlots - 2);
             if (s_last) {
                 __threadfence();
                 for (int32_t sid = tid >> 5; sid < tk.n_side; sid += kTileThreads >> 5) side_finish(tk, P, sid, lane);
@@ -916,6 +936,7 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_tile(TileK tk, CallK P)
             }
         }
     }
+    TILE_TRACE(kTraceSlots - 1);
 }
 
 __global__ void __launch_bounds__(256) k_side_final(TileK tk, CallK P)
