@@ -9,6 +9,7 @@ import glob
 import io
 import json
 import os
+import re
 import subprocess
 import sys
 
@@ -83,8 +84,35 @@ def main(src, dst):
                     md.append(f"  - {k}: {d[k]}")
         md.append("")
     open(dst + ".md", "w").write("\n".join(md) + "\n")
+    update_traffic(ncu)
     json.dump({"bench": lines, "ncu": ncu}, open(dst + ".json", "w"), indent=1)
     print(dst + ".md")
+
+
+_UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+
+
+def _bytes(v):
+    num, unit = v.split()
+    return float(num) * _UNIT[unit]
+
+
+def update_traffic(ncu):
+    """profiles/traffic.json: DRAM read+write bytes per launch of the dominant
+    kernel, from `ncu --set full` captures named prof_c<cfg>_<variant>.ncu-rep
+    (bench.py reports it as roofline.traffic)."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "profiles", "traffic.json")
+    d = json.load(open(path)) if os.path.exists(path) else {}
+    for rep, rows in ncu.items():
+        m = re.match(r"prof_c(\d)_(\w+?)\.ncu-rep", rep)
+        if not m or not rows:
+            continue
+        r = rows[0]
+        if "dram__bytes_read.sum" not in r:
+            continue
+        d.setdefault(f"cfg{m.group(1)}", {})[m.group(2)] = _bytes(r["dram__bytes_read.sum"]) + \
+            _bytes(r["dram__bytes_write.sum"])
+    json.dump(d, open(path, "w"), indent=1, sort_keys=True)
 
 
 if __name__ == "__main__":
