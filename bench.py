@@ -252,6 +252,13 @@ def run_sweep(args):
             steps = args.steps if (v != "color" or C <= 512) else max(3, args.steps // 10)
             per = time_calls(ctx, nl, x, A, b, stream, steps, 3, flush)
             rec["ms"][v] = per[len(per) // 2]
+        # NEXT-1: COLOR under the degree-threshold hybrid rule (hub nodes leave
+        # the conflict relation; their entries take the side sum)
+        ctx_h = Context.from_netlist(nl, variant="color", rule="hybrid", heavy_degree=args.heavy_degree)
+        rec["C_hybrid"] = ctx_h.stats()["n_colors"]
+        per = time_calls(ctx_h, nl, x, A, b, stream, args.steps, 3, flush)
+        rec["ms"]["color_hybrid"] = per[len(per) // 2]
+        ctx_h.close()
         rec["fet_per_s"] = {v: nl.n_dev / (ms * 1e-3) for v, ms in rec["ms"].items()}
         line = json.dumps(rec)
         print(line, flush=True)
@@ -269,6 +276,9 @@ def main():
     ap.add_argument("--config", type=int, default=DEFAULT_CONFIG)
     ap.add_argument("--variant", default="auto", choices=["auto", "color", "atomic", "gather", "tile"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--rule", default="exclude_rails", choices=["exclude_rails", "paper", "hybrid"],
+                    help="conflict relation of the colouring (COLOR variant)")
+    ap.add_argument("--heavy-degree", type=int, default=64, help="hybrid rule threshold")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=10.0)
     ap.add_argument("--no-e2e", action="store_true")
@@ -298,7 +308,7 @@ def main():
     dev = torch.device("cuda", torch.cuda.current_device())
 
     nl = netgen.config(args.config)
-    ctx = Context.from_netlist(nl, variant=args.variant)
+    ctx = Context.from_netlist(nl, variant=args.variant, rule=args.rule, heavy_degree=args.heavy_degree)
     st = ctx.stats()
     stream = torch.cuda.Stream()
     x = torch.from_numpy(nl.x).to(dev)
@@ -357,7 +367,9 @@ def main():
     # CUDA events on the launching stream over the timed region
     hbm, peak_src = peaks()
     alg = algorithmic_bytes(nl.n_dev, ctx.n, ctx.nnz)
-    phases = {"atomic": ["k_atomic"], "color": ["k_color x C", "k_rail_final"],
+    phases = {"atomic": ["k_atomic"],
+              "color": (["k_color_h x C", "k_side_chunks + k_side_apply"] if args.rule == "hybrid"
+                        else ["k_color x C", "k_rail_final"]),
               "gather": ["k_gather_eval", "k_gather_reduce", "k_gather_heavy"],
               "tile": ["k_tile"]}[variant]
     phase_avg = {name: phase_ms[i] / max(1, n_timed) for i, name in enumerate(phases)}
@@ -406,7 +418,7 @@ def main():
             "data": "synthetic",
             "config": {"workload": netgen.CONFIG_NAMES[args.config], "config_index": args.config,
                        "n_dev": nl.n_dev, "n": ctx.n, "nnz": ctx.nnz, "colors": st["n_colors"],
-                       "variant": variant, "tune_ms": st["tune_ms"],
+                       "variant": variant, "tune_ms": st["tune_ms"], "rule": args.rule,
                        "l2": "flushed before every step (256 MiB write)",
                        "parallelism": "replicas" if world > 1 else "single",
                        "p10_ms": per_sorted[len(per) // 10], "p50_ms": per_sorted[len(per) // 2],

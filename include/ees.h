@@ -63,7 +63,14 @@ typedef enum {
     EES_CONFLICT_EXCLUDE_RAILS = 0, /* edge iff two FETs share a node that is neither ground nor a rail;
                                        rail x rail entries of A and rail rows of b then take a
                                        deterministic side reduction (DESIGN.md §2 reading R1) */
-    EES_CONFLICT_PAPER = 1          /* paper-literal: edge iff two FETs share any non-ground node */
+    EES_CONFLICT_PAPER = 1,         /* paper-literal: edge iff two FETs share any non-ground node */
+    EES_CONFLICT_HYBRID = 2         /* degree-threshold hybrid: rails and every
+                                       node with more than `heavy_degree` incident FETs leave the
+                                       relation; under EES_COLOR, an entry of A whose row and column
+                                       both left it (or a b row that left it) and that more than one
+                                       FET stamps is written by no colour phase: its contributions go
+                                       to fixed scratch slots and a deterministic segmented sum adds
+                                       them after the last colour */
 } ees_conflict_rule;
 
 enum { EES_MAX_MODELS = 16, EES_MAX_RAILS = 8 };
@@ -96,6 +103,7 @@ typedef struct {
     int32_t variant;                /* ees_variant */
     int32_t conflict_rule;          /* ees_conflict_rule */
     int32_t flags;                  /* 0, or EES_SETUP_HOST_ONLY */
+    int32_t heavy_degree;           /* EES_CONFLICT_HYBRID threshold (incident FETs); 0 = 64 */
 } ees_desc;
 
 /* ees_desc.flags: build only the host-side topology (pattern, slots,
@@ -119,6 +127,9 @@ typedef struct {
     int32_t tile_blob_max;                  /* largest per-tile blob (bytes) */
     int64_t n_tile_items;                   /* device copies over all tiles (>= n_dev) */
     double tune_ms[5];                      /* EES_AUTO: measured ms per call of [_, COLOR, ATOMIC, GATHER, TILE] */
+    int32_t n_excluded_nodes;               /* nodes outside the conflict relation */
+    int32_t n_color_side_targets;           /* EES_CONFLICT_HYBRID: entries summed after the colours */
+    int64_t n_color_side_contributions;     /* their contributions (scratch slots) */
 } ees_stats_t;
 
 /* Build everything that depends only on topology ("constructs the FET
@@ -175,7 +186,8 @@ ees_status ees_stats(const ees_ctx *ctx, ees_stats_t *out);
 
 /* Per-phase device timing (S:326 PhaseTimings).  When enabled, every
  * ees_eval_stamp records CUDA events on the call's stream around each kernel
- * group ("phase"):  COLOR {0: colour kernels, 1: rail finalise},
+ * group ("phase"):  COLOR {0: colour kernels, 1: rail finalise or, under
+ * EES_CONFLICT_HYBRID, the side segmented sum},
  * ATOMIC {0: k_atomic},  GATHER {0: evaluate to scratch, 1: segmented
  * reduction, 2: heavy-target finalise},  TILE {0: k_tile}. */
 ees_status ees_set_timing(ees_ctx *ctx, int32_t enable);

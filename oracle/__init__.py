@@ -166,29 +166,47 @@ def reference(nl, A0=None, b0=None, patt=None):
 
 
 # ---------------------------------------------------------------- colouring
-def excluded_mask(nl, rule="exclude_rails"):
+def node_fanout(nl):
+    """Distinct FETs incident on each node (a FET with two terminals on one
+    node counts once)."""
+    T = np.stack([nl.d, nl.g, nl.s, nl.b], axis=1).astype(np.int64)
+    deg = np.zeros(max(1, nl.n_nodes), np.int64)
+    for a in range(4):
+        t = T[:, a]
+        first = t >= 0
+        for c in range(a):
+            first &= T[:, c] != t
+        np.add.at(deg, t[first], 1)
+    return deg
+
+
+def excluded_mask(nl, rule="exclude_rails", heavy_degree=64):
     """Nodes removed from the conflict relation: rails under SURVEY A1's
-    reading ("exclude_rails"), none under the paper-literal rule ("paper")."""
+    reading ("exclude_rails"), none under the paper-literal rule ("paper"),
+    rails and every node with more than `heavy_degree` incident FETs under
+    SURVEY §8(f) NEXT-1's degree-threshold hybrid ("hybrid")."""
     ex = np.zeros(max(1, nl.n_nodes), np.uint8)
-    if rule == "exclude_rails" and len(nl.rails):
+    if rule in ("exclude_rails", "hybrid") and len(nl.rails):
         ex[nl.rails] = 1
+    if rule == "hybrid":
+        ex[node_fanout(nl) > heavy_degree] = 1
     elif rule not in ("exclude_rails", "paper"):
         raise ValueError(rule)
     return ex
 
 
-def greedy_color(nl, rule="exclude_rails"):
+def greedy_color(nl, rule="exclude_rails", heavy_degree=64):
     """First-fit greedy in netlist order -> (color int32[N], C)."""
-    ex = excluded_mask(nl, rule)
+    ex = excluded_mask(nl, rule, heavy_degree)
     color = np.zeros(max(1, nl.n_dev), np.int32)
     Cn = lib().orc_greedy_color(nl.n_nodes, nl.n_dev, _p(nl.d), _p(nl.g), _p(nl.s), _p(nl.b),
                                 _p(ex), _p(color))
     return color[:nl.n_dev], int(Cn)
 
 
-def color_violations(nl, color, n_colors, rule="exclude_rails"):
+def color_violations(nl, color, n_colors, rule="exclude_rails", heavy_degree=64):
     """Exhaustive validity scan: 0 iff conflict-free."""
-    ex = excluded_mask(nl, rule)
+    ex = excluded_mask(nl, rule, heavy_degree)
     color = np.ascontiguousarray(color, np.int32)
     return int(lib().orc_color_violations(nl.n_nodes, nl.n_dev, _p(nl.d), _p(nl.g), _p(nl.s),
                                           _p(nl.b), _p(ex), _p(color), int(n_colors)))

@@ -17,7 +17,7 @@ if not os.path.exists(LIB_PATH):
 
 EES_OK, EES_EINVAL, EES_ENOMEM, EES_ECUDA, EES_ESTATE = 0, -1, -2, -3, -4
 EES_AUTO, EES_COLOR, EES_ATOMIC, EES_GATHER, EES_TILE = 0, 1, 2, 3, 4
-EES_CONFLICT_EXCLUDE_RAILS, EES_CONFLICT_PAPER = 0, 1
+EES_CONFLICT_EXCLUDE_RAILS, EES_CONFLICT_PAPER, EES_CONFLICT_HYBRID = 0, 1, 2
 EES_MAX_MODELS, EES_MAX_RAILS = 16, 8
 EES_SETUP_HOST_ONLY = 1
 EES_HOST_ASSIGN = 1
@@ -36,7 +36,7 @@ class ees_desc(C.Structure):
                 ("d", P), ("g", P), ("s", P), ("b", P), ("w", P), ("l", P), ("model", P),
                 ("vprev", P), ("n_models", i32), ("models", P), ("n_rails", i32), ("rails", P),
                 ("n_extra_entries", i64), ("extra_row", P), ("extra_col", P), ("gmin", f64),
-                ("variant", i32), ("conflict_rule", i32), ("flags", i32)]
+                ("variant", i32), ("conflict_rule", i32), ("flags", i32), ("heavy_degree", i32)]
 
 
 class ees_stats_t(C.Structure):
@@ -46,7 +46,9 @@ class ees_stats_t(C.Structure):
                 ("n_rail_entries", i32), ("n_heavy_targets", i32), ("launches_per_call", i32),
                 ("setup_s", f64), ("setup_pattern_s", f64), ("setup_color_s", f64),
                 ("n_tiles", i32), ("n_heavy_nodes", i32), ("n_side_targets", i32),
-                ("tile_blob_max", i32), ("n_tile_items", i64), ("tune_ms", f64 * 5)]
+                ("tile_blob_max", i32), ("n_tile_items", i64), ("tune_ms", f64 * 5),
+                ("n_excluded_nodes", i32), ("n_color_side_targets", i32),
+                ("n_color_side_contributions", i64)]
 
 
 lib = C.CDLL(LIB_PATH)

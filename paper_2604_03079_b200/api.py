@@ -12,7 +12,8 @@ from . import _lib as L
 VARIANTS = {"auto": L.EES_AUTO, "color": L.EES_COLOR, "atomic": L.EES_ATOMIC,
             "gather": L.EES_GATHER, "tile": L.EES_TILE}
 VARIANT_NAMES = {v: k for k, v in VARIANTS.items()}
-RULES = {"exclude_rails": L.EES_CONFLICT_EXCLUDE_RAILS, "paper": L.EES_CONFLICT_PAPER}
+RULES = {"exclude_rails": L.EES_CONFLICT_EXCLUDE_RAILS, "paper": L.EES_CONFLICT_PAPER,
+         "hybrid": L.EES_CONFLICT_HYBRID}
 
 
 class EESError(RuntimeError):
@@ -39,7 +40,7 @@ class Context:
 
     def __init__(self, *, n_nodes, n_extra, d, g, s, b, w, l, model, vprev, models,
                  rails=(), extra_row=(), extra_col=(), gmin=1e-12, variant="auto",
-                 rule="exclude_rails", host_only=False):
+                 rule="exclude_rails", heavy_degree=0, host_only=False):
         self._keep = dict(d=_arr(d, np.int32), g=_arr(g, np.int32), s=_arr(s, np.int32),
                           b=_arr(b, np.int32), w=_arr(w, np.float64), l=_arr(l, np.float64),
                           model=_arr(model, np.int32), vprev=_arr(vprev, np.float64),
@@ -60,7 +61,7 @@ class Context:
             extra_col=_ptr(k["ec"]), gmin=float(gmin),
             variant=VARIANTS[variant] if isinstance(variant, str) else int(variant),
             conflict_rule=RULES[rule] if isinstance(rule, str) else int(rule),
-            flags=L.EES_SETUP_HOST_ONLY if host_only else 0)
+            flags=L.EES_SETUP_HOST_ONLY if host_only else 0, heavy_degree=int(heavy_degree))
         h = C.c_void_p()
         _check(L.lib.ees_setup(C.byref(desc), C.byref(h)), "ees_setup")
         self._h = h
@@ -69,12 +70,13 @@ class Context:
         self.n, self.nnz, self.n_dev = st["n"], st["nnz"], st["n_dev"]
 
     @classmethod
-    def from_netlist(cls, nl, variant="auto", rule="exclude_rails", gmin=None, host_only=False):
+    def from_netlist(cls, nl, variant="auto", rule="exclude_rails", gmin=None, host_only=False,
+                     heavy_degree=0):
         return cls(n_nodes=nl.n_nodes, n_extra=nl.n_extra, d=nl.d, g=nl.g, s=nl.s, b=nl.b,
                    w=nl.w, l=nl.l, model=nl.model, vprev=nl.vprev, models=nl.models,
                    rails=nl.rails, extra_row=nl.extra_row, extra_col=nl.extra_col,
                    gmin=nl.gmin if gmin is None else gmin, variant=variant, rule=rule,
-                   host_only=host_only)
+                   heavy_degree=heavy_degree, host_only=host_only)
 
     # ------------------------------------------------------------ queries
     def pattern(self):

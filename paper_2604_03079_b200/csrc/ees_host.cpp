@@ -56,6 +56,10 @@ struct ees_ctx {
     int32_t n_rail_a = 0, n_rail_entries = 0;
     int32_t rail_target[kMaxRailEntries] = {};
     Layout L_atomic, L_color, L_gather;
+    // EES_CONFLICT_HYBRID: colour-major 16-slot layout, side sum, race-probe codes
+    bool hybrid = false;
+    Layout L_colorh, L_probe;
+    SideK sk{};
     GatherK gk{};
     TileK tk{};
     std::vector<int64_t> color_blk_off;   // [C+1] block offsets of colours into partials
@@ -125,8 +129,10 @@ ees_status validate(const ees_desc *d)
         return EES_EINVAL;
     if (!(d->gmin >= 0.0) || !std::isfinite(d->gmin)) return EES_EINVAL;
     if (d->variant < EES_AUTO || d->variant > EES_TILE) return EES_EINVAL;
-    if (d->conflict_rule != EES_CONFLICT_EXCLUDE_RAILS && d->conflict_rule != EES_CONFLICT_PAPER)
+    if (d->conflict_rule != EES_CONFLICT_EXCLUDE_RAILS && d->conflict_rule != EES_CONFLICT_PAPER &&
+        d->conflict_rule != EES_CONFLICT_HYBRID)
         return EES_EINVAL;
+    if (d->heavy_degree < 0) return EES_EINVAL;
     if (d->flags & ~EES_SETUP_HOST_ONLY) return EES_EINVAL;
     for (int k = 0; k < d->n_models; k++) {
         const ees_model &m = d->models[k];
@@ -408,6 +414,22 @@ ees_status enqueue(ees_ctx *c, int32_t variant, const double *x, double h, doubl
         PhaseMark m(c, st, 0, timed);
         e = launch_atomic(c->L_atomic.k(), call, c->atomic_grid, st);
         nl = c->n_dev ? 1 : 0;
+    } else if (variant == EES_COLOR && c->hybrid) {
+        const DevK dv = c->L_colorh.k();
+        {
+            PhaseMark m(c, st, 0, timed);
+            for (int32_t col = 0; col < c->n_colors && e == cudaSuccess; col++) {
+                e = launch_color_h(dv, call, c->color_ptr[col], c->color_ptr[col + 1] - c->color_ptr[col],
+                                   c->sk.buf, st);
+                nl++;
+            }
+        }
+        if (e == cudaSuccess && c->sk.n_side) {
+            PhaseMark m(c, st, 1, timed);
+            int k = 0;
+            e = launch_side_sum(c->sk, call, st, &k);
+            nl += k;
+        }
     } else if (variant == EES_COLOR && c->color_coop) {
         PhaseMark m(c, st, 0, timed);
         e = launch_color_coop(c->L_color.k(), call, c->d_color_ptr, c->n_colors, c->coop_partials,
@@ -543,6 +565,137 @@ ees_status build_layouts(const ees_desc *d, ees_ctx *c, const std::vector<int32_
     return EES_OK;
 }
 
+// COLOR under EES_CONFLICT_HYBRID.  A target can be
+// written by two FETs of one colour only if every node it names left the
+// conflict relation: an A entry whose row and column are both excluded, or
+// the b row of an excluded node.  Such a target stamped by more than one FET
+// is a side target: each of its contributions gets its own scratch slot
+// (contiguous per target, netlist order, then pair order) and a segmented sum
+// adds them after the last colour.  Every other target keeps a plain RMW.
+ees_status build_hybrid(const ees_desc *d, ees_ctx *c, const std::vector<int32_t> &raw_slot,
+                        const std::vector<uint8_t> &excluded)
+{
+    const int64_t N = c->n_dev, nnz = c->nnz, NT = nnz + c->n;
+    const int32_t *TT[4] = {d->d, d->g, d->s, d->b};
+    auto target = [&](int64_t i, int p) -> int64_t {     // p < 12: A pair, else b row p-12
+        if (p < NPAIR) return raw_slot[p * N + i];
+        const int32_t r = TT[p - NPAIR][i];
+        return r >= 0 ? nnz + r : -1;
+    };
+    auto candidate = [&](int64_t i, int p) -> bool {
+        if (p < NPAIR) return excluded[TT[kPairRow[p]][i]] && excluded[TT[kPairCol[p]][i]];
+        return excluded[TT[p - NPAIR][i]] != 0;
+    };
+    // distinct FETs per candidate target
+    std::vector<int32_t> writers((size_t)NT, 0), last((size_t)NT, -1);
+    for (int64_t i = 0; i < N; i++)
+        for (int p = 0; p < NPAIR + 4; p++) {
+            const int64_t g = target(i, p);
+            if (g < 0 || !candidate(i, p) || last[g] == (int32_t)i) continue;
+            last[g] = (int32_t)i;
+            writers[g]++;
+        }
+    // side ids in target order; contributions per side target
+    std::vector<int32_t> sid((size_t)NT, -1), side_gid;
+    for (int64_t g = 0; g < NT; g++)
+        if (writers[g] >= 2) {
+            sid[g] = (int32_t)side_gid.size();
+            side_gid.push_back((int32_t)g);
+        }
+    const int32_t ns = (int32_t)side_gid.size();
+    std::vector<int64_t> sptr((size_t)ns + 1, 0);
+    for (int64_t i = 0; i < N; i++)
+        for (int p = 0; p < NPAIR + 4; p++) {
+            const int64_t g = target(i, p);
+            if (g >= 0 && candidate(i, p) && sid[g] >= 0) sptr[sid[g] + 1]++;
+        }
+    for (int32_t k = 0; k < ns; k++) sptr[k + 1] += sptr[k];
+    if (sptr[ns] > INT32_MAX - 2) return EES_EINVAL;
+    // 16 codes per FET, netlist order
+    std::vector<int32_t> code((size_t)(16 * N));
+    {
+        std::vector<int64_t> fill(sptr.begin(), sptr.end() - 1);
+        for (int64_t i = 0; i < N; i++)
+            for (int p = 0; p < NPAIR + 4; p++) {
+                const int64_t g = target(i, p);
+                int32_t v;
+                if (g < 0) v = -1;
+                else if (candidate(i, p) && sid[g] >= 0) v = (int32_t)(-2 - fill[sid[g]]++);
+                else v = (int32_t)(p < NPAIR ? g : g - nnz);
+                code[(size_t)p * N + i] = v;
+            }
+    }
+    // chunks
+    std::vector<int64_t> chunk_lo(1, 0);
+    std::vector<int32_t> side_chunk(1, 0);
+    for (int32_t k = 0; k < ns; k++) {
+        for (int64_t lo = sptr[k]; lo < sptr[k + 1]; lo += kChunk)
+            chunk_lo.push_back(std::min<int64_t>(sptr[k + 1], lo + kChunk));
+        side_chunk.push_back((int32_t)chunk_lo.size() - 1);
+    }
+    c->st.n_color_side_targets = ns;
+    c->st.n_color_side_contributions = sptr[ns];
+    if (c->host_only) return EES_OK;
+    // colour-major copy
+    std::vector<int32_t> perm((size_t)N);
+    {
+        std::vector<int64_t> fill(c->color_ptr.begin(), c->color_ptr.end() - 1);
+        for (int64_t i = 0; i < N; i++) perm[fill[c->color[i]]++] = (int32_t)i;
+    }
+    std::vector<int32_t> code_c((size_t)(16 * N));
+    std::vector<double> beta_c((size_t)N), v0_c((size_t)(3 * N));
+    std::vector<uint8_t> model_c((size_t)N);
+    std::vector<int4> term_c((size_t)N);
+#pragma omp parallel for schedule(static)
+    for (int64_t q = 0; q < N; q++) {
+        const int64_t i = perm[q];
+        const ees_model &m = c->models[d->model[i]];
+        beta_c[q] = (m.kp * d->w[i]) / d->l[i];
+        for (int t = 0; t < 3; t++) v0_c[t * N + q] = d->vprev[t * N + i];
+        model_c[q] = (uint8_t)d->model[i];
+        term_c[q] = make_int4(d->d[i], d->g[i], d->s[i], d->b[i]);
+        for (int p = 0; p < 16; p++) code_c[(size_t)p * N + q] = code[(size_t)p * N + i];
+    }
+    Layout &L = c->L_colorh;
+    L.N = N;
+    TRY(upload(c, &L.term, term_c.data(), N));
+    TRY(upload(c, &L.beta, beta_c.data(), N));
+    TRY(upload(c, &L.v0, v0_c.data(), 3 * N));
+    TRY(upload(c, &L.model, model_c.data(), N));
+    TRY(upload(c, &L.slot, code_c.data(), 16 * N));
+    // race-probe codes (netlist order): side targets coded -2, as rails elsewhere
+    {
+        std::vector<int32_t> pslot((size_t)(NPAIR * N));
+        std::vector<int4> pterm((size_t)N);
+        for (int64_t i = 0; i < N; i++) {
+            for (int p = 0; p < NPAIR; p++) {
+                const int32_t v = code[(size_t)p * N + i];
+                pslot[(size_t)p * N + i] = v <= -2 ? -2 : v;
+            }
+            int32_t t4[4];
+            for (int a = 0; a < 4; a++) {
+                const int32_t v = code[(size_t)(NPAIR + a) * N + i];
+                t4[a] = v <= -2 ? -2 : v;
+            }
+            pterm[i] = make_int4(t4[0], t4[1], t4[2], t4[3]);
+        }
+        Layout &P = c->L_probe;
+        P.N = N;
+        TRY(upload(c, &P.term, pterm.data(), N));
+        TRY(upload(c, &P.slot, pslot.data(), NPAIR * N));
+    }
+    SideK &k = c->sk;
+    k.n_side = ns;
+    k.n_chunks = (int32_t)chunk_lo.size() - 1;
+    k.nnz = nnz;
+    TRY(dalloc(c, &k.buf, (size_t)sptr[ns]));
+    TRY(upload(c, const_cast<int64_t **>(&k.chunk_lo), chunk_lo.data(), chunk_lo.size()));
+    TRY(upload(c, const_cast<int32_t **>(&k.side_gid), side_gid.data(), side_gid.size()));
+    TRY(upload(c, const_cast<int32_t **>(&k.side_chunk), side_chunk.data(), side_chunk.size()));
+    TRY(dalloc(c, &k.chunk_part, (size_t)k.n_chunks));
+    return EES_OK;
+}
+
 // GATHER: compact contribution buffer + transposed per-target lists.
 ees_status build_gather(const ees_desc *d, ees_ctx *c, const std::vector<int32_t> &raw_slot)
 {
@@ -666,6 +819,7 @@ ees_status build_tile(const ees_desc *d, ees_ctx *c, const std::vector<int32_t> 
     TRY(up(&k.blob, th.blob));
     TRY(up(&k.sd_gid, th.sd_gid));
     TRY(up(&k.sd_part, th.sd_part));
+    TRY(up(&k.hot_gid, th.hot_gid));
     k.n_side = th.n_side;
     k.side_inline = th.n_parts <= kSideInlineParts;
     k.n_hot = th.n_hot;
@@ -707,7 +861,11 @@ ees_status autotune(ees_ctx *c, bool full)
     const char *mode = std::getenv("EES_COLOR_MODE");   // debug knob: "launch" | "coop"
     for (int32_t v = EES_COLOR; v <= (full ? EES_TILE : EES_COLOR) && rc == EES_OK; v++) {
         double ms;
-        if (v == EES_COLOR && mode && (!std::strcmp(mode, "launch") || !std::strcmp(mode, "coop"))) {
+        if (v == EES_COLOR && c->hybrid) {
+            c->color_coop = 0;
+            if (c->n_colors > 512) { c->st.tune_ms[v] = -1; continue; }
+            ms = time_variant(v);
+        } else if (v == EES_COLOR && mode && (!std::strcmp(mode, "launch") || !std::strcmp(mode, "coop"))) {
             c->color_coop = !std::strcmp(mode, "coop") && c->coop_grid > 0;
             ms = time_variant(v);
         } else if (v == EES_COLOR) {
@@ -780,8 +938,16 @@ ees_status setup_impl(const ees_desc *d, ees_ctx *c)
     // colouring
     const double tc = now_s();
     std::vector<uint8_t> excluded((size_t)std::max(1, c->n_nodes), 0);
-    if (d->conflict_rule == EES_CONFLICT_EXCLUDE_RAILS)
+    if (d->conflict_rule != EES_CONFLICT_PAPER)
         for (int32_t r : c->rails) excluded[r] = 1;
+    if (d->conflict_rule == EES_CONFLICT_HYBRID) {
+        // nodes with more than K incident FETs leave the relation
+        const int64_t K = d->heavy_degree > 0 ? d->heavy_degree : 64;
+        for (int32_t v = 0; v < c->n_nodes; v++)
+            if (iptr[v + 1] - iptr[v] > K) excluded[v] = 1;
+        c->hybrid = true;
+    }
+    for (int32_t v = 0; v < c->n_nodes; v++) c->st.n_excluded_nodes += excluded[v];
     int32_t maxdeg = 0;
     c->n_colors = greedy_color(d, excluded, c->color, maxdeg);
     c->color_ptr.assign((size_t)c->n_colors + 1, 0);
@@ -804,12 +970,14 @@ ees_status setup_impl(const ees_desc *d, ees_ctx *c)
         for (int64_t i = 0; i < N; i++)
             nc += (d->d[i] >= 0) + (d->g[i] >= 0) + (d->s[i] >= 0) + (d->b[i] >= 0);
         c->st.n_contributions = nc;
+        if (c->hybrid) TRY(build_hybrid(d, c, raw_slot, excluded));
         TRY(build_tile(d, c, raw_slot, iptr, idev));
         c->variant = d->variant == EES_AUTO ? EES_ATOMIC : d->variant;
         c->st.setup_s = now_s() - t0;
         return EES_OK;
     }
     TRY(build_layouts(d, c, raw_slot, rail_ord));
+    if (c->hybrid) TRY(build_hybrid(d, c, raw_slot, excluded));
     TRY(build_gather(d, c, raw_slot));
     TRY(build_tile(d, c, raw_slot, iptr, idev));
     int sms = 148;
@@ -1047,7 +1215,8 @@ ees_status ees_race_probe(ees_ctx *c, const int32_t *color, int64_t *n_conflicts
     for (int32_t k = 0; k < C && e == cudaSuccess; k++) {
         cudaMemsetAsync(cnt_a, 0, sizeof(int32_t) * c->nnz, 0);
         cudaMemsetAsync(cnt_b, 0, sizeof(int32_t) * c->n, 0);
-        e = launch_race_probe(c->L_atomic.k(), dperm, ptr[k], ptr[k + 1] - ptr[k], cnt_a, cnt_b, 0);
+        e = launch_race_probe(c->hybrid ? c->L_probe.k() : c->L_atomic.k(), dperm, ptr[k], ptr[k + 1] - ptr[k],
+                              cnt_a, cnt_b, 0);
         if (e == cudaSuccess) e = launch_count_conflicts(cnt_a, c->nnz, dout, 0);
         if (e == cudaSuccess) e = launch_count_conflicts(cnt_b, c->n, dout, 0);
     }

@@ -82,40 +82,59 @@ struct GatherK {
 // TILE layout (ees_tile.cpp builds it; k_tile consumes it).  Rows are cut
 // into tiles; a tile's items are the FETs incident on its rows (boundary FETs
 // are copied into every tile they touch).  Each item's 16 contributions
-// (12 A pairs, 4 b rows) land in shared memory at slot p*kTileItems + item;
-// every owned target sums its slot list (u16) in a fixed order.  Everything a
-// tile needs except x and the A/b values is one 16-byte-aligned blob that a
-// TMA bulk copy (cp.async.bulk + mbarrier) brings into shared memory, double
-// buffered across the tiles a persistent CTA processes:
+// (12 A pairs, 4 b rows) land in shared memory at slot p*kTileItems + item.
+// The tile's targets are segments of one contribution list: owned targets
+// (every contributor in this tile; ascending global id) then side entries
+// (this tile's part of a target shared by several tiles).  The list is cut
+// into kTileThreads equal chunks of K entries, so every thread sums the same
+// number of contributions in a fixed order (a balanced segmented sum); a
+// segment that crosses a chunk boundary is completed from the per-thread
+// carries in thread order.  Everything a tile needs except x and the A/b
+// values is one 16-byte-aligned blob that a TMA bulk copy (cp.async.bulk +
+// mbarrier) brings into shared memory, kStages tiles ahead:
 //   TileHdr
 //   items:   term int4[ni] | beta f64[ni] | v0 f64[3][ni] | model u8[ni] (pad 16)
-//   program: runs int2[n_runs] (global start, length) | lstart u16[n_own+1] |
-//            lst u16[n_lst] (pad 16)
-//   side:    SideEnt[n_sent] | slst u16[n_slst] (pad 16)
-// Local target j maps to global target (A index, or nnz + b row) through the
-// runs; its contributions are lst[lstart[j] .. lstart[j+1]).
+//   xg:      int32[n_x] global ids of the owned targets after the tile rows'
+//            CSR block [a0, a0+na) and b rows [b0, b0+nb) (heavy-row slices,
+//            heavy x heavy targets); owned target j is A[a0+j] (j < na),
+//            b[b0+j-na] (j < na+nb), else global target xg[j-na-nb]
+//   tw:      u16[kTileThreads] per thread: first segment id | kTwCont | kTwNoEnd
+//   ent:     u16[K][kTileThreads] (thread-interleaved): byte offset 8*slot of the
+//            contribution in shared memory | kEntEnd on the
+//            last entry of a segment; padding points at the zero slot (pad 16)
+//   side:    SideEnt[n_sent] (pad 16)
+// Contributions of a FET whose source and bulk are one node (every PMOS of the
+// inverter configs) are merged at evaluation (DB into DS, BD into SD, BB into
+// SS, J[B] into J[S]) and the merged-away slots are not listed.
 constexpr int kTileItems = 128;      // max items (FET copies) per tile = threads per CTA
 constexpr int kTileThreads = 128;
 constexpr int kHeavyDeg = 64;        // nodes with more incident FETs are heavy
-constexpr int kStageMax = 12288;     // bytes of one pipeline stage (a tile blob)
+constexpr int kStageMax = 10496;     // bytes of one pipeline stage (a tile blob)
 constexpr int kStages = 3;           // TMA pipeline depth (blobs in flight per CTA)
-constexpr int kTilePrefetch = 6;     // owned targets whose A/b value a thread prefetches
+constexpr int kTilePrefetch = 4;     // owned targets whose A/b value a thread prefetches
+constexpr int kSegMax = 768;         // owned targets + side entries per tile
+constexpr int kZeroSlot = 16 * kTileItems;   // s_c[kZeroSlot] == 0.0 (list padding)
+constexpr uint16_t kEntEnd = 0x8000;
+constexpr uint16_t kTwCont = 0x8000;     // the thread's first entry continues a segment
+constexpr uint16_t kTwNoEnd = 0x4000;    // no segment ends in the thread's chunk
+constexpr uint16_t kTwSid = 0x0FFF;
 constexpr int64_t kSideInlineParts = 8192;   // up to this many parts: last CTA finalises
 constexpr int kMaxHot = 16;          // side targets pre-reduced per CTA (rails): parts = CTAs, not tiles
+static_assert(kSegMax <= kTwSid + 1, "segment ids must fit the thread word");
+static_assert(8 * kZeroSlot < kEntEnd, "entry byte offsets must fit 15 bits");
 
 struct TileHdr {
-    uint16_t n_items, n_own, n_runs, n_lst;
-    uint16_t n_sent, n_slst;
+    uint16_t n_items, n_own, n_x, n_sent, K, pad0;
+    int32_t a0, na, b0, nb;          // implicit owned targets: A[a0, a0+na), b[b0, b0+nb)
     uint32_t bytes;                  // blob size, multiple of 16
-    uint32_t off_prog, off_side;     // byte offsets of the program and side sections
-    uint32_t pad;
+    uint32_t off_x, off_tw, off_ent, off_side;   // byte offsets of the sections
+    uint32_t pad1[4];
 };
-static_assert(sizeof(TileHdr) == 28 || sizeof(TileHdr) == 32, "TileHdr layout");
+static_assert(sizeof(TileHdr) == 64, "TileHdr layout");
 
 struct SideEnt {
     int32_t sid;                     // side target
     int32_t slot;                    // this tile's part slot in `part`, or -1-h for hot target h
-    uint16_t lbeg, lcnt;             // range in slst
 };
 
 struct TileK {
@@ -128,6 +147,7 @@ struct TileK {
     int32_t n_hot;                 // hot side targets: CTA b's part at part[hot_base + h*grid + b]
     int64_t hot_base;
     const int32_t *sd_gid;         // [n_side] global target
+    const int32_t *hot_gid;        // [n_hot] global target of each hot side target
     const int32_t *sd_part;        // [n_side+1] partial ranges
     uint32_t *done;                // CTA completion ticket, self-resetting
     double *part;                  // [n_side_entries]
@@ -143,10 +163,11 @@ struct TileHost {
     int32_t n_tiles = 0, n_heavy = 0, n_side = 0;
     int64_t n_items = 0, n_owned = 0, n_side_entries = 0;
     int64_t n_parts = 0, hot_base = 0;
+    int64_t n_listed = 0, n_padded = 0;    // list entries, and with chunk padding
     int32_t blob_max = 0, n_hot = 0;
     std::vector<int64_t> blob_off;
     std::vector<uint8_t> blob;
-    std::vector<int32_t> sd_gid, sd_part;
+    std::vector<int32_t> sd_gid, sd_part, hot_gid;
 };
 // ees_tile.cpp.  Per-FET data for the item sections: beta (computed by the
 // caller exactly as for the other layouts), vprev [3][N], model.
@@ -158,7 +179,27 @@ bool build_tile_host(int64_t N, int32_t n_nodes, int32_t n, int64_t nnz, const i
                      TileHost &out);
 #endif
 
+// COLOR under EES_CONFLICT_HYBRID.  The layout is the
+// colour-major DevK with `slot` = [16][N]: 12 A pairs then 4 b rows, each
+// >= 0 (a target written with a plain read-modify-write: no two FETs of one
+// colour share it), -1 (none), or <= -2 (scratch slot -2-code: the target is
+// a side target, summed after the last colour).  Side targets' scratch slots
+// are contiguous per target (netlist order, then pair order), cut into
+// chunks of at most kChunk contributions.
+struct SideK {
+    double *buf;                 // [n_contrib] one slot per side contribution
+    int32_t n_side, n_chunks;
+    int64_t nnz;
+    const int64_t *chunk_lo;     // [n_chunks+1] ranges of buf
+    const int32_t *side_gid;     // [n_side] global target (A index, or nnz + b row)
+    const int32_t *side_chunk;   // [n_side+1] chunks of each side target
+    double *chunk_part;          // [n_chunks]
+};
+
 // ---- launchers (ees_kernels.cu); all asynchronous on `st` ----
+cudaError_t launch_color_h(const DevK &dv16, const CallK &call, int64_t begin, int64_t count,
+                           double *side_buf, cudaStream_t st);
+cudaError_t launch_side_sum(const SideK &sk, const CallK &call, cudaStream_t st, int *n_launches);
 int tile_blocks_per_sm();
 cudaError_t launch_tile(const TileK &tk, const CallK &call, int grid, cudaStream_t st, int *n_launches);
 cudaError_t launch_atomic(const DevK &dv, const CallK &call, int grid, cudaStream_t st);

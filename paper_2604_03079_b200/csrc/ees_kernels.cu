@@ -373,6 +373,93 @@ __global__ void k_gather_heavy(GatherK gk, CallK P)
 }
 
 // ---------------------------------------------------------------------------
+// COLOR under the degree-threshold hybrid rule: one
+// launch per colour; targets no two FETs of a colour share get a plain RMW,
+// side targets (heavy x heavy entries, heavy b rows with several writers) get
+// their contribution stored in its own scratch slot.  After the last colour,
+// k_side_chunks sums each chunk of a side target's slots (fixed tree) and
+// k_side_apply adds the chunk sums of each target in chunk order.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kBlock) k_color_h(DevK dv, CallK P, int64_t begin, int64_t count,
+                                                    double *side)
+{
+    __shared__ CardK s_cards[EES_MAX_MODELS];
+    for (int k = threadIdx.x; k < P.n_models; k += blockDim.x) s_cards[k] = P.cards[k];
+    __syncthreads();
+    const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= count) return;
+    const int64_t i = begin + q;
+    int32_t slot[NPAIR + 4];
+#pragma unroll
+    for (int p = 0; p < NPAIR + 4; p++) slot[p] = __ldg(dv.slot + (int64_t)p * dv.N + i);
+    const int4 T = __ldg(dv.term + i);
+    const double beta = __ldg(dv.beta + i);
+    const double a0 = __ldg(dv.v0 + i), a1 = __ldg(dv.v0 + dv.N + i), a2 = __ldg(dv.v0 + 2 * dv.N + i);
+    const int m = __ldg(dv.model + i);
+    const double VD = T.x >= 0 ? __ldg(P.x + T.x) : 0.0;
+    const double VG = T.y >= 0 ? __ldg(P.x + T.y) : 0.0;
+    const double VS = T.z >= 0 ? __ldg(P.x + T.z) : 0.0;
+    Stamp st;
+    eval_fet(s_cards[m], beta, P.gmin, VD, VG, VS, a0, a1, a2, st);
+#pragma unroll
+    for (int p = 0; p < NPAIR; p++) {
+        if (slot[p] >= 0) P.A[slot[p]] += st.y[p];
+        else if (slot[p] <= -2) side[-2 - slot[p]] = st.y[p];
+    }
+#pragma unroll
+    for (int a = 0; a < 4; a++) {
+        const int32_t k = slot[NPAIR + a];
+        if (k >= 0) P.b[k] += st.j[a];
+        else if (k <= -2) side[-2 - k] = st.j[a];
+    }
+}
+
+__global__ void __launch_bounds__(kBlock) k_side_chunks(SideK sk)
+{
+    __shared__ double s_w[kBlock / 32];
+    const int64_t lo = sk.chunk_lo[blockIdx.x], hi = sk.chunk_lo[blockIdx.x + 1];
+    double v = 0.0;
+    for (int64_t k = lo + threadIdx.x; k < hi; k += blockDim.x) v += sk.buf[k];
+    v = warp_sum(v);
+    if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); w++) t += s_w[w];
+        sk.chunk_part[blockIdx.x] = t;
+    }
+}
+
+__global__ void k_side_apply(SideK sk, CallK P)
+{
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= sk.n_side) return;
+    double t = 0.0;
+    for (int32_t c = sk.side_chunk[s]; c < sk.side_chunk[s + 1]; c++) t += sk.chunk_part[c];
+    const int64_t g = sk.side_gid[s];
+    if (g < sk.nnz) P.A[g] += t;
+    else P.b[g - sk.nnz] += t;
+}
+
+cudaError_t launch_color_h(const DevK &dv16, const CallK &call, int64_t begin, int64_t count,
+                           double *side_buf, cudaStream_t st)
+{
+    if (count == 0) return cudaSuccess;
+    k_color_h<<<(unsigned)((count + kBlock - 1) / kBlock), kBlock, 0, st>>>(dv16, call, begin, count, side_buf);
+    return cudaPeekAtLastError();
+}
+
+cudaError_t launch_side_sum(const SideK &sk, const CallK &call, cudaStream_t st, int *n_launches)
+{
+    *n_launches = 0;
+    if (sk.n_side == 0) return cudaSuccess;
+    k_side_chunks<<<sk.n_chunks, kBlock, 0, st>>>(sk);
+    k_side_apply<<<(sk.n_side + 127) / 128, 128, 0, st>>>(sk, call);
+    *n_launches = 2;
+    return cudaPeekAtLastError();
+}
+
+// ---------------------------------------------------------------------------
 // Race instrument: per colour, count distinct-device writers
 // of every non-rail A entry and b row.
 // ---------------------------------------------------------------------------
@@ -687,7 +774,8 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase)
         : "memory");
 }
 
-constexpr size_t kTileSmem = sizeof(double) * 16 * kTileItems + kStages * (size_t)kStageMax;
+constexpr int kSlots = kZeroSlot + 2;          // 16 contributions per item + the zero slot (+pad)
+constexpr size_t kTileSmem = sizeof(double) * (kSlots + kSegMax + kTileThreads) + kStages * (size_t)kStageMax;
 
 // Views into one staged tile blob (layout in ees_internal.h).
 struct TileView {
@@ -695,10 +783,9 @@ struct TileView {
     const int4 *term;
     const double *beta, *v0;
     const uint8_t *model;
-    const int2 *runs;
-    const uint16_t *lstart, *lst;
+    const int32_t *xg;
+    const uint16_t *tw, *ent;
     const SideEnt *sents;
-    const uint16_t *slst;
 };
 
 __device__ __forceinline__ TileView tile_view(const unsigned char *blob)
@@ -706,24 +793,34 @@ __device__ __forceinline__ TileView tile_view(const unsigned char *blob)
     TileView v;
     v.hdr = *reinterpret_cast<const TileHdr *>(blob);
     const int ni = v.hdr.n_items;
-    const unsigned char *items = blob + ((sizeof(TileHdr) + 15) & ~(size_t)15);
+    const unsigned char *items = blob + sizeof(TileHdr);
     v.term = reinterpret_cast<const int4 *>(items);
     v.beta = reinterpret_cast<const double *>(items + 16 * (size_t)ni);
     v.v0 = v.beta + ni;
     v.model = reinterpret_cast<const uint8_t *>(v.v0 + 3 * (size_t)ni);
-    v.runs = reinterpret_cast<const int2 *>(blob + v.hdr.off_prog);
-    v.lstart = reinterpret_cast<const uint16_t *>(v.runs + v.hdr.n_runs);
-    v.lst = v.lstart + v.hdr.n_own + 1;
+    v.xg = reinterpret_cast<const int32_t *>(blob + v.hdr.off_x);
+    v.tw = reinterpret_cast<const uint16_t *>(blob + v.hdr.off_tw);
+    v.ent = reinterpret_cast<const uint16_t *>(blob + v.hdr.off_ent);
     v.sents = reinterpret_cast<const SideEnt *>(blob + v.hdr.off_side);
-    v.slst = reinterpret_cast<const uint16_t *>(v.sents + v.hdr.n_sent);
     return v;
 }
 
+// Address of owned target j (< n_own): the tile rows' CSR block, their b
+// rows, then the explicit ids.
+__device__ __forceinline__ double *owned_ptr(const TileView &v, const TileK &tk, const CallK &P, int j)
+{
+    const int na = v.hdr.na, nab = na + v.hdr.nb;
+    if (j < na) return P.A + v.hdr.a0 + j;
+    if (j < nab) return P.b + v.hdr.b0 + (j - na);
+    const int32_t g = v.xg[j - nab];
+    return g < tk.nnz ? P.A + g : P.b + (g - tk.nnz);
+}
+
 // What a thread gathers from global memory for one tile: its item's node
-// voltages and the current values of the targets it owns.
+// voltages and the current values of the owned targets it writes.
 struct TileRegs {
     double VD, VG, VS;
-    int32_t gid[kTilePrefetch];
+    double *dst[kTilePrefetch];
     double pre[kTilePrefetch];
 };
 
@@ -738,34 +835,12 @@ __device__ __forceinline__ void tile_gather(const TileView &v, const TileK &tk, 
         R.VG = T.y >= 0 ? __ldg(P.x + T.y) : 0.0;
         R.VS = T.z >= 0 ? __ldg(P.x + T.z) : 0.0;
     }
-    int r = 0, rbase = 0;
 #pragma unroll
     for (int k = 0; k < kTilePrefetch; k++) {
         const int j = tid + k * kTileThreads;
-        R.gid[k] = -1;
-        R.pre[k] = 0.0;
-        if (j < v.hdr.n_own) {
-            while (j >= rbase + v.runs[r].y) { rbase += v.runs[r].y; r++; }
-            const int32_t g = v.runs[r].x + (j - rbase);
-            R.gid[k] = g;
-            R.pre[k] = g < tk.nnz ? P.A[g] : P.b[g - tk.nnz];
-        }
+        R.dst[k] = j < v.hdr.n_own ? owned_ptr(v, tk, P, j) : nullptr;
+        R.pre[k] = R.dst[k] ? *R.dst[k] : 0.0;
     }
-}
-
-__device__ __forceinline__ double sum_list(const double *s_c, const uint16_t *lst, int l0, int l1)
-{
-    double s = 0.0;
-    int l = l0;
-    for (; l + 4 <= l1; l += 4) {            // four independent loads, summed in list order
-        const double a = s_c[lst[l]], b = s_c[lst[l + 1]], c = s_c[lst[l + 2]], d = s_c[lst[l + 3]];
-        s += a;
-        s += b;
-        s += c;
-        s += d;
-    }
-    for (; l < l1; l++) s += s_c[lst[l]];
-    return s;
 }
 
 // Fixed-order sum of one side target's parts by a whole warp (fixed lane
@@ -794,20 +869,22 @@ __device__ __forceinline__ void side_finish(const TileK &tk, const CallK &P, int
 
 // ---------------------------------------------------------------------------
 // TILE (deterministic, one launch, +1 for many side targets): persistent CTAs
-// walk the tiles blockIdx.x, +gridDim.x, ...  Pipeline per CTA:
-//   * thread 0 keeps the next tile's blob in flight (TMA bulk copy into the
-//     other stage of a double buffer);
-//   * each thread holds in registers the x values of its item and the current
-//     A/b values of the targets it owns for the current tile, and gathers
-//     those of the next tile while the current tile's sums run;
-//   1. evaluate one item (FET copy) from shared memory, stage its 16
-//      contributions in shared memory;
-//   2. each owned target (all contributors in this tile) sums its slot list in
-//      list order and stores value + sum -- no other CTA writes it;
-//   3. side targets (heavy x heavy entries, heavy b rows shared by tiles):
-//      store this tile's part; after every tile, a fence + a ticket: the last
-//      CTA sums the parts of every side target in part order (few parts), or
-//      k_side_final does it (many).
+// walk the tiles blockIdx.x, +gridDim.x, ...  Per tile t:
+//   eval   each thread evaluates one item (FET copy) from the staged blob and
+//          stores its 16 contributions in shared memory; then it gathers the
+//          x values and current A/b values of tile t+1 (whose blob is already
+//          in shared memory) so their latency hides behind the sums;
+//   B1     contributions complete; the stage of tile t-1 is free -> thread 0
+//          issues the TMA bulk copy of tile t-1+kStages*G into it;
+//   sums   balanced segmented sum: thread j adds its K list entries in order,
+//          stores a segment's sum at its end, its trailing partial as a carry;
+//   B2     fix-up: a segment that began in earlier chunks adds their carries
+//          (nearest first; fixed order);
+//   B3     write: owned target j -> value + sum (a plain store, no other CTA
+//          writes it, coalesced along runs); side entries -> part slots, or
+//          the CTA's hot partial (rails) in tile order.
+// After the last tile, hot partials are stored per CTA, and side targets are
+// summed in part order by the last CTA (few parts) or k_side_final.
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ unsigned long long globaltimer()
 {
@@ -817,22 +894,33 @@ __device__ __forceinline__ unsigned long long globaltimer()
 }
 #define TILE_TRACE(slot)                                                            \
     do {                                                                            \
-        if (tk.trace && tid == 0 && (slot) < kTraceSlots)                           \
+        if (kTrace && tid == 0 && (slot) < kTraceSlots)                             \
             tk.trace[(size_t)blockIdx.x * kTraceSlots + (slot)] = globaltimer();    \
     } while (0)
 
+template <bool kTrace>
 __global__ void __launch_bounds__(kTileThreads, 4) k_tile(TileK tk, CallK P)
 {
     extern __shared__ __align__(16) unsigned char smem[];
-    double *s_c = reinterpret_cast<double *>(smem);                       // [16][kTileItems]
-    unsigned char *s_stage = smem + sizeof(double) * 16 * kTileItems;      // [kStages][kStageMax]
+    double *s_c = reinterpret_cast<double *>(smem);          // [16][kTileItems] + zero slot
+    double *s_seg = s_c + kSlots;                            // [kSegMax] segment sums
+    double *s_carry = s_seg + kSegMax;                       // [kTileThreads]
+    unsigned char *s_stage = reinterpret_cast<unsigned char *>(s_carry + kTileThreads);
     __shared__ CardK s_cards[EES_MAX_MODELS];
     __shared__ __align__(8) uint64_t s_bar[kStages];
-    __shared__ double s_hot[kMaxHot];
+    __shared__ double s_hot[kMaxHot], s_hot_pre[kMaxHot];
+    __shared__ double *s_hot_dst[kMaxHot];
     __shared__ int s_last;
     const int tid = threadIdx.x, lane = tid & 31;
     const int32_t G = gridDim.x;
     if (tid < kMaxHot) s_hot[tid] = 0.0;
+    if (tid < tk.n_hot) {            // hot side targets: only the finisher writes them
+        const int32_t g = tk.hot_gid[tid];
+        double *d = g < tk.nnz ? P.A + g : P.b + (g - tk.nnz);
+        s_hot_dst[tid] = d;
+        s_hot_pre[tid] = *d;
+    }
+    if (tid == 0) s_c[kZeroSlot] = 0.0;
     auto issue = [&](int32_t tile, int stage) {
         const int64_t off = tk.blob_off[tile];
         const uint32_t bytes = (uint32_t)(tk.blob_off[tile + 1] - off);
@@ -860,6 +948,7 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_tile(TileK tk, CallK P)
         tile_gather(v, tk, P, cur);
     }
     TILE_TRACE(1);
+    const unsigned char *s_cb = reinterpret_cast<const unsigned char *>(s_c);
     for (int32_t t = t0; t < tk.n_tiles; t += G, it++) {
         const int32_t tn = t + G;
         const int sn = stage + 1 == kStages ? 0 : stage + 1;
@@ -868,12 +957,19 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_tile(TileK tk, CallK P)
             Stamp st;
             eval_fet(s_cards[v.model[tid]], v.beta[tid], P.gmin, cur.VD, cur.VG, cur.VS, v.v0[tid],
                      v.v0[ni + tid], v.v0[2 * ni + tid], st);
+            const int4 T = v.term[tid];
+            if (T.z == T.w && T.z != -1) {        // source tied to bulk: one entry each (ees_internal.h)
+                st.y[DS] += st.y[DB];
+                st.y[SD] += st.y[BD];
+                st.y[SS] += st.y[BB];
+                st.j[2] += st.j[3];
+            }
 #pragma unroll
             for (int p = 0; p < NPAIR; p++) s_c[p * kTileItems + tid] = st.y[p];
 #pragma unroll
             for (int a = 0; a < 4; a++) s_c[(NPAIR + a) * kTileItems + tid] = st.j[a];
         }
-        // next tile: its blob was issued >= one iteration ago; start its gathers now
+        // next tile: its blob was issued >= one tile ago; start its gathers now
         TileView vn;
         if (tn < tk.n_tiles) {
             mbar_wait(&s_bar[sn], (parity >> sn) & 1u);
@@ -882,46 +978,63 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_tile(TileK tk, CallK P)
             tile_gather(vn, tk, P, nxt);
         }
         TILE_TRACE(2 + 4 * it);
-        __syncthreads();
+        __syncthreads();                                        // B1
+        if (tid == 0 && it > 0) {
+            const int32_t tr = t - G + kStages * G;             // refill the stage of tile t-G
+            if (tr < tk.n_tiles) issue(tr, stage == 0 ? kStages - 1 : stage - 1);
+        }
+        // balanced segmented sum (entries are byte offsets into s_c | kEntEnd)
+        const uint16_t w = v.tw[tid];
+        {
+            const int K = v.hdr.K;
+            const uint16_t *e = v.ent + tid;
+            int sid = w & kTwSid;
+            double s = 0.0;
+#pragma unroll 4
+            for (int k = 0; k < K; k++) {
+                const uint32_t x = e[k * kTileThreads];
+                s += *reinterpret_cast<const double *>(s_cb + (x & 0x7FFFu));
+                if (x & kEntEnd) {
+                    s_seg[sid++] = s;
+                    s = 0.0;
+                }
+            }
+            s_carry[tid] = s;
+        }
         TILE_TRACE(3 + 4 * it);
-        // owned targets
+        __syncthreads();                                        // B2
+        if ((w & (kTwCont | kTwNoEnd)) == kTwCont) {
+            int k = tid - 1;
+            double acc = s_carry[k];
+            while ((v.tw[k] & (kTwCont | kTwNoEnd)) == (kTwCont | kTwNoEnd)) {
+                k--;
+                acc += s_carry[k];
+            }
+            s_seg[w & kTwSid] += acc;
+        }
+        __syncthreads();                                        // B3
+        TILE_TRACE(4 + 4 * it);
+        const int n_own = v.hdr.n_own;
 #pragma unroll
-        for (int k = 0; k < kTilePrefetch; k++) {
-            const int j = tid + k * kTileThreads;
-            if (j < v.hdr.n_own) {
-                const double s = sum_list(s_c, v.lst, v.lstart[j], v.lstart[j + 1]);
-                const int32_t g = cur.gid[k];
-                if (g < tk.nnz) P.A[g] = cur.pre[k] + s;
-                else P.b[g - tk.nnz] = cur.pre[k] + s;
-            }
-        }
-        if (v.hdr.n_own > kTilePrefetch * kTileThreads) {
-            int r = 0, rbase = 0;
-            for (int j = tid + kTilePrefetch * kTileThreads; j < v.hdr.n_own; j += kTileThreads) {
-                while (j >= rbase + v.runs[r].y) { rbase += v.runs[r].y; r++; }
-                const int32_t g = v.runs[r].x + (j - rbase);
-                const double s = sum_list(s_c, v.lst, v.lstart[j], v.lstart[j + 1]);
-                if (g < tk.nnz) P.A[g] += s;
-                else P.b[g - tk.nnz] += s;
-            }
-        }
+        for (int k = 0; k < kTilePrefetch; k++)
+            if (cur.dst[k]) *cur.dst[k] = cur.pre[k] + s_seg[tid + k * kTileThreads];
+        for (int j = tid + kTilePrefetch * kTileThreads; j < n_own; j += kTileThreads)
+            *owned_ptr(v, tk, P, j) += s_seg[j];
         // side parts (plain stores; ordered by the fence + ticket below); a hot
         // target appears at most once per tile, so one thread owns s_hot[h] here
         for (int e = tid; e < v.hdr.n_sent; e += kTileThreads) {
             const SideEnt se = v.sents[e];
-            const double part = sum_list(s_c, v.slst, se.lbeg, se.lbeg + se.lcnt);
+            const double part = s_seg[n_own + e];
             if (se.slot >= 0) tk.part[se.slot] = part;
             else s_hot[-1 - se.slot] += part;
         }
-        TILE_TRACE(4 + 4 * it);
-        __syncthreads();          // s_c and this stage are free again
         TILE_TRACE(5 + 4 * it);
-        if (tid == 0 && t + kStages * G < tk.n_tiles) issue(t + kStages * G, stage);
         stage = sn;
         v = vn;
         cur = nxt;
     }
     if (tk.n_side) {
+        __syncthreads();
         for (int h = tid; h < tk.n_hot; h += kTileThreads) tk.part[tk.hot_base + (int64_t)h * G + blockIdx.x] = s_hot[h];
         if (tk.side_inline) {
             __threadfence();
@@ -931,7 +1044,26 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_tile(TileK tk, CallK P)
             TILE_TRACE(kTraceSlots - 2);
             if (s_last) {
                 __threadfence();
-                for (int32_t sid = tid >> 5; sid < tk.n_side; sid += kTileThreads >> 5) side_finish(tk, P, sid, lane);
+                // hot targets (one part per CTA): a warp each, fixed lane
+                // stride, eight loads in flight per lane, fixed shuffle tree
+                for (int h = tid >> 5; h < tk.n_hot; h += kTileThreads >> 5) {
+                    const double *pp = tk.part + tk.hot_base + (int64_t)h * G;
+                    double u = 0.0;
+                    for (int q0 = 0; q0 < G; q0 += 256) {
+                        double a[8];
+#pragma unroll
+                        for (int r = 0; r < 8; r++) {
+                            const int q = q0 + r * 32 + lane;
+                            a[r] = q < G ? __ldcg(pp + q) : 0.0;
+                        }
+#pragma unroll
+                        for (int r = 0; r < 8; r++) u += a[r];
+                    }
+                    u = warp_sum(u);
+                    if (lane == 0) *s_hot_dst[h] = s_hot_pre[h] + u;
+                }
+                for (int32_t sid = tid >> 5; sid < tk.n_side; sid += kTileThreads >> 5)
+                    if (__ldg(tk.sd_part + 2 * sid) < tk.hot_base || tk.n_hot == 0) side_finish(tk, P, sid, lane);
                 if (tid == 0) *tk.done = 0;
             }
         }
@@ -947,9 +1079,10 @@ __global__ void __launch_bounds__(256) k_side_final(TileK tk, CallK P)
 
 int tile_blocks_per_sm()
 {
-    cudaFuncSetAttribute(k_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmem);
+    cudaFuncSetAttribute(k_tile<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmem);
+    cudaFuncSetAttribute(k_tile<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmem);
     int nb = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_tile, kTileThreads, kTileSmem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_tile<false>, kTileThreads, kTileSmem);
     return nb > 0 ? nb : 1;
 }
 
@@ -957,7 +1090,8 @@ cudaError_t launch_tile(const TileK &tk, const CallK &call, int grid, cudaStream
 {
     *n_launches = 0;
     if (tk.n_tiles == 0) return cudaSuccess;
-    k_tile<<<grid, kTileThreads, kTileSmem, st>>>(tk, call);
+    if (tk.trace) k_tile<true><<<grid, kTileThreads, kTileSmem, st>>>(tk, call);
+    else k_tile<false><<<grid, kTileThreads, kTileSmem, st>>>(tk, call);
     *n_launches = 1;
     if (tk.n_side && !tk.side_inline) {
         k_side_final<<<(unsigned)((tk.n_side * 32 + 255) / 256), 256, 0, st>>>(tk, call);

@@ -23,14 +23,14 @@ namespace ees {
 namespace {
 constexpr int32_t kUnset = -1;
 constexpr int32_t kSide = -2;
-// Upper bound of a tile's blob while it is being formed: header, items (49 B),
-// owned targets (2 B list start each), runs (8 B; one per row-range break,
-// heavy slice entry and heavy x heavy target), list entries (2 B per live
-// contribution of the items), heavy x heavy contributions as side entries
-// (12 B) -- plus padding of the three sections.
-constexpr int64_t kBlobFixed = 32 + 48 + 2;
-constexpr int64_t kOwnMax = 4096;      // u16 list starts also bound the owned count
-
+// Upper bound of a tile's blob while it is being formed: items (49 B + 2 B
+// per listed contribution), one padding entry per owned target nobody stamps
+// (2 B), explicit ids of heavy-row slice targets (4 B), heavy x heavy targets
+// (4 B id or an 8 B side entry) -- plus the fixed per-tile parts: header,
+// thread words (256 B), list padding to whole chunks (< 256 B) and the
+// padding of four sections.
+constexpr int64_t kBlobFixed = 64 + 256 + 256 + 64;
+constexpr int64_t kOwnMax = kSegMax;   // owned targets + side entries (s_seg capacity)
 size_t pad16(size_t x) { return (x + 15) & ~(size_t)15; }
 }  // namespace
 
@@ -42,6 +42,13 @@ bool build_tile_host(int64_t N, int32_t n_nodes, int32_t n, int64_t nnz, const i
                      TileHost &out)
 {
     static_assert(kOwnMax > 64, "tile budget too small");
+    // source tied to bulk: the kernel merges DB/BD/BB/J[B] into DS/SD/SS/J[S]
+    auto merged = [&](int64_t i) { return TT[2][i] == TT[3][i] && TT[2][i] != -1; };
+    // is contribution p (12 pairs, then 4 b rows) of FET i in a list?
+    auto listed_c = [&](int64_t i, int p) -> bool {
+        if (p < NPAIR) return raw_slot[p * N + i] >= 0 && !(merged(i) && (p == DB || p == BD || p == BB));
+        return TT[p - NPAIR][i] >= 0 && !(p == NPAIR + 3 && merged(i));
+    };
     const int32_t NN = std::max(1, n_nodes);
     // A light row whose FETs alone overflow a tile (pathological: many heavy x
     // heavy entries on few FETs) is promoted to heavy and the partition redone.
@@ -75,9 +82,18 @@ bool build_tile_host(int64_t N, int32_t n_nodes, int32_t n, int64_t nnz, const i
     };
     auto live_count = [&](int64_t i) {
         int32_t k = 0;
-        for (int p = 0; p < NPAIR; p++) k += raw_slot[p * N + i] >= 0;
-        for (int a = 0; a < 4; a++) k += TT[a][i] >= 0;
+        for (int p = 0; p < NPAIR + 4; p++) k += listed_c(i, p);
         return k;
+    };
+    // targets some FET stamps (an owned target nobody stamps costs one padding entry)
+    std::vector<uint8_t> has_c((size_t)(nnz + n), 0);
+    for (int64_t i = 0; i < N; i++)
+        for (int p = 0; p < NPAIR + 4; p++)
+            if (listed_c(i, p)) has_c[p < NPAIR ? raw_slot[p * N + i] : nnz + TT[p - NPAIR][i]] = 1;
+    auto empty_in_row = [&](int32_t r) {
+        int64_t e = has_c[nnz + r] ? 0 : 1;
+        for (int32_t k = row_ptr[r]; k < row_ptr[r + 1]; k++) e += !has_c[k];
+        return e;
     };
     // heavy x heavy contributions of a FET (owned by its home tile or side)
     auto hh_count = [&](int64_t i) {
@@ -143,11 +159,14 @@ bool build_tile_host(int64_t N, int32_t n_nodes, int32_t n, int64_t nnz, const i
     std::fill(hh_seen.begin(), hh_seen.end(), -1);
     for (int32_t v = 0; v < n_nodes; v++) {
         if (heavy[v]) continue;
+        // a tile's rows are consecutive, so its owned entries of A and b are
+        // one CSR block and one row range (implicit ids in the blob)
+        if (!cur.empty() && last_row != v - 1) close_tile();
         for (int pass = 0; pass < 2; pass++) {
             int32_t fresh = 0;
             const int64_t hs = hs_ptr[v + 1] - hs_ptr[v];
             int64_t add_own = (row_ptr[v + 1] - row_ptr[v]) + 1 + hs;
-            int64_t add_bytes = 2 * add_own + 8 * (hs + ((!cur.empty() && last_row == v - 1) ? 0 : 2));
+            int64_t add_bytes = 2 * empty_in_row(v) + 4 * hs;
             for (int64_t k = iptr[v]; k < iptr[v + 1]; k++) {
                 const int32_t i = idev[k];
                 if (mark[i] != t) {
@@ -157,7 +176,7 @@ bool build_tile_host(int64_t N, int32_t n_nodes, int32_t n, int64_t nnz, const i
                 if (home[i] < 0) {
                     const int32_t hh = hh_new(i, t);
                     add_own += hh;
-                    add_bytes += 22 * hh;
+                    add_bytes += 12 * hh;
                 }
             }
             const bool over = (int64_t)cur.size() + fresh > kTileItems || own + add_own > kOwnMax ||
@@ -193,7 +212,7 @@ bool build_tile_host(int64_t N, int32_t n_nodes, int32_t n, int64_t nnz, const i
     for (int64_t i = 0; i < N; i++)
         if (home[i] < 0) {
             const int32_t add = hh_count(i);
-            const int64_t add_bytes = 49 + 2 * live_count(i) + 22 * add;
+            const int64_t add_bytes = 49 + 2 * live_count(i) + 12 * add;
             if (!cur.empty() && ((int64_t)cur.size() + 1 > kTileItems || own + add > kOwnMax ||
                                  bytes + add_bytes > kStageMax))
                 close_tile();
@@ -232,9 +251,9 @@ bool build_tile_host(int64_t N, int32_t n_nodes, int32_t n, int64_t nnz, const i
     // ---- per tile: blob = header | items | owned program | side entries
     std::vector<int32_t> sid_of((size_t)NT, -1);
     std::vector<std::pair<int32_t, uint16_t>> con, side;
-    std::vector<int32_t> gids;
-    std::vector<std::pair<int32_t, int32_t>> runs;
-    std::vector<uint16_t> lstart, lst, slst;
+    std::vector<int32_t> gids, xg;
+    std::vector<uint16_t> ent, tw;
+    std::vector<int32_t> seg_of;
     std::vector<SideEnt> sents;
     std::vector<int32_t> sent_tile_sid;     // side id of each entry, in emission order
     out.blob_off.push_back(0);
@@ -259,17 +278,15 @@ bool build_tile_host(int64_t N, int32_t n_nodes, int32_t n, int64_t nnz, const i
             const int32_t i = item_dev[q];
             const int32_t loc = q - q0;
             for (int p = 0; p < NPAIR + 4; p++) {
+                if (!listed_c(i, p)) continue;
                 int64_t g;
                 int32_t r, c;
                 if (p < NPAIR) {
-                    const int32_t k = raw_slot[p * N + i];
-                    if (k < 0) continue;
-                    g = k;
+                    g = raw_slot[p * N + i];
                     r = TT[pair_row(p)][i];
                     c = TT[pair_col(p)][i];
                 } else {
                     r = TT[p - NPAIR][i];
-                    if (r < 0) continue;
                     g = nnz + r;
                     c = r;
                 }
@@ -288,58 +305,135 @@ bool build_tile_host(int64_t N, int32_t n_nodes, int32_t n, int64_t nnz, const i
         };
         std::stable_sort(con.begin(), con.end(), by_target);
         std::stable_sort(side.begin(), side.end(), by_target);
-        // owned lists in target order; runs of consecutive global ids
-        lstart.assign(1, 0);
-        lst.clear();
-        runs.clear();
-        size_t ci = 0;
-        for (size_t j = 0; j < gids.size(); j++) {
-            const int32_t g = gids[j];
-            if (ci < con.size() && con[ci].first < g) return false;   // contribution without an owned slot
-            while (ci < con.size() && con[ci].first == g) lst.push_back(con[ci++].second);
-            lstart.push_back((uint16_t)lst.size());
-            if (!runs.empty() && runs.back().first + runs.back().second == g) runs.back().second++;
-            else runs.emplace_back(g, 1);
+        // segments, in owned order: the tile rows' CSR block [a0, a0+na) and
+        // b rows [b0, b0+nb) (implicit ids; an entry nobody stamps gets one
+        // padding entry), then the other owned targets (heavy-row slices and
+        // heavy x heavy targets; explicit ids, ascending), then side entries
+        int32_t a0 = 0, na = 0, b0 = 0, nb = 0;
+        if (tile_rows_ptr[tt + 1] > tile_rows_ptr[tt]) {
+            const int32_t r0 = tile_rows[tile_rows_ptr[tt]], r1 = tile_rows[tile_rows_ptr[tt + 1] - 1];
+            if (r1 - r0 + 1 != tile_rows_ptr[tt + 1] - tile_rows_ptr[tt]) return false;   // rows not consecutive
+            a0 = row_ptr[r0];
+            na = row_ptr[r1 + 1] - a0;
+            b0 = r0;
+            nb = r1 - r0 + 1;
         }
-        if (ci != con.size()) return false;
-        listed += (int64_t)lst.size();
+        ent.clear();
+        xg.clear();
+        size_t ci = 0;
+        int32_t seg = 0;
+        auto take = [&](int64_t g) {      // the segment of target g: its entries, or one pad
+            const size_t c0 = ci;
+            while (ci < con.size() && con[ci].first == g) ci++;
+            if (ci == c0) ent.push_back((uint16_t)(8 * kZeroSlot | kEntEnd));
+            for (size_t k = c0; k < ci; k++) ent.push_back((uint16_t)(8 * con[k].second | (k + 1 == ci ? kEntEnd : 0)));
+            seg_of.resize(ent.size(), seg);
+            seg++;
+        };
+        seg_of.clear();
+        // con is sorted by target: extras below a0, the CSR block, extras up to
+        // nnz, then b rows (the tile's range and heavy extras)
+        std::vector<int64_t> extra_g;
+        {
+            size_t k = 0;
+            while (k < con.size()) {
+                const int64_t g = con[k].first;
+                const bool mainA = g >= a0 && g < (int64_t)a0 + na;
+                const bool mainB = g >= nnz + b0 && g < nnz + b0 + nb;
+                if (!mainA && !mainB) {
+                    if (std::find(gids.begin(), gids.end(), (int32_t)g) == gids.end()) return false;
+                    extra_g.push_back(g);
+                }
+                while (k < con.size() && con[k].first == g) k++;
+            }
+        }
+        // walk con once per class (it is sorted; each class is a sorted subset)
+        std::vector<std::pair<int32_t, uint16_t>> con_all;
+        con_all.swap(con);
+        auto class_of = [&](int64_t g) {
+            if (g >= a0 && g < (int64_t)a0 + na) return 0;
+            if (g >= nnz + b0 && g < nnz + b0 + nb) return 1;
+            return 2;
+        };
+        for (int cls = 0; cls < 3; cls++) {
+            con.clear();
+            for (auto &e2 : con_all)
+                if (class_of(e2.first) == cls) con.push_back(e2);
+            ci = 0;
+            if (cls == 0)
+                for (int64_t g = a0; g < (int64_t)a0 + na; g++) take(g);
+            else if (cls == 1)
+                for (int64_t g = nnz + b0; g < nnz + b0 + nb; g++) take(g);
+            else
+                for (int64_t g : extra_g) {
+                    take(g);
+                    xg.push_back((int32_t)g);
+                }
+            if (ci != con.size()) return false;
+        }
+        const int32_t n_own = seg;
+        listed += (int64_t)con_all.size();
+        con.swap(con_all);
         // side entries (slot filled below, once every side target's entry count is known)
         sents.clear();
-        slst.clear();
+        int32_t n_sent = 0;
         for (size_t k = 0; k < side.size(); k++) {
-            if (k == 0 || side[k].first != side[k - 1].first) {
-                int32_t &sid = sid_of[side[k].first];
+            const int32_t g = side[k].first;
+            if (k == 0 || g != side[k - 1].first) {
+                int32_t &sid = sid_of[g];
                 if (sid < 0) {
                     sid = (int32_t)out.sd_gid.size();
-                    out.sd_gid.push_back(side[k].first);
+                    out.sd_gid.push_back(g);
                 }
                 SideEnt se;
                 se.sid = sid;
                 se.slot = -1;
-                se.lbeg = (uint16_t)slst.size();
-                se.lcnt = 0;
                 sents.push_back(se);
                 sent_tile_sid.push_back(sid);
+                n_sent++;
             }
-            slst.push_back(side[k].second);
-            sents.back().lcnt++;
+            const bool last = k + 1 == side.size() || side[k + 1].first != g;
+            ent.push_back((uint16_t)(8 * side[k].second | (last ? kEntEnd : 0)));
+            seg_of.push_back(n_own + n_sent - 1);
+        }
+        listed += (int64_t)side.size();
+        if (n_own + n_sent > kSegMax) return false;
+        // equal chunks of K entries per thread, thread-interleaved
+        const int64_t L = (int64_t)ent.size();
+        const int32_t K = (int32_t)((L + kTileThreads - 1) / kTileThreads);
+        tw.assign(kTileThreads, 0);
+        for (int32_t th2 = 0; th2 < kTileThreads; th2++) {
+            const int64_t p0 = (int64_t)th2 * K;
+            if (p0 >= L) {
+                tw[th2] = kTwNoEnd;
+                continue;
+            }
+            uint16_t w = (uint16_t)seg_of[p0];
+            if (p0 > 0 && seg_of[p0 - 1] == seg_of[p0]) w |= kTwCont;
+            bool any_end = false;
+            for (int64_t p2 = p0; p2 < std::min<int64_t>(L, p0 + K); p2++) any_end |= (ent[p2] & kEntEnd) != 0;
+            if (!any_end) w |= kTwNoEnd;
+            tw[th2] = w;
         }
         // emit the blob
         TileHdr hdr;
         std::memset(&hdr, 0, sizeof(hdr));
         hdr.n_items = (uint16_t)ni;
-        hdr.n_own = (uint16_t)gids.size();
-        hdr.n_runs = (uint16_t)runs.size();
-        hdr.n_lst = (uint16_t)lst.size();
-        hdr.n_sent = (uint16_t)sents.size();
-        hdr.n_slst = (uint16_t)slst.size();
+        hdr.n_own = (uint16_t)n_own;
+        hdr.n_x = (uint16_t)xg.size();
+        hdr.n_sent = (uint16_t)n_sent;
+        hdr.K = (uint16_t)K;
+        hdr.a0 = a0;
+        hdr.na = na;
+        hdr.b0 = b0;
+        hdr.nb = nb;
         const size_t items_bytes = pad16((size_t)ni * 49);
-        hdr.off_prog = (uint32_t)(pad16(sizeof(TileHdr)) + items_bytes);
-        const size_t prog_bytes = pad16(8 * runs.size() + 2 * lstart.size() + 2 * lst.size());
-        hdr.off_side = (uint32_t)(hdr.off_prog + prog_bytes);
-        const size_t side_bytes = pad16(sizeof(SideEnt) * sents.size() + 2 * slst.size());
-        const size_t bytes = hdr.off_side + side_bytes;
-        if (bytes > (size_t)kStageMax || gids.size() > 65535 || lst.size() > 65535) return false;
+        hdr.off_x = (uint32_t)(pad16(sizeof(TileHdr)) + items_bytes);
+        hdr.off_tw = (uint32_t)(hdr.off_x + 4 * xg.size());
+        hdr.off_ent = (uint32_t)(hdr.off_tw + 2 * kTileThreads);
+        hdr.off_side = (uint32_t)pad16(hdr.off_ent + 2 * (size_t)K * kTileThreads);
+        const size_t bytes = pad16(hdr.off_side + sizeof(SideEnt) * sents.size());
+        if (bytes > (size_t)kStageMax || K > 65535) return false;
         hdr.bytes = (uint32_t)bytes;
         const size_t base = out.blob.size();
         out.blob.resize(base + bytes, 0);
@@ -359,31 +453,26 @@ bool build_tile_host(int64_t N, int32_t n_nodes, int32_t n, int64_t nnz, const i
             for (int k = 0; k < 3; k++) v0[k * ni + q] = vprev[k * N + i];
             md[q] = (uint8_t)model[i];
         }
-        uint8_t *pp = bp + hdr.off_prog;
-        for (auto &rn : runs) {
-            const int32_t v2[2] = {rn.first, rn.second};
-            std::memcpy(pp, v2, 8);
-            pp += 8;
+        if (!xg.empty()) std::memcpy(bp + hdr.off_x, xg.data(), 4 * xg.size());
+        std::memcpy(bp + hdr.off_tw, tw.data(), 2 * tw.size());
+        uint16_t *ep = reinterpret_cast<uint16_t *>(bp + hdr.off_ent);
+        for (int64_t k = 0; k < (int64_t)K * kTileThreads; k++) {
+            const int64_t th2 = k / K, kk = k % K;     // logical position k -> thread th2, step kk
+            ep[kk * kTileThreads + th2] = k < L ? ent[k] : (uint16_t)(8 * kZeroSlot);
         }
-        std::memcpy(pp, lstart.data(), 2 * lstart.size());
-        pp += 2 * lstart.size();
-        if (!lst.empty()) std::memcpy(pp, lst.data(), 2 * lst.size());
-        uint8_t *sp = bp + hdr.off_side;
-        if (!sents.empty()) std::memcpy(sp, sents.data(), sizeof(SideEnt) * sents.size());
-        sp += sizeof(SideEnt) * sents.size();
-        if (!slst.empty()) std::memcpy(sp, slst.data(), 2 * slst.size());
+        if (!sents.empty()) std::memcpy(bp + hdr.off_side, sents.data(), sizeof(SideEnt) * sents.size());
         out.blob_off.push_back((int64_t)out.blob.size());
         out.blob_max = std::max(out.blob_max, (int32_t)bytes);
-        out.n_owned += (int64_t)gids.size();
-        out.n_side_entries += (int64_t)sents.size();
-        listed += (int64_t)slst.size();
+        out.n_owned += n_own;
+        out.n_side_entries += n_sent;
+        out.n_listed += L;
+        out.n_padded += (int64_t)K * kTileThreads;
     }
     // every live contribution is listed exactly once (owned or side)
     {
         int64_t live = 0;
-        for (int64_t k = 0; k < NPAIR * N; k++) live += raw_slot[k] >= 0;
         for (int64_t i = 0; i < N; i++)
-            for (int a = 0; a < 4; a++) live += TT[a][i] >= 0;
+            for (int p = 0; p < NPAIR + 4; p++) live += listed_c(i, p);
         if (listed != live) return false;
     }
     // partial slots.  Side targets with parts in far more tiles than there are
@@ -398,7 +487,10 @@ bool build_tile_host(int64_t N, int32_t n_nodes, int32_t n, int64_t nnz, const i
     std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return cnt[a] > cnt[b]; });
     std::vector<int32_t> hot_of((size_t)out.n_side, -1);
     for (int32_t k = 0; k < out.n_side && k < kMaxHot; k++)
-        if (cnt[order[k]] > 4 * (int64_t)grid) hot_of[order[k]] = out.n_hot++;
+        if (cnt[order[k]] > 4 * (int64_t)grid) {
+            hot_of[order[k]] = out.n_hot++;
+            out.hot_gid.push_back(out.sd_gid[order[k]]);
+        }
     out.sd_part.assign((size_t)out.n_side + 1, 0);
     std::vector<int64_t> base((size_t)out.n_side, 0);
     int64_t cold = 0;

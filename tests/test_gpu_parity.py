@@ -64,7 +64,7 @@ def assert_pattern(ctx, ref):
 
 # ---------------------------------------------------------------- reduced configs
 @pytest.mark.parametrize("cfg", [0, 1, 2, 3, 4])
-@pytest.mark.parametrize("rule", ["exclude_rails", "paper"])
+@pytest.mark.parametrize("rule", ["exclude_rails", "paper", "hybrid"])
 def test_parity_reduced(cuda_ok, cfg, rule):
     nl = netgen.config(cfg, 0.01 if cfg else 1.0)
     if rule == "paper" and cfg in (2, 4):
@@ -264,3 +264,33 @@ def test_color_forms(cuda_ok, mode, monkeypatch):
         A2, b2 = gpu_run(ctx, nl)
         assert np.array_equal(A1, A2) and np.array_equal(b1, b2)
         ctx.close()
+
+
+# ---------------------------------------------------------------- NEXT-1 hybrid colouring
+@pytest.mark.parametrize("cfg,K", [(2, 16), (2, 64), (4, 64), (1, 64), (3, 16)])
+def test_hybrid_color_full_size(cuda_ok, cfg, K):
+    """SURVEY §8(f) NEXT-1 at full size: COLOR under the degree-threshold
+    hybrid (few colours even on the SRAM and hub configs), every entry within
+    tolerance, colouring equal to the oracle's, race-free on the device, and
+    bitwise reproducible."""
+    nl = netgen.config(cfg)
+    ref = reference(nl, key=("full", cfg))
+    ctx = ctx_for(nl, variant="color", rule="hybrid", heavy_degree=K)
+    col, C = ctx.colors()
+    ocol, oC = oracle.greedy_color(nl, "hybrid", K)
+    assert C == oC and np.array_equal(col, ocol)
+    assert C <= 40
+    assert ctx.race_probe() == 0
+    A1, b1 = gpu_run(ctx, nl)
+    assert_parity(ref, A1, b1, f"cfg{cfg} hybrid K={K} color")
+    A2, b2 = gpu_run(ctx, nl)
+    assert np.array_equal(A1, A2) and np.array_equal(b1, b2)
+    ctx.close()
+
+
+def test_hybrid_race_probe_detects_corruption(cuda_ok):
+    nl = netgen.sram_6t(32, 64)
+    ctx = ctx_for(nl, variant="color", rule="hybrid", heavy_degree=16)
+    col, C = ctx.colors()
+    assert C == 5 and ctx.race_probe() == 0
+    assert ctx.race_probe(np.zeros_like(col)) > 0

@@ -65,6 +65,35 @@ def test_colouring_random_small(seed):
         assert C_ == oC and np.array_equal(col, ocol)
 
 
+@pytest.mark.parametrize("K", [4, 16, 64])
+@pytest.mark.parametrize("cfg", [0, 1, 2, 3, 4])
+def test_hybrid_colouring_equals_oracle(cfg, K):
+    """the library's degree-threshold hybrid colouring
+    equals the oracle's first-fit over the same excluded set."""
+    nl = netgen.config(cfg, 0.01)
+    c = _ctx(nl, rule="hybrid", heavy_degree=K)
+    col, C_ = c.colors()
+    ocol, oC = oracle.greedy_color(nl, "hybrid", K)
+    assert C_ == oC and np.array_equal(col, ocol)
+    assert oracle.color_violations(nl, col, C_, "hybrid", K) == 0
+    st = c.stats()
+    assert st["n_excluded_nodes"] == int(oracle.excluded_mask(nl, "hybrid", K)[:nl.n_nodes].sum())
+
+
+def test_hybrid_side_targets_sram():
+    """SRAM R x Cc with K = 16: the bit and word lines leave the relation.
+    Side targets are the heavy diagonals and heavy b rows (WL, BL, BLB: 3 per
+    column/row group) plus the rail's; the (BL, WL) cross entries have one
+    writer each and stay plain."""
+    R, Cc = 64, 128
+    nl = netgen.sram_6t(R, Cc)
+    st = _ctx(nl, rule="hybrid", heavy_degree=16).stats()
+    heavy = R + 2 * Cc                       # word lines + bit lines (+ the rail)
+    assert st["n_excluded_nodes"] == heavy + 1
+    assert st["n_color_side_targets"] == 2 * (heavy + 1)
+    assert st["n_colors"] == 5
+
+
 def test_full_size_colour_counts():
     """C(cfg0..cfg2) = 4, 6, 2052 (rails excluded); the
     library's incidence/bitset first-fit equals the plain oracle at full size."""

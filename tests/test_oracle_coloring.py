@@ -7,10 +7,24 @@ import netgen
 import oracle
 
 
-def brute_first_fit(nl, rule="exclude_rails"):
+def brute_excluded(nl, rule, K=64):
+    """Nodes outside the relation, by plain Python: rails (A1), plus nodes
+    with more than K distinct incident FETs under the NEXT-1 hybrid."""
+    ex = set(nl.rails.tolist()) if rule in ("exclude_rails", "hybrid") else set()
+    if rule == "hybrid":
+        fan = {}
+        for row in zip(nl.d.tolist(), nl.g.tolist(), nl.s.tolist(), nl.b.tolist()):
+            for t in set(row):
+                if t >= 0:
+                    fan[t] = fan.get(t, 0) + 1
+        ex |= {t for t, f in fan.items() if f > K}
+    return ex
+
+
+def brute_first_fit(nl, rule="exclude_rails", K=64):
     """Independent: explicit edge list by pairwise node sharing (P:60 'share
     at least one non-ground node'), then first-fit in index order."""
-    ex = set(nl.rails.tolist()) if rule == "exclude_rails" else set()
+    ex = brute_excluded(nl, rule, K)
     T = np.stack([nl.d, nl.g, nl.s, nl.b], 1)
     sets = [set(t for t in row if t >= 0 and t not in ex) for row in T.tolist()]
     N = len(sets)
@@ -130,3 +144,41 @@ def test_conflict_iff_shared_slot(cfg):
     for i in range(len(T)):
         for j in range(i + 1, len(T)):
             assert bool(slots[i] & slots[j]) == bool(nodes[i] & nodes[j])
+
+
+def test_hybrid_counts():
+    """excluding every node with more than 16
+    incident FETs collapses SRAM 64x128 from 260 colours to 5 and the hub
+    netlist (60k inverters) from its max hub fanout to 4."""
+    nl = netgen.sram_6t(64, 128)
+    assert oracle.greedy_color(nl)[1] == 260
+    c, C = oracle.greedy_color(nl, "hybrid", 16)
+    assert C == 5 and oracle.color_violations(nl, c, C, "hybrid", 16) == 0
+    nl = netgen.hub_netlist(60000)
+    assert oracle.greedy_color(nl)[1] == int(oracle.node_fanout(nl)[np.setdiff1d(
+        np.arange(nl.n_nodes), nl.rails)].max())
+    c, C = oracle.greedy_color(nl, "hybrid", 16)
+    assert C == 4 and oracle.color_violations(nl, c, C, "hybrid", 16) == 0
+
+
+def test_hybrid_reduces_to_exclude_rails():
+    """With K at least the largest non-rail fanout, the hybrid excludes only
+    the rails: the colouring is the A1 one."""
+    nl = netgen.ring_oscillators(10, 101, fanout=4)
+    K = int(oracle.node_fanout(nl)[np.setdiff1d(np.arange(nl.n_nodes), nl.rails)].max())
+    assert np.array_equal(oracle.greedy_color(nl, "hybrid", K)[0], oracle.greedy_color(nl)[0])
+    assert oracle.greedy_color(nl, "hybrid", K - 1)[1] < oracle.greedy_color(nl)[1]
+
+
+@pytest.mark.parametrize("seed", range(30))
+def test_hybrid_random_graphs_match_brute_force(seed):
+    rng = np.random.Generator(np.random.PCG64(500 + seed))
+    N = int(rng.integers(1, 200))
+    nn = int(rng.integers(2, N // 2 + 3))
+    T = rng.integers(-1, nn, size=(N, 4))
+    rails = [int(rng.integers(0, nn))] if seed % 2 else []
+    nl = fets([tuple(t) for t in T], nn, rails=rails)
+    for K in (1, 3, 8):
+        c, C = oracle.greedy_color(nl, "hybrid", K)
+        assert np.array_equal(c, brute_first_fit(nl, "hybrid", K))
+        assert oracle.color_violations(nl, c, C, "hybrid", K) == 0

@@ -42,10 +42,10 @@ def main():
         if not ok.any():
             break
         prev = tr[:, 1] if i == 0 else tr[:, s - 1]
-        print(f" tile{i}: eval {q(np.where(ok, tr[:, s] - prev, -1))}")
-        print(f"        bar1 {q(np.where(ok, tr[:, s + 1] - tr[:, s], -1))}")
-        print(f"        sums {q(np.where(ok, tr[:, s + 2] - tr[:, s + 1], -1))}")
-        print(f"        bar2 {q(np.where(ok, tr[:, s + 3] - tr[:, s + 2], -1))}")
+        print(f" tile{i}: eval+gather {q(np.where(ok, tr[:, s] - prev, -1))}")
+        print(f"        B1+sums {q(np.where(ok, tr[:, s + 1] - tr[:, s], -1))}")
+        print(f"        B2+fix+B3 {q(np.where(ok, tr[:, s + 2] - tr[:, s + 1], -1))}")
+        print(f"        write {q(np.where(ok, tr[:, s + 3] - tr[:, s + 2], -1))}")
     print(" ticket    ", q(rel[:, 62]))
     print(" end       ", q(rel[:, 63]))
 
