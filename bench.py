@@ -7,7 +7,8 @@
 
 One step = one ees_eval_stamp call over the whole netlist (every §8(a) row:
 evaluation + stamping + rail side-reduction), inputs resident in HBM, L2
-flushed (256 MiB write) before every step, A and b cleared outside the timed
+flushed before every step (256 MiB write, then read back so L2 holds clean
+lines), A and b cleared outside the timed
 region (the caller's clear).  Timing: CUDA events on the launching
 stream around each call, summed over exactly K steps, barrier + synchronize
 on both sides, max over ranks.  N>1 runs N independent replicas (DESIGN.md
@@ -205,12 +206,35 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+class L2Flush:
+    """Evicts L2 before a step: writes a 256 MiB buffer (> the 126 MB L2),
+    then (mode "clean", the default) reads it back, so the lines left in L2
+    are clean and the timed kernel does not pay for writing back the flush's
+    own dirty data.  Mode "write" is the write alone."""
+
+    def __init__(self, dev, mode="clean"):
+        import torch
+        self.buf = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+        self.mode = mode
+        self.sink = torch.empty(1, dtype=torch.float32, device=dev)
+
+    def __call__(self, k):
+        import torch
+        self.buf.fill_(float(k & 0xFF))
+        if self.mode == "clean":
+            torch.sum(self.buf, dim=0, keepdim=True, out=self.sink)
+
+    def describe(self):
+        return ("flushed before every step: 256 MiB write" +
+                (" then read back (L2 left clean)" if self.mode == "clean" else ""))
+
+
 def time_calls(ctx, nl, x, A, b, stream, steps, warmup, flush):
     """Per-call device ms (CUDA events on `stream`), L2 flushed before each."""
     import torch
     for k in range(warmup):
         with torch.cuda.stream(stream):
-            flush.fill_(k & 0xFF)
+            flush(k)
             A.zero_(); b.zero_()
         ctx.eval_stamp(x, nl.h, A, b, stream=stream)
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -218,7 +242,7 @@ def time_calls(ctx, nl, x, A, b, stream, steps, warmup, flush):
     torch.cuda.synchronize()
     for k in range(steps):
         with torch.cuda.stream(stream):
-            flush.fill_(k & 0xFF)
+            flush(k)
             A.zero_(); b.zero_()
         evs[k][0].record(stream)
         ctx.eval_stamp(x, nl.h, A, b, stream=stream)
@@ -236,7 +260,7 @@ def run_sweep(args):
     torch.cuda.set_device(0)
     dev = torch.device("cuda", 0)
     stream = torch.cuda.Stream()
-    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
+    flush = L2Flush(dev, args.flush)
     out = open(args.sweep_out, "w") if args.sweep_out else None
     for C in [int(c) for c in args.sweep_c.split(",")]:
         nl = netgen.gen_synth(args.sweep_n, C)
@@ -274,11 +298,16 @@ def main():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--config", type=int, default=DEFAULT_CONFIG)
+    ap.add_argument("--netlist", default=None,
+                    help="another workload by name instead of --config (netgen.named: adder64, "
+                         "adder64_r14, adder64_r89, cfgN@scale)")
     ap.add_argument("--variant", default="auto", choices=["auto", "color", "atomic", "gather", "tile"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--rule", default="exclude_rails", choices=["exclude_rails", "paper", "hybrid"],
                     help="conflict relation of the colouring (COLOR variant)")
     ap.add_argument("--heavy-degree", type=int, default=64, help="hybrid rule threshold")
+    ap.add_argument("--flush", default="clean", choices=["clean", "write"],
+                    help="L2 flush before each step: write 256 MiB (+ read it back: clean)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=10.0)
     ap.add_argument("--no-e2e", action="store_true")
@@ -307,19 +336,19 @@ def main():
         torch.cuda.set_device(0)
     dev = torch.device("cuda", torch.cuda.current_device())
 
-    nl = netgen.config(args.config)
+    nl = netgen.named(args.netlist) if args.netlist else netgen.config(args.config)
     ctx = Context.from_netlist(nl, variant=args.variant, rule=args.rule, heavy_degree=args.heavy_degree)
     st = ctx.stats()
     stream = torch.cuda.Stream()
     x = torch.from_numpy(nl.x).to(dev)
     A = torch.zeros(ctx.nnz, dtype=torch.float64, device=dev)
     b = torch.zeros(ctx.n, dtype=torch.float64, device=dev)
-    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
+    flush = L2Flush(dev, args.flush)
     torch.cuda.synchronize()
 
     def step_pre(k):
         with torch.cuda.stream(stream):
-            flush.fill_(k & 0xFF)          # evict A, b, x, device data from L2
+            flush(k)                       # evict A, b, x, device data from L2
             A.zero_()
             b.zero_()
 
@@ -376,7 +405,7 @@ def main():
     kern_ms = sum(phase_avg.values())
     achieved = alg / (kern_ms * 1e-3) / 1e9
     roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-            "frac": achieved / hbm, "traffic": load_traffic(args.config, variant),
+            "frac": achieved / hbm, "traffic": None if args.netlist else load_traffic(args.config, variant),
             "kernel": " + ".join(phases), "kernel_ms": kern_ms, "phase_ms": phase_avg,
             "algorithmic_bytes_per_launch": alg, "peak_source": peak_src,
             "per_unit": "48 B/FET + 8 B/unknown (x) + 16 B/nonzero (A RMW) + 16 B/unknown (b RMW)"}
@@ -416,10 +445,12 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": {"workload": netgen.CONFIG_NAMES[args.config], "config_index": args.config,
+            "config": {"workload": (f"{nl.name} ({nl.n_dev} FETs)" if args.netlist
+                                    else netgen.CONFIG_NAMES[args.config]),
+                       "config_index": None if args.netlist else args.config,
                        "n_dev": nl.n_dev, "n": ctx.n, "nnz": ctx.nnz, "colors": st["n_colors"],
                        "variant": variant, "tune_ms": st["tune_ms"], "rule": args.rule,
-                       "l2": "flushed before every step (256 MiB write)",
+                       "l2": flush.describe(),
                        "parallelism": "replicas" if world > 1 else "single",
                        "p10_ms": per_sorted[len(per) // 10], "p50_ms": per_sorted[len(per) // 2],
                        "p90_ms": per_sorted[(9 * len(per)) // 10], "setup_s": st["setup_s"]},

@@ -315,6 +315,118 @@ def gen_synth(n_dev: int, c_target: int, seed: int = 5, models=None) -> Netlist:
 
 
 # --------------------------------------------------------------------------
+# Benchmark 2: 64-bit ripple-carry adder of 28T CMOS full adders
+# (Fig. 6; the figure is missing, so the textbook mirror adder is
+# used) and the R14 / R89 series-resistor variants
+# --------------------------------------------------------------------------
+# One bit, terminals (d, g, s, b) over the bit's local nets; "VDD" and "GND"
+# are the supplies.  Carry stage nCo = NOT(AB + C(A+B)), sum stage
+# nS = NOT(ABC + nCo(A+B+C)), then inverters Cout = NOT nCo, S = NOT nS.
+# 14 PMOS (bulk VDD) then 14 NMOS (bulk GND) -- 28T; its non-ground terminal
+# attachments number 89, the paper's "all transistor-to-transistor
+# connections" of R89.
+_FA28_P = [  # d, g, s
+    ("x1", "A", "VDD"), ("x1", "B", "VDD"), ("nCo", "C", "x1"),
+    ("x2", "A", "VDD"), ("nCo", "B", "x2"),
+    ("x3", "A", "VDD"), ("x3", "B", "VDD"), ("x3", "C", "VDD"), ("nS", "nCo", "x3"),
+    ("x4", "A", "VDD"), ("x5", "B", "x4"), ("nS", "C", "x5"),
+    ("Co", "nCo", "VDD"), ("S", "nS", "VDD"),
+]
+_FA28_N = [
+    ("y1", "A", "GND"), ("y1", "B", "GND"), ("nCo", "C", "y1"),
+    ("nCo", "A", "y2"), ("y2", "B", "GND"),
+    ("y3", "A", "GND"), ("y3", "B", "GND"), ("y3", "C", "GND"), ("nS", "nCo", "y3"),
+    ("nS", "A", "y4"), ("y4", "B", "y5"), ("y5", "C", "GND"),
+    ("Co", "nCo", "GND"), ("S", "nS", "GND"),
+]
+_FA28_LOCAL = ["x1", "x2", "x3", "x4", "x5", "y1", "y2", "y3", "y4", "y5", "nCo", "nS", "S"]
+
+
+def full_adder_28t(bits: int = 64, seed: int = 9, models=None) -> Netlist:
+    """Benchmark 2 baseline: `bits` cascaded 28T full adders; carry
+    out of bit k is the carry in of bit k+1.  Nodes: Cin, then per bit A, B,
+    the 13 local nets and Co; VDD (the rail) and its source branch last.
+    Primary inputs (A, B, Cin) are ordinary nodes (their sources are linear
+    devices outside the hot path).  W ~ U[0.2, 5] um, L ~ U[0.05, 0.5] um."""
+    rng = _rng(seed)
+    per_bit = 2 + len(_FA28_LOCAL) + 1
+    n_nodes = 1 + bits * per_bit + 1
+    vdd = n_nodes - 1
+    d, g, s, b, model, stage = [], [], [], [], [], []
+    cin = 0
+    for k in range(bits):
+        base = 1 + k * per_bit
+        node = {"A": base, "B": base + 1, "C": cin, "VDD": vdd, "GND": -1}
+        for j, nm in enumerate(_FA28_LOCAL):
+            node[nm] = base + 2 + j
+        node["Co"] = base + 2 + len(_FA28_LOCAL)
+        for pol, table in ((1, _FA28_P), (0, _FA28_N)):
+            for dn, gn, sn in table:
+                d.append(node[dn]); g.append(node[gn]); s.append(node[sn])
+                b.append(vdd if pol else -1)
+                model.append(pol)
+                stage.append(k)
+        cin = node["Co"]
+    N = len(d)
+    w, l = _wl_uniform(rng, N)
+    er, ec = _vdd_branch(vdd, n_nodes)
+    return _finish(f"adder{bits}_28t", n_nodes, 1, np.array(d), np.array(g), np.array(s),
+                   np.array(b), w, l, np.array(model, np.int32), models or bench_models(), [vdd],
+                   er, ec, rng, dict(stage=np.array(stage, np.int32), bits=bits))
+
+
+def insert_resistors(nl: Netlist, per_stage, seed: int = 10) -> Netlist:
+    """R14 / R89: in every stage, split `per_stage` randomly
+    chosen non-ground terminal attachments ("all" = every one, R89) off
+    their net: the terminal moves to a fresh node joined to the old one by a
+    1 mOhm series resistor.  The resistors are linear devices: only their
+    pattern entries (old,old), (old,new), (new,old), (new,new) are added to
+    the caller's extra entries; the FETs keep their sizes and cards.  New
+    nodes take the old node's voltages (a 1 mOhm resistor carries ~no drop)."""
+    rng = _rng(seed)
+    T = np.stack([nl.d, nl.g, nl.s, nl.b], 1).astype(np.int64).copy()
+    stage = nl.meta["stage"]
+    n_old = nl.n_nodes
+    new_of = []                     # old node of each new node
+    er, ec = [list(nl.extra_row)], [list(nl.extra_col)]
+    rows, cols = [], []
+    for k in range(int(stage.max()) + 1 if len(stage) else 0):
+        fets = np.nonzero(stage == k)[0]
+        att = [(i, a) for i in fets for a in range(4) if T[i, a] >= 0]
+        if per_stage == "all":
+            pick = att
+        else:
+            idx = rng.choice(len(att), size=min(int(per_stage), len(att)), replace=False)
+            pick = [att[j] for j in sorted(idx)]
+        for i, a in pick:
+            old = int(T[i, a])
+            new = n_old + len(new_of)
+            new_of.append(old)
+            T[i, a] = new
+            rows += [old, old, new, new]
+            cols += [old, new, old, new]
+    n_new = len(new_of)
+    n_nodes = n_old + n_new
+    # old nodes keep their ids, new nodes follow them, branch unknowns move up
+    def remap(v):
+        v = np.asarray(v, np.int64)
+        return np.where(v >= n_old, v + n_new, v)
+    extra_row = np.concatenate([remap(nl.extra_row), np.array(rows, np.int64)]) if rows else remap(nl.extra_row)
+    extra_col = np.concatenate([remap(nl.extra_col), np.array(cols, np.int64)]) if cols else remap(nl.extra_col)
+    x = np.concatenate([nl.x[:n_old], nl.x[np.array(new_of, np.int64)] if n_new else [], nl.x[n_old:]])
+    xp = np.concatenate([nl.x_prev[:n_old], nl.x_prev[np.array(new_of, np.int64)] if n_new else [],
+                         nl.x_prev[n_old:]])
+    out = Netlist(name=f"{nl.name}_R{per_stage if per_stage != 'all' else 'all'}", n_nodes=n_nodes,
+                  n_extra=nl.n_extra, d=T[:, 0].astype(np.int32), g=T[:, 1].astype(np.int32),
+                  s=T[:, 2].astype(np.int32), b=T[:, 3].astype(np.int32), w=nl.w.copy(), l=nl.l.copy(),
+                  model=nl.model.copy(), models=nl.models, rails=nl.rails.copy(),
+                  extra_row=extra_row.astype(np.int32), extra_col=extra_col.astype(np.int32),
+                  x=x, x_prev=xp, vprev=nl.vprev.copy(), h=nl.h, gmin=nl.gmin,
+                  meta=dict(nl.meta, resistors=n_new, new_of=np.array(new_of, np.int32)))
+    return out
+
+
+# --------------------------------------------------------------------------
 # tiny hand circuits (tests)
 # --------------------------------------------------------------------------
 def custom(name, n_nodes, terms, model, models, w=None, l=None, rails=(),
@@ -385,3 +497,18 @@ CONFIG_NAMES = {
     3: "cfg3 random 4M FETs / 1M nodes",
     4: "cfg4 clock/bus hubs 8M FETs",
 }
+
+
+def named(name: str) -> Netlist:
+    """Extra workloads by name (bench.py --netlist): Benchmark 2's adder and
+    its resistor variants, cfgN[@scale]."""
+    if name == "adder64":
+        return full_adder_28t(64)
+    if name == "adder64_r14":
+        return insert_resistors(full_adder_28t(64), 14)
+    if name == "adder64_r89":
+        return insert_resistors(full_adder_28t(64), "all")
+    if name.startswith("cfg"):
+        i, _, sc = name[3:].partition("@")
+        return config(int(i), float(sc) if sc else 1.0)
+    raise ValueError(name)

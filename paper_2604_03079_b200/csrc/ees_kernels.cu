@@ -777,42 +777,53 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase)
 constexpr int kSlots = kZeroSlot + 2;          // 16 contributions per item + the zero slot (+pad)
 constexpr size_t kTileSmem = sizeof(double) * (kSlots + kSegMax + kTileThreads) + kStages * (size_t)kStageMax;
 
-// Views into one staged tile blob (layout in ees_internal.h).
+// View of one staged tile blob (layout in ees_internal.h): only the blob's
+// shared-memory address lives in registers; header fields and section
+// pointers are read / derived on use.
 struct TileView {
-    TileHdr hdr;
-    const int4 *term;
-    const double *beta, *v0;
-    const uint8_t *model;
-    const int32_t *xg;
-    const uint16_t *tw, *ent;
-    const SideEnt *sents;
+    const unsigned char *b;
+    __device__ __forceinline__ const TileHdr &hdr() const { return *reinterpret_cast<const TileHdr *>(b); }
+    __device__ __forceinline__ const int4 *term() const
+    {
+        return reinterpret_cast<const int4 *>(b + sizeof(TileHdr));
+    }
+    __device__ __forceinline__ const double *beta(int ni) const
+    {
+        return reinterpret_cast<const double *>(b + sizeof(TileHdr) + 16 * ni);
+    }
+    __device__ __forceinline__ const uint8_t *model(int ni) const
+    {
+        return b + sizeof(TileHdr) + 16 * ni + 32 * ni;
+    }
+    __device__ __forceinline__ const int32_t *xg() const
+    {
+        return reinterpret_cast<const int32_t *>(b + hdr().off_x);
+    }
+    __device__ __forceinline__ const uint16_t *tw() const
+    {
+        return reinterpret_cast<const uint16_t *>(b + hdr().off_tw);
+    }
+    __device__ __forceinline__ const uint16_t *ent() const
+    {
+        return reinterpret_cast<const uint16_t *>(b + hdr().off_ent);
+    }
+    __device__ __forceinline__ const SideEnt *sents() const
+    {
+        return reinterpret_cast<const SideEnt *>(b + hdr().off_side);
+    }
 };
 
-__device__ __forceinline__ TileView tile_view(const unsigned char *blob)
-{
-    TileView v;
-    v.hdr = *reinterpret_cast<const TileHdr *>(blob);
-    const int ni = v.hdr.n_items;
-    const unsigned char *items = blob + sizeof(TileHdr);
-    v.term = reinterpret_cast<const int4 *>(items);
-    v.beta = reinterpret_cast<const double *>(items + 16 * (size_t)ni);
-    v.v0 = v.beta + ni;
-    v.model = reinterpret_cast<const uint8_t *>(v.v0 + 3 * (size_t)ni);
-    v.xg = reinterpret_cast<const int32_t *>(blob + v.hdr.off_x);
-    v.tw = reinterpret_cast<const uint16_t *>(blob + v.hdr.off_tw);
-    v.ent = reinterpret_cast<const uint16_t *>(blob + v.hdr.off_ent);
-    v.sents = reinterpret_cast<const SideEnt *>(blob + v.hdr.off_side);
-    return v;
-}
+__device__ __forceinline__ TileView tile_view(const unsigned char *blob) { return TileView{blob}; }
 
 // Address of owned target j (< n_own): the tile rows' CSR block, their b
 // rows, then the explicit ids.
 __device__ __forceinline__ double *owned_ptr(const TileView &v, const TileK &tk, const CallK &P, int j)
 {
-    const int na = v.hdr.na, nab = na + v.hdr.nb;
-    if (j < na) return P.A + v.hdr.a0 + j;
-    if (j < nab) return P.b + v.hdr.b0 + (j - na);
-    const int32_t g = v.xg[j - nab];
+    const TileHdr &h = v.hdr();
+    const int na = h.na, nab = na + h.nb;
+    if (j < na) return P.A + h.a0 + j;
+    if (j < nab) return P.b + h.b0 + (j - na);
+    const int32_t g = v.xg()[j - nab];
     return g < tk.nnz ? P.A + g : P.b + (g - tk.nnz);
 }
 
@@ -829,8 +840,8 @@ __device__ __forceinline__ void tile_gather(const TileView &v, const TileK &tk, 
 {
     const int tid = threadIdx.x;
     R.VD = R.VG = R.VS = 0.0;
-    if (tid < v.hdr.n_items) {
-        const int4 T = v.term[tid];
+    if (tid < v.hdr().n_items) {
+        const int4 T = v.term()[tid];
         R.VD = T.x >= 0 ? __ldg(P.x + T.x) : 0.0;
         R.VG = T.y >= 0 ? __ldg(P.x + T.y) : 0.0;
         R.VS = T.z >= 0 ? __ldg(P.x + T.z) : 0.0;
@@ -838,7 +849,7 @@ __device__ __forceinline__ void tile_gather(const TileView &v, const TileK &tk, 
 #pragma unroll
     for (int k = 0; k < kTilePrefetch; k++) {
         const int j = tid + k * kTileThreads;
-        R.dst[k] = j < v.hdr.n_own ? owned_ptr(v, tk, P, j) : nullptr;
+        R.dst[k] = j < v.hdr().n_own ? owned_ptr(v, tk, P, j) : nullptr;
         R.pre[k] = R.dst[k] ? *R.dst[k] : 0.0;
     }
 }
@@ -848,23 +859,22 @@ __device__ __forceinline__ void tile_gather(const TileView &v, const TileK &tk, 
 __device__ __forceinline__ void side_finish(const TileK &tk, const CallK &P, int32_t sid, int lane)
 {
     const int32_t q0 = __ldg(tk.sd_part + 2 * sid), q1 = __ldg(tk.sd_part + 2 * sid + 1);
+    const int32_t g = __ldg(tk.sd_gid + sid);
+    double *dst = g < tk.nnz ? P.A + g : P.b + (g - tk.nnz);
+    const double pre = lane == 0 ? *dst : 0.0;
     double u = 0.0;
-    int32_t q = q0 + lane;
-    for (; q + 96 < q1; q += 128) {
-        const double a = __ldcg(tk.part + q), b = __ldcg(tk.part + q + 32);
-        const double c = __ldcg(tk.part + q + 64), d = __ldcg(tk.part + q + 96);
-        u += a;
-        u += b;
-        u += c;
-        u += d;
+    for (int32_t qb = q0; qb < q1; qb += 256) {
+        double a[8];
+#pragma unroll
+        for (int r = 0; r < 8; r++) {
+            const int32_t q = qb + r * 32 + lane;
+            a[r] = q < q1 ? __ldcg(tk.part + q) : 0.0;
+        }
+#pragma unroll
+        for (int r = 0; r < 8; r++) u += a[r];
     }
-    for (; q < q1; q += 32) u += __ldcg(tk.part + q);
     u = warp_sum(u);
-    if (lane == 0) {
-        const int32_t g = __ldg(tk.sd_gid + sid);
-        if (g < tk.nnz) P.A[g] += u;
-        else P.b[g - tk.nnz] += u;
-    }
+    if (lane == 0) *dst = pre + u;
 }
 
 // ---------------------------------------------------------------------------
@@ -952,12 +962,13 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_tile(TileK tk, CallK P)
     for (int32_t t = t0; t < tk.n_tiles; t += G, it++) {
         const int32_t tn = t + G;
         const int sn = stage + 1 == kStages ? 0 : stage + 1;
-        const int ni = v.hdr.n_items;
+        const int ni = v.hdr().n_items;
         if (tid < ni) {
             Stamp st;
-            eval_fet(s_cards[v.model[tid]], v.beta[tid], P.gmin, cur.VD, cur.VG, cur.VS, v.v0[tid],
-                     v.v0[ni + tid], v.v0[2 * ni + tid], st);
-            const int4 T = v.term[tid];
+            const double *bt = v.beta(ni);
+            eval_fet(s_cards[v.model(ni)[tid]], bt[tid], P.gmin, cur.VD, cur.VG, cur.VS, bt[ni + tid],
+                     bt[2 * ni + tid], bt[3 * ni + tid], st);
+            const int4 T = v.term()[tid];
             if (T.z == T.w && T.z != -1) {        // source tied to bulk: one entry each (ees_internal.h)
                 st.y[DS] += st.y[DB];
                 st.y[SD] += st.y[BD];
@@ -983,21 +994,33 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_tile(TileK tk, CallK P)
             const int32_t tr = t - G + kStages * G;             // refill the stage of tile t-G
             if (tr < tk.n_tiles) issue(tr, stage == 0 ? kStages - 1 : stage - 1);
         }
-        // balanced segmented sum (entries are byte offsets into s_c | kEntEnd)
-        const uint16_t w = v.tw[tid];
+        // balanced segmented sum (entries are byte offsets into s_c | kEntEnd);
+        // four entries' loads are issued before their adds
+        const uint16_t w = v.tw()[tid];
         {
-            const int K = v.hdr.K;
-            const uint16_t *e = v.ent + tid;
-            int sid = w & kTwSid;
+            const int K = v.hdr().K;
+            const uint16_t *e = v.ent() + tid;
+            double *sp = s_seg + (w & kTwSid);
             double s = 0.0;
-#pragma unroll 4
-            for (int k = 0; k < K; k++) {
-                const uint32_t x = e[k * kTileThreads];
-                s += *reinterpret_cast<const double *>(s_cb + (x & 0x7FFFu));
-                if (x & kEntEnd) {
-                    s_seg[sid++] = s;
-                    s = 0.0;
-                }
+            auto val = [&](uint32_t x) { return *reinterpret_cast<const double *>(s_cb + (x & 0x7FFFu)); };
+            int k = 0;
+            for (; k + 4 <= K; k += 4) {
+                const uint32_t x0 = e[k * kTileThreads], x1 = e[(k + 1) * kTileThreads];
+                const uint32_t x2 = e[(k + 2) * kTileThreads], x3 = e[(k + 3) * kTileThreads];
+                const double v0 = val(x0), v1 = val(x1), v2 = val(x2), v3 = val(x3);
+                s += v0;
+                if (x0 & kEntEnd) { *sp++ = s; s = 0.0; }
+                s += v1;
+                if (x1 & kEntEnd) { *sp++ = s; s = 0.0; }
+                s += v2;
+                if (x2 & kEntEnd) { *sp++ = s; s = 0.0; }
+                s += v3;
+                if (x3 & kEntEnd) { *sp++ = s; s = 0.0; }
+            }
+            for (; k < K; k++) {
+                const uint32_t x0 = e[k * kTileThreads];
+                s += val(x0);
+                if (x0 & kEntEnd) { *sp++ = s; s = 0.0; }
             }
             s_carry[tid] = s;
         }
@@ -1006,7 +1029,8 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_tile(TileK tk, CallK P)
         if ((w & (kTwCont | kTwNoEnd)) == kTwCont) {
             int k = tid - 1;
             double acc = s_carry[k];
-            while ((v.tw[k] & (kTwCont | kTwNoEnd)) == (kTwCont | kTwNoEnd)) {
+            const uint16_t *tw = v.tw();
+            while ((tw[k] & (kTwCont | kTwNoEnd)) == (kTwCont | kTwNoEnd)) {
                 k--;
                 acc += s_carry[k];
             }
@@ -1014,7 +1038,7 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_tile(TileK tk, CallK P)
         }
         __syncthreads();                                        // B3
         TILE_TRACE(4 + 4 * it);
-        const int n_own = v.hdr.n_own;
+        const int n_own = v.hdr().n_own;
 #pragma unroll
         for (int k = 0; k < kTilePrefetch; k++)
             if (cur.dst[k]) *cur.dst[k] = cur.pre[k] + s_seg[tid + k * kTileThreads];
@@ -1022,8 +1046,8 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_tile(TileK tk, CallK P)
             *owned_ptr(v, tk, P, j) += s_seg[j];
         // side parts (plain stores; ordered by the fence + ticket below); a hot
         // target appears at most once per tile, so one thread owns s_hot[h] here
-        for (int e = tid; e < v.hdr.n_sent; e += kTileThreads) {
-            const SideEnt se = v.sents[e];
+        for (int e = tid; e < v.hdr().n_sent; e += kTileThreads) {
+            const SideEnt se = v.sents()[e];
             const double part = s_seg[n_own + e];
             if (se.slot >= 0) tk.part[se.slot] = part;
             else s_hot[-1 - se.slot] += part;

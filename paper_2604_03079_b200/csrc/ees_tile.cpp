@@ -161,7 +161,7 @@ bool build_tile_host(int64_t N, int32_t n_nodes, int32_t n, int64_t nnz, const i
         if (heavy[v]) continue;
         // a tile's rows are consecutive, so its owned entries of A and b are
         // one CSR block and one row range (implicit ids in the blob)
-        if (!cur.empty() && last_row != v - 1) close_tile();
+        if ((int32_t)tile_rows.size() > tile_rows_ptr.back() && last_row != v - 1) close_tile();
         for (int pass = 0; pass < 2; pass++) {
             int32_t fresh = 0;
             const int64_t hs = hs_ptr[v + 1] - hs_ptr[v];
@@ -487,7 +487,7 @@ bool build_tile_host(int64_t N, int32_t n_nodes, int32_t n, int64_t nnz, const i
     std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return cnt[a] > cnt[b]; });
     std::vector<int32_t> hot_of((size_t)out.n_side, -1);
     for (int32_t k = 0; k < out.n_side && k < kMaxHot; k++)
-        if (cnt[order[k]] > 4 * (int64_t)grid) {
+        if (cnt[order[k]] > (int64_t)grid) {
             hot_of[order[k]] = out.n_hot++;
             out.hot_gid.push_back(out.sd_gid[order[k]]);
         }

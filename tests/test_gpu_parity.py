@@ -294,3 +294,29 @@ def test_hybrid_race_probe_detects_corruption(cuda_ok):
     col, C = ctx.colors()
     assert C == 5 and ctx.race_probe() == 0
     assert ctx.race_probe(np.zeros_like(col)) > 0
+
+
+# ---------------------------------------------------------------- Benchmark 2 (NEXT-3)
+@pytest.mark.parametrize("variant_of", ["baseline", "R14", "R89"])
+@pytest.mark.parametrize("rule", ["exclude_rails", "paper"])
+def test_adder_parity(cuda_ok, variant_of, rule):
+    """the 64-bit 28T ripple-carry adder and its R14 / R89
+    series-resistor variants, every stamping variant, both conflict rules
+    (paper rule: C = 896 / 1 for the baseline / R89, Table II)."""
+    nl = netgen.full_adder_28t(64)
+    if variant_of == "R14":
+        nl = netgen.insert_resistors(nl, 14)
+    elif variant_of == "R89":
+        nl = netgen.insert_resistors(nl, "all")
+    ref = reference(nl)
+    ctx = ctx_for(nl, rule=rule)
+    assert_pattern(ctx, ref)
+    col, C = ctx.colors()
+    ocol, oC = oracle.greedy_color(nl, rule)
+    assert C == oC and np.array_equal(col, ocol)
+    if rule == "paper":
+        assert C == {"baseline": 896, "R89": 1}.get(variant_of, C)
+    assert ctx.race_probe() == 0
+    for v in VARIANTS:
+        assert_parity(ref, *gpu_run(ctx, nl, v), f"{nl.name} {rule} {v}")
+    ctx.close()

@@ -178,3 +178,22 @@ def test_tile_structure_random(seed):
     nl = netgen.custom("r", nn, [tuple(t) for t in T], 0, netgen.bench_models(), rails=rails)
     st = _ctx(nl).stats()
     assert st["n_tile_items"] >= N
+
+
+@pytest.mark.parametrize("split", [None, 14, "all"])
+@pytest.mark.parametrize("rule", ["exclude_rails", "paper", "hybrid"])
+def test_adder_setup_equals_oracle(split, rule):
+    """Benchmark 2 netlists (NEXT-3): pattern (with the resistors'
+    extra entries) and colouring equal the oracle's; tiles build even when
+    split nets leave rows with no FET."""
+    nl = netgen.full_adder_28t(64)
+    if split is not None:
+        nl = netgen.insert_resistors(nl, split)
+    c = _ctx(nl, rule=rule)
+    rp, ci = c.pattern()
+    orp, oci, _ = oracle.pattern(nl)
+    assert np.array_equal(rp, orp) and np.array_equal(ci, oci)
+    col, C_ = c.colors()
+    ocol, oC = oracle.greedy_color(nl, rule)
+    assert C_ == oC and np.array_equal(col, ocol)
+    assert c.stats()["n_tiles"] >= 1

@@ -182,3 +182,37 @@ def test_hybrid_random_graphs_match_brute_force(seed):
         c, C = oracle.greedy_color(nl, "hybrid", K)
         assert np.array_equal(c, brute_first_fit(nl, "hybrid", K))
         assert oracle.color_violations(nl, c, C, "hybrid", K) == 0
+
+
+# ---------------------------------------------------------------- Benchmark 2 (NEXT-3)
+def test_adder_28t_matches_paper_counts():
+    """P:101-105 / Table II: the 64-bit ripple-carry adder of 28T
+    full adders has 1,792 FETs and 89 non-ground terminal attachments per bit
+    (R89 = "all transistor-to-transistor connections"); under the paper's
+    conflict rule (P:60, VDD shared by every PMOS) greedy gives C = 896;
+    after R89 every FET is on private nets and C = 1."""
+    nl = netgen.full_adder_28t(64)
+    assert nl.n_dev == 1792
+    T = np.stack([nl.d, nl.g, nl.s, nl.b], 1)
+    assert (T >= 0).sum() == 89 * 64
+    c, C = oracle.greedy_color(nl, "paper")
+    assert C == 896 and oracle.color_violations(nl, c, C, "paper") == 0
+    r89 = netgen.insert_resistors(nl, "all")
+    assert r89.meta["resistors"] == 89 * 64
+    for rule in ("paper", "exclude_rails"):
+        assert oracle.greedy_color(r89, rule)[1] == 1
+
+
+def test_adder_resistor_split_is_topological():
+    """A series resistor moves one terminal to a fresh node: per FET the
+    multiset of (old) nets is unchanged, and the new node's only other
+    attachment is the resistor (linear extra entries)."""
+    nl = netgen.full_adder_28t(4)
+    r = netgen.insert_resistors(nl, 14, seed=3)
+    new_of = r.meta["new_of"]
+    assert len(new_of) == 14 * 4
+    T0 = np.stack([nl.d, nl.g, nl.s, nl.b], 1)
+    T1 = np.stack([r.d, r.g, r.s, r.b], 1).astype(np.int64)
+    back = np.where(T1 >= nl.n_nodes, new_of[np.clip(T1 - nl.n_nodes, 0, None)], T1)
+    assert np.array_equal(back, T0)
+    assert np.array_equal(np.sort(np.unique(T1[T1 >= nl.n_nodes])), np.arange(nl.n_nodes, r.n_nodes))
