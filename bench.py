@@ -45,6 +45,12 @@ def peaks():
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+# FP64 operations of one evaluation as written in eval_fet1 (ees_kernels.cu;
+# SURVEY §8(c) steps 1-8, both region branches evaluated, FMA = 2): the
+# source-level count, ~46 in SURVEY §8(d).
+FLOPS_PER_EVAL = 47
+
+
 def algorithmic_bytes(n_dev, n, nnz):
     """SURVEY §8(d) compulsory bytes per call: 48 B device data per FET
     (4 x int32 terminals, f64 beta, 3 x f64 v_prev) + x read once (8 B per
@@ -271,9 +277,9 @@ def run_sweep(args):
         b = torch.zeros(ctx.n, dtype=torch.float64, device=dev)
         rec = {"C": st["n_colors"], "n_dev": nl.n_dev, "nnz": ctx.nnz, "auto": st["variant_chosen"],
                "ms": {}}
-        for v in ("color", "atomic", "gather", "tile"):
+        for v in ("color", "atomic", "gather", "tile", "color_buf"):
             ctx.set_variant(v)
-            steps = args.steps if (v != "color" or C <= 512) else max(3, args.steps // 10)
+            steps = args.steps if (v not in ("color", "color_buf") or C <= 512) else max(3, args.steps // 10)
             per = time_calls(ctx, nl, x, A, b, stream, steps, 3, flush)
             rec["ms"][v] = per[len(per) // 2]
         # NEXT-1: COLOR under the degree-threshold hybrid rule (hub nodes leave
@@ -301,11 +307,12 @@ def main():
     ap.add_argument("--netlist", default=None,
                     help="another workload by name instead of --config (netgen.named: adder64, "
                          "adder64_r14, adder64_r89, cfgN@scale)")
-    ap.add_argument("--variant", default="auto", choices=["auto", "color", "atomic", "gather", "tile"])
+    ap.add_argument("--variant", default="auto", choices=["auto", "color", "atomic", "gather", "tile", "color_buf"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--rule", default="exclude_rails", choices=["exclude_rails", "paper", "hybrid"],
                     help="conflict relation of the colouring (COLOR variant)")
     ap.add_argument("--heavy-degree", type=int, default=64, help="hybrid rule threshold")
+    ap.add_argument("--work", type=int, default=1, help="S:229 work multiplier (FP64-bound probe)")
     ap.add_argument("--flush", default="clean", choices=["clean", "write"],
                     help="L2 flush before each step: write 256 MiB (+ read it back: clean)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -338,6 +345,8 @@ def main():
 
     nl = netgen.named(args.netlist) if args.netlist else netgen.config(args.config)
     ctx = Context.from_netlist(nl, variant=args.variant, rule=args.rule, heavy_degree=args.heavy_degree)
+    if args.work > 1:
+        ctx.set_work(args.work)
     st = ctx.stats()
     stream = torch.cuda.Stream()
     x = torch.from_numpy(nl.x).to(dev)
@@ -400,7 +409,8 @@ def main():
               "color": (["k_color_h x C", "k_side_chunks + k_side_apply"] if args.rule == "hybrid"
                         else ["k_color x C", "k_rail_final"]),
               "gather": ["k_gather_eval", "k_gather_reduce", "k_gather_heavy"],
-              "tile": ["k_tile"]}[variant]
+              "tile": ["k_tile"],
+              "color_buf": ["k_gather_eval (t_calc)", "k_color_stamp x C + side sum (t_stamp)"]}[variant]
     phase_avg = {name: phase_ms[i] / max(1, n_timed) for i, name in enumerate(phases)}
     kern_ms = sum(phase_avg.values())
     achieved = alg / (kern_ms * 1e-3) / 1e9
@@ -409,6 +419,19 @@ def main():
             "kernel": " + ".join(phases), "kernel_ms": kern_ms, "phase_ms": phase_avg,
             "algorithmic_bytes_per_launch": alg, "peak_source": peak_src,
             "per_unit": "48 B/FET + 8 B/unknown (x) + 16 B/nonzero (A RMW) + 16 B/unknown (b RMW)"}
+    if args.work > 1:
+        # S:229 work multiplier: evaluation arithmetic x k puts the path on the
+        # FP64 pipe; peak = this device's FMA throughput measured now
+        from paper_2604_03079_b200 import fp64_peak
+        fpk = fp64_peak()
+        flops = FLOPS_PER_EVAL * args.work * nl.n_dev
+        ach = flops / (kern_ms * 1e-3) / 1e12
+        roof = {"bound": "fp64", "achieved": ach, "peak": fpk, "unit": "TFLOP/s", "frac": ach / fpk,
+                "traffic": None, "kernel": roof["kernel"], "kernel_ms": kern_ms, "phase_ms": phase_avg,
+                "algorithmic_flops_per_launch": flops,
+                "peak_source": "measured now (ees_fp64_peak: independent DFMA chains, one wave)",
+                "per_unit": f"{FLOPS_PER_EVAL} FP64 flops per evaluation x work {args.work}",
+                "hbm_frac": achieved / hbm}
 
     # end to end through the host-buffer ABI call (pinned buffers)
     e2e = None
@@ -450,6 +473,7 @@ def main():
                        "config_index": None if args.netlist else args.config,
                        "n_dev": nl.n_dev, "n": ctx.n, "nnz": ctx.nnz, "colors": st["n_colors"],
                        "variant": variant, "tune_ms": st["tune_ms"], "rule": args.rule,
+                       "work": args.work,
                        "l2": flush.describe(),
                        "parallelism": "replicas" if world > 1 else "single",
                        "p10_ms": per_sorted[len(per) // 10], "p50_ms": per_sorted[len(per) // 2],

@@ -53,9 +53,13 @@ typedef enum {
     EES_COLOR = 1,       /* colour-phased: one phase per colour, plain read-modify-write */
     EES_ATOMIC = 2,      /* one pass, FP64 atomicAdd (RED) into A and b */
     EES_GATHER = 3,      /* deterministic: contributions to scratch, per-entry segmented reduction */
-    EES_TILE = 4         /* deterministic, one launch: per-CTA row tiles; contributions staged in
+    EES_TILE = 4,        /* deterministic, one launch: per-CTA row tiles; contributions staged in
                             shared memory and gathered per owned entry; entries shared by tiles
                             (heavy x heavy: rails, hubs) reduced from per-tile partials */
+    EES_COLOR_BUF = 5    /* the paper's non-fused "Color" (Table I):
+                            one parallel compute phase into a contribution buffer, then one
+                            plain-RMW stamp phase per colour reading it (EES_GATHER is the
+                            "loadomp" analogue: compute to the buffer, ordered stamp) */
 } ees_variant;
 
 /* Conflict relation for the colouring (P:60 and SURVEY A1). */
@@ -126,7 +130,8 @@ typedef struct {
     int32_t n_tiles, n_heavy_nodes, n_side_targets;   /* EES_TILE structure */
     int32_t tile_blob_max;                  /* largest per-tile blob (bytes) */
     int64_t n_tile_items;                   /* device copies over all tiles (>= n_dev) */
-    double tune_ms[5];                      /* EES_AUTO: measured ms per call of [_, COLOR, ATOMIC, GATHER, TILE] */
+    double tune_ms[6];                      /* EES_AUTO: measured ms per call of
+                                               [_, COLOR, ATOMIC, GATHER, TILE, COLOR_BUF] */
     int32_t n_excluded_nodes;               /* nodes outside the conflict relation */
     int32_t n_color_side_targets;           /* EES_CONFLICT_HYBRID: entries summed after the colours */
     int64_t n_color_side_contributions;     /* their contributions (scratch slots) */
@@ -187,7 +192,8 @@ ees_status ees_stats(const ees_ctx *ctx, ees_stats_t *out);
 /* Per-phase device timing (S:326 PhaseTimings).  When enabled, every
  * ees_eval_stamp records CUDA events on the call's stream around each kernel
  * group ("phase"):  COLOR {0: colour kernels, 1: rail finalise or, under
- * EES_CONFLICT_HYBRID, the side segmented sum},
+ * EES_CONFLICT_HYBRID, the side segmented sum},  COLOR_BUF {0: compute to
+ * the buffer (t_calc), 1: colour stamp kernels + side sum (t_stamp)},
  * ATOMIC {0: k_atomic},  GATHER {0: evaluate to scratch, 1: segmented
  * reduction, 2: heavy-target finalise},  TILE {0: k_tile}. */
 ees_status ees_set_timing(ees_ctx *ctx, int32_t enable);
@@ -210,6 +216,25 @@ ees_status ees_race_probe(ees_ctx *ctx, const int32_t *color, int64_t *n_conflic
  * stored, 5+4i end; 62 ticket taken, 63 end.  Synchronous. */
 ees_status ees_tile_trace(ees_ctx *ctx, const double *x, double h, double *A_vals, double *b,
                           ees_stream stream, uint64_t *trace, int64_t cap, int32_t *n_ctas);
+
+/* State update after an accepted time step (S:212 update_state; Fig. 1,
+ * P:40-45): every FET's companion state becomes the converged branch
+ * voltages at x, v_prev = (VG - VS, VG - VD, VD - VB), replacing the vprev
+ * given at setup for all later ees_eval_stamp calls.
+ *   x       device pointer, [n] FP64, the converged solution
+ *   stream  enqueue only, like ees_eval_stamp; x must stay valid until done.
+ * Errors: EES_EINVAL (null x), EES_ESTATE (host-only context), EES_ECUDA. */
+ees_status ees_accept(ees_ctx *ctx, const double *x, ees_stream stream);
+
+/* SPEC S:229 work multiplier: evaluation repeats its arithmetic `work`
+ * times (>= 1; default 1) to emulate a costlier model such as BSIM4;
+ * results are unchanged.  Errors: EES_EINVAL for work < 1. */
+ees_status ees_set_work(ees_ctx *ctx, int32_t work);
+
+/* Measures the FP64 FMA throughput of the current device (one resident
+ * wave of independent FMA chains; the FP64 roofline denominator).
+ * Synchronous.  *tflops out. */
+ees_status ees_fp64_peak(double *tflops);
 
 ees_status ees_destroy(ees_ctx *ctx);
 

@@ -16,7 +16,7 @@ if not os.path.exists(LIB_PATH):
                       " -- the CUDA path has no CPU fallback")
 
 EES_OK, EES_EINVAL, EES_ENOMEM, EES_ECUDA, EES_ESTATE = 0, -1, -2, -3, -4
-EES_AUTO, EES_COLOR, EES_ATOMIC, EES_GATHER, EES_TILE = 0, 1, 2, 3, 4
+EES_AUTO, EES_COLOR, EES_ATOMIC, EES_GATHER, EES_TILE, EES_COLOR_BUF = 0, 1, 2, 3, 4, 5
 EES_CONFLICT_EXCLUDE_RAILS, EES_CONFLICT_PAPER, EES_CONFLICT_HYBRID = 0, 1, 2
 EES_MAX_MODELS, EES_MAX_RAILS = 16, 8
 EES_SETUP_HOST_ONLY = 1
@@ -46,7 +46,7 @@ class ees_stats_t(C.Structure):
                 ("n_rail_entries", i32), ("n_heavy_targets", i32), ("launches_per_call", i32),
                 ("setup_s", f64), ("setup_pattern_s", f64), ("setup_color_s", f64),
                 ("n_tiles", i32), ("n_heavy_nodes", i32), ("n_side_targets", i32),
-                ("tile_blob_max", i32), ("n_tile_items", i64), ("tune_ms", f64 * 5),
+                ("tile_blob_max", i32), ("n_tile_items", i64), ("tune_ms", f64 * 6),
                 ("n_excluded_nodes", i32), ("n_color_side_targets", i32),
                 ("n_color_side_contributions", i64)]
 
@@ -64,14 +64,19 @@ lib.ees_set_timing.argtypes = [P, i32]
 lib.ees_phase_times.argtypes = [P, P, C.POINTER(i32)]
 lib.ees_tile_trace.argtypes = [P, P, f64, P, P, P, P, i64, C.POINTER(i32)]
 lib.ees_race_probe.argtypes = [P, P, C.POINTER(i64)]
+lib.ees_accept.argtypes = [P, P, P]
+lib.ees_set_work.argtypes = [P, i32]
+lib.ees_fp64_peak.argtypes = [C.POINTER(f64)]
 lib.ees_destroy.argtypes = [P]
 lib.ees_strerror.argtypes = [i32]
 lib.ees_strerror.restype = C.c_char_p
 for _f in ("ees_setup", "ees_pattern", "ees_find_slot", "ees_colors", "ees_eval_stamp",
            "ees_eval_stamp_host", "ees_set_variant", "ees_stats", "ees_race_probe", "ees_destroy",
-           "ees_set_timing", "ees_phase_times", "ees_tile_trace"):
+           "ees_set_timing", "ees_phase_times", "ees_tile_trace", "ees_accept", "ees_set_work",
+           "ees_fp64_peak"):
     getattr(lib, _f).restype = i32
 
 EXPORTS = ["ees_setup", "ees_pattern", "ees_find_slot", "ees_colors", "ees_eval_stamp",
            "ees_eval_stamp_host", "ees_set_variant", "ees_stats", "ees_set_timing",
-           "ees_phase_times", "ees_tile_trace", "ees_race_probe", "ees_destroy", "ees_strerror"]
+           "ees_phase_times", "ees_tile_trace", "ees_race_probe", "ees_accept", "ees_set_work",
+           "ees_fp64_peak", "ees_destroy", "ees_strerror"]

@@ -10,7 +10,7 @@ import numpy as np
 from . import _lib as L
 
 VARIANTS = {"auto": L.EES_AUTO, "color": L.EES_COLOR, "atomic": L.EES_ATOMIC,
-            "gather": L.EES_GATHER, "tile": L.EES_TILE}
+            "gather": L.EES_GATHER, "tile": L.EES_TILE, "color_buf": L.EES_COLOR_BUF}
 VARIANT_NAMES = {v: k for k, v in VARIANTS.items()}
 RULES = {"exclude_rails": L.EES_CONFLICT_EXCLUDE_RAILS, "paper": L.EES_CONFLICT_PAPER,
          "hybrid": L.EES_CONFLICT_HYBRID}
@@ -33,6 +33,13 @@ def _arr(a, dtype):
 
 def _ptr(a):
     return C.c_void_p(a.ctypes.data) if a.size else None
+
+
+def fp64_peak():
+    """ees_fp64_peak: measured FP64 FMA TFLOP/s of the current CUDA device."""
+    t = C.c_double()
+    _check(L.lib.ees_fp64_peak(C.byref(t)), "ees_fp64_peak")
+    return t.value
 
 
 class Context:
@@ -104,7 +111,7 @@ class Context:
         st = L.ees_stats_t()
         _check(L.lib.ees_stats(self._h, C.byref(st)), "ees_stats")
         out = {f: getattr(st, f) for f, _ in L.ees_stats_t._fields_ if f != "tune_ms"}
-        out["tune_ms"] = {VARIANT_NAMES[v]: st.tune_ms[v] for v in (1, 2, 3, 4)}
+        out["tune_ms"] = {VARIANT_NAMES[v]: st.tune_ms[v] for v in (1, 2, 3, 4, 5)}
         out["variant_chosen"] = VARIANT_NAMES[st.variant_chosen]
         return out
 
@@ -157,6 +164,22 @@ class Context:
                                          ptr(A, self.nnz, "A"), ptr(b, self.n, "b"),
                                          C.c_void_p(sh), L.EES_HOST_ASSIGN if assign else 0),
                "ees_eval_stamp_host")
+
+    def accept(self, x, stream=None):
+        """ees_accept: v_prev of every FET <- the branch voltages at x (a
+        contiguous float64 CUDA tensor of n elements)."""
+        import torch
+        if not (isinstance(x, torch.Tensor) and x.is_cuda and x.dtype == torch.float64
+                and x.is_contiguous() and x.numel() == self.n):
+            raise ValueError(f"x: need a contiguous float64 CUDA tensor of {self.n} elements")
+        if stream is None:
+            stream = torch.cuda.current_stream()
+        sh = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+        _check(L.lib.ees_accept(self._h, C.c_void_p(x.data_ptr()), C.c_void_p(sh)), "ees_accept")
+
+    def set_work(self, work):
+        """ees_set_work: SPEC S:229 work multiplier (>= 1)."""
+        _check(L.lib.ees_set_work(self._h, int(work)), "ees_set_work")
 
     def tile_trace(self, x, h, A, b, stream=None):
         """Debug: one traced EES_TILE call -> uint64 array [n_ctas, 64] of

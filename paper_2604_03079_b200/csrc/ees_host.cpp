@@ -60,6 +60,7 @@ struct ees_ctx {
     bool hybrid = false;
     Layout L_colorh, L_probe;
     SideK sk{};
+    int32_t *d_perm = nullptr;            // colour-major position -> netlist index (COLOR_BUF)
     GatherK gk{};
     TileK tk{};
     std::vector<int64_t> color_blk_off;   // [C+1] block offsets of colours into partials
@@ -72,6 +73,7 @@ struct ees_ctx {
     int atomic_grid = 1;
     int32_t variant = EES_ATOMIC;
     int32_t launches = 0;
+    int32_t work = 1;                     // S:229 work multiplier
     bool host_only = false;
     // phase timing
     bool timing = false;
@@ -128,7 +130,7 @@ ees_status validate(const ees_desc *d)
     if (d->n_extra_entries < 0 || (d->n_extra_entries && (!d->extra_row || !d->extra_col)))
         return EES_EINVAL;
     if (!(d->gmin >= 0.0) || !std::isfinite(d->gmin)) return EES_EINVAL;
-    if (d->variant < EES_AUTO || d->variant > EES_TILE) return EES_EINVAL;
+    if (d->variant < EES_AUTO || d->variant > EES_COLOR_BUF) return EES_EINVAL;
     if (d->conflict_rule != EES_CONFLICT_EXCLUDE_RAILS && d->conflict_rule != EES_CONFLICT_PAPER &&
         d->conflict_rule != EES_CONFLICT_HYBRID)
         return EES_EINVAL;
@@ -360,6 +362,7 @@ CallK make_call(const ees_ctx *c, const double *x, double h, double *A, double *
     k.A = A;
     k.b = b;
     k.gmin = c->gmin;
+    k.work = c->work;
     k.n_models = (int32_t)c->models.size();
     k.n_rail_nodes = (int32_t)c->rails.size();
     for (size_t r = 0; r < c->rails.size(); r++) k.rail_node[r] = c->rails[r];
@@ -449,6 +452,27 @@ ees_status enqueue(ees_ctx *c, int32_t variant, const double *x, double h, doubl
             PhaseMark m(c, st, 1, timed);
             e = launch_rail_finalize(call, c->partials, c->color_blk_off[c->n_colors], st);
             nl++;
+        }
+    } else if (variant == EES_COLOR_BUF) {
+        {
+            PhaseMark m(c, st, 0, timed);
+            int k = 0;
+            e = launch_gather_phase(c->L_gather.k(), c->gk, call, st, 0, &k);
+            nl += k;
+        }
+        {
+            PhaseMark m(c, st, 1, timed);
+            const DevK dv = c->L_colorh.k();
+            for (int32_t col = 0; col < c->n_colors && e == cudaSuccess; col++) {
+                e = launch_color_stamp(dv, c->gk, call, c->d_perm, c->color_ptr[col],
+                                       c->color_ptr[col + 1] - c->color_ptr[col], c->sk.buf, st);
+                nl++;
+            }
+            if (e == cudaSuccess && c->sk.n_side) {
+                int k = 0;
+                e = launch_side_sum(c->sk, call, st, &k);
+                nl += k;
+            }
         }
     } else if (variant == EES_TILE) {
         PhaseMark m(c, st, 0, timed);
@@ -633,7 +657,7 @@ ees_status build_hybrid(const ees_desc *d, ees_ctx *c, const std::vector<int32_t
             chunk_lo.push_back(std::min<int64_t>(sptr[k + 1], lo + kChunk));
         side_chunk.push_back((int32_t)chunk_lo.size() - 1);
     }
-    c->st.n_color_side_targets = ns;
+    c->st.n_color_side_targets = ns;           // side targets of the colour-phased stamps
     c->st.n_color_side_contributions = sptr[ns];
     if (c->host_only) return EES_OK;
     // colour-major copy
@@ -656,6 +680,7 @@ ees_status build_hybrid(const ees_desc *d, ees_ctx *c, const std::vector<int32_t
         term_c[q] = make_int4(d->d[i], d->g[i], d->s[i], d->b[i]);
         for (int p = 0; p < 16; p++) code_c[(size_t)p * N + q] = code[(size_t)p * N + i];
     }
+    TRY(upload(c, &c->d_perm, perm.data(), perm.size()));
     Layout &L = c->L_colorh;
     L.N = N;
     TRY(upload(c, &L.term, term_c.data(), N));
@@ -859,9 +884,12 @@ ees_status autotune(ees_ctx *c, bool full)
         return ms / reps;
     };
     const char *mode = std::getenv("EES_COLOR_MODE");   // debug knob: "launch" | "coop"
-    for (int32_t v = EES_COLOR; v <= (full ? EES_TILE : EES_COLOR) && rc == EES_OK; v++) {
+    for (int32_t v = EES_COLOR; v <= (full ? EES_COLOR_BUF : EES_COLOR) && rc == EES_OK; v++) {
         double ms;
-        if (v == EES_COLOR && c->hybrid) {
+        if (v == EES_COLOR_BUF) {
+            if (c->n_colors > 512) { c->st.tune_ms[v] = -1; continue; }
+            ms = time_variant(v);
+        } else if (v == EES_COLOR && c->hybrid) {
             c->color_coop = 0;
             if (c->n_colors > 512) { c->st.tune_ms[v] = -1; continue; }
             ms = time_variant(v);
@@ -970,14 +998,14 @@ ees_status setup_impl(const ees_desc *d, ees_ctx *c)
         for (int64_t i = 0; i < N; i++)
             nc += (d->d[i] >= 0) + (d->g[i] >= 0) + (d->s[i] >= 0) + (d->b[i] >= 0);
         c->st.n_contributions = nc;
-        if (c->hybrid) TRY(build_hybrid(d, c, raw_slot, excluded));
+        TRY(build_hybrid(d, c, raw_slot, excluded));
         TRY(build_tile(d, c, raw_slot, iptr, idev));
         c->variant = d->variant == EES_AUTO ? EES_ATOMIC : d->variant;
         c->st.setup_s = now_s() - t0;
         return EES_OK;
     }
     TRY(build_layouts(d, c, raw_slot, rail_ord));
-    if (c->hybrid) TRY(build_hybrid(d, c, raw_slot, excluded));
+    TRY(build_hybrid(d, c, raw_slot, excluded));      // COLOR (hybrid rule) and COLOR_BUF
     TRY(build_gather(d, c, raw_slot));
     TRY(build_tile(d, c, raw_slot, iptr, idev));
     int sms = 148;
@@ -1110,17 +1138,47 @@ ees_status ees_eval_stamp_host(ees_ctx *c, const double *x, double h, double *A,
 
 ees_status ees_set_variant(ees_ctx *c, int32_t variant)
 {
-    if (!c || variant < EES_AUTO || variant > EES_TILE) return EES_EINVAL;
+    if (!c || variant < EES_AUTO || variant > EES_COLOR_BUF) return EES_EINVAL;
     if (variant == EES_AUTO) {
         double best = 1e300;
         int32_t bv = c->variant;
-        for (int v = EES_COLOR; v <= EES_TILE; v++)
+        for (int v = EES_COLOR; v <= EES_COLOR_BUF; v++)
             if (c->st.tune_ms[v] > 0 && c->st.tune_ms[v] < best) { best = c->st.tune_ms[v]; bv = v; }
         c->variant = bv;
     } else {
         c->variant = variant;
     }
     return EES_OK;
+}
+
+ees_status ees_accept(ees_ctx *c, const double *x, ees_stream stream)
+{
+    if (!c) return EES_EINVAL;
+    if (c->host_only) return EES_ESTATE;
+    if (c->n_dev == 0) return EES_OK;
+    if (!x) return EES_EINVAL;
+    cudaStream_t st = (cudaStream_t)stream;
+    const CallK call = make_call(c, x, 1.0, nullptr, nullptr);
+    // ATOMIC and GATHER share one netlist-order copy of the state
+    cudaError_t e = launch_accept_soa(c->L_gather.term, c->n_dev, call, c->L_gather.v0, st);
+    if (e == cudaSuccess) e = launch_accept_soa(c->L_color.term, c->n_dev, call, c->L_color.v0, st);
+    if (e == cudaSuccess && c->hybrid)
+        e = launch_accept_soa(c->L_colorh.term, c->n_dev, call, c->L_colorh.v0, st);
+    if (e == cudaSuccess) e = launch_accept_tile(c->tk, call, const_cast<uint8_t *>(c->tk.blob), st);
+    return e == cudaSuccess ? EES_OK : EES_ECUDA;
+}
+
+ees_status ees_set_work(ees_ctx *c, int32_t work)
+{
+    if (!c || work < 1) return EES_EINVAL;
+    c->work = work;
+    return EES_OK;
+}
+
+ees_status ees_fp64_peak(double *tflops)
+{
+    if (!tflops) return EES_EINVAL;
+    return measure_fp64_peak(tflops) == cudaSuccess ? EES_OK : EES_ECUDA;
 }
 
 ees_status ees_stats(const ees_ctx *c, ees_stats_t *out)

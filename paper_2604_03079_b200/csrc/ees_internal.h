@@ -40,6 +40,7 @@ struct CallK {
     double *A;
     double *b;
     double gmin;
+    int32_t work;                     // S:229 work multiplier (>= 1)
     int32_t n_models;
     int32_t n_rail_nodes;
     int32_t n_rail_a;                 // rail entries [0, n_rail_a) are A slots, the rest b rows
@@ -98,7 +99,9 @@ struct GatherK {
 //            CSR block [a0, a0+na) and b rows [b0, b0+nb) (heavy-row slices,
 //            heavy x heavy targets); owned target j is A[a0+j] (j < na),
 //            b[b0+j-na] (j < na+nb), else global target xg[j-na-nb]
-//   tw:      u16[kTileThreads] per thread: first segment id | kTwCont | kTwNoEnd
+//   tw:      u32[kTileThreads] per thread: first segment id (low 16 bits) | the
+//            number of preceding chunks whose carries complete that segment
+//            (high 16 bits; 0 unless it continues from them and ends here)
 //   ent:     u16[K][kTileThreads] (thread-interleaved): byte offset 8*slot of the
 //            contribution in shared memory | kEntEnd on the
 //            last entry of a segment; padding points at the zero slot (pad 16)
@@ -111,16 +114,12 @@ constexpr int kTileThreads = 128;
 constexpr int kHeavyDeg = 64;        // nodes with more incident FETs are heavy
 constexpr int kStageMax = 10496;     // bytes of one pipeline stage (a tile blob)
 constexpr int kStages = 3;           // TMA pipeline depth (blobs in flight per CTA)
-constexpr int kTilePrefetch = 4;     // owned targets whose A/b value a thread prefetches
 constexpr int kSegMax = 768;         // owned targets + side entries per tile
 constexpr int kZeroSlot = 16 * kTileItems;   // s_c[kZeroSlot] == 0.0 (list padding)
 constexpr uint16_t kEntEnd = 0x8000;
-constexpr uint16_t kTwCont = 0x8000;     // the thread's first entry continues a segment
-constexpr uint16_t kTwNoEnd = 0x4000;    // no segment ends in the thread's chunk
-constexpr uint16_t kTwSid = 0x0FFF;
+constexpr uint32_t kTwSid = 0xFFFFu;
 constexpr int64_t kSideInlineParts = 8192;   // up to this many parts: last CTA finalises
 constexpr int kMaxHot = 16;          // side targets pre-reduced per CTA (rails): parts = CTAs, not tiles
-static_assert(kSegMax <= kTwSid + 1, "segment ids must fit the thread word");
 static_assert(8 * kZeroSlot < kEntEnd, "entry byte offsets must fit 15 bits");
 
 struct TileHdr {
@@ -200,6 +199,11 @@ struct SideK {
 cudaError_t launch_color_h(const DevK &dv16, const CallK &call, int64_t begin, int64_t count,
                            double *side_buf, cudaStream_t st);
 cudaError_t launch_side_sum(const SideK &sk, const CallK &call, cudaStream_t st, int *n_launches);
+cudaError_t launch_color_stamp(const DevK &dv16, const GatherK &gk, const CallK &call, const int32_t *perm,
+                               int64_t begin, int64_t count, double *side_buf, cudaStream_t st);
+cudaError_t launch_accept_soa(const int4 *term, int64_t N, const CallK &call, double *v0, cudaStream_t st);
+cudaError_t launch_accept_tile(const TileK &tk, const CallK &call, unsigned char *blob, cudaStream_t st);
+cudaError_t measure_fp64_peak(double *tflops);
 int tile_blocks_per_sm();
 cudaError_t launch_tile(const TileK &tk, const CallK &call, int grid, cudaStream_t st, int *n_launches);
 cudaError_t launch_atomic(const DevK &dv, const CallK &call, int grid, cudaStream_t st);

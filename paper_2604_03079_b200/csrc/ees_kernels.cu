@@ -32,9 +32,9 @@ struct Stamp {
     double j[4];
 };
 
-__device__ __forceinline__ void eval_fet(const CardK &cd, double beta, double gmin, double VD,
-                                         double VG, double VS, double v0gs, double v0gd,
-                                         double v0db, Stamp &st)
+__device__ __forceinline__ void eval_fet1(const CardK &cd, double beta, double gmin, double VD,
+                                          double VG, double VS, double v0gs, double v0gd,
+                                          double v0db, Stamp &st)
 {
     const double p = cd.p;
     const double vgs = p * (VG - VS);               // reflected frame
@@ -79,12 +79,31 @@ __device__ __forceinline__ void eval_fet(const CardK &cd, double beta, double gm
     st.j[3] = -qdb;
 }
 
+// SPEC S:229 work multiplier: the evaluation arithmetic is repeated `work`
+// times (BSIM4 cost emulation).  Each repetition reads
+// the biases through a dependency on the previous result (+0.0 * y: exact
+// for finite y), so the compiler cannot drop it; the result is the same.
+// Kernels are instantiated with kRep = false (work == 1, no loop) and true.
+template <bool kRep>
+__device__ __forceinline__ void eval_fet(const CardK &cd, double beta, double gmin, double VD,
+                                         double VG, double VS, double v0gs, double v0gd,
+                                         double v0db, Stamp &st, int work)
+{
+    eval_fet1(cd, beta, gmin, VD, VG, VS, v0gs, v0gd, v0db, st);
+    if (kRep)
+    for (int r = 1; r < work; r++) {
+        const double z = 0.0 * st.y[DD];
+        eval_fet1(cd, beta, gmin, VD + z, VG + z, VS + z, v0gs, v0gd, v0db, st);
+    }
+}
+
 __device__ __forceinline__ double volt(int t, const double *__restrict__ x, const double *s_railx)
 {
     return t >= 0 ? __ldg(x + t) : (t == -1 ? 0.0 : s_railx[-2 - t]);
 }
 
 // Load + evaluate device i of layout dv.  Returns terminal codes in T.
+template <bool kRep>
 __device__ __forceinline__ void load_eval(const DevK &dv, const CallK &P, const CardK *s_cards,
                                           const double *s_railx, int64_t i, int4 &T, Stamp &st)
 {
@@ -97,7 +116,7 @@ __device__ __forceinline__ void load_eval(const DevK &dv, const CallK &P, const 
     const double VD = volt(T.x, P.x, s_railx);
     const double VG = volt(T.y, P.x, s_railx);
     const double VS = volt(T.z, P.x, s_railx);
-    eval_fet(s_cards[m], beta, P.gmin, VD, VG, VS, a0, a1, a2, st);
+    eval_fet<kRep>(s_cards[m], beta, P.gmin, VD, VG, VS, a0, a1, a2, st, P.work);
 }
 
 __device__ __forceinline__ void load_call_smem(const CallK &P, CardK *s_cards, double *s_railx)
@@ -168,6 +187,7 @@ __device__ __forceinline__ void merge_source_bulk(const int4 &T, Stamp &st, int3
 // rail entries reduced per block, one atomic per block and entry at the end.
 // All per-device loads (data + 12 slots) are issued before the x gather.
 // ---------------------------------------------------------------------------
+template <bool kRep>
 __global__ void __launch_bounds__(kBlock, 4) k_atomic(DevK dv, CallK P)
 {
     __shared__ CardK s_cards[EES_MAX_MODELS];
@@ -199,7 +219,7 @@ __global__ void __launch_bounds__(kBlock, 4) k_atomic(DevK dv, CallK P)
             const double VD = volt(T.x, P.x, s_railx);
             const double VG = volt(T.y, P.x, s_railx);
             const double VS = volt(T.z, P.x, s_railx);
-            eval_fet(s_cards[m], beta, P.gmin, VD, VG, VS, a0, a1, a2, st);
+            eval_fet<kRep>(s_cards[m], beta, P.gmin, VD, VG, VS, a0, a1, a2, st, P.work);
             tc[0] = T.x; tc[1] = T.y; tc[2] = T.z; tc[3] = T.w;
             merge_source_bulk(T, st, slot, tc);
 #pragma unroll
@@ -230,6 +250,7 @@ __global__ void __launch_bounds__(kBlock, 4) k_atomic(DevK dv, CallK P)
 // so plain read-modify-write is race-free.  Rail entries go to a
 // per-block partial (deterministic), summed by k_rail_final.
 // ---------------------------------------------------------------------------
+template <bool kRep>
 __global__ void __launch_bounds__(kBlock) k_color(DevK dv, CallK P, int64_t begin, int64_t count,
                                                   double *partials)
 {
@@ -250,7 +271,7 @@ __global__ void __launch_bounds__(kBlock) k_color(DevK dv, CallK P, int64_t begi
     if (valid) {
 #pragma unroll
         for (int p = 0; p < NPAIR; p++) slot[p] = __ldg(dv.slot + (int64_t)p * dv.N + i);
-        load_eval(dv, P, s_cards, s_railx, i, T, st);
+        load_eval<kRep>(dv, P, s_cards, s_railx, i, T, st);
         tc[0] = T.x; tc[1] = T.y; tc[2] = T.z; tc[3] = T.w;
         merge_source_bulk(T, st, slot, tc);
 #pragma unroll
@@ -303,6 +324,7 @@ __global__ void __launch_bounds__(kBlock) k_rail_final(CallK P, const double *pa
 // are split into fixed chunks reduced by whole blocks (K3b tail blocks) and
 // summed in chunk order by K3c.
 // ---------------------------------------------------------------------------
+template <bool kRep>
 __global__ void __launch_bounds__(kBlock) k_gather_eval(DevK dv, GatherK gk, CallK P)
 {
     __shared__ CardK s_cards[EES_MAX_MODELS];
@@ -318,7 +340,7 @@ __global__ void __launch_bounds__(kBlock) k_gather_eval(DevK dv, GatherK gk, Cal
     if (i < dv.N) {
         int4 T;
         Stamp st;
-        load_eval(dv, P, s_cards, s_railx, i, T, st);
+        load_eval<kRep>(dv, P, s_cards, s_railx, i, T, st);
         const int tc[4] = {T.x, T.y, T.z, T.w};
         int o = gk.off[i] - base;
 #pragma unroll
@@ -380,6 +402,7 @@ __global__ void k_gather_heavy(GatherK gk, CallK P)
 // k_side_chunks sums each chunk of a side target's slots (fixed tree) and
 // k_side_apply adds the chunk sums of each target in chunk order.
 // ---------------------------------------------------------------------------
+template <bool kRep>
 __global__ void __launch_bounds__(kBlock) k_color_h(DevK dv, CallK P, int64_t begin, int64_t count,
                                                     double *side)
 {
@@ -400,7 +423,7 @@ __global__ void __launch_bounds__(kBlock) k_color_h(DevK dv, CallK P, int64_t be
     const double VG = T.y >= 0 ? __ldg(P.x + T.y) : 0.0;
     const double VS = T.z >= 0 ? __ldg(P.x + T.z) : 0.0;
     Stamp st;
-    eval_fet(s_cards[m], beta, P.gmin, VD, VG, VS, a0, a1, a2, st);
+    eval_fet<kRep>(s_cards[m], beta, P.gmin, VD, VG, VS, a0, a1, a2, st, P.work);
 #pragma unroll
     for (int p = 0; p < NPAIR; p++) {
         if (slot[p] >= 0) P.A[slot[p]] += st.y[p];
@@ -412,6 +435,47 @@ __global__ void __launch_bounds__(kBlock) k_color_h(DevK dv, CallK P, int64_t be
         if (k >= 0) P.b[k] += st.j[a];
         else if (k <= -2) side[-2 - k] = st.j[a];
     }
+}
+
+// The paper's non-fused "Color" (Table I; NEXT-2): after k_gather_eval
+// has written every FET's live contributions to the buffer (netlist order,
+// off[i]), one launch per colour stamps them: thread q of colour c reads FET
+// perm[q]'s contributions and applies the same codes as k_color_h.
+__global__ void __launch_bounds__(kBlock) k_color_stamp(DevK dv16, GatherK gk, CallK P, const int32_t *perm,
+                                                        int64_t begin, int64_t count, double *side)
+{
+    const int64_t q0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q0 >= count) return;
+    const int64_t q = begin + q0;
+    const int64_t i = __ldg(perm + q);
+    const int4 T = __ldg(dv16.term + q);
+    const int tc[4] = {T.x, T.y, T.z, T.w};
+    int32_t o = __ldg(gk.off + i);
+#pragma unroll
+    for (int p = 0; p < NPAIR; p++)
+        if (tc[pair_row(p)] >= 0 && tc[pair_col(p)] >= 0) {
+            const double y = gk.buf[o++];
+            const int32_t k = __ldg(dv16.slot + (int64_t)p * dv16.N + q);
+            if (k >= 0) P.A[k] += y;
+            else if (k <= -2) side[-2 - k] = y;
+        }
+#pragma unroll
+    for (int a = 0; a < 4; a++)
+        if (tc[a] >= 0) {
+            const double j = gk.buf[o++];
+            const int32_t k = __ldg(dv16.slot + (int64_t)(NPAIR + a) * dv16.N + q);
+            if (k >= 0) P.b[k] += j;
+            else if (k <= -2) side[-2 - k] = j;
+        }
+}
+
+cudaError_t launch_color_stamp(const DevK &dv16, const GatherK &gk, const CallK &call, const int32_t *perm,
+                               int64_t begin, int64_t count, double *side_buf, cudaStream_t st)
+{
+    if (count == 0) return cudaSuccess;
+    k_color_stamp<<<(unsigned)((count + kBlock - 1) / kBlock), kBlock, 0, st>>>(dv16, gk, call, perm, begin,
+                                                                                count, side_buf);
+    return cudaPeekAtLastError();
 }
 
 __global__ void __launch_bounds__(kBlock) k_side_chunks(SideK sk)
@@ -445,7 +509,9 @@ cudaError_t launch_color_h(const DevK &dv16, const CallK &call, int64_t begin, i
                            double *side_buf, cudaStream_t st)
 {
     if (count == 0) return cudaSuccess;
-    k_color_h<<<(unsigned)((count + kBlock - 1) / kBlock), kBlock, 0, st>>>(dv16, call, begin, count, side_buf);
+    const unsigned grid = (unsigned)((count + kBlock - 1) / kBlock);
+    if (call.work > 1) k_color_h<true><<<grid, kBlock, 0, st>>>(dv16, call, begin, count, side_buf);
+    else k_color_h<false><<<grid, kBlock, 0, st>>>(dv16, call, begin, count, side_buf);
     return cudaPeekAtLastError();
 }
 
@@ -457,6 +523,104 @@ cudaError_t launch_side_sum(const SideK &sk, const CallK &call, cudaStream_t st,
     k_side_apply<<<(sk.n_side + 127) / 128, 128, 0, st>>>(sk, call);
     *n_launches = 2;
     return cudaPeekAtLastError();
+}
+
+// ---------------------------------------------------------------------------
+// NEXT-4 state update (S:212 update_state, Fig. 1 accept branch): after a
+// converged step at x, every FET's companion state becomes the converged
+// branch voltages v_prev = (VG - VS, VG - VD, VD - VB) (physical frame), in
+// every layout's copy of it.  k_accept_soa: one SoA layout (terms plain or
+// rail-coded); k_accept_tile: the item sections of the TILE blobs.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kBlock) k_accept_soa(const int4 *term, int64_t N, CallK P, double *v0)
+{
+    __shared__ double s_railx[EES_MAX_RAILS];
+    for (int k = threadIdx.x; k < P.n_rail_nodes; k += blockDim.x) s_railx[k] = P.x[P.rail_node[k]];
+    __syncthreads();
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
+        const int4 T = term[i];
+        const double VD = volt(T.x, P.x, s_railx), VG = volt(T.y, P.x, s_railx);
+        const double VS = volt(T.z, P.x, s_railx), VB = volt(T.w, P.x, s_railx);
+        v0[i] = VG - VS;
+        v0[N + i] = VG - VD;
+        v0[2 * N + i] = VD - VB;
+    }
+}
+
+__global__ void __launch_bounds__(kTileThreads) k_accept_tile(TileK tk, CallK P, unsigned char *blob)
+{
+    unsigned char *b = blob + tk.blob_off[blockIdx.x];
+    const int ni = reinterpret_cast<const TileHdr *>(b)->n_items;
+    const int4 *term = reinterpret_cast<const int4 *>(b + sizeof(TileHdr));
+    double *v0 = reinterpret_cast<double *>(b + sizeof(TileHdr) + 16 * (size_t)ni) + ni;
+    for (int i = threadIdx.x; i < ni; i += blockDim.x) {
+        const int4 T = term[i];
+        const double VD = T.x >= 0 ? P.x[T.x] : 0.0, VG = T.y >= 0 ? P.x[T.y] : 0.0;
+        const double VS = T.z >= 0 ? P.x[T.z] : 0.0, VB = T.w >= 0 ? P.x[T.w] : 0.0;
+        v0[i] = VG - VS;
+        v0[ni + i] = VG - VD;
+        v0[2 * ni + i] = VD - VB;
+    }
+}
+
+cudaError_t launch_accept_soa(const int4 *term, int64_t N, const CallK &call, double *v0, cudaStream_t st)
+{
+    if (N == 0) return cudaSuccess;
+    const int64_t grid = std::min<int64_t>((N + kBlock - 1) / kBlock, 148 * 16);
+    k_accept_soa<<<(unsigned)grid, kBlock, 0, st>>>(term, N, call, v0);
+    return cudaPeekAtLastError();
+}
+
+cudaError_t launch_accept_tile(const TileK &tk, const CallK &call, unsigned char *blob, cudaStream_t st)
+{
+    if (tk.n_tiles == 0) return cudaSuccess;
+    k_accept_tile<<<tk.n_tiles, kTileThreads, 0, st>>>(tk, call, blob);
+    return cudaPeekAtLastError();
+}
+
+// ---------------------------------------------------------------------------
+// FP64 pipe peak: 8 independent FMA chains per thread, one
+// resident wave; flops = 2 * 8 * iters per thread.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_fp64_peak(double *out, int iters, double a, double c)
+{
+    double r[8];
+#pragma unroll
+    for (int k = 0; k < 8; k++) r[k] = threadIdx.x * 1e-9 + k;
+    for (int it = 0; it < iters; it++) {
+#pragma unroll
+        for (int k = 0; k < 8; k++) r[k] = fma(r[k], a, c);
+    }
+    double t = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; k++) t += r[k];
+    if (t == 12345.678) out[0] = t;      // practically never: keeps the chains live
+}
+
+cudaError_t measure_fp64_peak(double *tflops)
+{
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    double *out = nullptr;
+    cudaError_t e = cudaMalloc(&out, sizeof(double));
+    if (e != cudaSuccess) return e;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    const int grid = sms * 8, iters = 1 << 14;
+    k_fp64_peak<<<grid, 256>>>(out, 64, 0.999999, 1e-7);       // warm-up
+    cudaEventRecord(e0);
+    k_fp64_peak<<<grid, 256>>>(out, iters, 0.999999, 1e-7);
+    cudaEventRecord(e1);
+    e = cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    *tflops = 2.0 * 8.0 * iters * (double)grid * 256 / (ms * 1e-3) / 1e12;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(out);
+    return e == cudaSuccess ? cudaPeekAtLastError() : e;
 }
 
 // ---------------------------------------------------------------------------
@@ -507,7 +671,7 @@ static size_t rail_smem(const CallK &P) { return sizeof(double) * (kBlock / 32) 
 int atomic_blocks_per_sm()
 {
     int nb = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_atomic, kBlock,
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_atomic<false>, kBlock,
                                                   sizeof(double) * (kBlock / 32) * kMaxRailEntries);
     return nb > 0 ? nb : 1;
 }
@@ -515,7 +679,8 @@ int atomic_blocks_per_sm()
 cudaError_t launch_atomic(const DevK &dv, const CallK &call, int grid, cudaStream_t st)
 {
     if (dv.N == 0) return cudaSuccess;
-    k_atomic<<<grid, kBlock, rail_smem(call), st>>>(dv, call);
+    if (call.work > 1) k_atomic<true><<<grid, kBlock, rail_smem(call), st>>>(dv, call);
+    else k_atomic<false><<<grid, kBlock, rail_smem(call), st>>>(dv, call);
     return cudaPeekAtLastError();
 }
 
@@ -554,6 +719,7 @@ __device__ __forceinline__ void fetch_dev(const DevK &dv, const CallK &P, const 
     f.VS = volt(f.T.z, P.x, s_railx);
 }
 
+template <bool kRep>
 __global__ void __launch_bounds__(kBlock, 2) k_color_coop(DevK dv, CallK P, const int64_t *cptr,
                                                           int32_t C, double *partials)
 {
@@ -586,7 +752,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_color_coop(DevK dv, CallK P, cons
             Stamp st;
             int tc[4] = {-1, -1, -1, -1};
             if (valid) {
-                eval_fet(s_cards[f.m], f.beta, P.gmin, f.VD, f.VG, f.VS, f.a0, f.a1, f.a2, st);
+                eval_fet<kRep>(s_cards[f.m], f.beta, P.gmin, f.VD, f.VG, f.VS, f.a0, f.a1, f.a2, st, P.work);
                 tc[0] = f.T.x; tc[1] = f.T.y; tc[2] = f.T.z; tc[3] = f.T.w;
                 merge_source_bulk(f.T, st, f.slot, tc);
 #pragma unroll
@@ -634,7 +800,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_color_coop(DevK dv, CallK P, cons
 int color_coop_blocks_per_sm()
 {
     int nb = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_color_coop, kBlock,
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_color_coop<true>, kBlock,
                                                   sizeof(double) * (kBlock / 32) * kMaxRailEntries);
     return nb;
 }
@@ -649,7 +815,8 @@ cudaError_t launch_color_coop(const DevK &dv, const CallK &call, const int64_t *
     int32_t a3 = C;
     double *a4 = partials;
     void *args[] = {&a0, &a1, &a2, &a3, &a4};
-    return cudaLaunchCooperativeKernel((const void *)k_color_coop, dim3(grid), dim3(kBlock), args,
+    const void *fn = call.work > 1 ? (const void *)k_color_coop<true> : (const void *)k_color_coop<false>;
+    return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kBlock), args,
                                        rail_smem(call), st);
 }
 
@@ -658,7 +825,8 @@ cudaError_t launch_color(const DevK &dv, const CallK &call, int64_t begin, int64
 {
     if (count == 0) return cudaSuccess;
     const int64_t grid = (count + kBlock - 1) / kBlock;
-    k_color<<<(unsigned)grid, kBlock, rail_smem(call), st>>>(dv, call, begin, count, partials);
+    if (call.work > 1) k_color<true><<<(unsigned)grid, kBlock, rail_smem(call), st>>>(dv, call, begin, count, partials);
+    else k_color<false><<<(unsigned)grid, kBlock, rail_smem(call), st>>>(dv, call, begin, count, partials);
     return cudaPeekAtLastError();
 }
 
@@ -677,7 +845,8 @@ cudaError_t launch_gather_phase(const DevK &dv, const GatherK &gk, const CallK &
     if (dv.N == 0) return cudaSuccess;
     if (phase == 0) {
         const int64_t grid = (dv.N + kBlock - 1) / kBlock;
-        k_gather_eval<<<(unsigned)grid, kBlock, 0, st>>>(dv, gk, call);
+        if (call.work > 1) k_gather_eval<true><<<(unsigned)grid, kBlock, 0, st>>>(dv, gk, call);
+        else k_gather_eval<false><<<(unsigned)grid, kBlock, 0, st>>>(dv, gk, call);
         *n_launches = 1;
     } else if (phase == 1) {
         const int64_t light = (gk.n_targets + kBlock - 1) / kBlock;
@@ -799,9 +968,9 @@ struct TileView {
     {
         return reinterpret_cast<const int32_t *>(b + hdr().off_x);
     }
-    __device__ __forceinline__ const uint16_t *tw() const
+    __device__ __forceinline__ const uint32_t *tw() const
     {
-        return reinterpret_cast<const uint16_t *>(b + hdr().off_tw);
+        return reinterpret_cast<const uint32_t *>(b + hdr().off_tw);
     }
     __device__ __forceinline__ const uint16_t *ent() const
     {
@@ -815,42 +984,87 @@ struct TileView {
 
 __device__ __forceinline__ TileView tile_view(const unsigned char *blob) { return TileView{blob}; }
 
-// Address of owned target j (< n_own): the tile rows' CSR block, their b
-// rows, then the explicit ids.
-__device__ __forceinline__ double *owned_ptr(const TileView &v, const TileK &tk, const CallK &P, int j)
-{
-    const TileHdr &h = v.hdr();
-    const int na = h.na, nab = na + h.nb;
-    if (j < na) return P.A + h.a0 + j;
-    if (j < nab) return P.b + h.b0 + (j - na);
-    const int32_t g = v.xg()[j - nab];
-    return g < tk.nnz ? P.A + g : P.b + (g - tk.nnz);
-}
-
 // What a thread gathers from global memory for one tile: its item's node
-// voltages and the current values of the owned targets it writes.
+// voltages and the current values of the owned targets it writes (targets
+// tid + 128 k of the A block, of the b rows and of the explicit ids).
+constexpr int kPreA = 3, kPreB = 1, kPreX = 1;
 struct TileRegs {
     double VD, VG, VS;
-    double *dst[kTilePrefetch];
-    double pre[kTilePrefetch];
+    double preA[kPreA], preB[kPreB], preX[kPreX];
 };
 
 __device__ __forceinline__ void tile_gather(const TileView &v, const TileK &tk, const CallK &P,
                                             TileRegs &R)
 {
     const int tid = threadIdx.x;
+    const TileHdr &h = v.hdr();
     R.VD = R.VG = R.VS = 0.0;
-    if (tid < v.hdr().n_items) {
+    if (tid < h.n_items) {
         const int4 T = v.term()[tid];
         R.VD = T.x >= 0 ? __ldg(P.x + T.x) : 0.0;
         R.VG = T.y >= 0 ? __ldg(P.x + T.y) : 0.0;
         R.VS = T.z >= 0 ? __ldg(P.x + T.z) : 0.0;
     }
+    const int na = h.na, nb = h.nb, nx = h.n_own - na - nb;
+    const double *pA = P.A + h.a0, *pB = P.b + h.b0;
 #pragma unroll
-    for (int k = 0; k < kTilePrefetch; k++) {
+    for (int k = 0; k < kPreA; k++) {
         const int j = tid + k * kTileThreads;
-        R.dst[k] = j < v.hdr().n_own ? owned_ptr(v, tk, P, j) : nullptr;
-        R.pre[k] = R.dst[k] ? *R.dst[k] : 0.0;
+        R.preA[k] = j < na ? pA[j] : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < kPreB; k++) {
+        const int j = tid + k * kTileThreads;
+        R.preB[k] = j < nb ? pB[j] : 0.0;
+    }
+    const int32_t *xg = v.xg();
+#pragma unroll
+    for (int k = 0; k < kPreX; k++) {
+        const int j = tid + k * kTileThreads;
+        R.preX[k] = 0.0;
+        if (j < nx) {
+            const int32_t g = xg[j];
+            R.preX[k] = g < tk.nnz ? P.A[g] : P.b[g - tk.nnz];
+        }
+    }
+}
+
+// The owned-target stores of one tile: value (prefetched) + segment sum; the
+// targets beyond the prefetched ones take a read-modify-write.
+__device__ __forceinline__ void tile_write(const TileView &v, const TileK &tk, const CallK &P, const TileRegs &R,
+                                           const double *s_seg)
+{
+    const int tid = threadIdx.x;
+    const TileHdr &h = v.hdr();
+    const int na = h.na, nb = h.nb, nx = h.n_own - na - nb;
+    double *pA = P.A + h.a0, *pB = P.b + h.b0;
+#pragma unroll
+    for (int k = 0; k < kPreA; k++) {
+        const int j = tid + k * kTileThreads;
+        if (j < na) pA[j] = R.preA[k] + s_seg[j];
+    }
+    for (int j = tid + kPreA * kTileThreads; j < na; j += kTileThreads) pA[j] += s_seg[j];
+#pragma unroll
+    for (int k = 0; k < kPreB; k++) {
+        const int j = tid + k * kTileThreads;
+        if (j < nb) pB[j] = R.preB[k] + s_seg[na + j];
+    }
+    for (int j = tid + kPreB * kTileThreads; j < nb; j += kTileThreads) pB[j] += s_seg[na + j];
+    const int32_t *xg = v.xg();
+    const double *sx = s_seg + na + nb;
+#pragma unroll
+    for (int k = 0; k < kPreX; k++) {
+        const int j = tid + k * kTileThreads;
+        if (j < nx) {
+            const int32_t g = xg[j];
+            double *d = g < tk.nnz ? P.A + g : P.b + (g - tk.nnz);
+            *d = R.preX[k] + sx[j];
+        }
+    }
+    for (int j = tid + kPreX * kTileThreads; j < nx; j += kTileThreads) {
+        const int32_t g = xg[j];
+        double *d = g < tk.nnz ? P.A + g : P.b + (g - tk.nnz);
+        *d += sx[j];
     }
 }
 
@@ -908,7 +1122,7 @@ __device__ __forceinline__ unsigned long long globaltimer()
             tk.trace[(size_t)blockIdx.x * kTraceSlots + (slot)] = globaltimer();    \
     } while (0)
 
-template <bool kTrace>
+template <bool kTrace, bool kRep>
 __global__ void __launch_bounds__(kTileThreads, 4) k_tile(TileK tk, CallK P)
 {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -966,8 +1180,8 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_tile(TileK tk, CallK P)
         if (tid < ni) {
             Stamp st;
             const double *bt = v.beta(ni);
-            eval_fet(s_cards[v.model(ni)[tid]], bt[tid], P.gmin, cur.VD, cur.VG, cur.VS, bt[ni + tid],
-                     bt[2 * ni + tid], bt[3 * ni + tid], st);
+            eval_fet<kRep>(s_cards[v.model(ni)[tid]], bt[tid], P.gmin, cur.VD, cur.VG, cur.VS, bt[ni + tid],
+                     bt[2 * ni + tid], bt[3 * ni + tid], st, P.work);
             const int4 T = v.term()[tid];
             if (T.z == T.w && T.z != -1) {        // source tied to bulk: one entry each (ees_internal.h)
                 st.y[DS] += st.y[DB];
@@ -996,7 +1210,7 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_tile(TileK tk, CallK P)
         }
         // balanced segmented sum (entries are byte offsets into s_c | kEntEnd);
         // four entries' loads are issued before their adds
-        const uint16_t w = v.tw()[tid];
+        const uint32_t w = v.tw()[tid];
         {
             const int K = v.hdr().K;
             const uint16_t *e = v.ent() + tid;
@@ -1026,24 +1240,16 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_tile(TileK tk, CallK P)
         }
         TILE_TRACE(3 + 4 * it);
         __syncthreads();                                        // B2
-        if ((w & (kTwCont | kTwNoEnd)) == kTwCont) {
-            int k = tid - 1;
-            double acc = s_carry[k];
-            const uint16_t *tw = v.tw();
-            while ((tw[k] & (kTwCont | kTwNoEnd)) == (kTwCont | kTwNoEnd)) {
-                k--;
-                acc += s_carry[k];
-            }
+        if (w >> 16) {                 // this chunk ends a segment begun in earlier chunks
+            const int chain = (int)(w >> 16);
+            double acc = s_carry[tid - 1];
+            for (int c = 2; c <= chain; c++) acc += s_carry[tid - c];
             s_seg[w & kTwSid] += acc;
         }
         __syncthreads();                                        // B3
         TILE_TRACE(4 + 4 * it);
         const int n_own = v.hdr().n_own;
-#pragma unroll
-        for (int k = 0; k < kTilePrefetch; k++)
-            if (cur.dst[k]) *cur.dst[k] = cur.pre[k] + s_seg[tid + k * kTileThreads];
-        for (int j = tid + kTilePrefetch * kTileThreads; j < n_own; j += kTileThreads)
-            *owned_ptr(v, tk, P, j) += s_seg[j];
+        tile_write(v, tk, P, cur, s_seg);
         // side parts (plain stores; ordered by the fence + ticket below); a hot
         // target appears at most once per tile, so one thread owns s_hot[h] here
         for (int e = tid; e < v.hdr().n_sent; e += kTileThreads) {
@@ -1103,10 +1309,13 @@ __global__ void __launch_bounds__(256) k_side_final(TileK tk, CallK P)
 
 int tile_blocks_per_sm()
 {
-    cudaFuncSetAttribute(k_tile<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmem);
-    cudaFuncSetAttribute(k_tile<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmem);
-    int nb = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_tile<false>, kTileThreads, kTileSmem);
+    cudaFuncSetAttribute(k_tile<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmem);
+    cudaFuncSetAttribute(k_tile<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmem);
+    cudaFuncSetAttribute(k_tile<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmem);
+    int nb = 0, nb2 = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_tile<false, false>, kTileThreads, kTileSmem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb2, k_tile<false, true>, kTileThreads, kTileSmem);
+    nb = nb2 > 0 && nb2 < nb ? nb2 : nb;      // one grid (the hot-part layout) serves both
     return nb > 0 ? nb : 1;
 }
 
@@ -1114,8 +1323,9 @@ cudaError_t launch_tile(const TileK &tk, const CallK &call, int grid, cudaStream
 {
     *n_launches = 0;
     if (tk.n_tiles == 0) return cudaSuccess;
-    if (tk.trace) k_tile<true><<<grid, kTileThreads, kTileSmem, st>>>(tk, call);
-    else k_tile<false><<<grid, kTileThreads, kTileSmem, st>>>(tk, call);
+    if (tk.trace) k_tile<true, false><<<grid, kTileThreads, kTileSmem, st>>>(tk, call);
+    else if (call.work > 1) k_tile<false, true><<<grid, kTileThreads, kTileSmem, st>>>(tk, call);
+    else k_tile<false, false><<<grid, kTileThreads, kTileSmem, st>>>(tk, call);
     *n_launches = 1;
     if (tk.n_side && !tk.side_inline) {
         k_side_final<<<(unsigned)((tk.n_side * 32 + 255) / 256), 256, 0, st>>>(tk, call);

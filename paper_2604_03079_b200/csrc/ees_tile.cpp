@@ -27,9 +27,9 @@ constexpr int32_t kSide = -2;
 // per listed contribution), one padding entry per owned target nobody stamps
 // (2 B), explicit ids of heavy-row slice targets (4 B), heavy x heavy targets
 // (4 B id or an 8 B side entry) -- plus the fixed per-tile parts: header,
-// thread words (256 B), list padding to whole chunks (< 256 B) and the
+// thread words (512 B), list padding to whole chunks (< 256 B) and the
 // padding of four sections.
-constexpr int64_t kBlobFixed = 64 + 256 + 256 + 64;
+constexpr int64_t kBlobFixed = 64 + 512 + 256 + 64;
 constexpr int64_t kOwnMax = kSegMax;   // owned targets + side entries (s_seg capacity)
 size_t pad16(size_t x) { return (x + 15) & ~(size_t)15; }
 }  // namespace
@@ -252,7 +252,8 @@ bool build_tile_host(int64_t N, int32_t n_nodes, int32_t n, int64_t nnz, const i
     std::vector<int32_t> sid_of((size_t)NT, -1);
     std::vector<std::pair<int32_t, uint16_t>> con, side;
     std::vector<int32_t> gids, xg;
-    std::vector<uint16_t> ent, tw;
+    std::vector<uint16_t> ent;
+    std::vector<uint32_t> tw;
     std::vector<int32_t> seg_of;
     std::vector<SideEnt> sents;
     std::vector<int32_t> sent_tile_sid;     // side id of each entry, in emission order
@@ -402,18 +403,25 @@ bool build_tile_host(int64_t N, int32_t n_nodes, int32_t n, int64_t nnz, const i
         const int64_t L = (int64_t)ent.size();
         const int32_t K = (int32_t)((L + kTileThreads - 1) / kTileThreads);
         tw.assign(kTileThreads, 0);
+        auto chunk_has_end = [&](int64_t th2) {
+            for (int64_t p2 = th2 * K; p2 < std::min<int64_t>(L, (th2 + 1) * K); p2++)
+                if (ent[p2] & kEntEnd) return true;
+            return false;
+        };
         for (int32_t th2 = 0; th2 < kTileThreads; th2++) {
             const int64_t p0 = (int64_t)th2 * K;
-            if (p0 >= L) {
-                tw[th2] = kTwNoEnd;
-                continue;
+            if (p0 >= L) continue;
+            uint32_t chain = 0;
+            if (p0 > 0 && seg_of[p0 - 1] == seg_of[p0] && chunk_has_end(th2)) {
+                // the segment began in earlier chunks: count them (each carries a partial)
+                int64_t k2 = th2 - 1;
+                chain = 1;
+                while (k2 > 0 && seg_of[k2 * K - 1] == seg_of[p0]) {
+                    k2--;
+                    chain++;
+                }
             }
-            uint16_t w = (uint16_t)seg_of[p0];
-            if (p0 > 0 && seg_of[p0 - 1] == seg_of[p0]) w |= kTwCont;
-            bool any_end = false;
-            for (int64_t p2 = p0; p2 < std::min<int64_t>(L, p0 + K); p2++) any_end |= (ent[p2] & kEntEnd) != 0;
-            if (!any_end) w |= kTwNoEnd;
-            tw[th2] = w;
+            tw[th2] = (uint32_t)seg_of[p0] | (chain << 16);
         }
         // emit the blob
         TileHdr hdr;
@@ -430,7 +438,7 @@ bool build_tile_host(int64_t N, int32_t n_nodes, int32_t n, int64_t nnz, const i
         const size_t items_bytes = pad16((size_t)ni * 49);
         hdr.off_x = (uint32_t)(pad16(sizeof(TileHdr)) + items_bytes);
         hdr.off_tw = (uint32_t)(hdr.off_x + 4 * xg.size());
-        hdr.off_ent = (uint32_t)(hdr.off_tw + 2 * kTileThreads);
+        hdr.off_ent = (uint32_t)(hdr.off_tw + 4 * kTileThreads);
         hdr.off_side = (uint32_t)pad16(hdr.off_ent + 2 * (size_t)K * kTileThreads);
         const size_t bytes = pad16(hdr.off_side + sizeof(SideEnt) * sents.size());
         if (bytes > (size_t)kStageMax || K > 65535) return false;
@@ -454,7 +462,7 @@ bool build_tile_host(int64_t N, int32_t n_nodes, int32_t n, int64_t nnz, const i
             md[q] = (uint8_t)model[i];
         }
         if (!xg.empty()) std::memcpy(bp + hdr.off_x, xg.data(), 4 * xg.size());
-        std::memcpy(bp + hdr.off_tw, tw.data(), 2 * tw.size());
+        std::memcpy(bp + hdr.off_tw, tw.data(), 4 * tw.size());
         uint16_t *ep = reinterpret_cast<uint16_t *>(bp + hdr.off_ent);
         for (int64_t k = 0; k < (int64_t)K * kTileThreads; k++) {
             const int64_t th2 = k / K, kk = k % K;     // logical position k -> thread th2, step kk
