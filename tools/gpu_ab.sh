@@ -1,8 +1,8 @@
-# A/B: same bench in several trees (with a parity spot-check in each)
+# A/B: same bench in several trees (usage: bash tools/gpu_ab.sh "<trees>" "<configs>" <variant>)
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out; rm -rf gpurun_out/*
-for tree in ab_a ab_b ab_v8 .; do
-  (cd $tree && timeout 600 python -m pytest tests -m gpu -q -x -k "parity_reduced and tile" > ../gpurun_out/ab_$(basename $tree)_pytest.log 2>&1)
-  for c in 3 2 4 1; do
-  (cd $tree && timeout 300 python bench.py --config $c --variant tile --no-cpu-baseline --no-e2e --steps 30) > gpurun_out/ab_$(basename $tree)_c$c.log 2>&1
+for tree in $1; do
+  for c in $2; do
+  (cd $tree && timeout 300 python bench.py --config $c --variant $3 --no-cpu-baseline --no-e2e --steps 30) > gpurun_out/ab_$(basename $tree)_c$c.log 2>&1
 done; done
+timeout 900 python -m pytest tests -m gpu -q -x -k "not full_size and not hybrid_color_full" > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/rc.txt
