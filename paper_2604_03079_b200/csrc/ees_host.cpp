@@ -852,8 +852,9 @@ ees_status build_tile(const ees_desc *d, ees_ctx *c, const std::vector<int32_t> 
     TRY(dalloc(c, &k.done, 1));
     if (cudaMemset(k.done, 0, sizeof(uint32_t)) != cudaSuccess) return EES_ECUDA;
     TRY(dalloc(c, &k.part, (size_t)th.n_parts));
-    // the grid the hot parts were laid out for (every CTA stores its hot parts)
-    c->tile_grid = grid;
+    // persistent CTAs: no more than tiles (the hot parts are laid out for
+    // `grid` CTAs; k_tile sums the first gridDim.x of them)
+    c->tile_grid = th.grid;
     return EES_OK;
 }
 

@@ -164,6 +164,7 @@ struct TileHost {
     int64_t n_parts = 0, hot_base = 0;
     int64_t n_listed = 0, n_padded = 0;    // list entries, and with chunk padding
     int32_t blob_max = 0, n_hot = 0;
+    int32_t grid = 1;                      // persistent CTAs the hot-part layout is made for
     std::vector<int64_t> blob_off;
     std::vector<uint8_t> blob;
     std::vector<int32_t> sd_gid, sd_part, hot_gid;

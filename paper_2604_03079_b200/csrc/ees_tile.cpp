@@ -485,7 +485,10 @@ bool build_tile_host(int64_t N, int32_t n_nodes, int32_t n, int64_t nnz, const i
     }
     // partial slots.  Side targets with parts in far more tiles than there are
     // CTAs (rails) are "hot": each CTA pre-sums its tiles' parts in tile order
-    // and stores one part (CTA order), so the final sum has `grid` terms.
+    // and stores one part (CTA order), so the final sum has `grid` terms; the
+    // kernel runs min(grid, tiles) CTAs, the grid this layout is made for.
+    grid = std::max(1, std::min(grid, T));
+    out.grid = grid;
     // Every other side target gets one part per contributing tile, in tile order.
     out.n_side = (int32_t)out.sd_gid.size();
     std::vector<int64_t> cnt((size_t)out.n_side, 0);
