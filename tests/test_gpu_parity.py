@@ -370,3 +370,57 @@ def test_fp64_peak_plausible(cuda_ok):
     from paper_2604_03079_b200 import fp64_peak
     t = fp64_peak()
     assert 5.0 < t < 200.0
+
+
+def test_cuda_graph_capture(cuda_ok):
+    """ees_eval_stamp only enqueues work, so an NR loop can capture it in a
+    CUDA graph (task: CUDA graphs instead of a tracing compiler): every
+    variant captured once and replayed matches the oracle; the TILE ticket
+    resets itself between replays."""
+    import torch
+    nl = netgen.config(1, 0.02)
+    ref = reference(nl)
+    ctx = ctx_for(nl)
+    dev = torch.device("cuda")
+    x = torch.from_numpy(nl.x).to(dev)
+    A = torch.zeros(ctx.nnz, dtype=torch.float64, device=dev)
+    b = torch.zeros(ctx.n, dtype=torch.float64, device=dev)
+    for v in VARIANTS:
+        ctx.set_variant(v)
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):                  # warm up outside the capture
+            ctx.eval_stamp(x, nl.h, A, b)
+        torch.cuda.current_stream().wait_stream(s)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            A.zero_()
+            b.zero_()
+            ctx.eval_stamp(x, nl.h, A, b)
+        for _ in range(3):
+            g.replay()
+        torch.cuda.synchronize()
+        assert_parity(ref, A.cpu().numpy(), b.cpu().numpy(), f"graph {v}")
+
+
+def test_star_giant_node(cuda_ok):
+    """Degenerate fanout: 3,000 FETs with every gate on one node (a 3,000-way
+    hub: one colour each, a single-entry hot spot for ATOMIC, a heavy side
+    target for TILE), both polarities, private drains."""
+    N = 3000
+    terms = [(i + 1, 0, -1 if i % 2 == 0 else N + 1, -1 if i % 2 == 0 else N + 1) for i in range(N)]
+    nl = netgen.custom("star", N + 2, terms, [i % 2 for i in range(N)], netgen.bench_models(),
+                       rails=[N + 1])
+    ref = reference(nl)
+    ctx = ctx_for(nl)
+    assert ctx.stats()["n_colors"] == N
+    for v in VARIANTS:
+        if v in ("color", "color_buf"):
+            continue                     # 3,000 colour launches; covered by the hybrid below
+        assert_parity(ref, *gpu_run(ctx, nl, v), f"star {v}")
+    ctx.close()
+    ctx = ctx_for(nl, rule="hybrid", heavy_degree=64, variant="color")
+    assert ctx.stats()["n_colors"] == 1
+    assert_parity(ref, *gpu_run(ctx, nl), "star hybrid color")
+    ctx.set_variant("color_buf")
+    assert_parity(ref, *gpu_run(ctx, nl), "star hybrid color_buf")

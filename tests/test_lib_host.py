@@ -142,6 +142,15 @@ def test_host_only_refuses_eval():
     assert _lib.lib.ees_eval_stamp(c._h, buf, 0.0, buf, buf, None) == _lib.EES_EINVAL
     assert _lib.lib.ees_eval_stamp(c._h, buf, float("nan"), buf, buf, None) == _lib.EES_EINVAL
     assert _lib.lib.ees_eval_stamp(None, buf, 1e-12, buf, buf, None) == _lib.EES_EINVAL
+    # NEXT-4 calls: no device state on a host-only context; argument checks first
+    assert _lib.lib.ees_accept(c._h, buf, None) == _lib.EES_ESTATE
+    assert _lib.lib.ees_accept(None, buf, None) == _lib.EES_EINVAL
+    assert _lib.lib.ees_set_work(c._h, 0) == _lib.EES_EINVAL
+    assert _lib.lib.ees_set_work(c._h, 50) == _lib.EES_OK
+    assert _lib.lib.ees_set_work(None, 2) == _lib.EES_EINVAL
+    assert _lib.lib.ees_fp64_peak(None) == _lib.EES_EINVAL
+    assert _lib.lib.ees_set_variant(c._h, 6) == _lib.EES_EINVAL
+    assert _lib.lib.ees_set_variant(c._h, _lib.EES_COLOR_BUF) == _lib.EES_OK
 
 
 def test_empty_netlist():
@@ -197,3 +206,23 @@ def test_adder_setup_equals_oracle(split, rule):
     ocol, oC = oracle.greedy_color(nl, rule)
     assert C_ == oC and np.array_equal(col, ocol)
     assert c.stats()["n_tiles"] >= 1
+
+
+def test_invalid_hybrid_threshold():
+    from paper_2604_03079_b200 import Context, EESError
+    nl = netgen.inverter_chain(4)
+    with pytest.raises(EESError):
+        Context.from_netlist(nl, rule="hybrid", heavy_degree=-1, host_only=True)
+    c = Context.from_netlist(nl, rule="hybrid", heavy_degree=0, host_only=True)   # 0 = default 64
+    assert c.stats()["n_excluded_nodes"] == 1                                      # the rail
+
+
+def test_tile_single_giant_node():
+    """TILE setup on a star: one light-by-count node would hold every FET;
+    it becomes heavy and its entries go to side parts (setup must not fail)."""
+    N = 3000
+    terms = [(i + 1, 0, -1, -1) for i in range(N)]            # all gates on node 0
+    nl = netgen.custom("star", N + 1, terms, 0, netgen.bench_models())
+    c = _ctx(nl)
+    st = c.stats()
+    assert st["n_tiles"] >= N // 128 and st["n_heavy_nodes"] >= 1 and st["n_side_targets"] >= 2
