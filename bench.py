@@ -93,7 +93,7 @@ class ClockSampler:
                0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
                0x100: "display_clock_setting"}
 
-    def __init__(self, index, period=0.005):
+    def __init__(self, index, period=0.001):
         self.index, self.period = index, period
         self.samples, self.reasons = [], set()
         self.max_mhz = None

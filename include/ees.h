@@ -212,8 +212,9 @@ ees_status ees_race_probe(ees_ctx *ctx, const int32_t *color, int64_t *n_conflic
 
 /* Debug: one EES_TILE call that also records %globaltimer stamps (ns) per
  * CTA into trace [n_ctas][64] (host, cap entries): slot 0 start, 1 first tile
- * staged, per tile i: 2+4i evaluated, 3+4i after the barrier, 4+4i sums
- * stored, 5+4i end; 62 ticket taken, 63 end.  Synchronous. */
+ * staged, per tile i < 15: 2+4i evaluated (and the next tile's gathers
+ * issued), 3+4i segment sums done, 4+4i carries fixed up, 5+4i owned entries
+ * stored; 62 ticket taken, 63 end.  Synchronous. */
 ees_status ees_tile_trace(ees_ctx *ctx, const double *x, double h, double *A_vals, double *b,
                           ees_stream stream, uint64_t *trace, int64_t cap, int32_t *n_ctas);
 
@@ -235,6 +236,12 @@ ees_status ees_set_work(ees_ctx *ctx, int32_t work);
  * wave of independent FMA chains; the FP64 roofline denominator).
  * Synchronous.  *tflops out. */
 ees_status ees_fp64_peak(double *tflops);
+
+/* Measures FP64 RED (atomicAdd without return) throughput of the current
+ * device in G lane-operations/s: mode 0 = every lane its own address
+ * (spread), mode 1 = all lanes of a warp on one address per warp.
+ * Synchronous.  (the atomic variant's ceiling.) */
+ees_status ees_red_throughput(int32_t mode, double *gops);
 
 ees_status ees_destroy(ees_ctx *ctx);
 

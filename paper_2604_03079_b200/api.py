@@ -42,6 +42,13 @@ def fp64_peak():
     return t.value
 
 
+def red_throughput(mode=0):
+    """ees_red_throughput: FP64 RED G lane-ops/s (0 spread, 1 same address per warp)."""
+    t = C.c_double()
+    _check(L.lib.ees_red_throughput(int(mode), C.byref(t)), "ees_red_throughput")
+    return t.value
+
+
 class Context:
     """ees_setup / ees_eval_stamp / ees_stats ... on one CUDA device."""
 

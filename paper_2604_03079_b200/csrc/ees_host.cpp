@@ -1182,6 +1182,12 @@ ees_status ees_fp64_peak(double *tflops)
     return measure_fp64_peak(tflops) == cudaSuccess ? EES_OK : EES_ECUDA;
 }
 
+ees_status ees_red_throughput(int32_t mode, double *gops)
+{
+    if (!gops || (mode != 0 && mode != 1)) return EES_EINVAL;
+    return measure_red_throughput(mode, gops) == cudaSuccess ? EES_OK : EES_ECUDA;
+}
+
 ees_status ees_stats(const ees_ctx *c, ees_stats_t *out)
 {
     if (!c || !out) return EES_EINVAL;

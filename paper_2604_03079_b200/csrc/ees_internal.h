@@ -205,6 +205,7 @@ cudaError_t launch_color_stamp(const DevK &dv16, const GatherK &gk, const CallK 
 cudaError_t launch_accept_soa(const int4 *term, int64_t N, const CallK &call, double *v0, cudaStream_t st);
 cudaError_t launch_accept_tile(const TileK &tk, const CallK &call, unsigned char *blob, cudaStream_t st);
 cudaError_t measure_fp64_peak(double *tflops);
+cudaError_t measure_red_throughput(int mode, double *gops);
 int tile_blocks_per_sm();
 cudaError_t launch_tile(const TileK &tk, const CallK &call, int grid, cudaStream_t st, int *n_launches);
 cudaError_t launch_atomic(const DevK &dv, const CallK &call, int grid, cudaStream_t st);

@@ -624,6 +624,49 @@ cudaError_t measure_fp64_peak(double *tflops)
 }
 
 // ---------------------------------------------------------------------------
+// FP64 RED throughput: every thread issues `iters` REDs of
+// 1.0 to a 64 MiB buffer -- its own address per iteration (mode 0, spread
+// over L2 slices) or its warp's one address (mode 1, same-address).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_red_peak(double *buf, int64_t n, int iters, int mode)
+{
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t T = (int64_t)gridDim.x * blockDim.x;
+    for (int it = 0; it < iters; it++) {
+        const int64_t k = mode == 0 ? (t + (int64_t)it * T) % n : ((t >> 5) * 37 + it) % n;
+        atomicAdd(buf + k, 1.0);
+    }
+}
+
+cudaError_t measure_red_throughput(int mode, double *gops)
+{
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t n = (64ll << 20) / 8;
+    double *buf = nullptr;
+    cudaError_t e = cudaMalloc(&buf, n * sizeof(double));
+    if (e != cudaSuccess) return e;
+    cudaMemset(buf, 0, n * sizeof(double));
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    const int grid = sms * 8, iters = 64;
+    k_red_peak<<<grid, 256>>>(buf, n, 4, mode);
+    cudaEventRecord(e0);
+    k_red_peak<<<grid, 256>>>(buf, n, iters, mode);
+    cudaEventRecord(e1);
+    e = cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    *gops = (double)iters * grid * 256 / (ms * 1e-3) / 1e9;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(buf);
+    return e == cudaSuccess ? cudaPeekAtLastError() : e;
+}
+
+// ---------------------------------------------------------------------------
 // Race instrument: per colour, count distinct-device writers
 // of every non-rail A entry and b row.
 // ---------------------------------------------------------------------------

@@ -372,6 +372,13 @@ def test_fp64_peak_plausible(cuda_ok):
     assert 5.0 < t < 200.0
 
 
+def test_red_throughput_plausible(cuda_ok):
+    """K6 microbenchmark: spread REDs beat same-address REDs."""
+    from paper_2604_03079_b200 import red_throughput
+    spread, same = red_throughput(0), red_throughput(1)
+    assert spread > 10.0 and same > 0.1 and spread > same
+
+
 def test_cuda_graph_capture(cuda_ok):
     """ees_eval_stamp only enqueues work, so an NR loop can capture it in a
     CUDA graph (task: CUDA graphs instead of a tracing compiler): every
