@@ -133,6 +133,7 @@ typedef struct {
     double tune_ms[6];                      /* EES_AUTO: measured ms per call of
                                                [_, COLOR, ATOMIC, GATHER, TILE, COLOR_BUF] */
     int32_t n_excluded_nodes;               /* nodes outside the conflict relation */
+    int32_t tile_form;                      /* EES_TILE: 0 items in the tile blobs, 1 items in HBM arrays */
     int32_t n_color_side_targets;           /* EES_CONFLICT_HYBRID: entries summed after the colours */
     int64_t n_color_side_contributions;     /* their contributions (scratch slots) */
 } ees_stats_t;

@@ -816,17 +816,45 @@ ees_status build_tile(const ees_desc *d, ees_ctx *c, const std::vector<int32_t> 
         const ees_model &m = c->models[d->model[i]];
         beta[i] = (m.kp * d->w[i]) / d->l[i];
     }
+    // TILE form (ees_internal.h): items in HBM arrays (form 1, 5 CTAs/SM)
+    // unless FETs are copied into several tiles, where the extra per-copy
+    // loads cost more than the occupancy gains (form 0; measured: cfg3 1.6x
+    // slower in form 1, cfg4 10% faster).  A FET is copied once more for
+    // every light terminal far (> 32 ids) from its others' rows.
+    int form = 1;
+    {
+        const int32_t NN = std::max(1, c->n_nodes);
+        std::vector<uint8_t> heavy((size_t)NN, 0);
+        for (int32_t v = 0; v < c->n_nodes; v++) heavy[v] = (iptr[v + 1] - iptr[v]) > kHeavyDeg;
+        for (int32_t r : c->rails) heavy[r] = 1;
+        int64_t extra = 0;
+        for (int64_t i = 0; i < N; i++) {
+            int32_t lo = INT32_MAX;
+            for (int a = 0; a < 4; a++)
+                if (TT[a][i] >= 0 && !heavy[TT[a][i]]) lo = std::min(lo, TT[a][i]);
+            for (int a = 0; a < 4; a++) {
+                const int32_t t = TT[a][i];
+                bool dup = false;
+                for (int b2 = 0; b2 < a; b2++) dup |= TT[b2][i] == t;
+                if (t >= 0 && !heavy[t] && !dup && t - lo > 32) extra++;
+            }
+        }
+        if (N && (double)extra / (double)N > 0.5) form = 0;
+        const char *f = std::getenv("EES_TILE_FORM");       // experiments: force a form
+        if (f && (f[0] == '0' || f[0] == '1')) form = f[0] - '0';
+    }
     int sms = 148, dev = 0;
-    int grid = sms * 4;
+    int grid = sms * tile_ctas(form);
     if (!c->host_only) {
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        grid = sms * tile_blocks_per_sm();
+        grid = sms * tile_blocks_per_sm(form);
     }
     TileHost th;
-    if (!build_tile_host(N, c->n_nodes, c->n, c->nnz, TT, raw_slot.data(), iptr, idev, c->rails,
+    if (!build_tile_host(form, N, c->n_nodes, c->n, c->nnz, TT, raw_slot.data(), iptr, idev, c->rails,
                          c->row_ptr, c->col_idx, beta.data(), d->vprev, d->model, grid, th))
         return EES_EINVAL;
+    c->st.tile_form = form;
     c->st.n_tiles = th.n_tiles;
     c->st.n_heavy_nodes = th.n_heavy;
     c->st.n_side_targets = th.n_side;
@@ -834,6 +862,7 @@ ees_status build_tile(const ees_desc *d, ees_ctx *c, const std::vector<int32_t> 
     c->st.tile_blob_max = th.blob_max;
     if (c->host_only) return EES_OK;
     TileK &k = c->tk;
+    k.form = form;
     k.n_tiles = th.n_tiles;
     k.nnz = c->nnz;
     auto up = [&](auto **dst, const auto &vec) {
@@ -842,6 +871,9 @@ ees_status build_tile(const ees_desc *d, ees_ctx *c, const std::vector<int32_t> 
     };
     TRY(up(&k.blob_off, th.blob_off));
     TRY(up(&k.blob, th.blob));
+    TRY(up(&k.item_beta, th.item_beta));
+    TRY(up(&k.item_v0, th.item_v0));
+    TRY(up(&k.item_model, th.item_model));
     TRY(up(&k.sd_gid, th.sd_gid));
     TRY(up(&k.sd_part, th.sd_part));
     TRY(up(&k.hot_gid, th.hot_gid));
@@ -1165,7 +1197,8 @@ ees_status ees_accept(ees_ctx *c, const double *x, ees_stream stream)
     if (e == cudaSuccess) e = launch_accept_soa(c->L_color.term, c->n_dev, call, c->L_color.v0, st);
     if (e == cudaSuccess && c->hybrid)
         e = launch_accept_soa(c->L_colorh.term, c->n_dev, call, c->L_colorh.v0, st);
-    if (e == cudaSuccess) e = launch_accept_tile(c->tk, call, const_cast<uint8_t *>(c->tk.blob), st);
+    if (e == cudaSuccess)
+        e = launch_accept_tile(c->tk, call, c->tk.form == 1 ? const_cast<double *>(c->tk.item_v0) : nullptr, st);
     return e == cudaSuccess ? EES_OK : EES_ECUDA;
 }
 

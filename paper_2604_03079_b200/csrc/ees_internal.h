@@ -94,7 +94,11 @@ struct GatherK {
 // values is one 16-byte-aligned blob that a TMA bulk copy (cp.async.bulk +
 // mbarrier) brings into shared memory, kStages tiles ahead:
 //   TileHdr
-//   items:   term int4[ni] | beta f64[ni] | v0 f64[3][ni] | model u8[ni] (pad 16)
+//   items:   form 0: term int4[ni] | beta f64[ni] | v0 f64[3][ni] | model u8[ni]
+//            form 1: term int4[ni]; the rest of an item (beta, v0[3], model)
+//            is in tile-order HBM arrays (kTileItems slots per tile) that each
+//            thread loads one tile ahead into registers -- smaller stages, so
+//            5 CTAs per SM instead of 4 (pad 16)
 //   xg:      int32[n_x] global ids of the owned targets after the tile rows'
 //            CSR block [a0, a0+na) and b rows [b0, b0+nb) (heavy-row slices,
 //            heavy x heavy targets); owned target j is A[a0+j] (j < na),
@@ -112,7 +116,11 @@ struct GatherK {
 constexpr int kTileItems = 128;      // max items (FET copies) per tile = threads per CTA
 constexpr int kTileThreads = 128;
 constexpr int kHeavyDeg = 64;        // nodes with more incident FETs are heavy
-constexpr int kStageMax = 10496;     // bytes of one pipeline stage (a tile blob)
+// TILE forms (chosen at setup from the FET copy factor, ees_host.cpp):
+// stage bytes (one tile blob), item bytes in the blob, CTAs per SM
+__host__ __device__ constexpr int stage_max(int form) { return form ? 6144 : 10496; }
+__host__ __device__ constexpr int item_blob_bytes(int form) { return form ? 16 : 49; }
+__host__ __device__ constexpr int tile_ctas(int form) { return form ? 5 : 4; }
 constexpr int kStages = 3;           // TMA pipeline depth (blobs in flight per CTA)
 constexpr int kSegMax = 768;         // owned targets + side entries per tile
 constexpr int kZeroSlot = 16 * kTileItems;   // s_c[kZeroSlot] == 0.0 (list padding)
@@ -137,6 +145,7 @@ struct SideEnt {
 };
 
 struct TileK {
+    int32_t form;                  // 0: whole items in the blob; 1: items' data in HBM arrays
     int32_t n_tiles;
     int64_t nnz;
     const int64_t *blob_off;       // [T+1] byte offsets into blob
@@ -148,6 +157,9 @@ struct TileK {
     const int32_t *sd_gid;         // [n_side] global target
     const int32_t *hot_gid;        // [n_hot] global target of each hot side target
     const int32_t *sd_part;        // [n_side+1] partial ranges
+    const double *item_beta;       // [n_tiles * kTileItems]
+    const double *item_v0;         // [n_tiles * kTileItems][3]
+    const uint8_t *item_model;     // [n_tiles * kTileItems]
     uint32_t *done;                // CTA completion ticket, self-resetting
     double *part;                  // [n_side_entries]
     unsigned long long *trace;     // debug: [grid][kTraceSlots] %globaltimer stamps, or null
@@ -167,11 +179,13 @@ struct TileHost {
     int32_t grid = 1;                      // persistent CTAs the hot-part layout is made for
     std::vector<int64_t> blob_off;
     std::vector<uint8_t> blob;
+    std::vector<double> item_beta, item_v0;
+    std::vector<uint8_t> item_model;
     std::vector<int32_t> sd_gid, sd_part, hot_gid;
 };
 // ees_tile.cpp.  Per-FET data for the item sections: beta (computed by the
 // caller exactly as for the other layouts), vprev [3][N], model.
-bool build_tile_host(int64_t N, int32_t n_nodes, int32_t n, int64_t nnz, const int32_t *const TT[4],
+bool build_tile_host(int form, int64_t N, int32_t n_nodes, int32_t n, int64_t nnz, const int32_t *const TT[4],
                      const int32_t *raw_slot, const std::vector<int64_t> &iptr,
                      const std::vector<int32_t> &idev, const std::vector<int32_t> &rails,
                      const std::vector<int32_t> &row_ptr, const std::vector<int32_t> &col_idx,
@@ -203,10 +217,10 @@ cudaError_t launch_side_sum(const SideK &sk, const CallK &call, cudaStream_t st,
 cudaError_t launch_color_stamp(const DevK &dv16, const GatherK &gk, const CallK &call, const int32_t *perm,
                                int64_t begin, int64_t count, double *side_buf, cudaStream_t st);
 cudaError_t launch_accept_soa(const int4 *term, int64_t N, const CallK &call, double *v0, cudaStream_t st);
-cudaError_t launch_accept_tile(const TileK &tk, const CallK &call, unsigned char *blob, cudaStream_t st);
+cudaError_t launch_accept_tile(const TileK &tk, const CallK &call, double *item_v0, cudaStream_t st);
 cudaError_t measure_fp64_peak(double *tflops);
 cudaError_t measure_red_throughput(int mode, double *gops);
-int tile_blocks_per_sm();
+int tile_blocks_per_sm(int form);
 cudaError_t launch_tile(const TileK &tk, const CallK &call, int grid, cudaStream_t st, int *n_launches);
 cudaError_t launch_atomic(const DevK &dv, const CallK &call, int grid, cudaStream_t st);
 cudaError_t launch_color(const DevK &dv, const CallK &call, int64_t begin, int64_t count,

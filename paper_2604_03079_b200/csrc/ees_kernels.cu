@@ -530,7 +530,7 @@ cudaError_t launch_side_sum(const SideK &sk, const CallK &call, cudaStream_t st,
 // converged step at x, every FET's companion state becomes the converged
 // branch voltages v_prev = (VG - VS, VG - VD, VD - VB) (physical frame), in
 // every layout's copy of it.  k_accept_soa: one SoA layout (terms plain or
-// rail-coded); k_accept_tile: the item sections of the TILE blobs.
+// rail-coded); k_accept_tile: the TILE item state (tile order, terms in the blobs).
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kBlock) k_accept_soa(const int4 *term, int64_t N, CallK P, double *v0)
 {
@@ -547,19 +547,22 @@ __global__ void __launch_bounds__(kBlock) k_accept_soa(const int4 *term, int64_t
     }
 }
 
-__global__ void __launch_bounds__(kTileThreads) k_accept_tile(TileK tk, CallK P, unsigned char *blob)
+__global__ void __launch_bounds__(kTileThreads) k_accept_tile(TileK tk, CallK P, double *item_v0)
 {
-    unsigned char *b = blob + tk.blob_off[blockIdx.x];
+    unsigned char *b = const_cast<unsigned char *>(tk.blob) + tk.blob_off[blockIdx.x];
     const int ni = reinterpret_cast<const TileHdr *>(b)->n_items;
     const int4 *term = reinterpret_cast<const int4 *>(b + sizeof(TileHdr));
-    double *v0 = reinterpret_cast<double *>(b + sizeof(TileHdr) + 16 * (size_t)ni) + ni;
+    // form 1: v0[3] per item in the tile-order array; form 0: v0[3][ni] in the blob
+    double *v0 = item_v0 ? item_v0 + (int64_t)blockIdx.x * kTileItems * 3
+                         : reinterpret_cast<double *>(b + sizeof(TileHdr) + 16 * (size_t)ni) + ni;
+    const int s1 = item_v0 ? 3 : 1, s2 = item_v0 ? 1 : ni;     // item stride, component stride
     for (int i = threadIdx.x; i < ni; i += blockDim.x) {
         const int4 T = term[i];
         const double VD = T.x >= 0 ? P.x[T.x] : 0.0, VG = T.y >= 0 ? P.x[T.y] : 0.0;
         const double VS = T.z >= 0 ? P.x[T.z] : 0.0, VB = T.w >= 0 ? P.x[T.w] : 0.0;
-        v0[i] = VG - VS;
-        v0[ni + i] = VG - VD;
-        v0[2 * ni + i] = VD - VB;
+        v0[s1 * i] = VG - VS;
+        v0[s1 * i + s2] = VG - VD;
+        v0[s1 * i + 2 * s2] = VD - VB;
     }
 }
 
@@ -571,10 +574,10 @@ cudaError_t launch_accept_soa(const int4 *term, int64_t N, const CallK &call, do
     return cudaPeekAtLastError();
 }
 
-cudaError_t launch_accept_tile(const TileK &tk, const CallK &call, unsigned char *blob, cudaStream_t st)
+cudaError_t launch_accept_tile(const TileK &tk, const CallK &call, double *item_v0, cudaStream_t st)
 {
     if (tk.n_tiles == 0) return cudaSuccess;
-    k_accept_tile<<<tk.n_tiles, kTileThreads, 0, st>>>(tk, call, blob);
+    k_accept_tile<<<tk.n_tiles, kTileThreads, 0, st>>>(tk, call, item_v0);
     return cudaPeekAtLastError();
 }
 
@@ -987,7 +990,8 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase)
 }
 
 constexpr int kSlots = kZeroSlot + 2;          // 16 contributions per item + the zero slot (+pad)
-constexpr size_t kTileSmem = sizeof(double) * (kSlots + kSegMax + kTileThreads) + kStages * (size_t)kStageMax;
+template <int kForm>
+constexpr size_t tile_smem() { return sizeof(double) * (kSlots + kSegMax + kTileThreads) + kStages * (size_t)stage_max(kForm); }
 
 // View of one staged tile blob (layout in ees_internal.h): only the blob's
 // shared-memory address lives in registers; header fields and section
@@ -999,6 +1003,7 @@ struct TileView {
     {
         return reinterpret_cast<const int4 *>(b + sizeof(TileHdr));
     }
+    // form 0: the item data after the terms
     __device__ __forceinline__ const double *beta(int ni) const
     {
         return reinterpret_cast<const double *>(b + sizeof(TileHdr) + 16 * ni);
@@ -1047,16 +1052,27 @@ __device__ __forceinline__ double *owned_ptr(const TileView &v, const TileK &tk,
 constexpr int kTilePrefetch = 4;
 struct TileRegs {
     double VD, VG, VS;
+    double beta, v0a, v0b, v0c;      // the item's data (HBM, tile order)
+    int model;
     double *dst[kTilePrefetch];
     double pre[kTilePrefetch];
 };
 
-__device__ __forceinline__ void tile_gather(const TileView &v, const TileK &tk, const CallK &P,
-                                            TileRegs &R)
+template <int kForm>
+__device__ __forceinline__ void tile_gather(const TileView &v, int32_t tile, const TileK &tk,
+                                            const CallK &P, TileRegs &R)
 {
     const int tid = threadIdx.x;
     R.VD = R.VG = R.VS = 0.0;
     if (tid < v.hdr().n_items) {
+        if (kForm == 1) {
+            const int64_t q = (int64_t)tile * kTileItems + tid;
+            R.beta = __ldg(tk.item_beta + q);
+            R.v0a = __ldg(tk.item_v0 + 3 * q);
+            R.v0b = __ldg(tk.item_v0 + 3 * q + 1);
+            R.v0c = __ldg(tk.item_v0 + 3 * q + 2);
+            R.model = __ldg(tk.item_model + q);
+        }
         const int4 T = v.term()[tid];
         R.VD = T.x >= 0 ? __ldg(P.x + T.x) : 0.0;
         R.VG = T.y >= 0 ? __ldg(P.x + T.y) : 0.0;
@@ -1124,8 +1140,8 @@ __device__ __forceinline__ unsigned long long globaltimer()
             tk.trace[(size_t)blockIdx.x * kTraceSlots + (slot)] = globaltimer();    \
     } while (0)
 
-template <bool kTrace, bool kRep>
-__global__ void __launch_bounds__(kTileThreads, 4) k_tile(TileK tk, CallK P)
+template <bool kTrace, bool kRep, int kForm>
+__global__ void __launch_bounds__(kTileThreads, tile_ctas(kForm)) k_tile(TileK tk, CallK P)
 {
     extern __shared__ __align__(16) unsigned char smem[];
     double *s_c = reinterpret_cast<double *>(smem);          // [16][kTileItems] + zero slot
@@ -1151,7 +1167,7 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_tile(TileK tk, CallK P)
         const int64_t off = tk.blob_off[tile];
         const uint32_t bytes = (uint32_t)(tk.blob_off[tile + 1] - off);
         mbar_expect_tx(&s_bar[stage], bytes);
-        tma_bulk_g2s(s_stage + (size_t)stage * kStageMax, tk.blob + off, bytes, &s_bar[stage]);
+        tma_bulk_g2s(s_stage + (size_t)stage * stage_max(kForm), tk.blob + off, bytes, &s_bar[stage]);
     };
     const int32_t t0 = blockIdx.x;
     if (tid == 0) {
@@ -1171,7 +1187,7 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_tile(TileK tk, CallK P)
         mbar_wait(&s_bar[0], 0);
         parity ^= 1u;
         v = tile_view(s_stage);
-        tile_gather(v, tk, P, cur);
+        tile_gather<kForm>(v, t0, tk, P, cur);
     }
     TILE_TRACE(1);
     const unsigned char *s_cb = reinterpret_cast<const unsigned char *>(s_c);
@@ -1181,9 +1197,14 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_tile(TileK tk, CallK P)
         const int ni = v.hdr().n_items;
         if (tid < ni) {
             Stamp st;
-            const double *bt = v.beta(ni);
-            eval_fet<kRep>(s_cards[v.model(ni)[tid]], bt[tid], P.gmin, cur.VD, cur.VG, cur.VS, bt[ni + tid],
-                     bt[2 * ni + tid], bt[3 * ni + tid], st, P.work);
+            if (kForm == 1) {
+                eval_fet<kRep>(s_cards[cur.model], cur.beta, P.gmin, cur.VD, cur.VG, cur.VS, cur.v0a, cur.v0b,
+                               cur.v0c, st, P.work);
+            } else {
+                const double *bt = v.beta(ni);
+                eval_fet<kRep>(s_cards[v.model(ni)[tid]], bt[tid], P.gmin, cur.VD, cur.VG, cur.VS, bt[ni + tid],
+                               bt[2 * ni + tid], bt[3 * ni + tid], st, P.work);
+            }
             const int4 T = v.term()[tid];
             if (T.z == T.w && T.z != -1) {        // source tied to bulk: one entry each (ees_internal.h)
                 st.y[DS] += st.y[DB];
@@ -1201,8 +1222,8 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_tile(TileK tk, CallK P)
         if (tn < tk.n_tiles) {
             mbar_wait(&s_bar[sn], (parity >> sn) & 1u);
             parity ^= 1u << sn;
-            vn = tile_view(s_stage + (size_t)sn * kStageMax);
-            tile_gather(vn, tk, P, nxt);
+            vn = tile_view(s_stage + (size_t)sn * stage_max(kForm));
+            tile_gather<kForm>(vn, tn, tk, P, nxt);
         }
         TILE_TRACE(2 + 4 * it);
         __syncthreads();                                        // B1
@@ -1313,25 +1334,37 @@ __global__ void __launch_bounds__(256) k_side_final(TileK tk, CallK P)
     if (sid < tk.n_side) side_finish(tk, P, sid, threadIdx.x & 31);
 }
 
-int tile_blocks_per_sm()
+template <int kForm>
+static int tile_bps()
 {
-    cudaFuncSetAttribute(k_tile<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmem);
-    cudaFuncSetAttribute(k_tile<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmem);
-    cudaFuncSetAttribute(k_tile<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTileSmem);
+    constexpr int smem = (int)tile_smem<kForm>();
+    cudaFuncSetAttribute(k_tile<false, false, kForm>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(k_tile<true, false, kForm>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(k_tile<false, true, kForm>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     int nb = 0, nb2 = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_tile<false, false>, kTileThreads, kTileSmem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb2, k_tile<false, true>, kTileThreads, kTileSmem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_tile<false, false, kForm>, kTileThreads, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb2, k_tile<false, true, kForm>, kTileThreads, smem);
     nb = nb2 > 0 && nb2 < nb ? nb2 : nb;      // one grid (the hot-part layout) serves both
     return nb > 0 ? nb : 1;
+}
+
+int tile_blocks_per_sm(int form) { return form == 1 ? tile_bps<1>() : tile_bps<0>(); }
+
+template <int kForm>
+static void launch_tile_form(const TileK &tk, const CallK &call, int grid, cudaStream_t st)
+{
+    constexpr size_t smem = tile_smem<kForm>();
+    if (tk.trace) k_tile<true, false, kForm><<<grid, kTileThreads, smem, st>>>(tk, call);
+    else if (call.work > 1) k_tile<false, true, kForm><<<grid, kTileThreads, smem, st>>>(tk, call);
+    else k_tile<false, false, kForm><<<grid, kTileThreads, smem, st>>>(tk, call);
 }
 
 cudaError_t launch_tile(const TileK &tk, const CallK &call, int grid, cudaStream_t st, int *n_launches)
 {
     *n_launches = 0;
     if (tk.n_tiles == 0) return cudaSuccess;
-    if (tk.trace) k_tile<true, false><<<grid, kTileThreads, kTileSmem, st>>>(tk, call);
-    else if (call.work > 1) k_tile<false, true><<<grid, kTileThreads, kTileSmem, st>>>(tk, call);
-    else k_tile<false, false><<<grid, kTileThreads, kTileSmem, st>>>(tk, call);
+    if (tk.form == 1) launch_tile_form<1>(tk, call, grid, st);
+    else launch_tile_form<0>(tk, call, grid, st);
     *n_launches = 1;
     if (tk.n_side && !tk.side_inline) {
         k_side_final<<<(unsigned)((tk.n_side * 32 + 255) / 256), 256, 0, st>>>(tk, call);

@@ -34,7 +34,7 @@ constexpr int64_t kOwnMax = kSegMax;   // owned targets + side entries (s_seg ca
 size_t pad16(size_t x) { return (x + 15) & ~(size_t)15; }
 }  // namespace
 
-bool build_tile_host(int64_t N, int32_t n_nodes, int32_t n, int64_t nnz, const int32_t *const TT[4],
+bool build_tile_host(int form, int64_t N, int32_t n_nodes, int32_t n, int64_t nnz, const int32_t *const TT[4],
                      const int32_t *raw_slot, const std::vector<int64_t> &iptr,
                      const std::vector<int32_t> &idev, const std::vector<int32_t> &rails,
                      const std::vector<int32_t> &row_ptr, const std::vector<int32_t> &col_idx,
@@ -42,6 +42,7 @@ bool build_tile_host(int64_t N, int32_t n_nodes, int32_t n, int64_t nnz, const i
                      TileHost &out)
 {
     static_assert(kOwnMax > 64, "tile budget too small");
+    const int64_t kStageMax = stage_max(form), kItemBlobBytes = item_blob_bytes(form);
     // source tied to bulk: the kernel merges DB/BD/BB/J[B] into DS/SD/SS/J[S]
     auto merged = [&](int64_t i) { return TT[2][i] == TT[3][i] && TT[2][i] != -1; };
     // is contribution p (12 pairs, then 4 b rows) of FET i in a list?
@@ -171,7 +172,7 @@ bool build_tile_host(int64_t N, int32_t n_nodes, int32_t n, int64_t nnz, const i
                 const int32_t i = idev[k];
                 if (mark[i] != t) {
                     fresh++;
-                    add_bytes += 49 + 2 * live_count(i);
+                    add_bytes += kItemBlobBytes + 2 * live_count(i);
                 }
                 if (home[i] < 0) {
                     const int32_t hh = hh_new(i, t);
@@ -212,7 +213,7 @@ bool build_tile_host(int64_t N, int32_t n_nodes, int32_t n, int64_t nnz, const i
     for (int64_t i = 0; i < N; i++)
         if (home[i] < 0) {
             const int32_t add = hh_count(i);
-            const int64_t add_bytes = 49 + 2 * live_count(i) + 12 * add;
+            const int64_t add_bytes = kItemBlobBytes + 2 * live_count(i) + 12 * add;
             if (!cur.empty() && ((int64_t)cur.size() + 1 > kTileItems || own + add > kOwnMax ||
                                  bytes + add_bytes > kStageMax))
                 close_tile();
@@ -435,7 +436,7 @@ bool build_tile_host(int64_t N, int32_t n_nodes, int32_t n, int64_t nnz, const i
         hdr.na = na;
         hdr.b0 = b0;
         hdr.nb = nb;
-        const size_t items_bytes = pad16((size_t)ni * 49);
+        const size_t items_bytes = pad16((size_t)ni * kItemBlobBytes);
         hdr.off_x = (uint32_t)(pad16(sizeof(TileHdr)) + items_bytes);
         hdr.off_tw = (uint32_t)(hdr.off_x + 4 * xg.size());
         hdr.off_ent = (uint32_t)(hdr.off_tw + 4 * kTileThreads);
@@ -449,16 +450,27 @@ bool build_tile_host(int64_t N, int32_t n_nodes, int32_t n, int64_t nnz, const i
         std::memcpy(bp, &hdr, sizeof(hdr));
         uint8_t *it = bp + pad16(sizeof(TileHdr));
         int4 *term = reinterpret_cast<int4 *>(it);
-        double *bt = reinterpret_cast<double *>(it + 16 * (size_t)ni);
-        double *v0 = bt + ni;
-        uint8_t *md = reinterpret_cast<uint8_t *>(v0 + 3 * (size_t)ni);
+        // form 0: beta, v0, model follow the terms in the blob; form 1: they
+        // live in tile-order arrays, kTileItems slots per tile (v0 per item)
+        const size_t ib = (size_t)tt * kTileItems;
+        if (form == 1 && out.item_beta.size() < ib + kTileItems) {
+            out.item_beta.resize(ib + kTileItems, 0.0);
+            out.item_v0.resize(3 * (ib + kTileItems), 0.0);
+            out.item_model.resize(ib + kTileItems, 0);
+        }
+        double *bt = form == 1 ? out.item_beta.data() + ib : reinterpret_cast<double *>(it + 16 * (size_t)ni);
+        double *v0b = bt + ni;                                     // form 0 only
+        uint8_t *md = form == 1 ? out.item_model.data() + ib : reinterpret_cast<uint8_t *>(v0b + 3 * (size_t)ni);
         for (int32_t q = 0; q < ni; q++) {
             const int32_t i = item_dev[q0 + q];
             int4 tv;
             tv.x = TT[0][i]; tv.y = TT[1][i]; tv.z = TT[2][i]; tv.w = TT[3][i];
             std::memcpy(term + q, &tv, sizeof(tv));
             bt[q] = beta[i];
-            for (int k = 0; k < 3; k++) v0[k * ni + q] = vprev[k * N + i];
+            for (int k = 0; k < 3; k++) {
+                if (form == 1) out.item_v0[(ib + q) * 3 + k] = vprev[k * N + i];
+                else v0b[k * ni + q] = vprev[k * N + i];
+            }
             md[q] = (uint8_t)model[i];
         }
         if (!xg.empty()) std::memcpy(bp + hdr.off_x, xg.data(), 4 * xg.size());
