@@ -431,3 +431,54 @@ def test_star_giant_node(cuda_ok):
     assert_parity(ref, *gpu_run(ctx, nl), "star hybrid color")
     ctx.set_variant("color_buf")
     assert_parity(ref, *gpu_run(ctx, nl), "star hybrid color_buf")
+
+
+# ---------------------------------------------------------------- NEXT-4: NR transient loop
+def _cpu_transient(nl, sources, x0, h, steps, tol):
+    """The same backward-Euler NR loop with every A, b from the oracle and a
+    numpy dense solve (Fig. 1)."""
+    xs = []
+    x = x0.copy()
+    vprev = nl.vprev.copy()
+    for _ in range(steps):
+        for _it in range(50):
+            nl2 = netgen.Netlist(**{**nl.__dict__, "x": x, "vprev": vprev})
+            ref = oracle.reference(nl2)
+            n = nl.n
+            A = np.zeros((n, n))
+            rows = np.repeat(np.arange(n), np.diff(ref["row_ptr"]))
+            np.add.at(A, (rows, ref["col_idx"]), ref["A"])
+            b = ref["b"].copy()
+            for node, br, v in sources:
+                A[node, br] += 1.0
+                A[br, node] += 1.0
+                b[br] += v
+            x_new = np.linalg.solve(A, b)
+            done = np.abs(x_new - x).max() <= tol
+            x = x_new
+            if done:
+                break
+        vprev = np.ascontiguousarray(netgen._vprev(x, nl.d, nl.g, nl.s, nl.b))
+        xs.append(x.copy())
+    return xs
+
+
+def test_transient_nr_loop_matches_oracle(cuda_ok):
+    """NEXT-4: a 5-step backward-Euler transient of two 11-stage ring
+    oscillators driven through ees_eval_stamp + ees_accept with a dense
+    solve equals the same loop run on the oracle (every step, every node)."""
+    import torch
+    from paper_2604_03079_b200.transient import Transient, rail_sources
+    nl = netgen.ring_oscillators(2, 11)
+    src = rail_sources(nl)
+    want = _cpu_transient(nl, src, nl.x.copy(), nl.h, 5, 1e-13)
+    for v in ("tile", "atomic", "color"):
+        ctx = ctx_for(nl, variant=v)
+        tr = Transient(ctx, src)
+        xs, its = tr.run(torch.from_numpy(nl.x.copy()).cuda(), nl.h, 5, abstol=1e-13, reltol=0.0)
+        assert max(its) < 50
+        for k, (g, w) in enumerate(zip(xs, want)):
+            g = g.cpu().numpy()
+            assert np.abs(g - w).max() <= 1e-9 * max(1.0, np.abs(w).max()), f"{v} step {k}"
+        assert abs(g[nl.rails[0]] - 1.0) < 1e-12       # the rail stays at its source
+        ctx.close()
