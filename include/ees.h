@@ -91,7 +91,7 @@ typedef struct {
 typedef struct {
     int32_t n_nodes;         /* non-ground nodes, >= 0 */
     int32_t n_extra;         /* branch unknowns after the nodes, >= 0 */
-    int64_t n_dev;           /* MOSFETs, >= 0 */
+    int64_t n_dev;           /* MOSFETs, 0 .. 2^31 - 2 (device lists use int32 indices) */
     const int32_t *d, *g, *s, *b;   /* host [n_dev], each in [-1, n_nodes); -1 = ground */
     const double *w, *l;            /* host [n_dev], metres, finite and > 0 */
     const int32_t *model;           /* host [n_dev], in [0, n_models) */

@@ -124,6 +124,7 @@ ees_status validate(const ees_desc *d)
 {
     if (!d) return EES_EINVAL;
     if (d->n_nodes < 0 || d->n_extra < 0 || d->n_dev < 0) return EES_EINVAL;
+    if (d->n_dev > INT32_MAX - 1) return EES_EINVAL;   // FET indices are int32 in every device list
     if ((int64_t)d->n_nodes + d->n_extra > INT32_MAX - 1) return EES_EINVAL;
     if (d->n_models < 1 || d->n_models > EES_MAX_MODELS || !d->models) return EES_EINVAL;
     if (d->n_rails < 0 || d->n_rails > EES_MAX_RAILS || (d->n_rails && !d->rails)) return EES_EINVAL;

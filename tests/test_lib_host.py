@@ -133,6 +133,19 @@ def test_invalid_descriptors():
         assert e.value.status == -1
 
 
+def test_descriptor_size_limits():
+    """n_dev beyond the int32 device lists, and negative sizes, are refused
+    before any array is read (the pointers here are deliberately null)."""
+    from paper_2604_03079_b200 import _lib
+    m = _lib.ees_model(1, 0, 0.3, 2e-5, 0.0, 0.0, 0.0, 0.0)
+    for n_dev, n_nodes in ((2 ** 31, 4), (-1, 4), (0, -1)):
+        desc = _lib.ees_desc(n_nodes=n_nodes, n_extra=0, n_dev=n_dev, n_models=1,
+                             models=C.cast(C.pointer(m), C.c_void_p), flags=_lib.EES_SETUP_HOST_ONLY)
+        h = C.c_void_p()
+        assert _lib.lib.ees_setup(C.byref(desc), C.byref(h)) == _lib.EES_EINVAL
+        assert not h.value
+
+
 def test_host_only_refuses_eval():
     from paper_2604_03079_b200 import _lib
     c = _ctx(netgen.inverter_chain(4))
