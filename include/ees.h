@@ -134,6 +134,7 @@ typedef struct {
                                                [_, COLOR, ATOMIC, GATHER, TILE, COLOR_BUF] */
     int32_t n_excluded_nodes;               /* nodes outside the conflict relation */
     int32_t tile_form;                      /* EES_TILE: 0 items in the tile blobs, 1 items in HBM arrays */
+    int32_t gather_form;                    /* EES_GATHER: 0 compact buffer + index lists, 1 target-ordered */
     int32_t n_color_side_targets;           /* EES_CONFLICT_HYBRID: entries summed after the colours */
     int64_t n_color_side_contributions;     /* their contributions (scratch slots) */
 } ees_stats_t;

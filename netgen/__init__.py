@@ -501,13 +501,16 @@ CONFIG_NAMES = {
 
 def named(name: str) -> Netlist:
     """Extra workloads by name (bench.py --netlist): Benchmark 2's adder and
-    its resistor variants, cfgN[@scale]."""
+    its resistor variants, cfgN[@scale], synth<N>_<C>."""
     if name == "adder64":
         return full_adder_28t(64)
     if name == "adder64_r14":
         return insert_resistors(full_adder_28t(64), 14)
     if name == "adder64_r89":
         return insert_resistors(full_adder_28t(64), "all")
+    if name.startswith("synth"):                       # synth<N>_<C>: gen_synth (B5)
+        n_dev, c_target = name[5:].split("_")
+        return gen_synth(int(n_dev), int(c_target))
     if name.startswith("cfg"):
         i, _, sc = name[3:].partition("@")
         return config(int(i), float(sc) if sc else 1.0)

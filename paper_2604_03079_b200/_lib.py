@@ -47,7 +47,8 @@ class ees_stats_t(C.Structure):
                 ("setup_s", f64), ("setup_pattern_s", f64), ("setup_color_s", f64),
                 ("n_tiles", i32), ("n_heavy_nodes", i32), ("n_side_targets", i32),
                 ("tile_blob_max", i32), ("n_tile_items", i64), ("tune_ms", f64 * 6),
-                ("n_excluded_nodes", i32), ("tile_form", i32), ("n_color_side_targets", i32),
+                ("n_excluded_nodes", i32), ("tile_form", i32), ("gather_form", i32),
+                ("n_color_side_targets", i32),
                 ("n_color_side_contributions", i64)]
 
 

@@ -457,9 +457,8 @@ ees_status enqueue(ees_ctx *c, int32_t variant, const double *x, double h, doubl
     } else if (variant == EES_COLOR_BUF) {
         {
             PhaseMark m(c, st, 0, timed);
-            int k = 0;
-            e = launch_gather_phase(c->L_gather.k(), c->gk, call, st, 0, &k);
-            nl += k;
+            e = launch_eval_compact(c->L_gather.k(), c->gk, call, st);
+            nl += c->n_dev ? 1 : 0;
         }
         {
             PhaseMark m(c, st, 1, timed);
@@ -722,8 +721,38 @@ ees_status build_hybrid(const ees_desc *d, ees_ctx *c, const std::vector<int32_t
     return EES_OK;
 }
 
-// GATHER: compact contribution buffer + transposed per-target lists.
-ees_status build_gather(const ees_desc *d, ees_ctx *c, const std::vector<int32_t> &raw_slot)
+// Locality of the stamp targets in netlist order: a FET whose light
+// terminals (fanout <= kHeavyDeg, not rails) lie far apart in node id (> 32)
+// is copied into several TILE tiles and scatters GATHER's target-ordered
+// stores.  True when that happens more than once per two FETs (cfg3's random
+// netlist: ~2 per FET; the inverter, SRAM and hub configs: ~0).
+bool scattered_topology(const ees_desc *d, const ees_ctx *c, const std::vector<int64_t> &iptr)
+{
+    const int64_t N = c->n_dev;
+    const int32_t *TT[4] = {d->d, d->g, d->s, d->b};
+    const int32_t NN = std::max(1, c->n_nodes);
+    std::vector<uint8_t> heavy((size_t)NN, 0);
+    for (int32_t v = 0; v < c->n_nodes; v++) heavy[v] = (iptr[v + 1] - iptr[v]) > kHeavyDeg;
+    for (int32_t r : c->rails) heavy[r] = 1;
+    int64_t extra = 0;
+    for (int64_t i = 0; i < N; i++) {
+        int32_t lo = INT32_MAX;
+        for (int a = 0; a < 4; a++)
+            if (TT[a][i] >= 0 && !heavy[TT[a][i]]) lo = std::min(lo, TT[a][i]);
+        for (int a = 0; a < 4; a++) {
+            const int32_t t = TT[a][i];
+            bool dup = false;
+            for (int b2 = 0; b2 < a; b2++) dup |= TT[b2][i] == t;
+            if (t >= 0 && !heavy[t] && !dup && t - lo > 32) extra++;
+        }
+    }
+    return N && (double)extra / (double)N > 0.5;
+}
+
+// GATHER: per-target contributor lists; the target-ordered buffer (form 1) or
+// the compact buffer with transposed index lists (form 0).
+ees_status build_gather(const ees_desc *d, ees_ctx *c, const std::vector<int32_t> &raw_slot,
+                        const std::vector<int64_t> &iptr)
 {
     const int64_t N = c->n_dev, nnz = c->nnz;
     const int64_t NT = nnz + c->n;
@@ -761,22 +790,32 @@ ees_status build_gather(const ees_desc *d, ees_ctx *c, const std::vector<int32_t
     std::vector<int64_t> hptr((size_t)nh + 1, 0);
     for (int32_t h = 0; h < nh; h++) hptr[h + 1] = hptr[h] + tcnt[heavy_target[h]];
     std::vector<int32_t> tidx((size_t)tptr[NT]), hidx((size_t)hl);
+    // target-ordered positions (light lists, then heavy lists) for EES_GATHER
+    const int64_t heavy_base = tptr[NT];
+    std::vector<int32_t> tpos((size_t)(16 * N), -1);
     {
         std::vector<int32_t> fill(tptr.begin(), tptr.end() - 1);
         std::vector<int64_t> hfill(hptr.begin(), hptr.end() - 1);
         for (int64_t i = 0; i < N; i++) {     // device order -> lists sorted by device
             int32_t q = off[i];
-            auto put = [&](int64_t t) {
-                if (hpos[t] >= 0) hidx[hfill[hpos[t]]++] = q;
-                else tidx[fill[t]++] = q;
+            auto put = [&](int64_t t, int p) {
+                if (hpos[t] >= 0) {
+                    const int64_t hk = hfill[hpos[t]]++;
+                    hidx[hk] = q;
+                    tpos[(size_t)p * N + i] = (int32_t)(heavy_base + hk);
+                } else {
+                    const int32_t lk = fill[t]++;
+                    tidx[lk] = q;
+                    tpos[(size_t)p * N + i] = lk;
+                }
                 q++;
             };
             for (int p = 0; p < NPAIR; p++) {
                 const int32_t k = raw_slot[p * N + i];
-                if (k >= 0) put(k);
+                if (k >= 0) put(k, p);
             }
             for (int a = 0; a < 4; a++)
-                if (TT[a][i] >= 0) put(nnz + TT[a][i]);
+                if (TT[a][i] >= 0) put(nnz + TT[a][i], NPAIR + a);
         }
     }
     // heavy lists are cut into chunks of kChunk; chunks of one target are
@@ -797,12 +836,29 @@ ees_status build_gather(const ees_desc *d, ees_ctx *c, const std::vector<int32_t
     TRY(upload(c, const_cast<int32_t **>(&g.off), off.data(), N + 1));
     TRY(dalloc(c, &g.buf, (size_t)ncontrib));
     TRY(upload(c, const_cast<int32_t **>(&g.tptr), tptr.data(), NT + 1));
-    TRY(upload(c, const_cast<int32_t **>(&g.tidx), tidx.data(), tidx.size()));
+
     TRY(upload(c, const_cast<int32_t **>(&g.chunk_beg), chunk_beg.data(), chunk_beg.size()));
-    TRY(upload(c, const_cast<int32_t **>(&g.hidx), hidx.data(), hidx.size()));
+
     TRY(dalloc(c, &g.chunk_part, (size_t)nchunks));
     TRY(upload(c, const_cast<int32_t **>(&g.heavy_target), heavy_target.data(), heavy_target.size()));
     TRY(upload(c, const_cast<int32_t **>(&g.heavy_chunk), heavy_chunk.data(), heavy_chunk.size()));
+    g.heavy_base = heavy_base;
+    // form 1 (target-ordered stores, streamed reduction) unless the targets are
+    // scattered in netlist order (cfg3: its stores then cost 8x, form 0 keeps
+    // the compact buffer and gathers by index); measured in profiles/r01_f_tile_ab.md
+    g.form = scattered_topology(d, c, iptr) ? 0 : 1;
+    {
+        const char *f = std::getenv("EES_GATHER_FORM");     // experiments: force a form
+        if (f && (f[0] == '0' || f[0] == '1')) g.form = f[0] - '0';
+    }
+    c->st.gather_form = g.form;
+    if (g.form == 0) {
+        TRY(upload(c, const_cast<int32_t **>(&g.tidx), tidx.data(), tidx.size()));
+        TRY(upload(c, const_cast<int32_t **>(&g.hidx), hidx.data(), hidx.size()));
+    } else {
+        TRY(dalloc(c, &g.tbuf, (size_t)ncontrib));
+        TRY(upload(c, const_cast<int32_t **>(&g.tpos), tpos.data(), tpos.size()));
+    }
     c->st.n_heavy_targets = nh;
     return EES_OK;
 }
@@ -820,27 +876,9 @@ ees_status build_tile(const ees_desc *d, ees_ctx *c, const std::vector<int32_t> 
     // TILE form (ees_internal.h): items in HBM arrays (form 1, 5 CTAs/SM)
     // unless FETs are copied into several tiles, where the extra per-copy
     // loads cost more than the occupancy gains (form 0; measured: cfg3 1.6x
-    // slower in form 1, cfg4 10% faster).  A FET is copied once more for
-    // every light terminal far (> 32 ids) from its others' rows.
-    int form = 1;
+    // slower in form 1, cfg4 10% faster).
+    int form = scattered_topology(d, c, iptr) ? 0 : 1;
     {
-        const int32_t NN = std::max(1, c->n_nodes);
-        std::vector<uint8_t> heavy((size_t)NN, 0);
-        for (int32_t v = 0; v < c->n_nodes; v++) heavy[v] = (iptr[v + 1] - iptr[v]) > kHeavyDeg;
-        for (int32_t r : c->rails) heavy[r] = 1;
-        int64_t extra = 0;
-        for (int64_t i = 0; i < N; i++) {
-            int32_t lo = INT32_MAX;
-            for (int a = 0; a < 4; a++)
-                if (TT[a][i] >= 0 && !heavy[TT[a][i]]) lo = std::min(lo, TT[a][i]);
-            for (int a = 0; a < 4; a++) {
-                const int32_t t = TT[a][i];
-                bool dup = false;
-                for (int b2 = 0; b2 < a; b2++) dup |= TT[b2][i] == t;
-                if (t >= 0 && !heavy[t] && !dup && t - lo > 32) extra++;
-            }
-        }
-        if (N && (double)extra / (double)N > 0.5) form = 0;
         const char *f = std::getenv("EES_TILE_FORM");       // experiments: force a form
         if (f && (f[0] == '0' || f[0] == '1')) form = f[0] - '0';
     }
@@ -1040,7 +1078,7 @@ ees_status setup_impl(const ees_desc *d, ees_ctx *c)
     }
     TRY(build_layouts(d, c, raw_slot, rail_ord));
     TRY(build_hybrid(d, c, raw_slot, excluded));      // COLOR (hybrid rule) and COLOR_BUF
-    TRY(build_gather(d, c, raw_slot));
+    TRY(build_gather(d, c, raw_slot, iptr));
     TRY(build_tile(d, c, raw_slot, iptr, idev));
     int sms = 148;
     int dev = 0;

@@ -78,6 +78,13 @@ struct GatherK {
     int32_t n_heavy;
     const int32_t *heavy_target;   // [n_heavy]
     const int32_t *heavy_chunk;    // [n_heavy+1]
+    // form 1 (EES_GATHER, chosen at setup): each contribution is stored at its
+    // place in its target's list, so the reduction streams the buffer; form 0:
+    // compact per-device buffer (buf) gathered through tidx / hidx
+    int32_t form;
+    double *tbuf;                  // [n_contrib]: light lists (tptr), then heavy lists (chunk_beg + heavy_base)
+    const int32_t *tpos;           // [16][N] position of each live contribution in tbuf, -1 none
+    int64_t heavy_base;            // first heavy entry in tbuf
 };
 
 // TILE layout (ees_tile.cpp builds it; k_tile consumes it).  Rows are cut
@@ -230,6 +237,7 @@ cudaError_t launch_color_coop(const DevK &dv, const CallK &call, const int64_t *
                               double *partials, int grid, cudaStream_t st);
 cudaError_t launch_rail_finalize(const CallK &call, const double *partials, int64_t n_blocks,
                                  cudaStream_t st);
+cudaError_t launch_eval_compact(const DevK &dv, const GatherK &gk, const CallK &call, cudaStream_t st);
 cudaError_t launch_gather(const DevK &dv, const GatherK &gk, const CallK &call, cudaStream_t st,
                           int *n_launches);
 // one GATHER phase: 0 evaluate, 1 reduce, 2 heavy finalise (for phase timing)

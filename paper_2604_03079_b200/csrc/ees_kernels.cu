@@ -383,6 +383,78 @@ __global__ void __launch_bounds__(kBlock) k_gather_reduce(GatherK gk, CallK P, i
     }
 }
 
+// ---------------------------------------------------------------------------
+// GATHER, target-ordered (form 1): the evaluation stores each contribution
+// straight at its place in its target's list (scattered stores, fire-and-
+// forget), so the reduction streams the buffer: a thread per target sums its
+// contiguous list in list order (neighbouring threads read neighbouring lists,
+// so a warp's loads share cache lines; deterministic).  Heavy lists
+// (> kHeavyLen) are chunk-reduced from their contiguous ranges.  (A warp-
+// shuffle segmented scan over 32 targets measured 1.4x slower: the lists are
+// short, profiles/r01_f_tile_ab.md.)
+// ---------------------------------------------------------------------------
+template <bool kRep>
+__global__ void __launch_bounds__(kBlock) k_gather_eval_t(DevK dv, GatherK gk, CallK P)
+{
+    __shared__ CardK s_cards[EES_MAX_MODELS];
+    __shared__ double s_railx[EES_MAX_RAILS];
+    load_call_smem(P, s_cards, s_railx);
+    __syncthreads();
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= dv.N) return;
+    int32_t pos[16];
+#pragma unroll
+    for (int p = 0; p < 16; p++) pos[p] = __ldg(gk.tpos + (int64_t)p * dv.N + i);
+    int4 T;
+    Stamp st;
+    load_eval<kRep>(dv, P, s_cards, s_railx, i, T, st);
+#pragma unroll
+    for (int p = 0; p < NPAIR; p++)
+        if (pos[p] >= 0) gk.tbuf[pos[p]] = st.y[p];
+#pragma unroll
+    for (int a = 0; a < 4; a++)
+        if (pos[NPAIR + a] >= 0) gk.tbuf[pos[NPAIR + a]] = st.j[a];
+}
+
+__global__ void __launch_bounds__(kBlock) k_gather_reduce_t(GatherK gk, CallK P, int64_t n_light_blocks)
+{
+    if (blockIdx.x < n_light_blocks) {
+        // thread per target over its contiguous list (neighbouring threads
+        // read neighbouring lists: the warp's loads share cache lines)
+        const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+        if (t >= gk.n_targets) return;
+        const int32_t b0 = gk.tptr[t], b1 = gk.tptr[t + 1];
+        if (b0 == b1) return;
+        double s = 0.0;
+        int32_t k = b0;
+        for (; k + 4 <= b1; k += 4) {
+            const double a = gk.tbuf[k], b = gk.tbuf[k + 1], c = gk.tbuf[k + 2], d = gk.tbuf[k + 3];
+            s += a;
+            s += b;
+            s += c;
+            s += d;
+        }
+        for (; k < b1; k++) s += gk.tbuf[k];
+        if (t < gk.nnz) P.A[t] += s;
+        else P.b[t - gk.nnz] += s;
+        return;
+    }
+    // heavy chunk: fixed-shape block reduction over a contiguous range
+    __shared__ double s_w[kBlock / 32];
+    const int64_t c = blockIdx.x - n_light_blocks;
+    const int64_t b0 = gk.heavy_base + gk.chunk_beg[c], b1 = gk.heavy_base + gk.chunk_beg[c + 1];
+    double v = 0.0;
+    for (int64_t k = b0 + threadIdx.x; k < b1; k += blockDim.x) v += gk.tbuf[k];
+    v = warp_sum(v);
+    if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); w++) t += s_w[w];
+        gk.chunk_part[c] = t;
+    }
+}
+
 __global__ void k_gather_heavy(GatherK gk, CallK P)
 {
     const int h = blockIdx.x * blockDim.x + threadIdx.x;
@@ -891,17 +963,33 @@ cudaError_t launch_gather_phase(const DevK &dv, const GatherK &gk, const CallK &
     if (dv.N == 0) return cudaSuccess;
     if (phase == 0) {
         const int64_t grid = (dv.N + kBlock - 1) / kBlock;
-        if (call.work > 1) k_gather_eval<true><<<(unsigned)grid, kBlock, 0, st>>>(dv, gk, call);
-        else k_gather_eval<false><<<(unsigned)grid, kBlock, 0, st>>>(dv, gk, call);
+        if (gk.form == 1) {
+            if (call.work > 1) k_gather_eval_t<true><<<(unsigned)grid, kBlock, 0, st>>>(dv, gk, call);
+            else k_gather_eval_t<false><<<(unsigned)grid, kBlock, 0, st>>>(dv, gk, call);
+        } else {
+            if (call.work > 1) k_gather_eval<true><<<(unsigned)grid, kBlock, 0, st>>>(dv, gk, call);
+            else k_gather_eval<false><<<(unsigned)grid, kBlock, 0, st>>>(dv, gk, call);
+        }
         *n_launches = 1;
     } else if (phase == 1) {
         const int64_t light = (gk.n_targets + kBlock - 1) / kBlock;
-        k_gather_reduce<<<(unsigned)(light + gk.n_chunks), kBlock, 0, st>>>(gk, call, light);
+        if (gk.form == 1) k_gather_reduce_t<<<(unsigned)(light + gk.n_chunks), kBlock, 0, st>>>(gk, call, light);
+        else k_gather_reduce<<<(unsigned)(light + gk.n_chunks), kBlock, 0, st>>>(gk, call, light);
         *n_launches = 1;
     } else if (gk.n_heavy) {
         k_gather_heavy<<<(gk.n_heavy + 127) / 128, 128, 0, st>>>(gk, call);
         *n_launches = 1;
     }
+    return cudaPeekAtLastError();
+}
+
+// COLOR_BUF's compute phase: the compact per-device ContributionBuffer
+cudaError_t launch_eval_compact(const DevK &dv, const GatherK &gk, const CallK &call, cudaStream_t st)
+{
+    if (dv.N == 0) return cudaSuccess;
+    const int64_t grid = (dv.N + kBlock - 1) / kBlock;
+    if (call.work > 1) k_gather_eval<true><<<(unsigned)grid, kBlock, 0, st>>>(dv, gk, call);
+    else k_gather_eval<false><<<(unsigned)grid, kBlock, 0, st>>>(dv, gk, call);
     return cudaPeekAtLastError();
 }
 
