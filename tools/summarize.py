@@ -15,8 +15,11 @@ import sys
 
 NCU = "/usr/local/cuda/bin/ncu"
 RAW_KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
-            "dram__throughput.avg.pct_of_peak_sustained_elapsed",
-            "lts__t_sectors_op_red.sum", "lts__t_requests_op_red.sum",
+            "dram__bytes.sum.per_second",
+            "dram__cycles_active.avg.pct_of_peak_sustained_elapsed",
+            "l1tex__t_requests_pipe_lsu_mem_global_op_red.sum",
+            "lts__t_requests_srcunit_tex_op_red.sum",
+            "lts__d_atomic_input_cycles_active.avg.pct_of_peak_sustained_elapsed",
             "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
             "smsp__sass_thread_inst_executed_op_dfma_pred_on.sum",
             "smsp__sass_thread_inst_executed_op_dadd_pred_on.sum",
