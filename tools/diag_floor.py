@@ -33,6 +33,17 @@ def main():
     one = torch.zeros(1, device=dev)
     print("trivial torch kernel, flushed: %.2f us" % timed(lambda: one.add_(1.0), fl))
     print("trivial torch kernel, warm:    %.2f us" % timed(lambda: one.add_(1.0), lambda k: None))
+    # streaming calibration: what a plain torch kernel achieves on cfg1's
+    # compulsory bytes (20.2 MB) after the same flush
+    for mb in (4, 20.2, 80, 400):
+        src = torch.ones(int(mb * 1e6 / 8), dtype=torch.float64, device=dev)
+        out = torch.zeros(1, dtype=torch.float64, device=dev)
+        t = timed(lambda: torch.sum(src, 0, out=out[0]), fl)
+        print("stream read %6.1f MB (torch sum), flushed: %8.2f us = %7.1f GB/s" % (mb, t, mb * 1e3 / t))
+        dst = torch.empty_like(src)
+        t = timed(lambda: dst.copy_(src), fl)
+        print("stream copy %6.1f MB (read+write), flushed: %8.2f us = %7.1f GB/s" % (mb, t, 2 * mb * 1e3 / t))
+        del src, dst
     for name, nl in (("1 FET", netgen.custom("one", 3, [(0, 1, 2, -1)], 0, netgen.bench_models())),
                      ("cfg0", netgen.config(0)), ("cfg1", netgen.config(1))):
         ctx = Context.from_netlist(nl)
