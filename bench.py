@@ -257,6 +257,34 @@ def time_calls(ctx, nl, x, A, b, stream, steps, warmup, flush):
     return sorted(e0.elapsed_time(e1) for e0, e1 in evs)
 
 
+def stream_reference(nbytes, dev, stream, pre, steps, achieved_gbs):
+    """Size calibration of the HBM roofline: a plain streaming read (torch.sum
+    over an FP64 tensor of the call's algorithmic bytes) timed the same way as
+    the call (same flush before each step, CUDA events on the same stream).
+    At small byte counts the flushed-L2 ramp, not the copy peak, bounds any
+    kernel (profiles/r01_l_ab.md); `frac` is the call's achieved bandwidth
+    over this one's."""
+    import torch
+    src = torch.ones(max(1, int(nbytes) // 8), dtype=torch.float64, device=dev)
+    out = torch.zeros(1, dtype=torch.float64, device=dev)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    with torch.cuda.stream(stream):
+        for k in range(3):
+            pre(k)
+            torch.sum(src, 0, out=out[0])
+        for k in range(steps):
+            pre(k)
+            evs[k][0].record(stream)
+            torch.sum(src, 0, out=out[0])
+            evs[k][1].record(stream)
+    torch.cuda.synchronize()
+    ms = sorted(a.elapsed_time(b) for a, b in evs)[steps // 2]
+    gbs = nbytes / (ms * 1e-3) / 1e9
+    del src
+    return {"kernel": "torch.sum over the algorithmic bytes (read-only stream), flushed",
+            "bytes": int(nbytes), "ms": ms, "gbs": gbs, "frac": achieved_gbs / gbs}
+
+
 def run_sweep(args):
     """B5: gen_synth N FETs as N/C cliques, C = 1..4096; every
     variant timed per C -> the stamping-variant crossover against the colour
@@ -419,6 +447,7 @@ def main():
             "kernel": " + ".join(phases), "kernel_ms": kern_ms, "phase_ms": phase_avg,
             "algorithmic_bytes_per_launch": alg, "peak_source": peak_src,
             "per_unit": "48 B/FET + 8 B/unknown (x) + 16 B/nonzero (A RMW) + 16 B/unknown (b RMW)"}
+    roof["stream_ref"] = stream_reference(alg, dev, stream, step_pre, min(args.steps, 30), achieved)
     if args.work > 1:
         # S:229 work multiplier: evaluation arithmetic x k puts the path on the
         # FP64 pipe; peak = this device's FMA throughput measured now
