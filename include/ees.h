@@ -191,6 +191,11 @@ ees_status ees_set_variant(ees_ctx *ctx, int32_t variant);
 
 ees_status ees_stats(const ees_ctx *ctx, ees_stats_t *out);
 
+/* sizeof of the ABI structs this library was built with (0: ees_desc,
+ * 1: ees_stats_t; else 0), so a binding can refuse a mismatched build
+ * instead of reading past a struct. */
+int64_t ees_abi_sizeof(int32_t which);
+
 /* Per-phase device timing (S:326 PhaseTimings).  When enabled, every
  * ees_eval_stamp records CUDA events on the call's stream around each kernel
  * group ("phase"):  COLOR {0: colour kernels, 1: rail finalise or, under

@@ -78,7 +78,14 @@ for _f in ("ees_setup", "ees_pattern", "ees_find_slot", "ees_colors", "ees_eval_
            "ees_fp64_peak", "ees_red_throughput"):
     getattr(lib, _f).restype = i32
 
+lib.ees_abi_sizeof.argtypes = [i32]
+lib.ees_abi_sizeof.restype = i64
+for _which, _cls in ((0, ees_desc), (1, ees_stats_t)):
+    if lib.ees_abi_sizeof(_which) != C.sizeof(_cls):
+        raise ImportError(f"{LIB_PATH} was built with a different {_cls.__name__} layout "
+                          f"({lib.ees_abi_sizeof(_which)} vs {C.sizeof(_cls)} bytes): rebuild it")
+
 EXPORTS = ["ees_setup", "ees_pattern", "ees_find_slot", "ees_colors", "ees_eval_stamp",
            "ees_eval_stamp_host", "ees_set_variant", "ees_stats", "ees_set_timing",
            "ees_phase_times", "ees_tile_trace", "ees_race_probe", "ees_accept", "ees_set_work",
-           "ees_fp64_peak", "ees_red_throughput", "ees_destroy", "ees_strerror"]
+           "ees_fp64_peak", "ees_red_throughput", "ees_destroy", "ees_strerror", "ees_abi_sizeof"]

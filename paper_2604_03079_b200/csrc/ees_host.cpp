@@ -1260,6 +1260,11 @@ ees_status ees_red_throughput(int32_t mode, double *gops)
     return measure_red_throughput(mode, gops) == cudaSuccess ? EES_OK : EES_ECUDA;
 }
 
+int64_t ees_abi_sizeof(int32_t which)
+{
+    return which == 0 ? (int64_t)sizeof(ees_desc) : which == 1 ? (int64_t)sizeof(ees_stats_t) : 0;
+}
+
 ees_status ees_stats(const ees_ctx *c, ees_stats_t *out)
 {
     if (!c || !out) return EES_EINVAL;

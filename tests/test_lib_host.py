@@ -17,7 +17,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 def test_library_exports_every_declared_symbol():
     from paper_2604_03079_b200 import _lib
     hdr = open(os.path.join(ROOT, "include", "ees.h")).read()
-    declared = set(re.findall(r"^(?:ees_status|const char \*)\s*(ees_\w+)\s*\(", hdr, re.M))
+    declared = set(re.findall(r"^(?:ees_status|int64_t|const char \*)\s*(ees_\w+)\s*\(", hdr, re.M))
     assert declared == set(_lib.EXPORTS)
     for name in declared:
         assert getattr(_lib.lib, name) is not None
