@@ -1,0 +1,61 @@
+"""bench.py on the GPU (task contract): the default-shaped JSON line on a small
+config carries every key the driver and the judge read (roofline with its
+size calibration, e2e through host buffers, clocks, launch count), and the
+B5 sweep mode prints one record per colour count."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _bench(args):
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), *args], capture_output=True,
+                       text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    return [json.loads(l) for l in r.stdout.splitlines() if l.startswith("{")]
+
+
+def test_bench_line_keys(cuda_ok):
+    (d,) = _bench(["--config", "0", "--steps", "5", "--warmup", "3", "--no-cpu-baseline"])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+              "scaling", "vs_baseline", "dtype", "data", "config", "roofline", "e2e", "gpu_launches", "clocks"):
+        assert k in d, k
+    assert d["n_gpus"] == 1 and d["steps"] == 5 and d["warmup"] == 3 and d["dtype"] == "f64"
+    assert d["value"] > 0 and d["value"] == pytest.approx(2000 / (d["ms_per_step"] * 1e-3), rel=1e-9)
+    r = d["roofline"]
+    assert r["bound"] == "hbm" and r["unit"] == "GB/s" and r["peak"] > 0
+    assert r["frac"] == pytest.approx(r["achieved"] / r["peak"], rel=1e-9)
+    assert r["algorithmic_bytes_per_launch"] == 48 * 2000 + 24 * d["config"]["n"] + 16 * d["config"]["nnz"]
+    s = r["stream_ref"]
+    assert s["bytes"] == r["algorithmic_bytes_per_launch"] and s["ms"] > 0
+    assert s["frac"] == pytest.approx(r["achieved"] / s["gbs"], rel=1e-9)
+    e = d["e2e"]
+    assert e["value"] > 0 and e["h2d_bytes_per_step"] == 8 * d["config"]["n"]
+    assert e["d2h_bytes_per_step"] == 8 * (d["config"]["n"] + d["config"]["nnz"])
+    assert d["gpu_launches"] >= 5
+    assert d["clocks"]["sm_max_mhz"] > 0 and "reasons" in d["clocks"]
+    assert d["config"]["workload"].startswith("cfg0")
+
+
+def test_bench_work_mode_fp64_roofline(cuda_ok):
+    (d,) = _bench(["--config", "0", "--steps", "3", "--warmup", "3", "--no-cpu-baseline", "--no-e2e",
+                   "--variant", "tile", "--work", "8"])
+    r = d["roofline"]
+    assert d["config"]["variant"] == "tile" and d["config"]["work"] == 8
+    assert r["bound"] == "fp64" and r["unit"] == "TFLOP/s" and 0 < r["frac"] < 1.5
+
+
+def test_bench_sweep_records(cuda_ok, tmp_path):
+    out = tmp_path / "sweep.jsonl"
+    recs = _bench(["--sweep", "--sweep-n", "20000", "--sweep-c", "1,16", "--steps", "3",
+                   "--sweep-out", str(out)])
+    assert [r["C"] for r in recs] == [1, 16]
+    for r in recs:
+        assert set(r["ms"]) == {"color", "atomic", "gather", "tile", "color_buf", "color_hybrid"}
+        assert all(v > 0 for v in r["ms"].values())
+    assert len(out.read_text().splitlines()) == 2
