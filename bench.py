@@ -200,11 +200,13 @@ def run_reference(args):
     el = time.perf_counter() - t0
     bl.close()
     value = nl.n_dev * args.steps / el
-    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 0,
+    # n_gpus: the launch's N (the oracle itself runs on rank 0's host cores only)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": {"workload": netgen.CONFIG_NAMES[args.config], "n_dev": nl.n_dev},
+            "config": {"workload": netgen.CONFIG_NAMES[args.config], "n_dev": nl.n_dev,
+                       "device": "host CPU (the oracle; no GPU work)"},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
                              "sample": f"{args.steps} full ColorFused calls of {nl.name}",
                              "cpu_model": cpu_model()},

@@ -65,14 +65,15 @@ def main(src, dst):
     os.makedirs(os.path.dirname(dst) or ".", exist_ok=True)
     lines = bench_lines(src)
     md = ["# bench + ncu summary", "", f"source: `{src}`", ""]
-    md.append("| file | config | variant | FET/s | ms/step | kernel ms | roofline frac | e2e FET/s |")
-    md.append("|---|---|---|---|---|---|---|---|")
+    md.append("| file | config | variant | FET/s | ms/step | kernel ms | roofline frac | frac of same-size stream | e2e FET/s |")
+    md.append("|---|---|---|---|---|---|---|---|---|")
     for j in lines:
         r = j.get("roofline", {})
         e = j.get("e2e") or {}
         md.append(f"| {j['_file']} | {j['config'].get('config_index')} | {j['config'].get('variant')} | "
                   f"{j['value']:.3e} | {j['ms_per_step']:.4f} | {r.get('kernel_ms', 0):.4f} | "
-                  f"{r.get('frac', 0):.3f} | {e.get('value', 0):.3e} |")
+                  f"{r.get('frac', 0):.3f} | {(r.get('stream_ref') or {}).get('frac', float('nan')):.3f} | "
+                  f"{e.get('value', 0):.3e} |")
     md.append("")
     reps = sorted(glob.glob(os.path.join(src, "*.ncu-rep")))
     ncu = {}
