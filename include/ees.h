@@ -25,7 +25,10 @@
  *    1e-12 * sum|elementary contributions| (BASELINE.json north_star).
  *
  * Thread-safety: different contexts are independent.  One context must not
- * be used by two calls at once (it owns scratch buffers).
+ * be used by two calls at once (it owns scratch buffers), and that includes
+ * the device side: calls of one context enqueued on different streams must be
+ * ordered by the caller (events), or their kernels may overlap and share the
+ * context's scratch (TILE side parts and ticket, GATHER buffers).
  */
 #ifndef EES_H
 #define EES_H
