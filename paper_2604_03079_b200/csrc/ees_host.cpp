@@ -37,7 +37,8 @@ struct Layout {
     double *v0 = nullptr;
     uint8_t *model = nullptr;
     int32_t *slot = nullptr;
-    DevK k() const { return DevK{N, term, beta, v0, model, slot}; }
+    int64_t cls_a = 0, cls_b = 0;         // ATOMIC order only (DevK)
+    DevK k() const { return DevK{N, term, beta, v0, model, slot, cls_a, cls_b}; }
 };
 
 }  // namespace
@@ -47,6 +48,7 @@ struct ees_ctx {
     int64_t n_dev = 0, nnz = 0;
     std::vector<int32_t> row_ptr, col_idx;
     std::vector<int32_t> color;
+    std::vector<int32_t> atomic_pos;      // netlist index -> position in the ATOMIC order
     int32_t n_colors = 0;
     std::vector<int64_t> color_ptr;
     std::vector<ees_model> models;
@@ -530,17 +532,57 @@ ees_status build_layouts(const ees_desc *d, ees_ctx *c, const std::vector<int32_
             slot_rail[p * N + i] = (k >= 0 && c->n_rail_a && is_rail_slot[k]) ? slotcode(k) : k;
         }
     }
-    Layout &La = c->L_atomic;
-    La.N = N;
-    TRY(upload(c, &La.term, term_rail.data(), N));
-    TRY(upload(c, &La.beta, beta.data(), N));
-    TRY(upload(c, &La.v0, v0.data(), 3 * N));
-    TRY(upload(c, &La.model, model.data(), N));
-    TRY(upload(c, &La.slot, slot_rail.data(), NPAIR * N));
-    Layout &Lg = c->L_gather;
-    Lg = La;
-    Lg.slot = nullptr;
+    // ATOMIC order: devices grouped by which slot codes are dead by structure
+    // -- A: source and bulk grounded (only DD DG GD GG can be live), B: bulk
+    // pairs dead (bulk grounded, or tied to the source and merged), C: the rest
+    // -- so k_atomic skips the dead codes' loads (and their DRAM sectors) from
+    // the device index alone (DevK::cls_a / cls_b), without a prior load.
+    {
+        std::vector<int32_t> aperm((size_t)N);
+        int64_t na = 0, nb = 0;
+        auto cls = [&](int64_t i) {
+            const int4 T = term_rail[i];
+            if (T.z == -1 && T.w == -1) return 0;
+            return (T.w == -1 || T.z == T.w) ? 1 : 2;
+        };
+        for (int64_t i = 0; i < N; i++) {
+            const int k = cls(i);
+            na += k == 0;
+            nb += k == 1;
+        }
+        int64_t fill[3] = {0, na, na + nb};
+        for (int64_t i = 0; i < N; i++) aperm[fill[cls(i)]++] = (int32_t)i;
+        c->atomic_pos.assign((size_t)N, 0);
+        std::vector<int4> term_a((size_t)N);
+        std::vector<double> beta_a((size_t)N), v0_a((size_t)(3 * N));
+        std::vector<uint8_t> model_a((size_t)N);
+        std::vector<int32_t> slot_a((size_t)(NPAIR * N));
+#pragma omp parallel for schedule(static)
+        for (int64_t q = 0; q < N; q++) {
+            const int64_t i = aperm[q];
+            c->atomic_pos[i] = (int32_t)q;
+            term_a[q] = term_rail[i];
+            beta_a[q] = beta[i];
+            for (int t = 0; t < 3; t++) v0_a[t * N + q] = v0[t * N + i];
+            model_a[q] = model[i];
+            for (int p = 0; p < NPAIR; p++) slot_a[p * N + q] = slot_rail[p * N + i];
+        }
+        Layout &La = c->L_atomic;
+        La.N = N;
+        La.cls_a = na;
+        La.cls_b = na + nb;
+        TRY(upload(c, &La.term, term_a.data(), N));
+        TRY(upload(c, &La.beta, beta_a.data(), N));
+        TRY(upload(c, &La.v0, v0_a.data(), 3 * N));
+        TRY(upload(c, &La.model, model_a.data(), N));
+        TRY(upload(c, &La.slot, slot_a.data(), NPAIR * N));
+    }
+    Layout &Lg = c->L_gather;      // netlist order (GATHER's device offsets)
+    Lg.N = N;
     TRY(upload(c, &Lg.term, term_plain.data(), N));
+    TRY(upload(c, &Lg.beta, beta.data(), N));
+    TRY(upload(c, &Lg.v0, v0.data(), 3 * N));
+    TRY(upload(c, &Lg.model, model.data(), N));
     // colour-major copy
     {
         std::vector<int32_t> perm((size_t)N);
@@ -1231,8 +1273,8 @@ ees_status ees_accept(ees_ctx *c, const double *x, ees_stream stream)
     if (!x) return EES_EINVAL;
     cudaStream_t st = (cudaStream_t)stream;
     const CallK call = make_call(c, x, 1.0, nullptr, nullptr);
-    // ATOMIC and GATHER share one netlist-order copy of the state
     cudaError_t e = launch_accept_soa(c->L_gather.term, c->n_dev, call, c->L_gather.v0, st);
+    if (e == cudaSuccess) e = launch_accept_soa(c->L_atomic.term, c->n_dev, call, c->L_atomic.v0, st);
     if (e == cudaSuccess) e = launch_accept_soa(c->L_color.term, c->n_dev, call, c->L_color.v0, st);
     if (e == cudaSuccess && c->hybrid)
         e = launch_accept_soa(c->L_colorh.term, c->n_dev, call, c->L_colorh.v0, st);
@@ -1346,6 +1388,8 @@ ees_status ees_race_probe(ees_ctx *c, const int32_t *color, int64_t *n_conflicts
         std::vector<int64_t> fill(ptr.begin(), ptr.end() - 1);
         for (int64_t i = 0; i < N; i++) perm[fill[col[i]]++] = (int32_t)i;
     }
+    if (!c->hybrid)                 // the probe reads the ATOMIC layout: its positions
+        for (int64_t q = 0; q < N; q++) perm[q] = c->atomic_pos[perm[q]];
     int32_t *dperm = nullptr, *cnt_a = nullptr, *cnt_b = nullptr;
     unsigned long long *dout = nullptr;
     cudaError_t e = cudaMalloc(&dperm, sizeof(int32_t) * perm.size());

@@ -60,6 +60,10 @@ struct DevK {
     const double *v0;      // [3][N]: v_gs, v_gd, v_db at the last accepted step
     const uint8_t *model;
     const int32_t *slot;   // [NPAIR][N] (null in the GATHER layout)
+    // ATOMIC order: devices [0, cls_a) have source and bulk grounded (codes
+    // other than DD DG GD GG are -1), [cls_a, cls_b) have dead bulk pairs
+    // (DB BD BB -1 or merged away); 0, 0 in the other layouts
+    int64_t cls_a, cls_b;
 };
 
 // GATHER layout extras

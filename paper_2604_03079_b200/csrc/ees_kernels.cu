@@ -214,8 +214,14 @@ __global__ void __launch_bounds__(kBlock, 4) k_atomic(DevK dv, CallK P)
             const double a1 = __ldg(dv.v0 + dv.N + i);
             const double a2 = __ldg(dv.v0 + 2 * dv.N + i);
             const int m = __ldg(dv.model + i);
+            // codes dead by the device's class are not loaded (DevK::cls_a / cls_b)
+            const bool dead_s = i < dv.cls_a, dead_b = i < dv.cls_b;
 #pragma unroll
-            for (int p = 0; p < NPAIR; p++) slot[p] = __ldg(dv.slot + (int64_t)p * dv.N + i);
+            for (int p = 0; p < NPAIR; p++) {
+                const bool sp = p == DS || p == GS || p == SD || p == SG || p == SS;
+                const bool bp = p == DB || p == BD || p == BB;
+                slot[p] = (dead_b && bp) || (dead_s && sp) ? -1 : __ldg(dv.slot + (int64_t)p * dv.N + i);
+            }
             const double VD = volt(T.x, P.x, s_railx);
             const double VG = volt(T.y, P.x, s_railx);
             const double VS = volt(T.z, P.x, s_railx);
