@@ -43,12 +43,25 @@ bool build_tile_host(int form, int64_t N, int32_t n_nodes, int32_t n, int64_t nn
 {
     static_assert(kOwnMax > 64, "tile budget too small");
     const int64_t kStageMax = stage_max(form), kItemBlobBytes = item_blob_bytes(form);
+    // a device's 12 slots and 4 terminals in one 64-byte record: the builder
+    // visits devices in row order (random in netlist order on scattered
+    // topologies), so one cache line per visit instead of sixteen
+    struct DevRec {
+        int32_t s[NPAIR];
+        int32_t t[4];
+    };
+    std::vector<DevRec> rec((size_t)std::max<int64_t>(1, N));
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < N; i++) {
+        for (int p = 0; p < NPAIR; p++) rec[i].s[p] = raw_slot[p * N + i];
+        for (int a = 0; a < 4; a++) rec[i].t[a] = TT[a][i];
+    }
     // source tied to bulk: the kernel merges DB/BD/BB/J[B] into DS/SD/SS/J[S]
-    auto merged = [&](int64_t i) { return TT[2][i] == TT[3][i] && TT[2][i] != -1; };
+    auto merged = [&](int64_t i) { return rec[i].t[2] == rec[i].t[3] && rec[i].t[2] != -1; };
     // is contribution p (12 pairs, then 4 b rows) of FET i in a list?
     auto listed_c = [&](int64_t i, int p) -> bool {
-        if (p < NPAIR) return raw_slot[p * N + i] >= 0 && !(merged(i) && (p == DB || p == BD || p == BB));
-        return TT[p - NPAIR][i] >= 0 && !(p == NPAIR + 3 && merged(i));
+        if (p < NPAIR) return rec[i].s[p] >= 0 && !(merged(i) && (p == DB || p == BD || p == BB));
+        return rec[i].t[p - NPAIR] >= 0 && !(p == NPAIR + 3 && merged(i));
     };
     const int32_t NN = std::max(1, n_nodes);
     // A light row whose FETs alone overflow a tile (pathological: many heavy x
@@ -66,14 +79,14 @@ bool build_tile_host(int form, int64_t N, int32_t n_nodes, int32_t n, int64_t nn
     auto hh_new = [&](int64_t i, int32_t tile) {
         int32_t k = 0;
         for (int p = 0; p < NPAIR; p++) {
-            const int32_t s2 = raw_slot[p * N + i];
-            if (s2 >= 0 && heavy[TT[pair_row(p)][i]] && heavy[TT[pair_col(p)][i]] && hh_seen[s2] != tile) {
+            const int32_t s2 = rec[i].s[p];
+            if (s2 >= 0 && heavy[rec[i].t[pair_row(p)]] && heavy[rec[i].t[pair_col(p)]] && hh_seen[s2] != tile) {
                 hh_seen[s2] = tile;
                 k++;
             }
         }
         for (int a = 0; a < 4; a++) {
-            const int32_t r = TT[a][i];
+            const int32_t r = rec[i].t[a];
             if (r >= 0 && heavy[r] && hh_seen[nnz + r] != tile) {
                 hh_seen[nnz + r] = tile;
                 k++;
@@ -90,7 +103,7 @@ bool build_tile_host(int form, int64_t N, int32_t n_nodes, int32_t n, int64_t nn
     std::vector<uint8_t> has_c((size_t)(nnz + n), 0);
     for (int64_t i = 0; i < N; i++)
         for (int p = 0; p < NPAIR + 4; p++)
-            if (listed_c(i, p)) has_c[p < NPAIR ? raw_slot[p * N + i] : nnz + TT[p - NPAIR][i]] = 1;
+            if (listed_c(i, p)) has_c[p < NPAIR ? rec[i].s[p] : nnz + rec[i].t[p - NPAIR]] = 1;
     auto empty_in_row = [&](int32_t r) {
         int64_t e = has_c[nnz + r] ? 0 : 1;
         for (int32_t k = row_ptr[r]; k < row_ptr[r + 1]; k++) e += !has_c[k];
@@ -100,9 +113,9 @@ bool build_tile_host(int form, int64_t N, int32_t n_nodes, int32_t n, int64_t nn
     auto hh_count = [&](int64_t i) {
         int32_t k = 0;
         for (int p = 0; p < NPAIR; p++)
-            if (raw_slot[p * N + i] >= 0 && heavy[TT[pair_row(p)][i]] && heavy[TT[pair_col(p)][i]]) k++;
+            if (rec[i].s[p] >= 0 && heavy[rec[i].t[pair_row(p)]] && heavy[rec[i].t[pair_col(p)]]) k++;
         for (int a = 0; a < 4; a++)
-            if (TT[a][i] >= 0 && heavy[TT[a][i]]) k++;
+            if (rec[i].t[a] >= 0 && heavy[rec[i].t[a]]) k++;
         return k;
     };
 
@@ -238,29 +251,44 @@ bool build_tile_host(int form, int64_t N, int32_t n_nodes, int32_t n, int64_t nn
     };
     for (int64_t i = 0; i < N; i++) {
         for (int p = 0; p < NPAIR; p++) {
-            const int32_t k = raw_slot[p * N + i];
-            if (k >= 0 && heavy[TT[pair_row(p)][i]] && heavy[TT[pair_col(p)][i]]) note_hh(k, home[i]);
+            const int32_t k = rec[i].s[p];
+            if (k >= 0 && heavy[rec[i].t[pair_row(p)]] && heavy[rec[i].t[pair_col(p)]]) note_hh(k, home[i]);
         }
         for (int a = 0; a < 4; a++) {
-            const int32_t r = TT[a][i];
+            const int32_t r = rec[i].t[a];
             if (r >= 0 && heavy[r]) note_hh(nnz + r, home[i]);
         }
     }
     for (int64_t g = 0; g < NT; g++)
         if (hh_owner[g] >= 0) hh_of_tile[hh_owner[g]].push_back((int32_t)g);
 
-    // ---- per tile: blob = header | items | owned program | side entries
-    std::vector<int32_t> sid_of((size_t)NT, -1);
-    std::vector<std::pair<int32_t, uint16_t>> con, side;
+    // ---- per tile: blob = header | items | owned program | side entries.
+    // Tiles are emitted in parallel into their own buffers (side entries carry
+    // their global target for now), then concatenated in tile order, where
+    // side ids are numbered by first appearance (the serial order).
+    struct TileOut {
+        std::vector<uint8_t> blob;
+        int64_t listed = 0, L = 0, padded = 0;
+        int32_t n_own = 0, n_sent = 0;
+        bool ok = true;
+    };
+    std::vector<TileOut> tout((size_t)T);
+    if (form == 1) {
+        out.item_beta.assign((size_t)T * kTileItems, 0.0);
+        out.item_v0.assign((size_t)T * kTileItems * 3, 0.0);
+        out.item_model.assign((size_t)T * kTileItems, 0);
+    }
+    bool all_ok = true;
+#pragma omp parallel
+    {
+    std::vector<std::pair<int32_t, uint16_t>> con, side, con_all;
     std::vector<int32_t> gids, xg;
     std::vector<uint16_t> ent;
     std::vector<uint32_t> tw;
     std::vector<int32_t> seg_of;
     std::vector<SideEnt> sents;
-    std::vector<int32_t> sent_tile_sid;     // side id of each entry, in emission order
-    out.blob_off.push_back(0);
-    int64_t listed = 0;
-    for (int32_t tt = 0; tt < T; tt++) {
+    std::vector<int64_t> extra_g;
+    auto emit_tile = [&](int32_t tt, TileOut &o) -> bool {
         // owned targets, ascending
         gids.clear();
         for (int32_t q = tile_rows_ptr[tt]; q < tile_rows_ptr[tt + 1]; q++) {
@@ -283,12 +311,13 @@ bool build_tile_host(int form, int64_t N, int32_t n_nodes, int32_t n, int64_t nn
                 if (!listed_c(i, p)) continue;
                 int64_t g;
                 int32_t r, c;
+                const DevRec &dr = rec[i];
                 if (p < NPAIR) {
-                    g = raw_slot[p * N + i];
-                    r = TT[pair_row(p)][i];
-                    c = TT[pair_col(p)][i];
+                    g = dr.s[p];
+                    r = dr.t[pair_row(p)];
+                    c = dr.t[pair_col(p)];
                 } else {
-                    r = TT[p - NPAIR][i];
+                    r = dr.t[p - NPAIR];
                     g = nnz + r;
                     c = r;
                 }
@@ -335,7 +364,7 @@ bool build_tile_host(int form, int64_t N, int32_t n_nodes, int32_t n, int64_t nn
         seg_of.clear();
         // con is sorted by target: extras below a0, the CSR block, extras up to
         // nnz, then b rows (the tile's range and heavy extras)
-        std::vector<int64_t> extra_g;
+        extra_g.clear();
         {
             size_t k = 0;
             while (k < con.size()) {
@@ -343,14 +372,14 @@ bool build_tile_host(int form, int64_t N, int32_t n_nodes, int32_t n, int64_t nn
                 const bool mainA = g >= a0 && g < (int64_t)a0 + na;
                 const bool mainB = g >= nnz + b0 && g < nnz + b0 + nb;
                 if (!mainA && !mainB) {
-                    if (std::find(gids.begin(), gids.end(), (int32_t)g) == gids.end()) return false;
+                    if (!std::binary_search(gids.begin(), gids.end(), (int32_t)g)) return false;
                     extra_g.push_back(g);
                 }
                 while (k < con.size() && con[k].first == g) k++;
             }
         }
         // walk con once per class (it is sorted; each class is a sorted subset)
-        std::vector<std::pair<int32_t, uint16_t>> con_all;
+        con_all.clear();
         con_all.swap(con);
         auto class_of = [&](int64_t g) {
             if (g >= a0 && g < (int64_t)a0 + na) return 0;
@@ -374,7 +403,7 @@ bool build_tile_host(int form, int64_t N, int32_t n_nodes, int32_t n, int64_t nn
             if (ci != con.size()) return false;
         }
         const int32_t n_own = seg;
-        listed += (int64_t)con_all.size();
+        o.listed += (int64_t)con_all.size();
         con.swap(con_all);
         // side entries (slot filled below, once every side target's entry count is known)
         sents.clear();
@@ -382,23 +411,17 @@ bool build_tile_host(int form, int64_t N, int32_t n_nodes, int32_t n, int64_t nn
         for (size_t k = 0; k < side.size(); k++) {
             const int32_t g = side[k].first;
             if (k == 0 || g != side[k - 1].first) {
-                int32_t &sid = sid_of[g];
-                if (sid < 0) {
-                    sid = (int32_t)out.sd_gid.size();
-                    out.sd_gid.push_back(g);
-                }
                 SideEnt se;
-                se.sid = sid;
+                se.sid = g;             // global target; numbered after the concatenation
                 se.slot = -1;
                 sents.push_back(se);
-                sent_tile_sid.push_back(sid);
                 n_sent++;
             }
             const bool last = k + 1 == side.size() || side[k + 1].first != g;
             ent.push_back((uint16_t)(8 * side[k].second | (last ? kEntEnd : 0)));
             seg_of.push_back(n_own + n_sent - 1);
         }
-        listed += (int64_t)side.size();
+        o.listed += (int64_t)side.size();
         if (n_own + n_sent > kSegMax) return false;
         // equal chunks of K entries per thread, thread-interleaved
         const int64_t L = (int64_t)ent.size();
@@ -444,27 +467,21 @@ bool build_tile_host(int form, int64_t N, int32_t n_nodes, int32_t n, int64_t nn
         const size_t bytes = pad16(hdr.off_side + sizeof(SideEnt) * sents.size());
         if (bytes > (size_t)kStageMax || K > 65535) return false;
         hdr.bytes = (uint32_t)bytes;
-        const size_t base = out.blob.size();
-        out.blob.resize(base + bytes, 0);
-        uint8_t *bp = out.blob.data() + base;
+        o.blob.assign(bytes, 0);
+        uint8_t *bp = o.blob.data();
         std::memcpy(bp, &hdr, sizeof(hdr));
         uint8_t *it = bp + pad16(sizeof(TileHdr));
         int4 *term = reinterpret_cast<int4 *>(it);
         // form 0: beta, v0, model follow the terms in the blob; form 1: they
         // live in tile-order arrays, kTileItems slots per tile (v0 per item)
-        const size_t ib = (size_t)tt * kTileItems;
-        if (form == 1 && out.item_beta.size() < ib + kTileItems) {
-            out.item_beta.resize(ib + kTileItems, 0.0);
-            out.item_v0.resize(3 * (ib + kTileItems), 0.0);
-            out.item_model.resize(ib + kTileItems, 0);
-        }
+        const size_t ib = (size_t)tt * kTileItems;     // form 1 arrays: preallocated, disjoint per tile
         double *bt = form == 1 ? out.item_beta.data() + ib : reinterpret_cast<double *>(it + 16 * (size_t)ni);
         double *v0b = bt + ni;                                     // form 0 only
         uint8_t *md = form == 1 ? out.item_model.data() + ib : reinterpret_cast<uint8_t *>(v0b + 3 * (size_t)ni);
         for (int32_t q = 0; q < ni; q++) {
             const int32_t i = item_dev[q0 + q];
             int4 tv;
-            tv.x = TT[0][i]; tv.y = TT[1][i]; tv.z = TT[2][i]; tv.w = TT[3][i];
+            tv.x = rec[i].t[0]; tv.y = rec[i].t[1]; tv.z = rec[i].t[2]; tv.w = rec[i].t[3];
             std::memcpy(term + q, &tv, sizeof(tv));
             bt[q] = beta[i];
             for (int k = 0; k < 3; k++) {
@@ -481,12 +498,62 @@ bool build_tile_host(int form, int64_t N, int32_t n_nodes, int32_t n, int64_t nn
             ep[kk * kTileThreads + th2] = k < L ? ent[k] : (uint16_t)(8 * kZeroSlot);
         }
         if (!sents.empty()) std::memcpy(bp + hdr.off_side, sents.data(), sizeof(SideEnt) * sents.size());
-        out.blob_off.push_back((int64_t)out.blob.size());
-        out.blob_max = std::max(out.blob_max, (int32_t)bytes);
-        out.n_owned += n_own;
-        out.n_side_entries += n_sent;
-        out.n_listed += L;
-        out.n_padded += (int64_t)K * kTileThreads;
+        o.n_own = n_own;
+        o.n_sent = n_sent;
+        o.L = L;
+        o.padded = (int64_t)K * kTileThreads;
+        return true;
+    };
+#pragma omp for schedule(dynamic, 64)
+    for (int32_t tt = 0; tt < T; tt++) {
+        TileOut &o = tout[tt];
+        o.ok = emit_tile(tt, o);
+        if (!o.ok) {
+#pragma omp atomic write
+            all_ok = false;
+        }
+    }
+    }   // omp parallel
+    if (!all_ok) return false;
+    // concatenate in tile order; number side targets by first appearance
+    std::vector<int32_t> sid_of((size_t)NT, -1);
+    std::vector<int32_t> sent_tile_sid;     // side id of each entry, in emission order
+    int64_t listed = 0;
+    out.blob_off.assign((size_t)T + 1, 0);
+    for (int32_t tt = 0; tt < T; tt++) {
+        const TileOut &o = tout[tt];
+        out.blob_off[tt + 1] = out.blob_off[tt] + (int64_t)o.blob.size();
+        out.blob_max = std::max(out.blob_max, (int32_t)o.blob.size());
+        out.n_owned += o.n_own;
+        out.n_side_entries += o.n_sent;
+        out.n_listed += o.L;
+        out.n_padded += o.padded;
+        listed += o.listed;
+    }
+    out.blob.resize((size_t)out.blob_off[T]);
+#pragma omp parallel for schedule(dynamic, 256)
+    for (int32_t tt = 0; tt < T; tt++) {
+        if (!tout[tt].blob.empty()) std::memcpy(out.blob.data() + out.blob_off[tt], tout[tt].blob.data(), tout[tt].blob.size());
+        std::vector<uint8_t>().swap(tout[tt].blob);
+    }
+    for (int32_t tt = 0; tt < T; tt++) {
+        uint8_t *bp = out.blob.data() + out.blob_off[tt];
+        TileHdr hdr;
+        std::memcpy(&hdr, bp, sizeof(hdr));
+        SideEnt *se = reinterpret_cast<SideEnt *>(bp + hdr.off_side);
+        for (int e = 0; e < hdr.n_sent; e++) {
+            SideEnt v;
+            std::memcpy(&v, se + e, sizeof(v));
+            const int32_t g = v.sid;
+            int32_t &sid = sid_of[g];
+            if (sid < 0) {
+                sid = (int32_t)out.sd_gid.size();
+                out.sd_gid.push_back(g);
+            }
+            v.sid = sid;
+            std::memcpy(se + e, &v, sizeof(v));
+            sent_tile_sid.push_back(sid);
+        }
     }
     // every live contribution is listed exactly once (owned or side)
     {
