@@ -1228,11 +1228,15 @@ __device__ __forceinline__ unsigned long long globaltimer()
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
-#define TILE_TRACE(slot)                                                            \
+// slots: 0 start, 1 first blob staged, 2+4*it .. 5+4*it per tile (while they
+// stay below kTraceSlots-2), kTraceSlots-2 side ticket, kTraceSlots-1 end
+#define TILE_TRACE_AT(slot, limit)                                                  \
     do {                                                                            \
-        if (kTrace && tid == 0 && (slot) < kTraceSlots)                             \
+        if (kTrace && tid == 0 && (slot) < (limit))                                 \
             tk.trace[(size_t)blockIdx.x * kTraceSlots + (slot)] = globaltimer();    \
     } while (0)
+#define TILE_TRACE(slot) TILE_TRACE_AT(slot, kTraceSlots - 2)
+#define TILE_TRACE_TAIL(slot) TILE_TRACE_AT(slot, kTraceSlots)
 
 template <bool kTrace, bool kRep, int kForm>
 __global__ void __launch_bounds__(kTileThreads, tile_ctas(kForm)) k_tile(TileK tk, CallK P)
@@ -1392,7 +1396,7 @@ __global__ void __launch_bounds__(kTileThreads, tile_ctas(kForm)) k_tile(TileK t
             __syncthreads();
             if (tid == 0) s_last = atomicAdd(tk.done, 1u) == (unsigned)G - 1;
             __syncthreads();
-            TILE_TRACE(kTraceSlots - 2);
+            TILE_TRACE_TAIL(kTraceSlots - 2);
             if (s_last) {
                 __threadfence();
                 // hot targets (one part per CTA): a warp each, fixed lane
@@ -1419,7 +1423,7 @@ __global__ void __launch_bounds__(kTileThreads, tile_ctas(kForm)) k_tile(TileK t
             }
         }
     }
-    TILE_TRACE(kTraceSlots - 1);
+    TILE_TRACE_TAIL(kTraceSlots - 1);
 }
 
 __global__ void __launch_bounds__(256) k_side_final(TileK tk, CallK P)

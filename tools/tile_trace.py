@@ -46,7 +46,8 @@ def main():
         print(f"        B1+sums {q(np.where(ok, tr[:, s + 1] - tr[:, s], -1))}")
         print(f"        B2+fix+B3 {q(np.where(ok, tr[:, s + 2] - tr[:, s + 1], -1))}")
         print(f"        write {q(np.where(ok, tr[:, s + 3] - tr[:, s + 2], -1))}")
-    print(" ticket    ", q(rel[:, 62]))
+    print(" ticket    ", q(rel[:, 62]), "(side targets finished by the last CTA)" if (tr[:, 62] > 0).any()
+          else "(none: no inline side finish)")
     print(" end       ", q(rel[:, 63]))
 
 
