@@ -482,3 +482,33 @@ def test_transient_nr_loop_matches_oracle(cuda_ok):
             assert np.abs(g - w).max() <= 1e-9 * max(1.0, np.abs(w).max()), f"{v} step {k}"
         assert abs(g[nl.rails[0]] - 1.0) < 1e-12       # the rail stays at its source
         ctx.close()
+
+
+def test_tile_results_independent_of_setup_threads(cuda_ok):
+    """TILE is deterministic and its layout must not depend on how many host
+    threads built it: A and b bit-identical for setups with 1 and 4 OpenMP
+    threads (subprocesses), and within tolerance of the oracle."""
+    import hashlib
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import hashlib, torch, netgen; from paper_2604_03079_b200 import Context\n"
+            "nl = netgen.config(4, 0.02); ctx = Context.from_netlist(nl, variant='tile')\n"
+            "x = torch.from_numpy(nl.x).cuda()\n"
+            "A = torch.zeros(ctx.nnz, dtype=torch.float64, device='cuda'); b = torch.zeros(ctx.n, dtype=torch.float64, device='cuda')\n"
+            "ctx.eval_stamp(x, nl.h, A, b); torch.cuda.synchronize()\n"
+            "print(hashlib.sha256(A.cpu().numpy().tobytes() + b.cpu().numpy().tobytes()).hexdigest())\n")
+    digests = []
+    for threads in ("1", "4"):
+        r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600,
+                           cwd=root, env=dict(os.environ, OMP_NUM_THREADS=threads))
+        assert r.returncode == 0, r.stderr[-2000:]
+        digests.append(r.stdout.strip().splitlines()[-1])
+    assert digests[0] == digests[1]
+    nl = netgen.config(4, 0.02)
+    ctx = ctx_for(nl, variant="tile")
+    A, b = gpu_run(ctx, nl)
+    assert_parity(reference(nl), A, b, "cfg4@0.02 tile")
+    assert hashlib.sha256(A.tobytes() + b.tobytes()).hexdigest() == digests[0]
+    ctx.close()

@@ -260,3 +260,26 @@ def test_tile_forms_build_within_stage(monkeypatch, form, stage):
         st = _ctx(nl).stats()
         assert st["tile_form"] == form
         assert st["n_tiles"] >= 1 and st["tile_blob_max"] <= stage, nl.name
+
+
+def test_tile_builder_independent_of_thread_count():
+    """The TILE blobs are emitted in parallel and concatenated in tile order:
+    the structure must not depend on the host thread count (setup with 1 and
+    with 4 OpenMP threads, in subprocesses)."""
+    import json
+    import subprocess
+    import sys
+    code = ("import json, netgen; from paper_2604_03079_b200 import Context\n"
+            "out = {}\n"
+            "for c in (2, 3, 4):\n"
+            "    st = Context.from_netlist(netgen.config(c, 0.02), host_only=True).stats()\n"
+            "    out[c] = [st[k] for k in ('n_tiles', 'n_tile_items', 'tile_blob_max', 'n_side_targets',"
+            " 'n_heavy_nodes', 'tile_form')]\n"
+            "print(json.dumps(out))\n")
+    res = []
+    for threads in ("1", "4"):
+        r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600,
+                           cwd=ROOT, env=dict(os.environ, OMP_NUM_THREADS=threads))
+        assert r.returncode == 0, r.stderr[-2000:]
+        res.append(json.loads(r.stdout.strip().splitlines()[-1]))
+    assert res[0] == res[1]
