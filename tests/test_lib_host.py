@@ -283,3 +283,12 @@ def test_tile_builder_independent_of_thread_count():
         assert r.returncode == 0, r.stderr[-2000:]
         res.append(json.loads(r.stdout.strip().splitlines()[-1]))
     assert res[0] == res[1]
+
+
+def test_abi_struct_sizes_match_binding():
+    """The binding refuses a library built with other struct layouts; the
+    library reports its own sizes (0: ees_desc, 1: ees_stats_t, else 0)."""
+    from paper_2604_03079_b200 import _lib
+    assert _lib.lib.ees_abi_sizeof(0) == C.sizeof(_lib.ees_desc)
+    assert _lib.lib.ees_abi_sizeof(1) == C.sizeof(_lib.ees_stats_t)
+    assert _lib.lib.ees_abi_sizeof(7) == 0
