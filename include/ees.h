@@ -253,6 +253,18 @@ ees_status ees_fp64_peak(double *tflops);
  * Synchronous.  (the atomic variant's ceiling.) */
 ees_status ees_red_throughput(int32_t mode, double *gops);
 
+/* Streaming probe (bench helper, the size calibration of the
+ * HBM roofline, §8(d)): enqueues ONE kernel on `stream` that reads
+ * `read_bytes` of `src` and writes `write_bytes` of `dst` with 16-byte
+ * vector accesses, grid-stride over one resident wave -- the read/write mix
+ * of an eval+stamp call's algorithmic bytes, timed by the caller's events.
+ *   src, dst  device pointers, 16-byte aligned, distinct; sizes are rounded
+ *             down to multiples of 16 bytes
+ *   sink      device pointer to one double (written only to keep the loads live)
+ * Errors: EES_EINVAL (null pointer, negative or misaligned), EES_ECUDA. */
+ees_status ees_stream_probe(const void *src, int64_t read_bytes, void *dst, int64_t write_bytes,
+                            double *sink, ees_stream stream);
+
 ees_status ees_destroy(ees_ctx *ctx);
 
 const char *ees_strerror(ees_status status);

@@ -69,13 +69,14 @@ lib.ees_accept.argtypes = [P, P, P]
 lib.ees_set_work.argtypes = [P, i32]
 lib.ees_fp64_peak.argtypes = [C.POINTER(f64)]
 lib.ees_red_throughput.argtypes = [i32, C.POINTER(f64)]
+lib.ees_stream_probe.argtypes = [P, i64, P, i64, P, P]
 lib.ees_destroy.argtypes = [P]
 lib.ees_strerror.argtypes = [i32]
 lib.ees_strerror.restype = C.c_char_p
 for _f in ("ees_setup", "ees_pattern", "ees_find_slot", "ees_colors", "ees_eval_stamp",
            "ees_eval_stamp_host", "ees_set_variant", "ees_stats", "ees_race_probe", "ees_destroy",
            "ees_set_timing", "ees_phase_times", "ees_tile_trace", "ees_accept", "ees_set_work",
-           "ees_fp64_peak", "ees_red_throughput"):
+           "ees_fp64_peak", "ees_red_throughput", "ees_stream_probe"):
     getattr(lib, _f).restype = i32
 
 lib.ees_abi_sizeof.argtypes = [i32]
@@ -88,4 +89,4 @@ for _which, _cls in ((0, ees_desc), (1, ees_stats_t)):
 EXPORTS = ["ees_setup", "ees_pattern", "ees_find_slot", "ees_colors", "ees_eval_stamp",
            "ees_eval_stamp_host", "ees_set_variant", "ees_stats", "ees_set_timing",
            "ees_phase_times", "ees_tile_trace", "ees_race_probe", "ees_accept", "ees_set_work",
-           "ees_fp64_peak", "ees_red_throughput", "ees_destroy", "ees_strerror", "ees_abi_sizeof"]
+           "ees_fp64_peak", "ees_red_throughput", "ees_stream_probe", "ees_destroy", "ees_strerror", "ees_abi_sizeof"]

@@ -49,6 +49,23 @@ def red_throughput(mode=0):
     return t.value
 
 
+def stream_probe(src, read_bytes, dst, write_bytes, sink, stream=None):
+    """ees_stream_probe: enqueue one streaming kernel reading read_bytes of
+    src and writing write_bytes of dst (CUDA tensors; sink: one float64)."""
+    import torch
+    for t in (src, dst, sink):
+        if not (isinstance(t, torch.Tensor) and t.is_cuda):
+            raise ValueError("stream_probe: CUDA tensors expected")
+    if read_bytes > src.numel() * src.element_size() or write_bytes > dst.numel() * dst.element_size():
+        raise ValueError("stream_probe: byte counts exceed the buffers")
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    sh = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+    _check(L.lib.ees_stream_probe(C.c_void_p(src.data_ptr()), int(read_bytes), C.c_void_p(dst.data_ptr()),
+                                  int(write_bytes), C.c_void_p(sink.data_ptr()), C.c_void_p(sh)),
+           "ees_stream_probe")
+
+
 class Context:
     """ees_setup / ees_eval_stamp / ees_stats ... on one CUDA device."""
 

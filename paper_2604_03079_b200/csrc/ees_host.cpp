@@ -1308,6 +1308,16 @@ ees_status ees_red_throughput(int32_t mode, double *gops)
     return measure_red_throughput(mode, gops) == cudaSuccess ? EES_OK : EES_ECUDA;
 }
 
+ees_status ees_stream_probe(const void *src, int64_t read_bytes, void *dst, int64_t write_bytes,
+                            double *sink, ees_stream stream)
+{
+    if (!src || !dst || !sink || read_bytes < 0 || write_bytes < 0) return EES_EINVAL;
+    if (((uintptr_t)src | (uintptr_t)dst) & 15) return EES_EINVAL;
+    return launch_stream_probe(src, read_bytes, dst, write_bytes, sink, (cudaStream_t)stream) == cudaSuccess
+               ? EES_OK
+               : EES_ECUDA;
+}
+
 int64_t ees_abi_sizeof(int32_t which)
 {
     return which == 0 ? (int64_t)sizeof(ees_desc) : which == 1 ? (int64_t)sizeof(ees_stats_t) : 0;

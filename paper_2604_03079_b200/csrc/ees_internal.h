@@ -231,6 +231,8 @@ cudaError_t launch_accept_soa(const int4 *term, int64_t N, const CallK &call, do
 cudaError_t launch_accept_tile(const TileK &tk, const CallK &call, double *item_v0, cudaStream_t st);
 cudaError_t measure_fp64_peak(double *tflops);
 cudaError_t measure_red_throughput(int mode, double *gops);
+cudaError_t launch_stream_probe(const void *src, int64_t read_bytes, void *dst, int64_t write_bytes,
+                                double *sink, cudaStream_t st);
 int tile_blocks_per_sm(int form);
 cudaError_t launch_tile(const TileK &tk, const CallK &call, int grid, cudaStream_t st, int *n_launches);
 cudaError_t launch_atomic(const DevK &dv, const CallK &call, int grid, cudaStream_t st);

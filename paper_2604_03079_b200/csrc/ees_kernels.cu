@@ -748,6 +748,62 @@ cudaError_t measure_red_throughput(int mode, double *gops)
 }
 
 // ---------------------------------------------------------------------------
+// Streaming probe (the size calibration of the HBM roofline):
+// one launch reads `nr` 16-byte vectors of src and writes `nw` vectors of dst
+// -- the read/write mix of one eval+stamp call's algorithmic bytes -- with
+// 16-byte non-allocating loads, four in flight per thread, grid-stride over a
+// grid of a whole number of waves.  The written values depend on the loads,
+// so neither side can be dropped.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double2 ld_stream(const double2 *p)
+{
+    double2 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+    return v;
+}
+
+__global__ void __launch_bounds__(256) k_stream_probe(const double2 *__restrict__ src, int64_t nr,
+                                                      double2 *__restrict__ dst, int64_t nw, double *sink)
+{
+    const int64_t T = (int64_t)gridDim.x * blockDim.x;
+    const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t n = nr > nw ? nr : nw;
+    double acc = 0.0;
+    int64_t i = t0;
+    for (; i + 3 * T < n; i += 4 * T) {
+        double2 v[4];
+#pragma unroll
+        for (int k = 0; k < 4; k++) v[k] = i + k * T < nr ? ld_stream(src + i + k * T) : make_double2(0.0, 0.0);
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            acc += v[k].x + v[k].y;
+            if (i + k * T < nw) dst[i + k * T] = make_double2(v[k].x + 1.0, v[k].y);
+        }
+    }
+    for (; i < n; i += T) {
+        const double2 v = i < nr ? ld_stream(src + i) : make_double2(0.0, 0.0);
+        acc += v.x + v.y;
+        if (i < nw) dst[i] = make_double2(v.x + 1.0, v.y);
+    }
+    if (acc == 12345.678) sink[0] = acc;      // practically never: keeps the loads live
+}
+
+cudaError_t launch_stream_probe(const void *src, int64_t read_bytes, void *dst, int64_t write_bytes,
+                                double *sink, cudaStream_t st)
+{
+    int dev = 0, sms = 148, bps = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_stream_probe, 256, 0);
+    const int64_t nr = read_bytes / 16, nw = write_bytes / 16;
+    const int64_t want = ((nr > nw ? nr : nw) + 255) / 256;
+    const int64_t grid = want < (int64_t)sms * (bps > 0 ? bps : 1) ? (want > 0 ? want : 1) : (int64_t)sms * (bps > 0 ? bps : 1);
+    k_stream_probe<<<(unsigned)grid, 256, 0, st>>>(static_cast<const double2 *>(src), nr, static_cast<double2 *>(dst),
+                                                   nw, sink);
+    return cudaPeekAtLastError();
+}
+
+// ---------------------------------------------------------------------------
 // Race instrument: per colour, count distinct-device writers
 // of every non-rail A entry and b row.
 // ---------------------------------------------------------------------------

@@ -42,5 +42,34 @@ def test_reference_arm_other_ranks_silent():
 
 def test_algorithmic_bytes_cfg1():
     """48 B/FET + 8 B/unknown + 16 B/nonzero + 16 B/unknown."""
-    assert bench.algorithmic_bytes(202000, 101002, 505003) == 48 * 202000 + 24 * 101002 + 16 * 505003
-    assert bench.algorithmic_bytes(0, 0, 0) == 0
+    rd, wr = bench.algorithmic_bytes(202000, 101002, 505003)
+    assert rd + wr == 48 * 202000 + 24 * 101002 + 16 * 505003
+    assert wr == 8 * 505003 + 8 * 101002           # A and b written back once
+    assert bench.algorithmic_bytes(0, 0, 0) == (0, 0)
+
+
+def test_host_cores_within_affinity():
+    """cpu_baseline's core count is the granted one (affinity / cgroup quota),
+    never more than the affinity mask (os.cpu_count() overstated)."""
+    import os
+    cores, info = bench.host_cores()
+    assert 1 <= cores <= len(os.sched_getaffinity(0))
+    assert info["affinity"] == len(os.sched_getaffinity(0))
+
+
+def test_traffic_tag_requires_source_hash(tmp_path, monkeypatch):
+    """A traffic figure from an ncu capture on other sources is reported as
+    stale (null), not as this code's."""
+    import json
+    prof = tmp_path / "profiles"
+    prof.mkdir()
+    (prof / "traffic.json").write_text(json.dumps({
+        "cfg4": {"tile": {"bytes": 123, "profile": "x", "src_hash": "0" * 16},
+                 "atomic": {"bytes": 7, "profile": "y", "src_hash": bench.source_hash()}}}))
+    monkeypatch.setattr(bench, "ROOT", str(tmp_path))
+    monkeypatch.setattr(bench, "source_hash", lambda: "f" * 16)
+    t, src = bench.load_traffic(4, "tile")
+    assert t is None and src["stale"]
+    monkeypatch.setattr(bench, "source_hash", lambda: "0" * 16)
+    t, src = bench.load_traffic(4, "tile")
+    assert t == 123 and not src.get("stale")

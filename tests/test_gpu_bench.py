@@ -21,7 +21,8 @@ def _bench(args):
 
 
 def test_bench_line_keys(cuda_ok):
-    (d,) = _bench(["--config", "0", "--steps", "5", "--warmup", "3", "--no-cpu-baseline"])
+    (d,) = _bench(["--config", "0", "--steps", "5", "--warmup", "3", "--no-cpu-baseline", "--per-config", "",
+                   "--small-calls", "50"])
     for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
               "scaling", "vs_baseline", "dtype", "data", "config", "roofline", "e2e", "gpu_launches", "clocks"):
         assert k in d, k
@@ -32,7 +33,7 @@ def test_bench_line_keys(cuda_ok):
     assert r["frac"] == pytest.approx(r["achieved"] / r["peak"], rel=1e-9)
     assert r["algorithmic_bytes_per_launch"] == 48 * 2000 + 24 * d["config"]["n"] + 16 * d["config"]["nnz"]
     s = r["stream_ref"]
-    assert s["bytes"] == r["algorithmic_bytes_per_launch"] and s["ms"] > 0
+    assert s["read_bytes"] + s["write_bytes"] == r["algorithmic_bytes_per_launch"] and s["ms"] > 0
     assert s["frac"] == pytest.approx(r["achieved"] / s["gbs"], rel=1e-9)
     e = d["e2e"]
     assert e["value"] > 0 and e["h2d_bytes_per_step"] == 8 * d["config"]["n"]
@@ -40,11 +41,24 @@ def test_bench_line_keys(cuda_ok):
     assert d["gpu_launches"] >= 5
     assert d["clocks"]["sm_max_mhz"] > 0 and "reasons" in d["clocks"]
     assert d["config"]["workload"].startswith("cfg0")
+    assert d["config"]["warm_l2"]["calls"] == 50 and d["config"]["graph_ms_per_call"] > 0
+
+
+def test_bench_per_config_records(cuda_ok):
+    """The headline line carries a per_config record per requested config,
+    each with its own throughput and roofline fraction."""
+    (d,) = _bench(["--config", "1", "--steps", "5", "--warmup", "3", "--no-cpu-baseline", "--no-e2e",
+                   "--per-config", "0", "--small-calls", "30"])
+    assert d["config"]["workload"].startswith("cfg1")
+    (pc,) = d["per_config"].values()
+    assert pc["workload"].startswith("cfg0") and pc["n_dev"] == 2000
+    assert pc["value"] == pytest.approx(2000 / (pc["ms_per_step"] * 1e-3), rel=1e-9)
+    assert 0 < pc["roofline"]["frac"] < 1 and pc["warm_l2"]["calls"] == 30
 
 
 def test_bench_work_mode_fp64_roofline(cuda_ok):
     (d,) = _bench(["--config", "0", "--steps", "3", "--warmup", "3", "--no-cpu-baseline", "--no-e2e",
-                   "--variant", "tile", "--work", "8"])
+                   "--variant", "tile", "--work", "8", "--small-calls", "20"])
     r = d["roofline"]
     assert d["config"]["variant"] == "tile" and d["config"]["work"] == 8
     assert r["bound"] == "fp64" and r["unit"] == "TFLOP/s" and 0 < r["frac"] < 1.5
