@@ -36,7 +36,6 @@ import json  # noqa: E402
 import math  # noqa: E402
 import statistics  # noqa: E402
 import sys  # noqa: E402
-import threading  # noqa: E402
 import time  # noqa: E402
 
 import numpy as np  # noqa: E402
@@ -126,56 +125,74 @@ def load_traffic(cfg, variant):
 
 
 class ClockSampler:
-    """Samples SM clock and throttle reasons via NVML while running."""
+    """Samples SM clock and throttle reasons while the GPU works: an
+    `nvidia-smi -lms` subprocess (no GIL contention with the enqueueing
+    thread; B200_PROFILING.md clocks line), timestamps kept, so the samples
+    inside the timed region can be told from those of the whole window."""
 
-    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
-               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
-               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
-               0x100: "display_clock_setting"}
+    FIELDS = ("timestamp,clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
 
-    def __init__(self, index, period=0.001):
-        self.index, self.period = index, period
-        self.samples, self.reasons = [], set()
-        self.max_mhz = None
-        self._stop = threading.Event()
-        self._t = None
+    def __init__(self, index, period_ms=10):
+        self.index, self.period_ms = index, period_ms
+        self.proc = None
+        self.marks = {}
+        self.rows = []
 
-    def __enter__(self):
+    def start(self):
+        import subprocess
         try:
-            import pynvml
-            pynvml.nvmlInit()
-            self._nv = pynvml
-            self._h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
-            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", str(self.period_ms)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:
-            self._nv = None
-            return self
-        self._t = threading.Thread(target=self._run, daemon=True)
-        self._t.start()
+            self.proc = None
+        time.sleep(0.3)                  # nvidia-smi start-up: its first samples precede the work
         return self
 
-    def _run(self):
-        nv = self._nv
-        while not self._stop.is_set():
-            try:
-                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
-                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
-                for bit, name in self.REASONS.items():
-                    if r & bit and name != "gpu_idle":
-                        self.reasons.add(name)
-            except Exception:
-                pass
-            time.sleep(self.period)
+    def mark(self, name):
+        self.marks[name] = time.time()
 
-    def __exit__(self, *a):
-        self._stop.set()
-        if self._t:
-            self._t.join()
+    def stop(self):
+        if self.proc is None:
+            return
+        time.sleep(2.5 * self.period_ms / 1e3)
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out = ""
+        import datetime
+        for line in out.splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                ts = datetime.datetime.strptime(f[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                self.rows.append((ts, float(f[1]), float(f[2]), f[4:8]))
+            except Exception:
+                continue
 
     def summary(self):
-        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
-                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
-                "samples": len(self.samples)}
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0,
+                    "source": "nvidia-smi unavailable"}
+        t0, t1 = self.marks.get("timed_start"), self.marks.get("timed_end")
+        w0, w1 = self.marks.get("window_start", 0), self.marks.get("window_end", 1e18)
+        timed = [r for r in self.rows if t0 is not None and t0 <= r[0] <= t1]
+        window = [r for r in self.rows if w0 <= r[0] <= w1] or self.rows
+        use = timed if len(timed) >= 3 else window
+        reasons = sorted({n for r in use for n, a in zip(self.NAMES, r[3]) if a.lower() == "active"})
+        return {"sm_mhz": statistics.median(r[1] for r in use), "sm_max_mhz": max(r[2] for r in use),
+                "reasons": reasons, "samples": len(use), "samples_timed_region": len(timed),
+                "sm_mhz_min": min(r[1] for r in use),
+                "source": (f"nvidia-smi -lms {self.period_ms}: " +
+                           ("samples inside the timed region" if use is timed else
+                            "samples from warm-up through the roofline pass (timed region too short "
+                            "for 3 samples)"))}
 
 
 # ---------------------------------------------------------------- CPU side
@@ -202,6 +219,12 @@ def host_cores():
             pass
     cores = aff if quota is None else max(1, min(aff, int(math.ceil(quota))))
     return cores, {"affinity": aff, "cgroup_quota_cpus": quota, "os_cpu_count": os.cpu_count()}
+
+
+# The granted cores, read before any OpenMP runtime starts: with OMP_PROC_BIND
+# set, libgomp pins the main thread to its first place when it initialises
+# (torch loads it), after which the thread's affinity mask shows one core.
+_HOST_CORES = host_cores()
 
 
 def cpu_model():
@@ -253,7 +276,7 @@ def cpu_baseline(nl, reps=5):
     the fastest multi-threaded kernel; the thread scaling is reported, and
     flagged when T threads give less than 2x of one."""
     import oracle
-    cores, cinfo = host_cores()
+    cores, cinfo = _HOST_CORES
     t_build = time.perf_counter()
     bl = oracle.Baseline(nl)
     t_build = time.perf_counter() - t_build
@@ -291,7 +314,7 @@ def run_reference(args):
         return
     nl = netgen.config(args.config)
     import oracle
-    cores, cinfo = host_cores()
+    cores, cinfo = _HOST_CORES
     bl = oracle.Baseline(nl)
     A = np.zeros(bl.nnz)
     b = np.zeros(nl.n)
@@ -451,6 +474,8 @@ def measure(ctx, nl, cfg, args, dev, stream, flush, world, steps, warmup, small=
             A.zero_()
             b.zero_()
 
+    if clk is not None:
+        clk.mark("window_start")
     with torch.cuda.stream(stream):
         for k in range(warmup):
             step_pre(k)
@@ -462,7 +487,7 @@ def measure(ctx, nl, cfg, args, dev, stream, flush, world, steps, warmup, small=
         dist.barrier()
     torch.cuda.synchronize()
     if clk is not None:
-        clk.__enter__()
+        clk.mark("timed_start")
     with torch.cuda.stream(stream):
         for k in range(steps):
             step_pre(k)
@@ -471,7 +496,7 @@ def measure(ctx, nl, cfg, args, dev, stream, flush, world, steps, warmup, small=
             evs[k][1].record(stream)
     torch.cuda.synchronize()
     if clk is not None:
-        clk.__exit__()
+        clk.mark("timed_end")
     if world > 1:
         dist.barrier()
     per = [e0.elapsed_time(e1) for e0, e1 in evs]
@@ -486,6 +511,8 @@ def measure(ctx, nl, cfg, args, dev, stream, flush, world, steps, warmup, small=
     torch.cuda.synchronize()
     phase_ms, n_timed = ctx.phase_times()
     ctx.set_timing(False)
+    if clk is not None:
+        clk.mark("window_end")
     st = ctx.stats()
     variant = st["variant_chosen"]
     hbm, peak_src = peaks()
@@ -630,7 +657,7 @@ def main():
     ap.add_argument("--sweep-out", default=None)
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
-    args.per_config = [int(c) for c in args.per_config.split(",") if c.strip() != ""]
+    args.per_config = [int(c) for c in args.per_config.replace("none", "").split(",") if c.strip() not in ("", "''")]
     if args.netlist or args.rule != "exclude_rails" or args.work > 1:
         args.per_config = []
     if args.impl == "reference":
@@ -659,9 +686,12 @@ def main():
     ctx = Context.from_netlist(nl, variant=args.variant, rule=args.rule, heavy_degree=args.heavy_degree)
     if args.work > 1:
         ctx.set_work(args.work)
-    clk = ClockSampler(torch.cuda.current_device())
-    r = measure(ctx, nl, cfg, args, dev, stream, flush, world, args.steps, args.warmup,
-                small=cfg in SMALL_CONFIGS, clk=clk)
+    clk = ClockSampler(torch.cuda.current_device()).start()
+    try:
+        r = measure(ctx, nl, cfg, args, dev, stream, flush, world, args.steps, args.warmup,
+                    small=cfg in SMALL_CONFIGS, clk=clk)
+    finally:
+        clk.stop()
     per = r["per"]
     max_ms = reduce_max(sum(per), world, dev)
     ms_per_step = max_ms / args.steps

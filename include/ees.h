@@ -109,14 +109,32 @@ typedef struct {
     double gmin;                    /* S, >= 0, added drain-source on every FET */
     int32_t variant;                /* ees_variant */
     int32_t conflict_rule;          /* ees_conflict_rule */
-    int32_t flags;                  /* 0, or EES_SETUP_HOST_ONLY */
+    int32_t flags;                  /* 0, or EES_SETUP_* bits (below) */
     int32_t heavy_degree;           /* EES_CONFLICT_HYBRID threshold (incident FETs); 0 = 64 */
 } ees_desc;
 
-/* ees_desc.flags: build only the host-side topology (pattern, slots,
- * colouring, statistics) without touching a GPU; ees_eval_stamp and
- * ees_race_probe then return EES_ESTATE.  For host-logic tests. */
-enum { EES_SETUP_HOST_ONLY = 1 };
+/* ees_desc.flags:
+ *  EES_SETUP_HOST_ONLY: build only the host-side topology (pattern, slots,
+ *    colouring, statistics) without touching a GPU; ees_eval_stamp and
+ *    ees_race_probe then return EES_ESTATE.  For host-logic tests.
+ *  Layout overrides (experiments and tests; by default setup chooses each
+ *  from the topology): at most one of each pair.
+ *    EES_SETUP_TILE_FORM0 / _FORM1     EES_TILE item data in the tile blobs /
+ *                                      in tile-order HBM arrays
+ *    EES_SETUP_GATHER_FORM0 / _FORM1   EES_GATHER compact buffer + index lists /
+ *                                      target-ordered buffer
+ *    EES_SETUP_COLOR_LAUNCH / _COOP    EES_COLOR one launch per colour /
+ *                                      one persistent cooperative kernel
+ *  Any other bit -> EES_EINVAL. */
+enum {
+    EES_SETUP_HOST_ONLY = 1,
+    EES_SETUP_TILE_FORM0 = 2,
+    EES_SETUP_TILE_FORM1 = 4,
+    EES_SETUP_GATHER_FORM0 = 8,
+    EES_SETUP_GATHER_FORM1 = 16,
+    EES_SETUP_COLOR_LAUNCH = 32,
+    EES_SETUP_COLOR_COOP = 64
+};
 
 typedef struct {
     int64_t n_dev, nnz, n_contributions;   /* contributions = live (entry, device) stamps */
@@ -151,13 +169,21 @@ typedef struct {
  * free them on return.  On error *out is NULL. */
 ees_status ees_setup(const ees_desc *desc, ees_ctx **out);
 
-/* Host CSR pattern, rows sorted by column, library-owned until ees_destroy.
- * A_vals[k] of ees_eval_stamp is the entry (row r, col col_idx[k]) with
- * row_ptr[r] <= k < row_ptr[r+1]. */
+/* The frozen sparsity pattern ("reserve ... finalize: the
+ * pattern is immutable, handles stay valid"; S:114-131 every ordered
+ * non-ground terminal pair of every device, deduplicated, plus the caller's
+ * extra entries): host CSR, rows sorted by column, library-owned until
+ * ees_destroy.  A_vals[k] of ees_eval_stamp is the entry (row r, col
+ * col_idx[k]) with row_ptr[r] <= k < row_ptr[r+1].
+ *   n, nnz, row_ptr, col_idx  outputs; each may be NULL (not written)
+ * Errors: EES_EINVAL for a NULL ctx. */
 ees_status ees_pattern(const ees_ctx *ctx, int32_t *n, int64_t *nnz,
                        const int32_t **row_ptr, const int32_t **col_idx);
 
-/* CSR index of (row, col), or *slot = -1 if absent. */
+/* EntryHandle lookup (a handle is the stable position of an
+ * entry in the frozen pattern; here the CSR index into A_vals): *slot = k
+ * with (row, col) at A_vals[k], or -1 if the pattern has no such entry.
+ * Errors: EES_EINVAL for a NULL ctx or slot, or row / col outside [0, n). */
 ees_status ees_find_slot(const ees_ctx *ctx, int32_t row, int32_t col, int64_t *slot);
 
 /* Host colour of every device (netlist order), library-owned. */
@@ -192,6 +218,11 @@ ees_status ees_eval_stamp_host(ees_ctx *ctx, const double *x, double h, double *
 /* Choose the variant later calls run (EES_AUTO = the one setup measured fastest). */
 ees_status ees_set_variant(ees_ctx *ctx, int32_t variant);
 
+/* Statistics of the context (SPEC S:285-293 color_stats: colour count, group
+ * sizes, busiest conflict node; S:326-329 KernelReport: the variant run and
+ * its timings) plus setup times and the TILE / GATHER / hybrid structure
+ * sizes, copied into *out (caller-owned).  Host-side only; never syncs the
+ * device.  Errors: EES_EINVAL for a NULL ctx or out. */
 ees_status ees_stats(const ees_ctx *ctx, ees_stats_t *out);
 
 /* sizeof of the ABI structs this library was built with (0: ees_desc,
@@ -264,6 +295,48 @@ ees_status ees_red_throughput(int32_t mode, double *gops);
  * Errors: EES_EINVAL (null pointer, negative or misaligned), EES_ECUDA. */
 ees_status ees_stream_probe(const void *src, int64_t read_bytes, void *dst, int64_t write_bytes,
                             double *sink, ees_stream stream);
+
+/* ---------------------------------------------------------------------------
+ * The steps either side of the hot path (SPEC.md
+ * newton_step S:423-432 "clear -> linear pre-pass -> device stamps -> solve").
+ * ------------------------------------------------------------------------- */
+
+/* Linear pre-pass ("linear devices are stamped first, sequentially";
+ * S:426): A_vals[slot[k]] += val[k] for k < n_a and b[row[k]] += bval[k] for
+ * k < n_b -- the caller's resistors, capacitor companions and ideal-source
+ * entries, pre-computed as (CSR index, value) pairs (ees_find_slot).  One
+ * kernel on `stream`, enqueue only.  Repeated slots / rows accumulate (FP64
+ * atomic adds, so their summation order is not fixed; distinct slots give
+ * deterministic results).
+ *   slot, val, row, bval, A_vals, b   device pointers
+ * Errors: EES_EINVAL (NULL ctx, negative counts, NULL pointer with a count),
+ * EES_ECUDA. */
+ees_status ees_stamp_linear(const ees_ctx *ctx, int64_t n_a, const int64_t *slot, const double *val,
+                            int64_t n_b, const int32_t *row, const double *bval, double *A_vals, double *b,
+                            ees_stream stream);
+
+/* Sparse LU solve of A x = b on the context's frozen pattern: the role of
+ * KLU in the paper's NR loop, on the GPU.  Symbolic analysis
+ * and pivoting once per topology, numeric refactorisation per NR iteration:
+ *  ees_solver_create  orders the pattern (symmetric AMD of A + A^T), factors
+ *                     A_vals_host (host, [nnz]) with partial pivoting on the
+ *                     host and hands ordering, pivots and L/U patterns to
+ *                     cuSOLVER's refactorisation (cusolverRf).  Synchronous.
+ *                     EES_EINVAL if A is singular at these values.
+ *  ees_solver_factor  refactorises at A_vals (device, [nnz]) with the same
+ *                     ordering and pivots, on the GPU; EES_EINVAL on a zero
+ *                     pivot (re-create the solver at the new values).
+ *  ees_solver_solve   x = A^-1 b (device [n]; x may alias b) with the last
+ *                     factorisation.
+ * factor and solve are ordered after the caller's stream and the stream
+ * after them through events (cuSOLVER's refactorisation runs on the legacy
+ * stream); no host synchronisation.  ees_solver_info: fill-in of L and U. */
+typedef struct ees_solver ees_solver;
+ees_status ees_solver_create(const ees_ctx *ctx, const double *A_vals_host, ees_solver **out);
+ees_status ees_solver_factor(ees_solver *solver, const double *A_vals, ees_stream stream);
+ees_status ees_solver_solve(ees_solver *solver, const double *b, double *x, ees_stream stream);
+ees_status ees_solver_info(const ees_solver *solver, int64_t *nnz_L, int64_t *nnz_U);
+ees_status ees_solver_destroy(ees_solver *solver);
 
 ees_status ees_destroy(ees_ctx *ctx);
 

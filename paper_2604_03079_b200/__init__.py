@@ -4,7 +4,7 @@
 binding is imported lazily so ``python -m paper_2604_03079_b200.build`` works
 before the library exists.
 """
-__all__ = ["Context", "EESError", "VARIANTS", "RULES", "fp64_peak", "red_throughput", "stream_probe"]
+__all__ = ["Context", "EESError", "VARIANTS", "RULES", "fp64_peak", "red_throughput", "stream_probe", "Solver"]
 
 
 def __getattr__(name):

@@ -20,6 +20,9 @@ EES_AUTO, EES_COLOR, EES_ATOMIC, EES_GATHER, EES_TILE, EES_COLOR_BUF = 0, 1, 2, 
 EES_CONFLICT_EXCLUDE_RAILS, EES_CONFLICT_PAPER, EES_CONFLICT_HYBRID = 0, 1, 2
 EES_MAX_MODELS, EES_MAX_RAILS = 16, 8
 EES_SETUP_HOST_ONLY = 1
+EES_SETUP_TILE_FORM0, EES_SETUP_TILE_FORM1 = 2, 4
+EES_SETUP_GATHER_FORM0, EES_SETUP_GATHER_FORM1 = 8, 16
+EES_SETUP_COLOR_LAUNCH, EES_SETUP_COLOR_COOP = 32, 64
 EES_HOST_ASSIGN = 1
 
 P = C.c_void_p
@@ -70,13 +73,21 @@ lib.ees_set_work.argtypes = [P, i32]
 lib.ees_fp64_peak.argtypes = [C.POINTER(f64)]
 lib.ees_red_throughput.argtypes = [i32, C.POINTER(f64)]
 lib.ees_stream_probe.argtypes = [P, i64, P, i64, P, P]
+lib.ees_stamp_linear.argtypes = [P, i64, P, P, i64, P, P, P, P, P]
+lib.ees_solver_create.argtypes = [P, P, C.POINTER(P)]
+lib.ees_solver_factor.argtypes = [P, P, P]
+lib.ees_solver_solve.argtypes = [P, P, P, P]
+lib.ees_solver_info.argtypes = [P, C.POINTER(i64), C.POINTER(i64)]
+lib.ees_solver_destroy.argtypes = [P]
 lib.ees_destroy.argtypes = [P]
 lib.ees_strerror.argtypes = [i32]
 lib.ees_strerror.restype = C.c_char_p
 for _f in ("ees_setup", "ees_pattern", "ees_find_slot", "ees_colors", "ees_eval_stamp",
            "ees_eval_stamp_host", "ees_set_variant", "ees_stats", "ees_race_probe", "ees_destroy",
            "ees_set_timing", "ees_phase_times", "ees_tile_trace", "ees_accept", "ees_set_work",
-           "ees_fp64_peak", "ees_red_throughput", "ees_stream_probe"):
+           "ees_fp64_peak", "ees_red_throughput", "ees_stream_probe", "ees_stamp_linear",
+           "ees_solver_create", "ees_solver_factor", "ees_solver_solve", "ees_solver_info",
+           "ees_solver_destroy"):
     getattr(lib, _f).restype = i32
 
 lib.ees_abi_sizeof.argtypes = [i32]
@@ -89,4 +100,5 @@ for _which, _cls in ((0, ees_desc), (1, ees_stats_t)):
 EXPORTS = ["ees_setup", "ees_pattern", "ees_find_slot", "ees_colors", "ees_eval_stamp",
            "ees_eval_stamp_host", "ees_set_variant", "ees_stats", "ees_set_timing",
            "ees_phase_times", "ees_tile_trace", "ees_race_probe", "ees_accept", "ees_set_work",
-           "ees_fp64_peak", "ees_red_throughput", "ees_stream_probe", "ees_destroy", "ees_strerror", "ees_abi_sizeof"]
+           "ees_fp64_peak", "ees_red_throughput", "ees_stream_probe", "ees_stamp_linear", "ees_solver_create",
+           "ees_solver_factor", "ees_solver_solve", "ees_solver_info", "ees_solver_destroy", "ees_destroy", "ees_strerror", "ees_abi_sizeof"]

@@ -35,6 +35,14 @@ def _ptr(a):
     return C.c_void_p(a.ctypes.data) if a.size else None
 
 
+def _flags(host_only, tile_form, gather_form, color_mode):
+    f = L.EES_SETUP_HOST_ONLY if host_only else 0
+    f |= {None: 0, 0: L.EES_SETUP_TILE_FORM0, 1: L.EES_SETUP_TILE_FORM1}[tile_form]
+    f |= {None: 0, 0: L.EES_SETUP_GATHER_FORM0, 1: L.EES_SETUP_GATHER_FORM1}[gather_form]
+    f |= {None: 0, "launch": L.EES_SETUP_COLOR_LAUNCH, "coop": L.EES_SETUP_COLOR_COOP}[color_mode]
+    return f
+
+
 def fp64_peak():
     """ees_fp64_peak: measured FP64 FMA TFLOP/s of the current CUDA device."""
     t = C.c_double()
@@ -71,7 +79,10 @@ class Context:
 
     def __init__(self, *, n_nodes, n_extra, d, g, s, b, w, l, model, vprev, models,
                  rails=(), extra_row=(), extra_col=(), gmin=1e-12, variant="auto",
-                 rule="exclude_rails", heavy_degree=0, host_only=False):
+                 rule="exclude_rails", heavy_degree=0, host_only=False, tile_form=None,
+                 gather_form=None, color_mode=None):
+        """Layout overrides (experiments, tests): tile_form / gather_form 0 or 1,
+        color_mode "launch" or "coop"; None = setup chooses (ees.h flags)."""
         self._keep = dict(d=_arr(d, np.int32), g=_arr(g, np.int32), s=_arr(s, np.int32),
                           b=_arr(b, np.int32), w=_arr(w, np.float64), l=_arr(l, np.float64),
                           model=_arr(model, np.int32), vprev=_arr(vprev, np.float64),
@@ -92,7 +103,7 @@ class Context:
             extra_col=_ptr(k["ec"]), gmin=float(gmin),
             variant=VARIANTS[variant] if isinstance(variant, str) else int(variant),
             conflict_rule=RULES[rule] if isinstance(rule, str) else int(rule),
-            flags=L.EES_SETUP_HOST_ONLY if host_only else 0, heavy_degree=int(heavy_degree))
+            flags=_flags(host_only, tile_form, gather_form, color_mode), heavy_degree=int(heavy_degree))
         h = C.c_void_p()
         _check(L.lib.ees_setup(C.byref(desc), C.byref(h)), "ees_setup")
         self._h = h
@@ -102,12 +113,12 @@ class Context:
 
     @classmethod
     def from_netlist(cls, nl, variant="auto", rule="exclude_rails", gmin=None, host_only=False,
-                     heavy_degree=0):
+                     heavy_degree=0, **layout):
         return cls(n_nodes=nl.n_nodes, n_extra=nl.n_extra, d=nl.d, g=nl.g, s=nl.s, b=nl.b,
                    w=nl.w, l=nl.l, model=nl.model, vprev=nl.vprev, models=nl.models,
                    rails=nl.rails, extra_row=nl.extra_row, extra_col=nl.extra_col,
                    gmin=nl.gmin if gmin is None else gmin, variant=variant, rule=rule,
-                   heavy_degree=heavy_degree, host_only=host_only)
+                   heavy_degree=heavy_degree, host_only=host_only, **layout)
 
     # ------------------------------------------------------------ queries
     def pattern(self):
@@ -229,6 +240,27 @@ class Context:
         _check(L.lib.ees_race_probe(self._h, cp, C.byref(n)), "ees_race_probe")
         return n.value
 
+    def stamp_linear(self, slot, val, row, bval, A, b, stream=None):
+        """ees_stamp_linear (the caller's linear pre-pass): A[slot] +=
+        val, b[row] += bval (CUDA tensors: slot int64, row int32, values
+        float64)."""
+        import torch
+        if stream is None:
+            stream = torch.cuda.current_stream()
+        sh = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+        for t, dt in ((slot, torch.int64), (val, torch.float64), (row, torch.int32), (bval, torch.float64),
+                      (A, torch.float64), (b, torch.float64)):
+            if not (t.is_cuda and t.dtype == dt and t.is_contiguous()):
+                raise ValueError("stamp_linear: contiguous CUDA tensors of the documented dtypes expected")
+        if slot.numel() != val.numel() or row.numel() != bval.numel():
+            raise ValueError("stamp_linear: slot/val and row/bval lengths differ")
+        if A.numel() != self.nnz or b.numel() != self.n:
+            raise ValueError("stamp_linear: A must have nnz and b n elements")
+        _check(L.lib.ees_stamp_linear(self._h, slot.numel(), C.c_void_p(slot.data_ptr()), C.c_void_p(val.data_ptr()),
+                                      row.numel(), C.c_void_p(row.data_ptr()), C.c_void_p(bval.data_ptr()),
+                                      C.c_void_p(A.data_ptr()), C.c_void_p(b.data_ptr()), C.c_void_p(sh)),
+               "ees_stamp_linear")
+
     def close(self):
         if getattr(self, "_h", None):
             L.lib.ees_destroy(self._h)
@@ -245,3 +277,52 @@ class Context:
 
     def __exit__(self, *a):
         self.close()
+
+
+class Solver:
+    """ees_solver_*: sparse LU of the context's pattern (KLU's role):
+    ordering + pivoting at construction (host values), GPU refactorisation
+    per factor() call, GPU triangular solves per solve() call."""
+
+    def __init__(self, ctx, A_host):
+        A_host = np.ascontiguousarray(A_host, np.float64)
+        if A_host.size != ctx.nnz:
+            raise ValueError("Solver: A_host must have nnz entries")
+        h = C.c_void_p()
+        _check(L.lib.ees_solver_create(ctx._h, C.c_void_p(A_host.ctypes.data), C.byref(h)), "ees_solver_create")
+        self._h, self.n, self.nnz = h, ctx.n, ctx.nnz
+
+    @staticmethod
+    def _sh(stream):
+        import torch
+        if stream is None:
+            stream = torch.cuda.current_stream()
+        return C.c_void_p(stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
+
+    def factor(self, A, stream=None):
+        if not (A.is_cuda and A.numel() == self.nnz and A.is_contiguous()):
+            raise ValueError("factor: a contiguous CUDA float64 tensor of nnz elements")
+        _check(L.lib.ees_solver_factor(self._h, C.c_void_p(A.data_ptr()), self._sh(stream)), "ees_solver_factor")
+
+    def solve(self, b, x, stream=None):
+        for t in (b, x):
+            if not (t.is_cuda and t.numel() == self.n and t.is_contiguous()):
+                raise ValueError("solve: contiguous CUDA float64 tensors of n elements")
+        _check(L.lib.ees_solver_solve(self._h, C.c_void_p(b.data_ptr()), C.c_void_p(x.data_ptr()),
+                                      self._sh(stream)), "ees_solver_solve")
+
+    def fill(self):
+        a, c = L.i64(), L.i64()
+        _check(L.lib.ees_solver_info(self._h, C.byref(a), C.byref(c)), "ees_solver_info")
+        return a.value, c.value
+
+    def close(self):
+        if getattr(self, "_h", None):
+            L.lib.ees_solver_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -18,7 +18,7 @@ INCLUDE = os.path.join(ROOT, "include")
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-SOURCES = ["ees_kernels.cu", "ees_host.cpp", "ees_tile.cpp"]
+SOURCES = ["ees_kernels.cu", "ees_host.cpp", "ees_tile.cpp", "ees_solve.cu"]
 HEADERS = ["ees_internal.h"]
 
 
@@ -39,7 +39,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
     objs = []
     for src in SOURCES:
         obj = os.path.join(BUILD, src + ".o")
-        cmd = [NVCC, *ARCH, "-lineinfo", "-O3", "-std=c++17", "-I", INCLUDE,
+        # EES_NVCC_DEFS: extra -D flags for A/B build trees (tools/ab_tree.sh); build time only
+        defs = os.environ.get("EES_NVCC_DEFS", "").split()
+        cmd = [NVCC, *ARCH, "-lineinfo", "-O3", "-std=c++17", "-I", INCLUDE, *defs,
                "-Xcompiler", "-fPIC,-fopenmp,-O3", "-c", os.path.join(CSRC, src), "-o", obj]
         if src.endswith(".cu"):
             cmd += ["-Xptxas", "-v", "--extended-lambda"]
@@ -50,8 +52,10 @@ def build(force: bool = False, verbose: bool = False) -> str:
             sys.stderr.write(r.stderr)
         objs.append(obj)
     tmp = LIB + ".tmp"
+    cudalib = os.path.join(os.path.dirname(os.path.dirname(NVCC)), "lib64")
     cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-cudart", "static",
-           "-Xcompiler", "-fopenmp", "-lgomp"]
+           "-Xcompiler", "-fopenmp", "-lgomp", "-L", cudalib, "-lcusolver", "-lcusparse",
+           "-Xlinker", "-rpath=" + cudalib]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")

@@ -77,6 +77,7 @@ struct ees_ctx {
     int32_t launches = 0;
     int32_t work = 1;                     // S:229 work multiplier
     bool host_only = false;
+    int32_t setup_flags = 0;              // ees_desc.flags
     // phase timing
     bool timing = false;
     struct Mark { int phase; cudaEvent_t a, b; };
@@ -138,7 +139,15 @@ ees_status validate(const ees_desc *d)
         d->conflict_rule != EES_CONFLICT_HYBRID)
         return EES_EINVAL;
     if (d->heavy_degree < 0) return EES_EINVAL;
-    if (d->flags & ~EES_SETUP_HOST_ONLY) return EES_EINVAL;
+    {
+        const int32_t known = EES_SETUP_HOST_ONLY | EES_SETUP_TILE_FORM0 | EES_SETUP_TILE_FORM1 |
+                              EES_SETUP_GATHER_FORM0 | EES_SETUP_GATHER_FORM1 | EES_SETUP_COLOR_LAUNCH |
+                              EES_SETUP_COLOR_COOP;
+        auto both = [&](int32_t a, int32_t b) { return (d->flags & a) && (d->flags & b); };
+        if ((d->flags & ~known) || both(EES_SETUP_TILE_FORM0, EES_SETUP_TILE_FORM1) ||
+            both(EES_SETUP_GATHER_FORM0, EES_SETUP_GATHER_FORM1) || both(EES_SETUP_COLOR_LAUNCH, EES_SETUP_COLOR_COOP))
+            return EES_EINVAL;
+    }
     for (int k = 0; k < d->n_models; k++) {
         const ees_model &m = d->models[k];
         if ((m.polarity != 1 && m.polarity != -1) || m.reserved != 0) return EES_EINVAL;
@@ -263,24 +272,43 @@ int32_t find_slot(const ees_ctx *c, int32_t r, int32_t col)
 
 // First-fit greedy colouring in netlist order over the
 // conflict nodes (non-ground; rails removed under EES_CONFLICT_EXCLUDE_RAILS).
-// Each node keeps the colours of its already-coloured devices: up to 4 inline,
-// then a bitset with a monotone "first non-full word" cursor, so a device on a
-// clique of size f costs O(1) amortised instead of O(f).
-struct NodeColors {
-    int32_t cnt = 0;       // inline colours, or -1 once converted to a bitset
-    int32_t inl[4];
-    int32_t big = -1;      // index into bitsets
-};
+// Each node keeps the colours of its already-coloured devices: a node with at
+// most kListMax incident devices in a list of its own (a slice of one pool
+// sized by the incidence counts, so memory is O(sum of degrees) whatever the
+// colour count), a busier node in a bitset with a monotone "first non-full
+// word" cursor, so a device on a clique of size f costs O(1) amortised
+// instead of O(f).
+constexpr int32_t kListMax = 64;
 
 int32_t greedy_color(const ees_desc *d, const std::vector<uint8_t> &excluded,
                      std::vector<int32_t> &color, int32_t &max_node_deg)
 {
     const int64_t N = d->n_dev;
+    const int32_t NN = std::max(1, d->n_nodes);
     color.assign((size_t)N, 0);
-    std::vector<NodeColors> nc((size_t)d->n_nodes);
+    // distinct incident devices per node (capacity of its list)
+    std::vector<int32_t> cap((size_t)NN, 0);
+    for (int64_t i = 0; i < N; i++) {
+        const int32_t T[4] = {d->d[i], d->g[i], d->s[i], d->b[i]};
+        for (int a = 0; a < 4; a++) {
+            bool dup = T[a] < 0 || excluded[T[a]];
+            for (int c = 0; c < a; c++) dup |= T[c] == T[a];
+            if (!dup) cap[T[a]]++;
+        }
+    }
+    std::vector<int64_t> lptr((size_t)NN + 1, 0);
+    std::vector<int32_t> big((size_t)NN, -1);          // index into bits, or -1 (list)
+    for (int32_t v = 0; v < d->n_nodes; v++) lptr[v + 1] = lptr[v] + (cap[v] <= kListMax ? cap[v] : 0);
+    std::vector<int32_t> pool((size_t)std::max<int64_t>(1, lptr[d->n_nodes]));
+    std::vector<int32_t> cnt((size_t)NN, 0);
     std::vector<std::vector<uint64_t>> bits;
     std::vector<int32_t> first_nonfull;
-    std::vector<int32_t> deg((size_t)d->n_nodes, 0);
+    for (int32_t v = 0; v < d->n_nodes; v++)
+        if (cap[v] > kListMax) {
+            big[v] = (int32_t)bits.size();
+            bits.emplace_back();
+            first_nonfull.push_back(0);
+        }
     int32_t C = 0;
     for (int64_t i = 0; i < N; i++) {
         int32_t U[4];
@@ -293,21 +321,20 @@ int32_t greedy_color(const ees_desc *d, const std::vector<uint8_t> &excluded,
             if (!dup) U[nu++] = T[a];
         }
         int64_t w = 0;
-        for (int k = 0; k < nu; k++) {
-            const NodeColors &s = nc[U[k]];
-            if (s.big >= 0) w = std::max<int64_t>(w, first_nonfull[s.big]);
-        }
+        for (int k = 0; k < nu; k++)
+            if (big[U[k]] >= 0) w = std::max<int64_t>(w, first_nonfull[big[U[k]]]);
         int32_t col;
         for (;; w++) {
             uint64_t m = 0;
             for (int k = 0; k < nu; k++) {
-                const NodeColors &s = nc[U[k]];
-                if (s.big >= 0) {
-                    const std::vector<uint64_t> &bv = bits[s.big];
+                const int32_t v = U[k];
+                if (big[v] >= 0) {
+                    const std::vector<uint64_t> &bv = bits[big[v]];
                     if (w < (int64_t)bv.size()) m |= bv[w];
                 } else {
-                    for (int q = 0; q < s.cnt; q++)
-                        if ((s.inl[q] >> 6) == w) m |= 1ull << (s.inl[q] & 63);
+                    const int32_t *l = pool.data() + lptr[v];
+                    for (int32_t q = 0; q < cnt[v]; q++)
+                        if ((l[q] >> 6) == w) m |= 1ull << (l[q] & 63);
                 }
             }
             if (~m) {
@@ -318,32 +345,21 @@ int32_t greedy_color(const ees_desc *d, const std::vector<uint8_t> &excluded,
         color[i] = col;
         if (col + 1 > C) C = col + 1;
         for (int k = 0; k < nu; k++) {
-            NodeColors &s = nc[U[k]];
-            deg[U[k]]++;
-            if (s.big < 0 && s.cnt < 4) {
-                s.inl[s.cnt++] = col;
+            const int32_t v = U[k];
+            if (big[v] < 0) {
+                pool[lptr[v] + cnt[v]++] = col;
                 continue;
             }
-            if (s.big < 0) {
-                s.big = (int32_t)bits.size();
-                bits.emplace_back();
-                first_nonfull.push_back(0);
-                for (int q = 0; q < s.cnt; q++) {
-                    const int32_t cc = s.inl[q];
-                    if ((int64_t)bits[s.big].size() <= (cc >> 6)) bits[s.big].resize((cc >> 6) + 1, 0);
-                    bits[s.big][cc >> 6] |= 1ull << (cc & 63);
-                }
-                s.cnt = -1;
-            }
-            std::vector<uint64_t> &bv = bits[s.big];
+            cnt[v]++;
+            std::vector<uint64_t> &bv = bits[big[v]];
             if ((int64_t)bv.size() <= (col >> 6)) bv.resize((col >> 6) + 1, 0);
             bv[col >> 6] |= 1ull << (col & 63);
-            int32_t &f = first_nonfull[s.big];
+            int32_t &f = first_nonfull[big[v]];
             while (f < (int32_t)bv.size() && bv[f] == ~0ull) f++;
         }
     }
     max_node_deg = 0;
-    for (int32_t v = 0; v < d->n_nodes; v++) max_node_deg = std::max(max_node_deg, deg[v]);
+    for (int32_t v = 0; v < d->n_nodes; v++) max_node_deg = std::max(max_node_deg, cnt[v]);
     return N ? C : 0;
 }
 
@@ -889,10 +905,8 @@ ees_status build_gather(const ees_desc *d, ees_ctx *c, const std::vector<int32_t
     // scattered in netlist order (cfg3: its stores then cost 8x, form 0 keeps
     // the compact buffer and gathers by index); measured in profiles/r01_f_tile_ab.md
     g.form = scattered_topology(d, c, iptr) ? 0 : 1;
-    {
-        const char *f = std::getenv("EES_GATHER_FORM");     // experiments: force a form
-        if (f && (f[0] == '0' || f[0] == '1')) g.form = f[0] - '0';
-    }
+    if (d->flags & EES_SETUP_GATHER_FORM0) g.form = 0;      // layout override (ees.h)
+    if (d->flags & EES_SETUP_GATHER_FORM1) g.form = 1;
     c->st.gather_form = g.form;
     if (g.form == 0) {
         TRY(upload(c, const_cast<int32_t **>(&g.tidx), tidx.data(), tidx.size()));
@@ -920,10 +934,8 @@ ees_status build_tile(const ees_desc *d, ees_ctx *c, const std::vector<int32_t> 
     // loads cost more than the occupancy gains (form 0; measured: cfg3 1.6x
     // slower in form 1, cfg4 10% faster).
     int form = scattered_topology(d, c, iptr) ? 0 : 1;
-    {
-        const char *f = std::getenv("EES_TILE_FORM");       // experiments: force a form
-        if (f && (f[0] == '0' || f[0] == '1')) form = f[0] - '0';
-    }
+    if (d->flags & EES_SETUP_TILE_FORM0) form = 0;          // layout override (ees.h)
+    if (d->flags & EES_SETUP_TILE_FORM1) form = 1;
     int sms = 148, dev = 0;
     int grid = sms * tile_ctas(form);
     if (!c->host_only) {
@@ -971,14 +983,33 @@ ees_status build_tile(const ees_desc *d, ees_ctx *c, const std::vector<int32_t> 
     return EES_OK;
 }
 
+// Scratch of the tuning calls only: freed when tuning ends (not kept for the
+// context's lifetime like the layouts).
+struct TuneScratch {
+    double *x = nullptr, *A = nullptr, *b = nullptr;
+    cudaStream_t st = nullptr;
+    ~TuneScratch()
+    {
+        if (st) cudaStreamSynchronize(st);
+        cudaFree(x);
+        cudaFree(A);
+        cudaFree(b);
+        if (st) cudaStreamDestroy(st);
+    }
+};
+
 ees_status autotune(ees_ctx *c, bool full)
 {
-    double *x, *A, *b;
-    TRY(dalloc(c, &x, (size_t)c->n));
-    TRY(dalloc(c, &A, (size_t)c->nnz));
-    TRY(dalloc(c, &b, (size_t)c->n));
-    cudaStream_t st;
-    if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) return EES_ECUDA;
+    TuneScratch sc;
+    if (cudaMalloc(&sc.x, sizeof(double) * std::max(1, c->n)) != cudaSuccess ||
+        cudaMalloc(&sc.A, sizeof(double) * std::max<int64_t>(1, c->nnz)) != cudaSuccess ||
+        cudaMalloc(&sc.b, sizeof(double) * std::max(1, c->n)) != cudaSuccess) {
+        cudaGetLastError();
+        return EES_ENOMEM;
+    }
+    if (cudaStreamCreateWithFlags(&sc.st, cudaStreamNonBlocking) != cudaSuccess) return EES_ECUDA;
+    double *x = sc.x, *A = sc.A, *b = sc.b;
+    cudaStream_t st = sc.st;
     cudaMemsetAsync(x, 0, sizeof(double) * std::max(1, c->n), st);
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
@@ -1003,7 +1034,9 @@ ees_status autotune(ees_ctx *c, bool full)
         }
         return best_ms;
     };
-    const char *mode = std::getenv("EES_COLOR_MODE");   // debug knob: "launch" | "coop"
+    // layout override (ees.h): force the COLOR form instead of timing both
+    const char *mode = (c->setup_flags & EES_SETUP_COLOR_LAUNCH) ? "launch"
+                       : (c->setup_flags & EES_SETUP_COLOR_COOP) ? "coop" : nullptr;
     for (int32_t v = EES_COLOR; v <= (full ? EES_COLOR_BUF : EES_COLOR) && rc == EES_OK; v++) {
         double ms;
         if (v == EES_COLOR_BUF) {
@@ -1036,7 +1069,6 @@ ees_status autotune(ees_ctx *c, bool full)
     }
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
-    cudaStreamDestroy(st);
     if (full) c->variant = bestv;
     return rc;
 }
@@ -1053,6 +1085,7 @@ ees_status setup_impl(const ees_desc *d, ees_ctx *c)
     c->rails.assign(d->rails, d->rails + d->n_rails);
     c->gmin = d->gmin;
     c->rule = d->conflict_rule;
+    c->setup_flags = d->flags;
     const int64_t N = d->n_dev;
 
     std::vector<int64_t> iptr;

@@ -92,67 +92,102 @@ struct GatherK {
 };
 
 // TILE layout (ees_tile.cpp builds it; k_tile consumes it).  Rows are cut
-// into tiles; a tile's items are the FETs incident on its rows (boundary FETs
-// are copied into every tile they touch).  Each item's 16 contributions
-// (12 A pairs, 4 b rows) land in shared memory at slot p*kTileItems + item.
-// The tile's targets are segments of one contribution list: owned targets
-// (every contributor in this tile; ascending global id) then side entries
-// (this tile's part of a target shared by several tiles).  The list is cut
-// into kTileThreads equal chunks of K entries, so every thread sums the same
-// number of contributions in a fixed order (a balanced segmented sum); a
-// segment that crosses a chunk boundary is completed from the per-thread
-// carries in thread order.  Everything a tile needs except x and the A/b
-// values is one 16-byte-aligned blob that a TMA bulk copy (cp.async.bulk +
-// mbarrier) brings into shared memory, kStages tiles ahead:
-//   TileHdr
-//   items:   form 0: term int4[ni] | beta f64[ni] | v0 f64[3][ni] | model u8[ni]
-//            form 1: term int4[ni]; the rest of an item (beta, v0[3], model)
-//            is in tile-order HBM arrays (kTileItems slots per tile) that each
-//            thread loads one tile ahead into registers -- smaller stages, so
-//            5 CTAs per SM instead of 4 (pad 16)
-//   xg:      int32[n_x] global ids of the owned targets after the tile rows'
-//            CSR block [a0, a0+na) and b rows [b0, b0+nb) (heavy-row slices,
-//            heavy x heavy targets); owned target j is A[a0+j] (j < na),
-//            b[b0+j-na] (j < na+nb), else global target xg[j-na-nb]
-//   tw:      u32[kTileThreads] per thread: first segment id (low 16 bits) | the
-//            number of preceding chunks whose carries complete that segment
-//            (high 16 bits; 0 unless it continues from them and ends here)
-//   ent:     u16[K][kTileThreads] (thread-interleaved): byte offset 8*slot of the
-//            contribution in shared memory | kEntEnd on the
-//            last entry of a segment; padding points at the zero slot (pad 16)
-//   side:    SideEnt[n_sent] (pad 16)
+// into tiles of consecutive light rows; a tile's items are the FETs incident
+// on its rows (boundary FETs are copied into every tile they touch).  Each
+// item's 16 contributions (12 A pairs, 4 b rows) land in shared memory at
+// slot p*kTileItems + item.  A tile OWNS every target (A entry or b row) all
+// of whose contributors are among its items: the rows' CSR block, their b
+// rows, heavy-row slices (h, c) of its light columns c, and heavy x heavy
+// targets whose contributors all live in it; a target shared by several
+// tiles (heavy x heavy: rails, hub diagonals) is a SIDE target, to which the
+// tile contributes one part.
+//
+// The tile's reduction program lists its targets by contribution count
+// ("length class"): class c holds n_c targets of exactly L_c contributions,
+// each as a 32-bit destination and L_c entries (byte offsets of the
+// contributions in the tile's shared-memory slots).  A thread sums one target
+// in list order (fixed-length unrolled loops for L <= 4; a longer target is
+// summed by a group of cls_group(L) lanes, each a fixed strided subset, then
+// a fixed shuffle tree) and adds the sum to
+// its destination with ONE reduction (RED.ADD.F64): every owned target is
+// written by exactly one thread in exactly one CTA, so A_vals[k] + sum is
+// formed once and the result equals a plain read-modify-write (deterministic;
+// the SM loads no old value).  A side target's contributions in the tile are
+// cut into pieces of at most kSidePiece entries, each its own program target
+// and part (plain store), or, for the hot side targets (rails), a running
+// sum per CTA and piece index in shared memory, in tile order.  Classes are
+// processed back to back by the CTA's threads with the lane position
+// continuing across classes (cls[c].rot), so the threads' loads stay even.  Everything a tile needs except x
+// (and, in form 1, the item data) is one 16-byte-aligned blob that a TMA bulk
+// copy (cp.async.bulk + mbarrier) brings into shared memory, kStages tiles
+// ahead:
+//   TileHdr (64 B) | TileCls[n_cls] (16 B each)
+//   items:  form 0: term int4[ni] | beta f64[ni] | v0 f64[3][ni] | model u8[ni]
+//           form 1: term int4[ni]; beta, v0[3], model in tile-order HBM arrays
+//           (kTileItems slots per tile) loaded one tile ahead into registers
+//   side:   SideEnt[n_sent]
+//   dst:    int32[n_tgt]: per class, the destinations of its targets (>= 0:
+//           global target g = A index, or nnz + b row; < 0: side entry -1-dst)
+//   ent:    u16: per class c, entries [L_c][n_c] (k-major: lanes of a warp
+//           read consecutive u16)
 // Contributions of a FET whose source and bulk are one node (every PMOS of the
 // inverter configs) are merged at evaluation (DB into DS, BD into SD, BB into
 // SS, J[B] into J[S]) and the merged-away slots are not listed.
 constexpr int kTileItems = 128;      // max items (FET copies) per tile = threads per CTA
 constexpr int kTileThreads = 128;
 constexpr int kHeavyDeg = 64;        // nodes with more incident FETs are heavy
+constexpr int kMaxCls = 15;          // distinct target lengths per tile
+constexpr int kSidePiece = 4;        // side-target entries per piece (an unrolled class)
+constexpr int kHotPieces = 24;       // pieces of one hot target per tile
 // TILE forms (chosen at setup from the FET copy factor, ees_host.cpp):
-// stage bytes (one tile blob), item bytes in the blob, CTAs per SM
-__host__ __device__ constexpr int stage_max(int form) { return form ? 6144 : 10496; }
+// stage bytes (one tile blob), item bytes in the blob, shared-memory slot
+// buffers (2: one barrier per tile), CTAs per SM
+__host__ __device__ constexpr int stage_max(int form) { return form ? 7680 : 11264; }
 __host__ __device__ constexpr int item_blob_bytes(int form) { return form ? 16 : 49; }
-__host__ __device__ constexpr int tile_ctas(int form) { return form ? 5 : 4; }
+#ifndef EES_TILE_BUF1
+#define EES_TILE_BUF1 1
+#endif
+#ifndef EES_TILE_BUF0
+#define EES_TILE_BUF0 1
+#endif
+__host__ __device__ constexpr int tile_bufs(int form) { return form ? EES_TILE_BUF1 : EES_TILE_BUF0; }
+__host__ __device__ constexpr int tile_ctas(int form) { return form ? (tile_bufs(1) == 2 ? 4 : 5) : (tile_bufs(0) == 2 ? 3 : 4); }
 constexpr int kStages = 3;           // TMA pipeline depth (blobs in flight per CTA)
-constexpr int kSegMax = 768;         // owned targets + side entries per tile
-constexpr int kZeroSlot = 16 * kTileItems;   // s_c[kZeroSlot] == 0.0 (list padding)
-constexpr uint16_t kEntEnd = 0x8000;
-constexpr uint32_t kTwSid = 0xFFFFu;
+constexpr int kScSlots = 16 * kTileItems + 2;   // contribution slots per buffer (+16-byte pad)
 constexpr int64_t kSideInlineParts = 8192;   // up to this many parts: last CTA finalises
 constexpr int kMaxHot = 16;          // side targets pre-reduced per CTA (rails): parts = CTAs, not tiles
-static_assert(8 * kZeroSlot < kEntEnd, "entry byte offsets must fit 15 bits");
+static_assert(8 * kScSlots < 65536, "entry byte offsets must fit 16 bits");
+
+// Lanes that sum one target of length L together (a power of two): one for
+// L <= 4, then about four entries per lane, at most a warp.
+__host__ __device__ constexpr int cls_group(int L)
+{
+    return L <= 4 ? 1 : L <= 8 ? 2 : L <= 16 ? 4 : L <= 32 ? 8 : L <= 64 ? 16 : 32;
+}
+
+struct TileCls {
+    uint16_t len;                    // contributions per target
+    uint16_t n;                      // targets
+    uint16_t ent;                    // u16 index of the class's first entry in ent[]
+    uint16_t dst;                    // index of the class's first destination in dst[]
+    uint16_t rot;                    // lane groups of cls_group(len) threads used before the
+                                     // class, mod the groups per CTA (kTileThreads / cls_group)
+    uint16_t pad[3];
+};
+static_assert(sizeof(TileCls) == 16, "TileCls layout");
 
 struct TileHdr {
-    uint16_t n_items, n_own, n_x, n_sent, K, pad0;
-    int32_t a0, na, b0, nb;          // implicit owned targets: A[a0, a0+na), b[b0, b0+nb)
+    uint16_t n_items, n_cls, n_sent, n_tgt;
     uint32_t bytes;                  // blob size, multiple of 16
-    uint32_t off_x, off_tw, off_ent, off_side;   // byte offsets of the sections
-    uint32_t pad1[4];
+    uint32_t off_items, off_side, off_dst, off_ent;   // byte offsets of the sections
+    uint32_t pad1[9];
 };
 static_assert(sizeof(TileHdr) == 64, "TileHdr layout");
 
 struct SideEnt {
     int32_t sid;                     // side target
-    int32_t slot;                    // this tile's part slot in `part`, or -1-h for hot target h
+    int32_t slot;                    // this piece's part slot in `part`, or -1-(h*kHotPieces+q) for
+                                     // piece q of hot target h
 };
 
 struct TileK {
@@ -185,7 +220,7 @@ struct TileHost {
     int32_t n_tiles = 0, n_heavy = 0, n_side = 0;
     int64_t n_items = 0, n_owned = 0, n_side_entries = 0;
     int64_t n_parts = 0, hot_base = 0;
-    int64_t n_listed = 0, n_padded = 0;    // list entries, and with chunk padding
+    int64_t n_listed = 0, n_padded = 0;    // list entries, and with class padding
     int32_t blob_max = 0, n_hot = 0;
     int32_t grid = 1;                      // persistent CTAs the hot-part layout is made for
     std::vector<int64_t> blob_off;

@@ -183,10 +183,39 @@ __device__ __forceinline__ void merge_source_bulk(const int4 &T, Stamp &st, int3
 }
 
 // ---------------------------------------------------------------------------
-// ATOMIC: grid-stride over devices (netlist order), RED.F64 into A and b;
+// ATOMIC: grid-stride over devices (class order), RED.F64 into A and b;
 // rail entries reduced per block, one atomic per block and entry at the end.
 // All per-device loads (data + 12 slots) are issued before the x gather.
+// Hot entries: lanes of a warp are consecutive devices, and
+// devices that share an entry are mostly consecutive in the netlist (a hub's
+// fanout, an inverter's N and P), so for each pair / row a warp first checks
+// (one shuffle + vote) whether a lane repeats its left neighbour's entry; if
+// so, a segmented warp scan sums each run of equal entries and only the run's
+// last lane issues the RED -- one same-address RED per run instead of one per
+// lane (the L2 serialises same-address atomics, P:31's lock analogue).
 // ---------------------------------------------------------------------------
+__device__ __forceinline__ void red_run(double *base, int32_t k, double v, int lane)
+{
+    const int32_t kp = __shfl_up_sync(0xffffffffu, k, 1);
+    const bool dup = lane > 0 && k >= 0 && k == kp;
+    if (__any_sync(0xffffffffu, dup)) {
+        const int32_t kn = __shfl_down_sync(0xffffffffu, k, 1);
+        bool f = !dup;                                   // lane has reached its run's head
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const double t = __shfl_up_sync(0xffffffffu, v, d);
+            const bool ft = __shfl_up_sync(0xffffffffu, f, d);
+            if (lane >= d && !f) {
+                v += t;
+                f = ft;
+            }
+        }
+        if (k >= 0 && (lane == 31 || kn != k)) atomicAdd(base + k, v);
+    } else if (k >= 0) {
+        atomicAdd(base + k, v);
+    }
+}
+
 template <bool kRep>
 __global__ void __launch_bounds__(kBlock, 4) k_atomic(DevK dv, CallK P)
 {
@@ -195,13 +224,14 @@ __global__ void __launch_bounds__(kBlock, 4) k_atomic(DevK dv, CallK P)
     extern __shared__ double s_acc[];   // [warps][n_rail_entries]
     load_call_smem(P, s_cards, s_railx);
     const int nw = blockDim.x >> 5;
+    const int lane = threadIdx.x & 31;
     for (int k = threadIdx.x; k < nw * P.n_rail_entries; k += blockDim.x) s_acc[k] = 0.0;
     __syncthreads();
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    // warp-uniform trip count so rail_accumulate's shuffles are full-warp
+    // warp-uniform trip count so the run scans' and rail_accumulate's shuffles are full-warp
     const int64_t base0 = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31);
     for (int64_t base = base0; base < dv.N; base += stride) {
-        const int64_t i = base + (threadIdx.x & 31);
+        const int64_t i = base + lane;
         const bool valid = i < dv.N;
         int4 T = make_int4(-1, -1, -1, -1);
         Stamp st;
@@ -228,16 +258,19 @@ __global__ void __launch_bounds__(kBlock, 4) k_atomic(DevK dv, CallK P)
             eval_fet<kRep>(s_cards[m], beta, P.gmin, VD, VG, VS, a0, a1, a2, st, P.work);
             tc[0] = T.x; tc[1] = T.y; tc[2] = T.z; tc[3] = T.w;
             merge_source_bulk(T, st, slot, tc);
-#pragma unroll
-            for (int p = 0; p < NPAIR; p++)
-                if (slot[p] >= 0) atomicAdd(P.A + slot[p], st.y[p]);
-#pragma unroll
-            for (int a = 0; a < 4; a++)
-                if (tc[a] >= 0) atomicAdd(P.b + tc[a], st.j[a]);
         } else {
 #pragma unroll
-            for (int p = 0; p < NPAIR; p++) slot[p] = -1;
+            for (int p = 0; p < NPAIR; p++) {
+                slot[p] = -1;
+                st.y[p] = 0.0;
+            }
+#pragma unroll
+            for (int a = 0; a < 4; a++) st.j[a] = 0.0;
         }
+#pragma unroll
+        for (int p = 0; p < NPAIR; p++) red_run(P.A, slot[p], st.y[p], lane);
+#pragma unroll
+        for (int a = 0; a < 4; a++) red_run(P.b, tc[a], st.j[a], lane);
         if (P.n_rail_entries) rail_accumulate(P, slot, tc, st, valid, s_acc);
     }
     if (P.n_rail_entries) {
@@ -628,11 +661,12 @@ __global__ void __launch_bounds__(kBlock) k_accept_soa(const int4 *term, int64_t
 __global__ void __launch_bounds__(kTileThreads) k_accept_tile(TileK tk, CallK P, double *item_v0)
 {
     unsigned char *b = const_cast<unsigned char *>(tk.blob) + tk.blob_off[blockIdx.x];
-    const int ni = reinterpret_cast<const TileHdr *>(b)->n_items;
-    const int4 *term = reinterpret_cast<const int4 *>(b + sizeof(TileHdr));
+    const TileHdr *h = reinterpret_cast<const TileHdr *>(b);
+    const int ni = h->n_items;
+    const int4 *term = reinterpret_cast<const int4 *>(b + h->off_items);
     // form 1: v0[3] per item in the tile-order array; form 0: v0[3][ni] in the blob
     double *v0 = item_v0 ? item_v0 + (int64_t)blockIdx.x * kTileItems * 3
-                         : reinterpret_cast<double *>(b + sizeof(TileHdr) + 16 * (size_t)ni) + ni;
+                         : reinterpret_cast<double *>(b + h->off_items + 16 * (size_t)ni) + ni;
     const int s1 = item_v0 ? 3 : 1, s2 = item_v0 ? 1 : ni;     // item stride, component stride
     for (int i = threadIdx.x; i < ni; i += blockDim.x) {
         const int4 T = term[i];
@@ -1087,19 +1121,27 @@ cudaError_t launch_count_conflicts(const int32_t *cnt, int64_t n, unsigned long 
 }
 
 // ---------------------------------------------------------------------------
-// TILE (deterministic, one launch): one CTA per row tile.
-//  0. thread 0 starts a TMA bulk copy (cp.async.bulk + mbarrier) of the tile's
-//     owned-target program (runs, list starts, slot lists) into shared memory;
-//  1. every thread evaluates one item (FET copy) and stages its 16
-//     contributions in shared memory; meanwhile, once the program has landed,
-//     each thread prefetches the current A/b values of the targets it owns;
-//  2. each owned target (all contributors in this tile) sums its slot list in
-//     list order and stores value + sum -- a plain store, no other CTA writes it;
-//  3. targets shared by several tiles (heavy x heavy entries: rails, hubs):
-//     one thread per (tile, target) sums the tile's part and stores it; the
-//     thread that brings the target's arrival counter to its part count has
-//     its warp sum all parts in part order (fixed lane stride + shuffle tree)
-//     and apply the result, then resets the counter.
+// TILE (deterministic, one launch; +1 when side targets are many): persistent
+// CTAs walk the row tiles blockIdx.x, +gridDim.x, ... (layout and the
+// ownership rule in ees_internal.h).  Per tile t:
+//   eval    each thread evaluates one item (FET copy) and stores its 16
+//           contributions in shared memory (one of tile_bufs(form) slot
+//           buffers); then it gathers the item data and x values of tile t+G,
+//           whose blob the TMA brought in a tile earlier, so their latency
+//           hides behind the reduction;
+//   B1      contributions complete, and every thread is done with tile t-G ->
+//           thread 0 refills tile t-G's stage with tile t+(kStages-1)G;
+//   reduce  per length class, each thread sums whole targets (fixed-length
+//           unrolled loops, list order) and adds each sum to its destination
+//           with one RED: A and b entries owned by this tile receive exactly
+//           one addition each, so the result equals a plain read-modify-write
+//           and no old value is loaded by the SM.  Long targets: one warp
+//           each (lane-strided, fixed shuffle tree).  Side targets: the part
+//           goes to its slot (plain store) or, for the hot ones (rails), into
+//           the CTA's running sum in shared memory (tile order);
+//   (B0)    with one slot buffer, a barrier before the next evaluation.
+// After the last tile, hot partials are stored per CTA, and side targets are
+// summed in part order by the last CTA (few parts) or k_side_final.
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void *p)
 {
@@ -1139,82 +1181,28 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase)
         : "memory");
 }
 
-constexpr int kSlots = kZeroSlot + 2;          // 16 contributions per item + the zero slot (+pad)
 template <int kForm>
-constexpr size_t tile_smem() { return sizeof(double) * (kSlots + kSegMax + kTileThreads) + kStages * (size_t)stage_max(kForm); }
-
-// View of one staged tile blob (layout in ees_internal.h): only the blob's
-// shared-memory address lives in registers; header fields and section
-// pointers are read / derived on use.
-struct TileView {
-    const unsigned char *b;
-    __device__ __forceinline__ const TileHdr &hdr() const { return *reinterpret_cast<const TileHdr *>(b); }
-    __device__ __forceinline__ const int4 *term() const
-    {
-        return reinterpret_cast<const int4 *>(b + sizeof(TileHdr));
-    }
-    // form 0: the item data after the terms
-    __device__ __forceinline__ const double *beta(int ni) const
-    {
-        return reinterpret_cast<const double *>(b + sizeof(TileHdr) + 16 * ni);
-    }
-    __device__ __forceinline__ const uint8_t *model(int ni) const
-    {
-        return b + sizeof(TileHdr) + 16 * ni + 32 * ni;
-    }
-    __device__ __forceinline__ const int32_t *xg() const
-    {
-        return reinterpret_cast<const int32_t *>(b + hdr().off_x);
-    }
-    __device__ __forceinline__ const uint32_t *tw() const
-    {
-        return reinterpret_cast<const uint32_t *>(b + hdr().off_tw);
-    }
-    __device__ __forceinline__ const uint16_t *ent() const
-    {
-        return reinterpret_cast<const uint16_t *>(b + hdr().off_ent);
-    }
-    __device__ __forceinline__ const SideEnt *sents() const
-    {
-        return reinterpret_cast<const SideEnt *>(b + hdr().off_side);
-    }
-};
-
-__device__ __forceinline__ TileView tile_view(const unsigned char *blob) { return TileView{blob}; }
-
-// Address of owned target j (< n_own): the tile rows' CSR block, their b
-// rows, then the explicit ids.
-__device__ __forceinline__ double *owned_ptr(const TileView &v, const TileK &tk, const CallK &P, int j)
+constexpr size_t tile_smem()
 {
-    const TileHdr &h = v.hdr();
-    const int na = h.na, nab = na + h.nb;
-    if (j < na) return P.A + h.a0 + j;
-    if (j < nab) return P.b + h.b0 + (j - na);
-    const int32_t g = v.xg()[j - nab];
-    return g < tk.nnz ? P.A + g : P.b + (g - tk.nnz);
+    return sizeof(double) * kScSlots * tile_bufs(kForm) + kStages * (size_t)stage_max(kForm);
 }
 
-// What a thread gathers from global memory for one tile: its item's node
-// voltages and the addresses and current values of the owned targets it
-// writes (the first kTilePrefetch per thread; the rest take an RMW).  The
-// A/b pointer per target, computed once here, measured faster than deriving
-// the three target ranges again at the stores (cfg3 440 vs 585 us).
-constexpr int kTilePrefetch = 4;
+// What a thread gathers from global memory one tile ahead: its item's node
+// voltages and (form 1) the item data from the tile-order arrays.
 struct TileRegs {
     double VD, VG, VS;
-    double beta, v0a, v0b, v0c;      // the item's data (HBM, tile order)
+    double beta, v0a, v0b, v0c;
     int model;
-    double *dst[kTilePrefetch];
-    double pre[kTilePrefetch];
 };
 
 template <int kForm>
-__device__ __forceinline__ void tile_gather(const TileView &v, int32_t tile, const TileK &tk,
+__device__ __forceinline__ void tile_gather(const unsigned char *blob, int32_t tile, const TileK &tk,
                                             const CallK &P, TileRegs &R)
 {
     const int tid = threadIdx.x;
+    const TileHdr *h = reinterpret_cast<const TileHdr *>(blob);
     R.VD = R.VG = R.VS = 0.0;
-    if (tid < v.hdr().n_items) {
+    if (tid < h->n_items) {
         if (kForm == 1) {
             const int64_t q = (int64_t)tile * kTileItems + tid;
             R.beta = __ldg(tk.item_beta + q);
@@ -1223,21 +1211,85 @@ __device__ __forceinline__ void tile_gather(const TileView &v, int32_t tile, con
             R.v0c = __ldg(tk.item_v0 + 3 * q + 2);
             R.model = __ldg(tk.item_model + q);
         }
-        const int4 T = v.term()[tid];
+        const int4 T = reinterpret_cast<const int4 *>(blob + h->off_items)[tid];
         R.VD = T.x >= 0 ? __ldg(P.x + T.x) : 0.0;
         R.VG = T.y >= 0 ? __ldg(P.x + T.y) : 0.0;
         R.VS = T.z >= 0 ? __ldg(P.x + T.z) : 0.0;
     }
+}
+
+// FP64 reduction without a result (RED.E.ADD.F64): fire and forget
+__device__ __forceinline__ void red_add(double *p, double v)
+{
+    asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+
+// Destination of one target (ees_internal.h): g >= 0 the global target --
+// one RED, the entry's only addition this call; g < 0 a side piece -- its
+// part slot (plain store, ordered by the ticket) or the CTA's running sum of
+// a hot target's piece index (one writer per tile).
+struct TileOut {
+    double *A, *Bm;            // A, and b - nnz (so that b row r is Bm + nnz + r)
+    int32_t nnz;
+};
+
+__device__ __forceinline__ void tile_put(const SideEnt *sents, const TileOut &o, const TileK &tk, double *s_hot,
+                                         int32_t g, double v)
+{
+    if (g >= 0) {
+        red_add((g < o.nnz ? o.A : o.Bm) + g, v);
+    } else {
+        const SideEnt se = sents[-1 - g];
+        if (se.slot >= 0) tk.part[se.slot] = v;
+        else s_hot[-1 - se.slot] += v;
+    }
+}
+
+// One short class (L <= 4, unrolled): targets k = rot-shifted thread index,
+// +kTileThreads, ...; dst[n], entries [L][n] (byte offsets into the slot
+// buffer), summed in list order.
+template <int L>
+__device__ __forceinline__ void tile_cls(int k, int n, int /*len*/, const int32_t *dst, const uint16_t *ent,
+                                         const unsigned char *sc, const SideEnt *sents, const TileOut &o,
+                                         const TileK &tk, double *s_hot)
+{
+    auto val = [&](int p, int k2) { return *reinterpret_cast<const double *>(sc + ent[p * n + k2]); };
+    for (; k < n; k += kTileThreads) {
+        const int32_t g = dst[k];
+        double v = val(0, k);
 #pragma unroll
-    for (int k = 0; k < kTilePrefetch; k++) {
-        const int j = tid + k * kTileThreads;
-        R.dst[k] = j < v.hdr().n_own ? owned_ptr(v, tk, P, j) : nullptr;
-        R.pre[k] = R.dst[k] ? *R.dst[k] : 0.0;
+        for (int p = 1; p < L; p++) v += val(p, k);
+        tile_put(sents, o, tk, s_hot, g, v);
+    }
+}
+
+// A class of longer targets (L > 4): a group of gs = cls_group(L) lanes per
+// target, lane j summing entries j, j+gs, ... in order, then a fixed xor
+// shuffle tree within the group; the group's first lane puts the sum.  All
+// lanes of a warp run the same number of iterations (shuffles need them).
+__device__ __forceinline__ void tile_cls_group(const TileCls c, const int32_t *dst, const uint16_t *ent,
+                                               const unsigned char *sc, const SideEnt *sents, const TileOut &o,
+                                               const TileK &tk, double *s_hot)
+{
+    const int L = c.len, n = c.n;
+    const int gs = cls_group(L), ng = kTileThreads / gs;
+    const int gi = (int)threadIdx.x / gs, lj = (int)threadIdx.x & (gs - 1);
+    const int k0 = (gi - (int)c.rot) & (ng - 1);
+    const int mine = k0 < n ? (n - 1 - k0) / ng + 1 : 0;
+    const int iters = __reduce_max_sync(0xffffffffu, mine);
+    for (int it = 0; it < iters; it++) {
+        const int k = k0 + it * ng;
+        const bool act = k < n;
+        double s = 0.0;
+        if (act)
+            for (int p = lj; p < L; p += gs) s += *reinterpret_cast<const double *>(sc + ent[p * n + k]);
+        for (int off = gs >> 1; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+        if (act && lj == 0) tile_put(sents, o, tk, s_hot, dst[k], s);
     }
 }
 
 // Fixed-order sum of one side target's parts by a whole warp (fixed lane
-// stride, four loads in flight per lane, shuffle tree).
+// stride, eight loads in flight per lane, shuffle tree).
 __device__ __forceinline__ void side_finish(const TileK &tk, const CallK &P, int32_t sid, int lane)
 {
     const int32_t q0 = __ldg(tk.sd_part + 2 * sid), q1 = __ldg(tk.sd_part + 2 * sid + 1);
@@ -1259,33 +1311,15 @@ __device__ __forceinline__ void side_finish(const TileK &tk, const CallK &P, int
     if (lane == 0) *dst = pre + u;
 }
 
-// ---------------------------------------------------------------------------
-// TILE (deterministic, one launch, +1 for many side targets): persistent CTAs
-// walk the tiles blockIdx.x, +gridDim.x, ...  Per tile t:
-//   eval   each thread evaluates one item (FET copy) from the staged blob and
-//          stores its 16 contributions in shared memory; then it gathers the
-//          x values and current A/b values of tile t+1 (whose blob is already
-//          in shared memory) so their latency hides behind the sums;
-//   B1     contributions complete; the stage of tile t-1 is free -> thread 0
-//          issues the TMA bulk copy of tile t-1+kStages*G into it;
-//   sums   balanced segmented sum: thread j adds its K list entries in order,
-//          stores a segment's sum at its end, its trailing partial as a carry;
-//   B2     fix-up: a segment that began in earlier chunks adds their carries
-//          (nearest first; fixed order);
-//   B3     write: owned target j -> value + sum (a plain store, no other CTA
-//          writes it, coalesced along runs); side entries -> part slots, or
-//          the CTA's hot partial (rails) in tile order.
-// After the last tile, hot partials are stored per CTA, and side targets are
-// summed in part order by the last CTA (few parts) or k_side_final.
-// ---------------------------------------------------------------------------
 __device__ __forceinline__ unsigned long long globaltimer()
 {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
-// slots: 0 start, 1 first blob staged, 2+4*it .. 5+4*it per tile (while they
-// stay below kTraceSlots-2), kTraceSlots-2 side ticket, kTraceSlots-1 end
+// slots: 0 start, 1 first blob staged, 2+2*it evaluated (next tile's gathers
+// issued), 3+2*it reduced and written (while below kTraceSlots-2),
+// kTraceSlots-2 side ticket, kTraceSlots-1 end
 #define TILE_TRACE_AT(slot, limit)                                                  \
     do {                                                                            \
         if (kTrace && tid == 0 && (slot) < (limit))                                 \
@@ -1297,32 +1331,35 @@ __device__ __forceinline__ unsigned long long globaltimer()
 template <bool kTrace, bool kRep, int kForm>
 __global__ void __launch_bounds__(kTileThreads, tile_ctas(kForm)) k_tile(TileK tk, CallK P)
 {
+    constexpr int kBuf = tile_bufs(kForm);
+    constexpr int kStage = stage_max(kForm);
     extern __shared__ __align__(16) unsigned char smem[];
-    double *s_c = reinterpret_cast<double *>(smem);          // [16][kTileItems] + zero slot
-    double *s_seg = s_c + kSlots;                            // [kSegMax] segment sums
-    double *s_carry = s_seg + kSegMax;                       // [kTileThreads]
-    unsigned char *s_stage = reinterpret_cast<unsigned char *>(s_carry + kTileThreads);
+    unsigned char *s_c = smem;                                           // [kBuf][kScSlots] doubles
+    unsigned char *s_stage = smem + sizeof(double) * kScSlots * kBuf;    // [kStages][kStage]
     __shared__ CardK s_cards[EES_MAX_MODELS];
     __shared__ __align__(8) uint64_t s_bar[kStages];
-    __shared__ double s_hot[kMaxHot], s_hot_pre[kMaxHot];
+    __shared__ double s_hot[kMaxHot * kHotPieces], s_hot_pre[kMaxHot];
     __shared__ double *s_hot_dst[kMaxHot];
     __shared__ int s_last;
-    const int tid = threadIdx.x, lane = tid & 31;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int32_t G = gridDim.x;
-    if (tid < kMaxHot) s_hot[tid] = 0.0;
+    for (int k = tid; k < kMaxHot * kHotPieces; k += kTileThreads) s_hot[k] = 0.0;
     if (tid < tk.n_hot) {            // hot side targets: only the finisher writes them
         const int32_t g = tk.hot_gid[tid];
         double *d = g < tk.nnz ? P.A + g : P.b + (g - tk.nnz);
         s_hot_dst[tid] = d;
         s_hot_pre[tid] = *d;
     }
-    if (tid == 0) s_c[kZeroSlot] = 0.0;
     auto issue = [&](int32_t tile, int stage) {
         const int64_t off = tk.blob_off[tile];
         const uint32_t bytes = (uint32_t)(tk.blob_off[tile + 1] - off);
         mbar_expect_tx(&s_bar[stage], bytes);
-        tma_bulk_g2s(s_stage + (size_t)stage * stage_max(kForm), tk.blob + off, bytes, &s_bar[stage]);
+        tma_bulk_g2s(s_stage + (size_t)stage * kStage, tk.blob + off, bytes, &s_bar[stage]);
     };
+    TileOut out;
+    out.A = P.A;
+    out.Bm = P.b - tk.nnz;
+    out.nnz = (int32_t)tk.nnz;                    // < 2^31 (setup)
     const int32_t t0 = blockIdx.x;
     if (tid == 0) {
         for (int k = 0; k < kStages; k++) mbar_init(&s_bar[k], 1);
@@ -1335,31 +1372,32 @@ __global__ void __launch_bounds__(kTileThreads, tile_ctas(kForm)) k_tile(TileK t
     uint32_t parity = 0;                 // bit k: phase of s_bar[k]
     int it = 0;
     int stage = 0;
-    TileRegs cur, nxt;
-    TileView v;
+    TileRegs ra, rb;
     if (t0 < tk.n_tiles) {
         mbar_wait(&s_bar[0], 0);
         parity ^= 1u;
-        v = tile_view(s_stage);
-        tile_gather<kForm>(v, t0, tk, P, cur);
+        tile_gather<kForm>(s_stage, t0, tk, P, ra);
     }
     TILE_TRACE(1);
-    const unsigned char *s_cb = reinterpret_cast<const unsigned char *>(s_c);
-    for (int32_t t = t0; t < tk.n_tiles; t += G, it++) {
-        const int32_t tn = t + G;
-        const int sn = stage + 1 == kStages ? 0 : stage + 1;
-        const int ni = v.hdr().n_items;
+    // one tile; the two register sets alternate (no copies between tiles)
+    auto step = [&](int32_t t, const TileRegs &cur, TileRegs &nxt) {
+        const unsigned char *blob = s_stage + (size_t)stage * kStage;
+        const TileHdr *h = reinterpret_cast<const TileHdr *>(blob);
+        unsigned char *sc = s_c + (kBuf == 2 ? (size_t)(it & 1) * 8 * kScSlots : 0);
+        double *scd = reinterpret_cast<double *>(sc);
+        const int ni = h->n_items;
         if (tid < ni) {
             Stamp st;
             if (kForm == 1) {
                 eval_fet<kRep>(s_cards[cur.model], cur.beta, P.gmin, cur.VD, cur.VG, cur.VS, cur.v0a, cur.v0b,
                                cur.v0c, st, P.work);
             } else {
-                const double *bt = v.beta(ni);
-                eval_fet<kRep>(s_cards[v.model(ni)[tid]], bt[tid], P.gmin, cur.VD, cur.VG, cur.VS, bt[ni + tid],
+                const double *bt = reinterpret_cast<const double *>(blob + h->off_items + 16 * ni);
+                const uint8_t *md = blob + h->off_items + 48 * ni;
+                eval_fet<kRep>(s_cards[md[tid]], bt[tid], P.gmin, cur.VD, cur.VG, cur.VS, bt[ni + tid],
                                bt[2 * ni + tid], bt[3 * ni + tid], st, P.work);
             }
-            const int4 T = v.term()[tid];
+            const int4 T = reinterpret_cast<const int4 *>(blob + h->off_items)[tid];
             if (T.z == T.w && T.z != -1) {        // source tied to bulk: one entry each (ees_internal.h)
                 st.y[DS] += st.y[DB];
                 st.y[SD] += st.y[BD];
@@ -1367,86 +1405,68 @@ __global__ void __launch_bounds__(kTileThreads, tile_ctas(kForm)) k_tile(TileK t
                 st.j[2] += st.j[3];
             }
 #pragma unroll
-            for (int p = 0; p < NPAIR; p++) s_c[p * kTileItems + tid] = st.y[p];
+            for (int p = 0; p < NPAIR; p++) scd[p * kTileItems + tid] = st.y[p];
 #pragma unroll
-            for (int a = 0; a < 4; a++) s_c[(NPAIR + a) * kTileItems + tid] = st.j[a];
+            for (int a = 0; a < 4; a++) scd[(NPAIR + a) * kTileItems + tid] = st.j[a];
         }
         // next tile: its blob was issued >= one tile ago; start its gathers now
-        TileView vn;
+        const int32_t tn = t + G;
+        const int sn = stage + 1 == kStages ? 0 : stage + 1;
         if (tn < tk.n_tiles) {
             mbar_wait(&s_bar[sn], (parity >> sn) & 1u);
             parity ^= 1u << sn;
-            vn = tile_view(s_stage + (size_t)sn * stage_max(kForm));
-            tile_gather<kForm>(vn, tn, tk, P, nxt);
+            tile_gather<kForm>(s_stage + (size_t)sn * kStage, tn, tk, P, nxt);
         }
-        TILE_TRACE(2 + 4 * it);
+        TILE_TRACE(2 + 2 * it);
         __syncthreads();                                        // B1
         if (tid == 0 && it > 0) {
             const int32_t tr = t - G + kStages * G;             // refill the stage of tile t-G
             if (tr < tk.n_tiles) issue(tr, stage == 0 ? kStages - 1 : stage - 1);
         }
-        // balanced segmented sum (entries are byte offsets into s_c | kEntEnd);
-        // four entries' loads are issued before their adds
-        const uint32_t w = v.tw()[tid];
         {
-            const int K = v.hdr().K;
-            const uint16_t *e = v.ent() + tid;
-            double *sp = s_seg + (w & kTwSid);
-            double s = 0.0;
-            auto val = [&](uint32_t x) { return *reinterpret_cast<const double *>(s_cb + (x & 0x7FFFu)); };
-            int k = 0;
-            for (; k + 4 <= K; k += 4) {
-                const uint32_t x0 = e[k * kTileThreads], x1 = e[(k + 1) * kTileThreads];
-                const uint32_t x2 = e[(k + 2) * kTileThreads], x3 = e[(k + 3) * kTileThreads];
-                const double v0 = val(x0), v1 = val(x1), v2 = val(x2), v3 = val(x3);
-                s += v0;
-                if (x0 & kEntEnd) { *sp++ = s; s = 0.0; }
-                s += v1;
-                if (x1 & kEntEnd) { *sp++ = s; s = 0.0; }
-                s += v2;
-                if (x2 & kEntEnd) { *sp++ = s; s = 0.0; }
-                s += v3;
-                if (x3 & kEntEnd) { *sp++ = s; s = 0.0; }
+            const TileCls *cls = reinterpret_cast<const TileCls *>(blob + sizeof(TileHdr));
+            const int32_t *dst = reinterpret_cast<const int32_t *>(blob + h->off_dst);
+            const uint16_t *ent = reinterpret_cast<const uint16_t *>(blob + h->off_ent);
+            const SideEnt *sents = reinterpret_cast<const SideEnt *>(blob + h->off_side);
+            const int ncl = h->n_cls;
+            for (int ci = 0; ci < ncl; ci++) {
+                const TileCls c = cls[ci];
+                const uint16_t *e = ent + c.ent;
+                const int32_t *dc = dst + c.dst;
+                if (c.len > 4) {                               // warp-uniform
+                    tile_cls_group(c, dc, e, sc, sents, out, tk, s_hot);
+                    continue;
+                }
+                const int k0 = ((int)threadIdx.x - (int)c.rot) & (kTileThreads - 1);
+                if (k0 >= c.n) continue;                       // no target of this class here
+                switch (c.len) {
+                case 1: tile_cls<1>(k0, c.n, 1, dc, e, sc, sents, out, tk, s_hot); break;
+                case 2: tile_cls<2>(k0, c.n, 2, dc, e, sc, sents, out, tk, s_hot); break;
+                case 3: tile_cls<3>(k0, c.n, 3, dc, e, sc, sents, out, tk, s_hot); break;
+                default: tile_cls<4>(k0, c.n, 4, dc, e, sc, sents, out, tk, s_hot); break;
+                }
             }
-            for (; k < K; k++) {
-                const uint32_t x0 = e[k * kTileThreads];
-                s += val(x0);
-                if (x0 & kEntEnd) { *sp++ = s; s = 0.0; }
-            }
-            s_carry[tid] = s;
         }
-        TILE_TRACE(3 + 4 * it);
-        __syncthreads();                                        // B2
-        if (w >> 16) {                 // this chunk ends a segment begun in earlier chunks
-            const int chain = (int)(w >> 16);
-            double acc = s_carry[tid - 1];
-            for (int c = 2; c <= chain; c++) acc += s_carry[tid - c];
-            s_seg[w & kTwSid] += acc;
-        }
-        __syncthreads();                                        // B3
-        TILE_TRACE(4 + 4 * it);
-        const int n_own = v.hdr().n_own;
-#pragma unroll
-        for (int k = 0; k < kTilePrefetch; k++)
-            if (cur.dst[k]) *cur.dst[k] = cur.pre[k] + s_seg[tid + k * kTileThreads];
-        for (int j = tid + kTilePrefetch * kTileThreads; j < n_own; j += kTileThreads)
-            *owned_ptr(v, tk, P, j) += s_seg[j];
-        // side parts (plain stores; ordered by the fence + ticket below); a hot
-        // target appears at most once per tile, so one thread owns s_hot[h] here
-        for (int e = tid; e < v.hdr().n_sent; e += kTileThreads) {
-            const SideEnt se = v.sents()[e];
-            const double part = s_seg[n_own + e];
-            if (se.slot >= 0) tk.part[se.slot] = part;
-            else s_hot[-1 - se.slot] += part;
-        }
-        TILE_TRACE(5 + 4 * it);
+        TILE_TRACE(3 + 2 * it);
+        if (kBuf == 1) __syncthreads();                         // B0: slots free for the next tile
         stage = sn;
-        v = vn;
-        cur = nxt;
+        it++;
+    };
+    for (int32_t t = t0; t < tk.n_tiles;) {
+        step(t, ra, rb);
+        t += G;
+        if (t >= tk.n_tiles) break;
+        step(t, rb, ra);
+        t += G;
     }
     if (tk.n_side) {
         __syncthreads();
-        for (int h = tid; h < tk.n_hot; h += kTileThreads) tk.part[tk.hot_base + (int64_t)h * G + blockIdx.x] = s_hot[h];
+        for (int h = tid; h < tk.n_hot; h += kTileThreads) {
+            double v = 0.0;
+#pragma unroll
+            for (int q = 0; q < kHotPieces; q++) v += s_hot[h * kHotPieces + q];   // piece order
+            tk.part[tk.hot_base + (int64_t)h * G + blockIdx.x] = v;
+        }
         if (tk.side_inline) {
             __threadfence();
             __syncthreads();
@@ -1457,7 +1477,7 @@ __global__ void __launch_bounds__(kTileThreads, tile_ctas(kForm)) k_tile(TileK t
                 __threadfence();
                 // hot targets (one part per CTA): a warp each, fixed lane
                 // stride, eight loads in flight per lane, fixed shuffle tree
-                for (int h = tid >> 5; h < tk.n_hot; h += kTileThreads >> 5) {
+                for (int h = warp; h < tk.n_hot; h += kTileThreads >> 5) {
                     const double *pp = tk.part + tk.hot_base + (int64_t)h * G;
                     double u = 0.0;
                     for (int q0 = 0; q0 < G; q0 += 256) {
@@ -1473,7 +1493,7 @@ __global__ void __launch_bounds__(kTileThreads, tile_ctas(kForm)) k_tile(TileK t
                     u = warp_sum(u);
                     if (lane == 0) *s_hot_dst[h] = s_hot_pre[h] + u;
                 }
-                for (int32_t sid = tid >> 5; sid < tk.n_side; sid += kTileThreads >> 5)
+                for (int32_t sid = warp; sid < tk.n_side; sid += kTileThreads >> 5)
                     if (__ldg(tk.sd_part + 2 * sid) < tk.hot_base || tk.n_hot == 0) side_finish(tk, P, sid, lane);
                 if (tid == 0) *tk.done = 0;
             }

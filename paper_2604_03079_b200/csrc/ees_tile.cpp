@@ -13,6 +13,7 @@
 // colour.
 #include <algorithm>
 #include <cstring>
+#include <functional>
 #include <numeric>
 #include <vector>
 
@@ -23,14 +24,19 @@ namespace ees {
 namespace {
 constexpr int32_t kUnset = -1;
 constexpr int32_t kSide = -2;
-// Upper bound of a tile's blob while it is being formed: items (49 B + 2 B
-// per listed contribution), one padding entry per owned target nobody stamps
-// (2 B), explicit ids of heavy-row slice targets (4 B), heavy x heavy targets
-// (4 B id or an 8 B side entry) -- plus the fixed per-tile parts: header,
-// thread words (512 B), list padding to whole chunks (< 256 B) and the
-// padding of four sections.
-constexpr int64_t kBlobFixed = 64 + 512 + 256 + 64;
-constexpr int64_t kOwnMax = kSegMax;   // owned targets + side entries (s_seg capacity)
+// Upper bound of a tile's blob while it is being formed.  Owned targets are
+// counted exactly: a target with L contributions costs a 4 B destination and
+// 2 B per entry; each distinct length in the tile costs an 8 B class header.
+// Items cost item_blob_bytes(form).  Heavy x heavy targets (owned by their
+// home tile, or side) are bounded: owned, a target with c contributions costs
+// 4 + 2c B and the class header of length c (counted like an owned target's);
+// side, at most ceil(c / kSidePiece) pieces of 4 B destination + 8 B side
+// entry + 2 B per entry, whose lengths (1..kSidePiece) take at most
+// kSidePiece class headers per tile (reserved in kBlobFixed) -> 12 B per
+// distinct target + 2 + 12 / kSidePiece = 5 B per contribution covers both.
+// Fixed: header + five section paddings + the side-piece class headers.
+constexpr int64_t kBlobFixed = (int64_t)sizeof(TileHdr) + 5 * 16 + kSidePiece * (int64_t)sizeof(TileCls);
+constexpr int64_t kHHTarget = 12, kHHContrib = 5;
 size_t pad16(size_t x) { return (x + 15) & ~(size_t)15; }
 }  // namespace
 
@@ -41,7 +47,6 @@ bool build_tile_host(int form, int64_t N, int32_t n_nodes, int32_t n, int64_t nn
                      const double *beta, const double *vprev, const int32_t *model, int32_t grid,
                      TileHost &out)
 {
-    static_assert(kOwnMax > 64, "tile budget too small");
     const int64_t kStageMax = stage_max(form), kItemBlobBytes = item_blob_bytes(form);
     // a device's 12 slots and 4 terminals in one 64-byte record: the builder
     // visits devices in row order (random in netlist order on scattered
@@ -71,42 +76,60 @@ bool build_tile_host(int form, int64_t N, int32_t n_nodes, int32_t n, int64_t nn
     std::vector<int32_t> hs_ptr, hs_k;
     std::vector<int32_t> tile_of_row, mark, home, cur, tile_rows_ptr, tile_rows, out_item_ptr, item_dev;
     int32_t t = 0;
-    int64_t own = 0, bytes = kBlobFixed;
+    int64_t bytes = kBlobFixed;
     int32_t last_row = -2;
-    // distinct heavy x heavy targets a FET brings to tile t (each costs at most
-    // one side entry + one run + one list start); marks them
+    // distinct heavy x heavy targets a FET brings to tile t; marks them, and
+    // returns their bytes beyond kHHContrib per contribution (kHHTarget each,
+    // plus the class header of their length if it would be new, as owned)
     std::vector<int32_t> hh_seen((size_t)(nnz + n), -1);
+    std::function<int64_t(int32_t, int32_t)> hh_len_bytes;      // set below (needs tcnt)
     auto hh_new = [&](int64_t i, int32_t tile) {
-        int32_t k = 0;
+        int64_t k = 0;
         for (int p = 0; p < NPAIR; p++) {
             const int32_t s2 = rec[i].s[p];
             if (s2 >= 0 && heavy[rec[i].t[pair_row(p)]] && heavy[rec[i].t[pair_col(p)]] && hh_seen[s2] != tile) {
                 hh_seen[s2] = tile;
-                k++;
+                k += kHHTarget + hh_len_bytes(s2, tile);
             }
         }
         for (int a = 0; a < 4; a++) {
             const int32_t r = rec[i].t[a];
             if (r >= 0 && heavy[r] && hh_seen[nnz + r] != tile) {
                 hh_seen[nnz + r] = tile;
-                k++;
+                k += kHHTarget + hh_len_bytes((int32_t)(nnz + r), tile);
             }
         }
         return k;
     };
-    auto live_count = [&](int64_t i) {
-        int32_t k = 0;
-        for (int p = 0; p < NPAIR + 4; p++) k += listed_c(i, p);
-        return k;
-    };
-    // targets some FET stamps (an owned target nobody stamps costs one padding entry)
-    std::vector<uint8_t> has_c((size_t)(nnz + n), 0);
+    // listed contributions per target (a target nobody stamps is not listed):
+    // an owned target's contributors all lie in its tile, so its program bytes
+    // are known before the partition
+    std::vector<int32_t> tcnt((size_t)(nnz + n), 0);
     for (int64_t i = 0; i < N; i++)
         for (int p = 0; p < NPAIR + 4; p++)
-            if (listed_c(i, p)) has_c[p < NPAIR ? rec[i].s[p] : nnz + rec[i].t[p - NPAIR]] = 1;
-    auto empty_in_row = [&](int32_t r) {
-        int64_t e = has_c[nnz + r] ? 0 : 1;
-        for (int32_t k = row_ptr[r]; k < row_ptr[r + 1]; k++) e += !has_c[k];
+            if (listed_c(i, p)) tcnt[p < NPAIR ? rec[i].s[p] : nnz + rec[i].t[p - NPAIR]]++;
+    // distinct target lengths of the tile being formed (class headers)
+    int32_t max_len = 1;
+    for (int64_t g = 0; g < nnz + n; g++) max_len = std::max(max_len, tcnt[g]);
+    std::vector<int32_t> len_tile((size_t)max_len + 1, -1);
+    auto tgt_bytes = [&](int32_t L, int32_t tile) -> int64_t {
+        if (L <= 0) return 0;
+        int64_t e = 4 + 2 * (int64_t)L;
+        if (len_tile[L] != tile) {
+            len_tile[L] = tile;
+            e += (int64_t)sizeof(TileCls);
+        }
+        return e;
+    };
+    hh_len_bytes = [&](int32_t g, int32_t tile) -> int64_t {
+        const int32_t L = tcnt[g];
+        if (L <= 0 || len_tile[L] == tile) return 0;
+        len_tile[L] = tile;
+        return (int64_t)sizeof(TileCls);
+    };
+    auto row_bytes = [&](int32_t r, int32_t tile) {       // the row's CSR entries and its b row
+        int64_t e = tgt_bytes(tcnt[nnz + r], tile);
+        for (int32_t k = row_ptr[r]; k < row_ptr[r + 1]; k++) e += tgt_bytes(tcnt[k], tile);
         return e;
     };
     // heavy x heavy contributions of a FET (owned by its home tile or side)
@@ -125,7 +148,6 @@ bool build_tile_host(int form, int64_t N, int32_t n_nodes, int32_t n, int64_t nn
         out_item_ptr.push_back((int32_t)item_dev.size());
         tile_rows_ptr.push_back((int32_t)tile_rows.size());
         cur.clear();
-        own = 0;
         bytes = kBlobFixed;
         t++;
     };
@@ -157,7 +179,7 @@ bool build_tile_host(int form, int64_t N, int32_t n_nodes, int32_t n, int64_t nn
                     if (c < n_nodes && !heavy[c]) hs_k[fill[c]++] = k;
                 }
     }
-    // ---- tiles of consecutive light rows: <= kTileItems FETs, <= kOwnMax targets
+    // ---- tiles of consecutive light rows: <= kTileItems FETs, <= kStageMax blob bytes
     tile_of_row.assign((size_t)NN, -1);
     mark.assign((size_t)std::max<int64_t>(1, N), -1);
     home.assign((size_t)std::max<int64_t>(1, N), -1);
@@ -167,10 +189,10 @@ bool build_tile_host(int form, int64_t N, int32_t n_nodes, int32_t n, int64_t nn
     out_item_ptr.assign(1, 0);
     item_dev.clear();
     t = 0;
-    own = 0;
     bytes = kBlobFixed;
     last_row = -2;
     std::fill(hh_seen.begin(), hh_seen.end(), -1);
+    std::fill(len_tile.begin(), len_tile.end(), -1);
     for (int32_t v = 0; v < n_nodes; v++) {
         if (heavy[v]) continue;
         // a tile's rows are consecutive, so its owned entries of A and b are
@@ -178,23 +200,17 @@ bool build_tile_host(int form, int64_t N, int32_t n_nodes, int32_t n, int64_t nn
         if ((int32_t)tile_rows.size() > tile_rows_ptr.back() && last_row != v - 1) close_tile();
         for (int pass = 0; pass < 2; pass++) {
             int32_t fresh = 0;
-            const int64_t hs = hs_ptr[v + 1] - hs_ptr[v];
-            int64_t add_own = (row_ptr[v + 1] - row_ptr[v]) + 1 + hs;
-            int64_t add_bytes = 2 * empty_in_row(v) + 4 * hs;
+            int64_t add_bytes = row_bytes(v, t);
+            for (int32_t k = hs_ptr[v]; k < hs_ptr[v + 1]; k++) add_bytes += tgt_bytes(tcnt[hs_k[k]], t);
             for (int64_t k = iptr[v]; k < iptr[v + 1]; k++) {
                 const int32_t i = idev[k];
                 if (mark[i] != t) {
                     fresh++;
-                    add_bytes += kItemBlobBytes + 2 * live_count(i);
+                    add_bytes += kItemBlobBytes;
                 }
-                if (home[i] < 0) {
-                    const int32_t hh = hh_new(i, t);
-                    add_own += hh;
-                    add_bytes += 12 * hh;
-                }
+                if (home[i] < 0) add_bytes += hh_new(i, t) + kHHContrib * hh_count(i);
             }
-            const bool over = (int64_t)cur.size() + fresh > kTileItems || own + add_own > kOwnMax ||
-                              bytes + add_bytes > kStageMax;
+            const bool over = (int64_t)cur.size() + fresh > kTileItems || bytes + add_bytes > kStageMax;
             if (over && pass == 0 && !cur.empty()) {
                 close_tile();
                 continue;
@@ -203,7 +219,6 @@ bool build_tile_host(int form, int64_t N, int32_t n_nodes, int32_t n, int64_t nn
                 promoted[v] = 1;
                 done = false;
             }
-            own += add_own;
             bytes += add_bytes;
             break;
         }
@@ -225,13 +240,10 @@ bool build_tile_host(int form, int64_t N, int32_t n_nodes, int32_t n, int64_t nn
     // FETs with no light terminal (all heavy or ground): orphan tiles
     for (int64_t i = 0; i < N; i++)
         if (home[i] < 0) {
-            const int32_t add = hh_count(i);
-            const int64_t add_bytes = kItemBlobBytes + 2 * live_count(i) + 12 * add;
-            if (!cur.empty() && ((int64_t)cur.size() + 1 > kTileItems || own + add > kOwnMax ||
-                                 bytes + add_bytes > kStageMax))
+            const int64_t add_bytes = kItemBlobBytes + (kHHTarget + (int64_t)sizeof(TileCls) + kHHContrib) * hh_count(i);
+            if (!cur.empty() && ((int64_t)cur.size() + 1 > kTileItems || bytes + add_bytes > kStageMax))
                 close_tile();
             home[i] = t;
-            own += add;
             bytes += add_bytes;
             cur.push_back((int32_t)i);
         }
@@ -262,7 +274,7 @@ bool build_tile_host(int form, int64_t N, int32_t n_nodes, int32_t n, int64_t nn
     for (int64_t g = 0; g < NT; g++)
         if (hh_owner[g] >= 0) hh_of_tile[hh_owner[g]].push_back((int32_t)g);
 
-    // ---- per tile: blob = header | items | owned program | side entries.
+    // ---- per tile: blob = header + classes | items | side | dst | ent.
     // Tiles are emitted in parallel into their own buffers (side entries carry
     // their global target for now), then concatenated in tile order, where
     // side ids are numbered by first appearance (the serial order).
@@ -281,13 +293,19 @@ bool build_tile_host(int form, int64_t N, int32_t n_nodes, int32_t n, int64_t nn
     bool all_ok = true;
 #pragma omp parallel
     {
-    std::vector<std::pair<int32_t, uint16_t>> con, side, con_all;
-    std::vector<int32_t> gids, xg;
-    std::vector<uint16_t> ent;
-    std::vector<uint32_t> tw;
-    std::vector<int32_t> seg_of;
+    std::vector<std::pair<int32_t, uint16_t>> con, side;
+    std::vector<int32_t> gids;
     std::vector<SideEnt> sents;
-    std::vector<int64_t> extra_g;
+    // one target of the program: destination, its entries con/side[beg, beg+len)
+    struct Tgt {
+        int32_t dst;
+        int32_t beg, len;
+        bool is_side;
+    };
+    std::vector<Tgt> tg;
+    std::vector<TileCls> cls;
+    std::vector<int32_t> dsts;
+    std::vector<uint16_t> ents;
     auto emit_tile = [&](int32_t tt, TileOut &o) -> bool {
         // owned targets, ascending
         gids.clear();
@@ -299,7 +317,7 @@ bool build_tile_host(int form, int64_t N, int32_t n_nodes, int32_t n, int64_t nn
         }
         gids.insert(gids.end(), hh_of_tile[tt].begin(), hh_of_tile[tt].end());
         std::sort(gids.begin(), gids.end());
-        // contributions of this tile's items
+        // contributions of this tile's items, (target, shared-memory slot)
         con.clear();
         side.clear();
         const int32_t q0 = out_item_ptr[tt];
@@ -331,146 +349,93 @@ bool build_tile_host(int form, int64_t N, int32_t n_nodes, int32_t n, int64_t nn
                 }
             }
         }
+        // entries of one target in item order, then pair order (stable)
         auto by_target = [](const std::pair<int32_t, uint16_t> &a, const std::pair<int32_t, uint16_t> &b) {
             return a.first < b.first;
         };
         std::stable_sort(con.begin(), con.end(), by_target);
         std::stable_sort(side.begin(), side.end(), by_target);
-        // segments, in owned order: the tile rows' CSR block [a0, a0+na) and
-        // b rows [b0, b0+nb) (implicit ids; an entry nobody stamps gets one
-        // padding entry), then the other owned targets (heavy-row slices and
-        // heavy x heavy targets; explicit ids, ascending), then side entries
-        int32_t a0 = 0, na = 0, b0 = 0, nb = 0;
-        if (tile_rows_ptr[tt + 1] > tile_rows_ptr[tt]) {
-            const int32_t r0 = tile_rows[tile_rows_ptr[tt]], r1 = tile_rows[tile_rows_ptr[tt + 1] - 1];
-            if (r1 - r0 + 1 != tile_rows_ptr[tt + 1] - tile_rows_ptr[tt]) return false;   // rows not consecutive
-            a0 = row_ptr[r0];
-            na = row_ptr[r1 + 1] - a0;
-            b0 = r0;
-            nb = r1 - r0 + 1;
+        // targets: owned (all contributors in this tile; destination = global
+        // target), then side pieces (this tile's contributions to a side
+        // target in pieces of <= kSidePiece entries, one side entry each)
+        tg.clear();
+        for (size_t k = 0; k < con.size();) {
+            const int64_t g = con[k].first;
+            size_t e = k;
+            while (e < con.size() && con[e].first == g) e++;
+            if (!std::binary_search(gids.begin(), gids.end(), (int32_t)g)) return false;
+            tg.push_back(Tgt{(int32_t)g, (int32_t)k, (int32_t)(e - k), false});
+            k = e;
         }
-        ent.clear();
-        xg.clear();
-        size_t ci = 0;
-        int32_t seg = 0;
-        auto take = [&](int64_t g) {      // the segment of target g: its entries, or one pad
-            const size_t c0 = ci;
-            while (ci < con.size() && con[ci].first == g) ci++;
-            if (ci == c0) ent.push_back((uint16_t)(8 * kZeroSlot | kEntEnd));
-            for (size_t k = c0; k < ci; k++) ent.push_back((uint16_t)(8 * con[k].second | (k + 1 == ci ? kEntEnd : 0)));
-            seg_of.resize(ent.size(), seg);
-            seg++;
-        };
-        seg_of.clear();
-        // con is sorted by target: extras below a0, the CSR block, extras up to
-        // nnz, then b rows (the tile's range and heavy extras)
-        extra_g.clear();
-        {
-            size_t k = 0;
-            while (k < con.size()) {
-                const int64_t g = con[k].first;
-                const bool mainA = g >= a0 && g < (int64_t)a0 + na;
-                const bool mainB = g >= nnz + b0 && g < nnz + b0 + nb;
-                if (!mainA && !mainB) {
-                    if (!std::binary_search(gids.begin(), gids.end(), (int32_t)g)) return false;
-                    extra_g.push_back(g);
-                }
-                while (k < con.size() && con[k].first == g) k++;
-            }
-        }
-        // walk con once per class (it is sorted; each class is a sorted subset)
-        con_all.clear();
-        con_all.swap(con);
-        auto class_of = [&](int64_t g) {
-            if (g >= a0 && g < (int64_t)a0 + na) return 0;
-            if (g >= nnz + b0 && g < nnz + b0 + nb) return 1;
-            return 2;
-        };
-        for (int cls = 0; cls < 3; cls++) {
-            con.clear();
-            for (auto &e2 : con_all)
-                if (class_of(e2.first) == cls) con.push_back(e2);
-            ci = 0;
-            if (cls == 0)
-                for (int64_t g = a0; g < (int64_t)a0 + na; g++) take(g);
-            else if (cls == 1)
-                for (int64_t g = nnz + b0; g < nnz + b0 + nb; g++) take(g);
-            else
-                for (int64_t g : extra_g) {
-                    take(g);
-                    xg.push_back((int32_t)g);
-                }
-            if (ci != con.size()) return false;
-        }
-        const int32_t n_own = seg;
-        o.listed += (int64_t)con_all.size();
-        con.swap(con_all);
-        // side entries (slot filled below, once every side target's entry count is known)
+        const int32_t n_own = (int32_t)tg.size();
         sents.clear();
-        int32_t n_sent = 0;
-        for (size_t k = 0; k < side.size(); k++) {
+        for (size_t k = 0; k < side.size();) {
             const int32_t g = side[k].first;
-            if (k == 0 || g != side[k - 1].first) {
+            size_t e = k;
+            while (e < side.size() && side[e].first == g) e++;
+            for (size_t p0 = k; p0 < e; p0 += kSidePiece) {
+                const size_t p1 = std::min(e, p0 + (size_t)kSidePiece);
                 SideEnt se;
                 se.sid = g;             // global target; numbered after the concatenation
                 se.slot = -1;
+                tg.push_back(Tgt{-1 - (int32_t)sents.size(), (int32_t)p0, (int32_t)(p1 - p0), true});
                 sents.push_back(se);
-                n_sent++;
             }
-            const bool last = k + 1 == side.size() || side[k + 1].first != g;
-            ent.push_back((uint16_t)(8 * side[k].second | (last ? kEntEnd : 0)));
-            seg_of.push_back(n_own + n_sent - 1);
+            k = e;
         }
-        o.listed += (int64_t)side.size();
-        if (n_own + n_sent > kSegMax) return false;
-        // equal chunks of K entries per thread, thread-interleaved
-        const int64_t L = (int64_t)ent.size();
-        const int32_t K = (int32_t)((L + kTileThreads - 1) / kTileThreads);
-        tw.assign(kTileThreads, 0);
-        auto chunk_has_end = [&](int64_t th2) {
-            for (int64_t p2 = th2 * K; p2 < std::min<int64_t>(L, (th2 + 1) * K); p2++)
-                if (ent[p2] & kEntEnd) return true;
-            return false;
-        };
-        for (int32_t th2 = 0; th2 < kTileThreads; th2++) {
-            const int64_t p0 = (int64_t)th2 * K;
-            if (p0 >= L) continue;
-            uint32_t chain = 0;
-            if (p0 > 0 && seg_of[p0 - 1] == seg_of[p0] && chunk_has_end(th2)) {
-                // the segment began in earlier chunks: count them (each carries a partial)
-                int64_t k2 = th2 - 1;
-                chain = 1;
-                while (k2 > 0 && seg_of[k2 * K - 1] == seg_of[p0]) {
-                    k2--;
-                    chain++;
+        const int32_t n_sent = (int32_t)sents.size();
+        o.listed += (int64_t)con.size() + (int64_t)side.size();
+        // classes: one per distinct length, longest first; targets in list order
+        std::stable_sort(tg.begin(), tg.end(), [](const Tgt &a, const Tgt &b) { return a.len > b.len; });
+        cls.clear();
+        dsts.clear();
+        ents.clear();
+        int64_t cum = 0;
+        for (size_t k = 0; k < tg.size();) {
+            size_t e = k;
+            while (e < tg.size() && tg[e].len == tg[k].len) e++;
+            const int32_t L = tg[k].len, nc = (int32_t)(e - k);
+            if (L > 65535 || nc > 65535 || ents.size() > 65535) return false;
+            TileCls tc;
+            std::memset(&tc, 0, sizeof(tc));
+            tc.len = (uint16_t)L;
+            tc.n = (uint16_t)nc;
+            tc.ent = (uint16_t)ents.size();
+            tc.dst = (uint16_t)dsts.size();
+            const int64_t gs = cls_group(L), ng = kTileThreads / gs;
+            tc.rot = (uint16_t)((cum / gs) % ng);
+            cls.push_back(tc);
+            for (size_t q = k; q < e; q++) dsts.push_back(tg[q].dst);
+            for (int32_t p = 0; p < L; p++)
+                for (size_t q = k; q < e; q++) {
+                    const Tgt &t2 = tg[q];
+                    ents.push_back((uint16_t)(8 * (t2.is_side ? side[t2.beg + p].second : con[t2.beg + p].second)));
                 }
-            }
-            tw[th2] = (uint32_t)seg_of[p0] | (chain << 16);
+            cum += (int64_t)nc * gs;          // lanes occupied
+            k = e;
         }
+        if (ents.size() > 65536) return false;
         // emit the blob
         TileHdr hdr;
         std::memset(&hdr, 0, sizeof(hdr));
         hdr.n_items = (uint16_t)ni;
-        hdr.n_own = (uint16_t)n_own;
-        hdr.n_x = (uint16_t)xg.size();
+        hdr.n_cls = (uint16_t)cls.size();
         hdr.n_sent = (uint16_t)n_sent;
-        hdr.K = (uint16_t)K;
-        hdr.a0 = a0;
-        hdr.na = na;
-        hdr.b0 = b0;
-        hdr.nb = nb;
+        hdr.n_tgt = (uint16_t)tg.size();
+        if (tg.size() > 65535 || n_sent > 65535) return false;
+        hdr.off_items = (uint32_t)pad16(sizeof(TileHdr) + sizeof(TileCls) * cls.size());
         const size_t items_bytes = pad16((size_t)ni * kItemBlobBytes);
-        hdr.off_x = (uint32_t)(pad16(sizeof(TileHdr)) + items_bytes);
-        hdr.off_tw = (uint32_t)(hdr.off_x + 4 * xg.size());
-        hdr.off_ent = (uint32_t)(hdr.off_tw + 4 * kTileThreads);
-        hdr.off_side = (uint32_t)pad16(hdr.off_ent + 2 * (size_t)K * kTileThreads);
-        const size_t bytes = pad16(hdr.off_side + sizeof(SideEnt) * sents.size());
-        if (bytes > (size_t)kStageMax || K > 65535) return false;
+        hdr.off_side = (uint32_t)(hdr.off_items + items_bytes);
+        hdr.off_dst = (uint32_t)pad16(hdr.off_side + sizeof(SideEnt) * sents.size());
+        hdr.off_ent = (uint32_t)pad16(hdr.off_dst + 4 * dsts.size());
+        const size_t bytes = pad16(hdr.off_ent + 2 * ents.size());
+        if (bytes > (size_t)kStageMax) return false;
         hdr.bytes = (uint32_t)bytes;
         o.blob.assign(bytes, 0);
         uint8_t *bp = o.blob.data();
         std::memcpy(bp, &hdr, sizeof(hdr));
-        uint8_t *it = bp + pad16(sizeof(TileHdr));
+        if (!cls.empty()) std::memcpy(bp + sizeof(TileHdr), cls.data(), sizeof(TileCls) * cls.size());
+        uint8_t *it = bp + hdr.off_items;
         int4 *term = reinterpret_cast<int4 *>(it);
         // form 0: beta, v0, model follow the terms in the blob; form 1: they
         // live in tile-order arrays, kTileItems slots per tile (v0 per item)
@@ -490,18 +455,13 @@ bool build_tile_host(int form, int64_t N, int32_t n_nodes, int32_t n, int64_t nn
             }
             md[q] = (uint8_t)model[i];
         }
-        if (!xg.empty()) std::memcpy(bp + hdr.off_x, xg.data(), 4 * xg.size());
-        std::memcpy(bp + hdr.off_tw, tw.data(), 4 * tw.size());
-        uint16_t *ep = reinterpret_cast<uint16_t *>(bp + hdr.off_ent);
-        for (int64_t k = 0; k < (int64_t)K * kTileThreads; k++) {
-            const int64_t th2 = k / K, kk = k % K;     // logical position k -> thread th2, step kk
-            ep[kk * kTileThreads + th2] = k < L ? ent[k] : (uint16_t)(8 * kZeroSlot);
-        }
         if (!sents.empty()) std::memcpy(bp + hdr.off_side, sents.data(), sizeof(SideEnt) * sents.size());
+        if (!dsts.empty()) std::memcpy(bp + hdr.off_dst, dsts.data(), 4 * dsts.size());
+        if (!ents.empty()) std::memcpy(bp + hdr.off_ent, ents.data(), 2 * ents.size());
         o.n_own = n_own;
         o.n_sent = n_sent;
-        o.L = L;
-        o.padded = (int64_t)K * kTileThreads;
+        o.L = (int64_t)con.size() + (int64_t)side.size();
+        o.padded = o.L;
         return true;
     };
 #pragma omp for schedule(dynamic, 64)
@@ -575,9 +535,27 @@ bool build_tile_host(int form, int64_t N, int32_t n_nodes, int32_t n, int64_t nn
     std::vector<int32_t> order((size_t)out.n_side);
     std::iota(order.begin(), order.end(), 0);
     std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return cnt[a] > cnt[b]; });
+    // pieces of one side target in one tile: a hot target keeps one running
+    // sum per piece index in the CTA (kHotPieces of them)
+    std::vector<int32_t> max_pieces((size_t)out.n_side, 0);
+    {
+        std::vector<int32_t> seen((size_t)out.n_side, -1), cnt_t((size_t)out.n_side, 0);
+        for (int32_t tt = 0; tt < T; tt++) {
+            const uint8_t *bp = out.blob.data() + out.blob_off[tt];
+            TileHdr hdr;
+            std::memcpy(&hdr, bp, sizeof(hdr));
+            const SideEnt *se = reinterpret_cast<const SideEnt *>(bp + hdr.off_side);
+            for (int e = 0; e < hdr.n_sent; e++) {
+                SideEnt v;
+                std::memcpy(&v, se + e, sizeof(v));
+                if (seen[v.sid] != tt) { seen[v.sid] = tt; cnt_t[v.sid] = 0; }
+                max_pieces[v.sid] = std::max(max_pieces[v.sid], ++cnt_t[v.sid]);
+            }
+        }
+    }
     std::vector<int32_t> hot_of((size_t)out.n_side, -1);
-    for (int32_t k = 0; k < out.n_side && k < kMaxHot; k++)
-        if (cnt[order[k]] > (int64_t)grid) {
+    for (int32_t k = 0; k < out.n_side && out.n_hot < kMaxHot; k++)
+        if (cnt[order[k]] > (int64_t)grid && max_pieces[order[k]] <= kHotPieces) {
             hot_of[order[k]] = out.n_hot++;
             out.hot_gid.push_back(out.sd_gid[order[k]]);
         }
@@ -607,6 +585,7 @@ bool build_tile_host(int form, int64_t N, int32_t n_nodes, int32_t n, int64_t nn
     }
     {
         std::vector<int64_t> fill(base);
+        std::vector<int32_t> seen((size_t)out.n_side, -1), q_t((size_t)out.n_side, 0);
         for (int32_t tt = 0; tt < T; tt++) {
             uint8_t *bp = out.blob.data() + out.blob_off[tt];
             TileHdr hdr;
@@ -615,7 +594,9 @@ bool build_tile_host(int form, int64_t N, int32_t n_nodes, int32_t n, int64_t nn
             for (int e = 0; e < hdr.n_sent; e++) {
                 SideEnt v;
                 std::memcpy(&v, se + e, sizeof(v));
-                v.slot = hot_of[v.sid] >= 0 ? -1 - hot_of[v.sid] : (int32_t)fill[v.sid]++;
+                if (seen[v.sid] != tt) { seen[v.sid] = tt; q_t[v.sid] = 0; }
+                const int32_t q = q_t[v.sid]++;           // piece index of this target in the tile
+                v.slot = hot_of[v.sid] >= 0 ? -1 - (hot_of[v.sid] * kHotPieces + q) : (int32_t)fill[v.sid]++;
                 std::memcpy(se + e, &v, sizeof(v));
             }
         }

@@ -1,20 +1,24 @@
-"""A minimal Newton-Raphson transient driver around the hot path (SURVEY.md
-§8(f) NEXT-4, "the steps either side"): the loop of PAPER.md Fig. 1
- and SPEC.md's newton_step / run_transient, for small
-circuits.
+"""The Newton-Raphson transient loop around the hot path (SURVEY.md §8(f)
+NEXT-4, "the steps either side"): the loop of PAPER.md Fig. 1 and
+SPEC.md's newton_step / run_transient.
 
-Per NR iteration (S:426 order): clear A and b; stamp the linear devices (the
-caller's pre-pass, S:302 -- here the ideal voltage sources that hold the
-rails); ``ees_eval_stamp`` (the hot path: every MOSFET evaluated and stamped
-on the GPU); solve ``A x = b``.  The solve is a dense LU through
-``torch.linalg.solve`` -- a library solve, sized for the small circuits this
-driver is for; the paper's sparse KLU / a cuDSS solve are out of
-scope.  On convergence, ``ees_accept`` stores the converged
+Per NR iteration (S:426 order), every step in libees.so on the GPU: clear A
+and b; ``ees_stamp_linear`` -- the caller's linear pre-pass, here the
+ideal voltage sources that hold the rails; ``ees_eval_stamp`` -- the hot
+path, every MOSFET evaluated and stamped; ``ees_solver_factor`` +
+``ees_solver_solve`` -- the sparse LU (KLU's role): ordering and
+pivots fixed at the first iteration (host), numeric refactorisation and
+triangular solves on the GPU; then the convergence test max|dx| <= abstol +
+reltol max|x|.  On convergence ``ees_accept`` stores the converged
 branch voltages as the companion-model state of the next step.
+This module only sequences those calls (and reads one convergence scalar
+back per iteration).
 """
 from __future__ import annotations
 
 import torch
+
+from .api import Solver
 
 
 class Transient:
@@ -29,45 +33,50 @@ class Transient:
         self.ctx = ctx
         self.dev = device or torch.device("cuda", torch.cuda.current_device())
         n = ctx.n
-        rp, ci = ctx.pattern()
-        rows = torch.repeat_interleave(torch.arange(n), torch.from_numpy(rp[1:] - rp[:-1]).long())
-        self.flat = (rows * n + torch.from_numpy(ci).long()).to(self.dev)
-        self.src_slots, self.src_rows, self.src_vals = [], [], []
+        slots, rows, vals = [], [], []
         for node, br, volts in sources:
             k1, k2 = ctx.find_slot(node, br), ctx.find_slot(br, node)
             if k1 < 0 or k2 < 0:
                 raise ValueError(f"pattern lacks the source entries of node {node} / branch {br}")
-            self.src_slots += [k1, k2]
-            self.src_rows.append(br)
-            self.src_vals.append(float(volts))
-        self.src_slots = torch.tensor(self.src_slots, dtype=torch.long, device=self.dev)
-        self.src_rows = torch.tensor(self.src_rows, dtype=torch.long, device=self.dev)
-        self.src_vals = torch.tensor(self.src_vals, dtype=torch.float64, device=self.dev)
+            slots += [k1, k2]                     # KCL: +i_br at the node; branch row: V(node)
+            rows.append(br)
+            vals.append(float(volts))             # = volts
+        self.lin_slot = torch.tensor(slots, dtype=torch.int64, device=self.dev)
+        self.lin_val = torch.ones(len(slots), dtype=torch.float64, device=self.dev)
+        self.lin_row = torch.tensor(rows, dtype=torch.int32, device=self.dev)
+        self.lin_bval = torch.tensor(vals, dtype=torch.float64, device=self.dev)
         self.A = torch.zeros(ctx.nnz, dtype=torch.float64, device=self.dev)
         self.b = torch.zeros(n, dtype=torch.float64, device=self.dev)
-        self.dense = torch.zeros(n * n, dtype=torch.float64, device=self.dev)
+        self.solver = None
         self.n = n
 
     def assemble(self, x, h):
         """A, b of one NR iteration at x (linear pre-pass, then the FET stamps)."""
         self.A.zero_()
         self.b.zero_()
-        self.A[self.src_slots] += 1.0                 # KCL: +i_br at the node; branch row: V(node)
-        self.b[self.src_rows] += self.src_vals        # = volts
+        self.ctx.stamp_linear(self.lin_slot, self.lin_val, self.lin_row, self.lin_bval, self.A, self.b)
         self.ctx.eval_stamp(x, h, self.A, self.b)
         return self.A, self.b
+
+    def solve(self, A, b, x_out):
+        """x_out = A^-1 b: the first call orders and pivots (host LU at these
+        values), every call refactorises on the GPU and solves."""
+        if self.solver is None:
+            self.solver = Solver(self.ctx, A.cpu().numpy())
+        self.solver.factor(A)
+        self.solver.solve(b, x_out)
+        return x_out
 
     def newton(self, x, h, abstol=1e-9, reltol=1e-6, max_iter=50):
         """NR iterations from x at step h until max|dx| <= abstol + reltol
         max|x| (S:426); returns (x, iterations)."""
         x = x.clone()
+        x_new = torch.empty_like(x)
         for it in range(1, max_iter + 1):
             A, b = self.assemble(x, h)
-            self.dense.zero_()
-            self.dense.index_put_((self.flat,), A, accumulate=True)
-            x_new = torch.linalg.solve(self.dense.view(self.n, self.n), b)
+            self.solve(A, b, x_new)
             dx = (x_new - x).abs().max().item()
-            x = x_new
+            x, x_new = x_new, x
             if dx <= abstol + reltol * x.abs().max().item():
                 return x, it
         raise RuntimeError(f"NR did not converge in {max_iter} iterations (last max|dx| = {dx:.3e})")
@@ -83,6 +92,11 @@ class Transient:
             xs.append(x)
             its.append(it)
         return xs, its
+
+    def close(self):
+        if self.solver is not None:
+            self.solver.close()
+            self.solver = None
 
 
 def rail_sources(nl, volts=1.0):

@@ -250,15 +250,14 @@ def test_abi_errors(cuda_ok):
 
 
 @pytest.mark.parametrize("mode", ["launch", "coop"])
-def test_color_forms(cuda_ok, mode, monkeypatch):
+def test_color_forms(cuda_ok, mode):
     """Both COLOR forms: one launch per colour (Table I ColorFused) and
     the persistent cooperative kernel with a grid barrier per colour (Table I
     Color "single parallel region", P:79)."""
-    monkeypatch.setenv("EES_COLOR_MODE", mode)
     for nl in (netgen.config(0), netgen.config(1, 0.05), netgen.gen_synth(5000, 40),
                netgen.ota_5t()):
         ref = reference(nl)
-        ctx = ctx_for(nl, variant="color")
+        ctx = ctx_for(nl, variant="color", color_mode=mode)
         A1, b1 = gpu_run(ctx, nl)
         assert_parity(ref, A1, b1, f"{nl.name} color/{mode}")
         A2, b2 = gpu_run(ctx, nl)

@@ -241,12 +241,11 @@ def test_tile_single_giant_node():
     assert st["n_tiles"] >= N // 128 and st["n_heavy_nodes"] >= 1 and st["n_side_targets"] >= 2
 
 
-@pytest.mark.parametrize("form,stage", [(0, 10496), (1, 6144)])
-def test_tile_forms_build_within_stage(monkeypatch, form, stage):
+@pytest.mark.parametrize("form,stage", [(0, 11264), (1, 7680)])
+def test_tile_forms_build_within_stage(form, stage):
     """Both TILE forms (items in the blob / in HBM arrays) build on every
     structure, each blob within its pipeline stage (the builder's byte bound
     is an upper bound: setup would fail otherwise)."""
-    monkeypatch.setenv("EES_TILE_FORM", str(form))
     nets = [netgen.config(c, 0.01 if c else 1.0) for c in range(5)]
     nets += [netgen.full_adder_28t(16), netgen.insert_resistors(netgen.full_adder_28t(8), "all"),
              netgen.ring_oscillators(20, 101, fanout=4), netgen.gen_synth(5000, 300)]
@@ -257,7 +256,7 @@ def test_tile_forms_build_within_stage(monkeypatch, form, stage):
         nets.append(netgen.custom("r", nn, [tuple(t) for t in T], 0, netgen.bench_models(),
                                   rails=[int(rng.integers(0, nn))]))
     for nl in nets:
-        st = _ctx(nl).stats()
+        st = _ctx(nl, tile_form=form).stats()
         assert st["tile_form"] == form
         assert st["n_tiles"] >= 1 and st["tile_blob_max"] <= stage, nl.name
 
