@@ -664,9 +664,15 @@ ees_status build_hybrid(const ees_desc *d, ees_ctx *c, const std::vector<int32_t
         const int32_t r = TT[p - NPAIR][i];
         return r >= 0 ? nnz + r : -1;
     };
+    // Rails take the side sum under every rule (as the rail partials of
+    // COLOR / ATOMIC do): under the paper rule no two FETs of a colour share
+    // a rail, but the rail diagonal would otherwise be a sequential sum over
+    // all colour phases (10^5 on cfg1), whose rounding can exceed 1e-12 sum|c|.
+    std::vector<uint8_t> side_node(excluded);
+    for (int32_t r : c->rails) side_node[r] = 1;
     auto candidate = [&](int64_t i, int p) -> bool {
-        if (p < NPAIR) return excluded[TT[kPairRow[p]][i]] && excluded[TT[kPairCol[p]][i]];
-        return excluded[TT[p - NPAIR][i]] != 0;
+        if (p < NPAIR) return side_node[TT[kPairRow[p]][i]] && side_node[TT[kPairCol[p]][i]];
+        return side_node[TT[p - NPAIR][i]] != 0;
     };
     // distinct FETs per candidate target
     std::vector<int32_t> writers((size_t)NT, 0), last((size_t)NT, -1);

@@ -103,7 +103,9 @@ struct GatherK {
 // tile contributes one part.
 //
 // The tile's reduction program lists its targets by contribution count
-// ("length class"): class c holds n_c targets of exactly L_c contributions,
+// ("length class"): short class c holds n_c targets of exactly L_c <= 4
+// contributions, a group class the targets of lengths 4 gs/2 < L <= 4 gs
+// (gs = cls_group(L) lanes per target);
 // each as a 32-bit destination and L_c entries (byte offsets of the
 // contributions in the tile's shared-memory slots).  A thread sums one target
 // in list order (fixed-length unrolled loops for L <= 4; a longer target is
@@ -128,8 +130,11 @@ struct GatherK {
 //   side:   SideEnt[n_sent]
 //   dst:    int32[n_tgt]: per class, the destinations of its targets (>= 0:
 //           global target g = A index, or nnz + b row; < 0: side entry -1-dst)
-//   ent:    u16: per class c, entries [L_c][n_c] (k-major: lanes of a warp
-//           read consecutive u16)
+//   meta:   u32[n_grp]: targets of group classes (L > 4): first entry (low 16
+//           bits, u16 index in ent[]) | length << 16
+//   ent:    u16: per short class c, entries [L_c][n_c] (k-major: lanes of a
+//           warp read consecutive u16); group classes: each target's entries
+//           contiguous (the lanes of its group read consecutive u16)
 // Contributions of a FET whose source and bulk are one node (every PMOS of the
 // inverter configs) are merged at evaluation (DB into DS, BD into SD, BB into
 // SS, J[B] into J[S]) and the merged-away slots are not listed.
@@ -152,27 +157,34 @@ __host__ __device__ constexpr int item_blob_bytes(int form) { return form ? 16 :
 #endif
 __host__ __device__ constexpr int tile_bufs(int form) { return form ? EES_TILE_BUF1 : EES_TILE_BUF0; }
 __host__ __device__ constexpr int tile_ctas(int form) { return form ? (tile_bufs(1) == 2 ? 4 : 5) : (tile_bufs(0) == 2 ? 3 : 4); }
+
 constexpr int kStages = 3;           // TMA pipeline depth (blobs in flight per CTA)
 constexpr int kScSlots = 16 * kTileItems + 2;   // contribution slots per buffer (+16-byte pad)
 constexpr int64_t kSideInlineParts = 8192;   // up to this many parts: last CTA finalises
 constexpr int kMaxHot = 16;          // side targets pre-reduced per CTA (rails): parts = CTAs, not tiles
 static_assert(8 * kScSlots < 65536, "entry byte offsets must fit 16 bits");
 
-// Lanes that sum one target of length L together (a power of two): one for
-// L <= 4, then about four entries per lane, at most a warp.
+// Targets of up to kShortMax contributions form short classes (one per exact
+// length, entries k-major, one thread per target); longer ones group classes
+// with cls_group(L) lanes per target (about four entries per lane, at most a
+// warp).  Measured (profiles/r02_ab.md): one thread for L = 5 beats two on
+// cfg2; lane groups for L > 6 beat one thread on cfg3.
+constexpr int kShortMax = 6;
 __host__ __device__ constexpr int cls_group(int L)
 {
-    return L <= 4 ? 1 : L <= 8 ? 2 : L <= 16 ? 4 : L <= 32 ? 8 : L <= 64 ? 16 : 32;
+    return L <= kShortMax ? 1 : L <= 8 ? 2 : L <= 16 ? 4 : L <= 32 ? 8 : L <= 64 ? 16 : 32;
 }
 
 struct TileCls {
-    uint16_t len;                    // contributions per target
+    uint16_t len;                    // contributions per target (1..kShortMax); 0: a group class
     uint16_t n;                      // targets
     uint16_t ent;                    // u16 index of the class's first entry in ent[]
     uint16_t dst;                    // index of the class's first destination in dst[]
-    uint16_t rot;                    // lane groups of cls_group(len) threads used before the
-                                     // class, mod the groups per CTA (kTileThreads / cls_group)
-    uint16_t pad[3];
+    uint16_t rot;                    // lane groups (of gs lanes) used before the class, mod the
+                                     // groups per CTA (kTileThreads / gs)
+    uint16_t lg;                     // group classes: log2 of the group size gs
+    uint16_t meta;                   // group classes: index of the first target's meta[] word
+    uint16_t pad;
 };
 static_assert(sizeof(TileCls) == 16, "TileCls layout");
 
@@ -180,7 +192,8 @@ struct TileHdr {
     uint16_t n_items, n_cls, n_sent, n_tgt;
     uint32_t bytes;                  // blob size, multiple of 16
     uint32_t off_items, off_side, off_dst, off_ent;   // byte offsets of the sections
-    uint32_t pad1[9];
+    uint32_t off_meta;
+    uint32_t pad1[8];
 };
 static_assert(sizeof(TileHdr) == 64, "TileHdr layout");
 

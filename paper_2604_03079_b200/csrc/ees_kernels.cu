@@ -1245,44 +1245,65 @@ __device__ __forceinline__ void tile_put(const SideEnt *sents, const TileOut &o,
     }
 }
 
-// One short class (L <= 4, unrolled): targets k = rot-shifted thread index,
-// +kTileThreads, ...; dst[n], entries [L][n] (byte offsets into the slot
-// buffer), summed in list order.
+// One target k of a short class: entries [len][n] (byte offsets into the
+// slot buffer), summed in list order; L > 0 the length at compile time
+// (unrolled), L = 0 at run time (len <= kShortMax).
 template <int L>
-__device__ __forceinline__ void tile_cls(int k, int n, int /*len*/, const int32_t *dst, const uint16_t *ent,
+__device__ __forceinline__ void tile_one(int k, int n, int len, const int32_t *dst, const uint16_t *ent,
                                          const unsigned char *sc, const SideEnt *sents, const TileOut &o,
                                          const TileK &tk, double *s_hot)
 {
-    auto val = [&](int p, int k2) { return *reinterpret_cast<const double *>(sc + ent[p * n + k2]); };
-    for (; k < n; k += kTileThreads) {
-        const int32_t g = dst[k];
-        double v = val(0, k);
+    const int32_t g = dst[k];
+    double v = *reinterpret_cast<const double *>(sc + ent[k]);
+    if (L > 0) {
 #pragma unroll
-        for (int p = 1; p < L; p++) v += val(p, k);
-        tile_put(sents, o, tk, s_hot, g, v);
+        for (int p = 1; p < L; p++) v += *reinterpret_cast<const double *>(sc + ent[p * n + k]);
+    } else {
+#pragma unroll 2
+        for (int p = 1; p < len; p++) v += *reinterpret_cast<const double *>(sc + ent[p * n + k]);
     }
+    tile_put(sents, o, tk, s_hot, g, v);
 }
 
-// A class of longer targets (L > 4): a group of gs = cls_group(L) lanes per
-// target, lane j summing entries j, j+gs, ... in order, then a fixed xor
-// shuffle tree within the group; the group's first lane puts the sum.  All
+// A group class (targets of L > kShortMax with one group size gs = cls_group(L)): a
+// group of gs lanes per target, lane j summing the target's entries j, j+gs,
+// ... in four fixed partial sums, then a fixed xor shuffle tree within the
+// group; the group's first lane puts the sum.  All
 // lanes of a warp run the same number of iterations (shuffles need them).
-__device__ __forceinline__ void tile_cls_group(const TileCls c, const int32_t *dst, const uint16_t *ent,
-                                               const unsigned char *sc, const SideEnt *sents, const TileOut &o,
-                                               const TileK &tk, double *s_hot)
+__device__ __forceinline__ void tile_cls_group(const TileCls c, int r, const int32_t *dst, const uint32_t *meta,
+                                               const uint16_t *ent, const unsigned char *sc,
+                                               const SideEnt *sents, const TileOut &o, const TileK &tk,
+                                               double *s_hot)
 {
-    const int L = c.len, n = c.n;
-    const int gs = cls_group(L), ng = kTileThreads / gs;
-    const int gi = (int)threadIdx.x / gs, lj = (int)threadIdx.x & (gs - 1);
-    const int k0 = (gi - (int)c.rot) & (ng - 1);
-    const int mine = k0 < n ? (n - 1 - k0) / ng + 1 : 0;
+    const int n = c.n, lg = c.lg, gs = 1 << lg;
+    static_assert(kTileThreads == 128, "lgn assumes 128 threads");
+    const int lgn = 7 - lg;                               // log2(kTileThreads / gs)
+    const int gi = r >> lg, lj = r & (gs - 1);
+    const int k0 = (gi - (int)c.rot) & ((1 << lgn) - 1);
+    const int mine = k0 < n ? ((n - 1 - k0) >> lgn) + 1 : 0;
     const int iters = __reduce_max_sync(0xffffffffu, mine);
     for (int it = 0; it < iters; it++) {
-        const int k = k0 + it * ng;
+        const int k = k0 + (it << lgn);
         const bool act = k < n;
         double s = 0.0;
-        if (act)
-            for (int p = lj; p < L; p += gs) s += *reinterpret_cast<const double *>(sc + ent[p * n + k]);
+        if (act) {
+            // the lane's entries lj, lj+gs, ...: four partial sums (fixed
+            // order, four loads in flight), combined as (s0 + s1) + (s2 + s3)
+            const uint32_t m = meta[k];
+            const uint16_t *e = ent + (m & 0xFFFFu);
+            const int L = (int)(m >> 16);
+            auto val = [&](int p) { return *reinterpret_cast<const double *>(sc + e[p]); };
+            double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+            int p = lj;
+            for (; p + 3 * gs < L; p += 4 * gs) {
+                s0 += val(p);
+                s1 += val(p + gs);
+                s2 += val(p + 2 * gs);
+                s3 += val(p + 3 * gs);
+            }
+            for (; p < L; p += gs) s0 += val(p);
+            s = (s0 + s1) + (s2 + s3);
+        }
         for (int off = gs >> 1; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
         if (act && lj == 0) tile_put(sents, o, tk, s_hot, dst[k], s);
     }
@@ -1328,47 +1349,173 @@ __device__ __forceinline__ unsigned long long globaltimer()
 #define TILE_TRACE(slot) TILE_TRACE_AT(slot, kTraceSlots - 2)
 #define TILE_TRACE_TAIL(slot) TILE_TRACE_AT(slot, kTraceSlots)
 
+// Evaluate item `it` of a staged tile and store its 16 contributions at
+// slots p*kTileItems + it of the slot buffer (ees_internal.h).
+template <bool kRep, int kForm>
+__device__ __forceinline__ void tile_eval_item(const unsigned char *blob, const TileRegs &cur, int it, double *scd,
+                                               const CardK *s_cards, const CallK &P)
+{
+    const TileHdr *h = reinterpret_cast<const TileHdr *>(blob);
+    const int ni = h->n_items;
+    Stamp st;
+    if (kForm == 1) {
+        eval_fet<kRep>(s_cards[cur.model], cur.beta, P.gmin, cur.VD, cur.VG, cur.VS, cur.v0a, cur.v0b, cur.v0c, st,
+                       P.work);
+    } else {
+        const double *bt = reinterpret_cast<const double *>(blob + h->off_items + 16 * ni);
+        const uint8_t *md = blob + h->off_items + 48 * ni;
+        eval_fet<kRep>(s_cards[md[it]], bt[it], P.gmin, cur.VD, cur.VG, cur.VS, bt[ni + it], bt[2 * ni + it],
+                       bt[3 * ni + it], st, P.work);
+    }
+    const int4 T = reinterpret_cast<const int4 *>(blob + h->off_items)[it];
+    if (T.z == T.w && T.z != -1) {        // source tied to bulk: one entry each (ees_internal.h)
+        st.y[DS] += st.y[DB];
+        st.y[SD] += st.y[BD];
+        st.y[SS] += st.y[BB];
+        st.j[2] += st.j[3];
+    }
+#pragma unroll
+    for (int p = 0; p < NPAIR; p++) scd[p * kTileItems + it] = st.y[p];
+#pragma unroll
+    for (int a = 0; a < 4; a++) scd[(NPAIR + a) * kTileItems + it] = st.j[a];
+}
+
+// The reduction program of one staged tile, run by kTileThreads threads with
+// thread index r (0 .. kTileThreads-1; whole warps).
+__device__ __forceinline__ void tile_reduce(const unsigned char *blob, const unsigned char *sc, int r,
+                                            const TileOut &out, const TileK &tk, double *s_hot)
+{
+    const TileHdr *h = reinterpret_cast<const TileHdr *>(blob);
+    const TileCls *cls = reinterpret_cast<const TileCls *>(blob + sizeof(TileHdr));
+    const int32_t *dst = reinterpret_cast<const int32_t *>(blob + h->off_dst);
+    const uint16_t *ent = reinterpret_cast<const uint16_t *>(blob + h->off_ent);
+    const SideEnt *sents = reinterpret_cast<const SideEnt *>(blob + h->off_side);
+    const uint32_t *meta = reinterpret_cast<const uint32_t *>(blob + h->off_meta);
+    const int ncl = h->n_cls;
+    int ci = 0;
+    for (; ci < ncl && cls[ci].len == 0; ci++)                // group classes (warp-uniform)
+        tile_cls_group(cls[ci], r, dst + cls[ci].dst, meta + cls[ci].meta, ent, sc, sents, out, tk, s_hot);
+    if (ci >= ncl) return;
+    // short classes, walked as one list: thread r takes short targets q =
+    // r - rot, +kTileThreads, ... (rot: lanes the group classes used), and
+    // advances through the classes as q passes their ends
+    TileCls c = cls[ci];
+    int qb = 0;                                               // first short index of class ci
+    for (int q = (r - (int)c.rot) & (kTileThreads - 1);; q += kTileThreads) {
+        while (q >= qb + (int)c.n) {
+            qb += c.n;
+            if (++ci >= ncl) return;
+            c = cls[ci];
+        }
+        const int k = q - qb;
+        const uint16_t *e = ent + c.ent;
+        const int32_t *dc = dst + c.dst;
+        switch (c.len) {
+        case 1: tile_one<1>(k, c.n, 1, dc, e, sc, sents, out, tk, s_hot); break;
+        case 2: tile_one<2>(k, c.n, 2, dc, e, sc, sents, out, tk, s_hot); break;
+        case 3: tile_one<3>(k, c.n, 3, dc, e, sc, sents, out, tk, s_hot); break;
+        case 4: tile_one<4>(k, c.n, 4, dc, e, sc, sents, out, tk, s_hot); break;
+        default: tile_one<0>(k, c.n, c.len, dc, e, sc, sents, out, tk, s_hot); break;
+        }
+    }
+}
+
+// After the last tile (all threads of the CTA): hot partials per CTA, then
+// the side targets summed in part order by the last CTA (ticket) unless
+// k_side_final does it.
+template <bool kTrace>
+__device__ __forceinline__ void tile_finish(const TileK &tk, const CallK &P, const double *s_hot,
+                                            double *const *s_hot_dst, const double *s_hot_pre, int *s_last)
+{
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nt = blockDim.x;
+    const int32_t G = gridDim.x;
+    if (!tk.n_side) return;
+    __syncthreads();
+    for (int h = tid; h < tk.n_hot; h += nt) {
+        double v = 0.0;
+#pragma unroll
+        for (int q = 0; q < kHotPieces; q++) v += s_hot[h * kHotPieces + q];   // piece order
+        tk.part[tk.hot_base + (int64_t)h * G + blockIdx.x] = v;
+    }
+    if (!tk.side_inline) return;
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) *s_last = atomicAdd(tk.done, 1u) == (unsigned)G - 1;
+    __syncthreads();
+    TILE_TRACE_TAIL(kTraceSlots - 2);
+    if (!*s_last) return;
+    __threadfence();
+    // hot targets (one part per CTA): a warp each, fixed lane stride, eight
+    // loads in flight per lane, fixed shuffle tree
+    for (int h = warp; h < tk.n_hot; h += nt >> 5) {
+        const double *pp = tk.part + tk.hot_base + (int64_t)h * G;
+        double u = 0.0;
+        for (int q0 = 0; q0 < G; q0 += 256) {
+            double a[8];
+#pragma unroll
+            for (int r = 0; r < 8; r++) {
+                const int q = q0 + r * 32 + lane;
+                a[r] = q < G ? __ldcg(pp + q) : 0.0;
+            }
+#pragma unroll
+            for (int r = 0; r < 8; r++) u += a[r];
+        }
+        u = warp_sum(u);
+        if (lane == 0) *s_hot_dst[h] = s_hot_pre[h] + u;
+    }
+    for (int32_t sid = warp; sid < tk.n_side; sid += nt >> 5)
+        if (__ldg(tk.sd_part + 2 * sid) < tk.hot_base || tk.n_hot == 0) side_finish(tk, P, sid, lane);
+    if (tid == 0) *tk.done = 0;
+}
+
+// TILE kernel prologue: hot targets, card copy, mbarriers and the first
+// NSTAGES blobs in flight.
+#define TILE_PROLOGUE(NT, NSTAGES)                                                               \
+    extern __shared__ __align__(16) unsigned char smem[];                                        \
+    __shared__ CardK s_cards[EES_MAX_MODELS];                                                    \
+    __shared__ __align__(8) uint64_t s_bar[NSTAGES];                                             \
+    __shared__ double s_hot[kMaxHot * kHotPieces], s_hot_pre[kMaxHot];                           \
+    __shared__ double *s_hot_dst[kMaxHot];                                                       \
+    __shared__ int s_last;                                                                       \
+    const int tid = threadIdx.x;                                                                 \
+    const int32_t G = gridDim.x;                                                                 \
+    for (int k = tid; k < kMaxHot * kHotPieces; k += (NT)) s_hot[k] = 0.0;                       \
+    if (tid < tk.n_hot) {            /* hot side targets: only the finisher writes them */       \
+        const int32_t g = tk.hot_gid[tid];                                                       \
+        double *d = g < tk.nnz ? P.A + g : P.b + (g - tk.nnz);                                   \
+        s_hot_dst[tid] = d;                                                                      \
+        s_hot_pre[tid] = *d;                                                                     \
+    }                                                                                            \
+    auto issue = [&](int32_t tile, int stage) {                                                  \
+        const int64_t off = tk.blob_off[tile];                                                   \
+        const uint32_t bytes = (uint32_t)(tk.blob_off[tile + 1] - off);                          \
+        mbar_expect_tx(&s_bar[stage], bytes);                                                    \
+        tma_bulk_g2s(s_stage + (size_t)stage * kStage, tk.blob + off, bytes, &s_bar[stage]);     \
+    };                                                                                           \
+    TileOut out;                                                                                 \
+    out.A = P.A;                                                                                 \
+    out.Bm = P.b - tk.nnz;                                                                       \
+    out.nnz = (int32_t)tk.nnz;                    /* < 2^31 (setup) */                           \
+    const int32_t t0 = blockIdx.x;                                                               \
+    if (tid == 0) {                                                                              \
+        for (int k = 0; k < (NSTAGES); k++) mbar_init(&s_bar[k], 1);                             \
+        for (int k = 0; k < (NSTAGES); k++)                                                      \
+            if (t0 + k * G < tk.n_tiles) issue(t0 + k * G, k);                                   \
+    }                                                                                            \
+    for (int k = tid; k < P.n_models; k += (NT)) s_cards[k] = P.cards[k];                        \
+    __syncthreads();                                                                             \
+    TILE_TRACE(0)
+
+// One CTA of kTileThreads threads does both phases of a tile (barriers B1,
+// and B0 with a single slot buffer).
 template <bool kTrace, bool kRep, int kForm>
 __global__ void __launch_bounds__(kTileThreads, tile_ctas(kForm)) k_tile(TileK tk, CallK P)
 {
     constexpr int kBuf = tile_bufs(kForm);
     constexpr int kStage = stage_max(kForm);
-    extern __shared__ __align__(16) unsigned char smem[];
+#define s_stage (smem + sizeof(double) * kScSlots * kBuf)
+    TILE_PROLOGUE(kTileThreads, kStages);
     unsigned char *s_c = smem;                                           // [kBuf][kScSlots] doubles
-    unsigned char *s_stage = smem + sizeof(double) * kScSlots * kBuf;    // [kStages][kStage]
-    __shared__ CardK s_cards[EES_MAX_MODELS];
-    __shared__ __align__(8) uint64_t s_bar[kStages];
-    __shared__ double s_hot[kMaxHot * kHotPieces], s_hot_pre[kMaxHot];
-    __shared__ double *s_hot_dst[kMaxHot];
-    __shared__ int s_last;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int32_t G = gridDim.x;
-    for (int k = tid; k < kMaxHot * kHotPieces; k += kTileThreads) s_hot[k] = 0.0;
-    if (tid < tk.n_hot) {            // hot side targets: only the finisher writes them
-        const int32_t g = tk.hot_gid[tid];
-        double *d = g < tk.nnz ? P.A + g : P.b + (g - tk.nnz);
-        s_hot_dst[tid] = d;
-        s_hot_pre[tid] = *d;
-    }
-    auto issue = [&](int32_t tile, int stage) {
-        const int64_t off = tk.blob_off[tile];
-        const uint32_t bytes = (uint32_t)(tk.blob_off[tile + 1] - off);
-        mbar_expect_tx(&s_bar[stage], bytes);
-        tma_bulk_g2s(s_stage + (size_t)stage * kStage, tk.blob + off, bytes, &s_bar[stage]);
-    };
-    TileOut out;
-    out.A = P.A;
-    out.Bm = P.b - tk.nnz;
-    out.nnz = (int32_t)tk.nnz;                    // < 2^31 (setup)
-    const int32_t t0 = blockIdx.x;
-    if (tid == 0) {
-        for (int k = 0; k < kStages; k++) mbar_init(&s_bar[k], 1);
-        for (int k = 0; k < kStages; k++)
-            if (t0 + k * G < tk.n_tiles) issue(t0 + k * G, k);
-    }
-    for (int k = tid; k < P.n_models; k += blockDim.x) s_cards[k] = P.cards[k];
-    __syncthreads();
-    TILE_TRACE(0);
     uint32_t parity = 0;                 // bit k: phase of s_bar[k]
     int it = 0;
     int stage = 0;
@@ -1382,33 +1529,9 @@ __global__ void __launch_bounds__(kTileThreads, tile_ctas(kForm)) k_tile(TileK t
     // one tile; the two register sets alternate (no copies between tiles)
     auto step = [&](int32_t t, const TileRegs &cur, TileRegs &nxt) {
         const unsigned char *blob = s_stage + (size_t)stage * kStage;
-        const TileHdr *h = reinterpret_cast<const TileHdr *>(blob);
         unsigned char *sc = s_c + (kBuf == 2 ? (size_t)(it & 1) * 8 * kScSlots : 0);
-        double *scd = reinterpret_cast<double *>(sc);
-        const int ni = h->n_items;
-        if (tid < ni) {
-            Stamp st;
-            if (kForm == 1) {
-                eval_fet<kRep>(s_cards[cur.model], cur.beta, P.gmin, cur.VD, cur.VG, cur.VS, cur.v0a, cur.v0b,
-                               cur.v0c, st, P.work);
-            } else {
-                const double *bt = reinterpret_cast<const double *>(blob + h->off_items + 16 * ni);
-                const uint8_t *md = blob + h->off_items + 48 * ni;
-                eval_fet<kRep>(s_cards[md[tid]], bt[tid], P.gmin, cur.VD, cur.VG, cur.VS, bt[ni + tid],
-                               bt[2 * ni + tid], bt[3 * ni + tid], st, P.work);
-            }
-            const int4 T = reinterpret_cast<const int4 *>(blob + h->off_items)[tid];
-            if (T.z == T.w && T.z != -1) {        // source tied to bulk: one entry each (ees_internal.h)
-                st.y[DS] += st.y[DB];
-                st.y[SD] += st.y[BD];
-                st.y[SS] += st.y[BB];
-                st.j[2] += st.j[3];
-            }
-#pragma unroll
-            for (int p = 0; p < NPAIR; p++) scd[p * kTileItems + tid] = st.y[p];
-#pragma unroll
-            for (int a = 0; a < 4; a++) scd[(NPAIR + a) * kTileItems + tid] = st.j[a];
-        }
+        if (tid < reinterpret_cast<const TileHdr *>(blob)->n_items)
+            tile_eval_item<kRep, kForm>(blob, cur, tid, reinterpret_cast<double *>(sc), s_cards, P);
         // next tile: its blob was issued >= one tile ago; start its gathers now
         const int32_t tn = t + G;
         const int sn = stage + 1 == kStages ? 0 : stage + 1;
@@ -1423,30 +1546,7 @@ __global__ void __launch_bounds__(kTileThreads, tile_ctas(kForm)) k_tile(TileK t
             const int32_t tr = t - G + kStages * G;             // refill the stage of tile t-G
             if (tr < tk.n_tiles) issue(tr, stage == 0 ? kStages - 1 : stage - 1);
         }
-        {
-            const TileCls *cls = reinterpret_cast<const TileCls *>(blob + sizeof(TileHdr));
-            const int32_t *dst = reinterpret_cast<const int32_t *>(blob + h->off_dst);
-            const uint16_t *ent = reinterpret_cast<const uint16_t *>(blob + h->off_ent);
-            const SideEnt *sents = reinterpret_cast<const SideEnt *>(blob + h->off_side);
-            const int ncl = h->n_cls;
-            for (int ci = 0; ci < ncl; ci++) {
-                const TileCls c = cls[ci];
-                const uint16_t *e = ent + c.ent;
-                const int32_t *dc = dst + c.dst;
-                if (c.len > 4) {                               // warp-uniform
-                    tile_cls_group(c, dc, e, sc, sents, out, tk, s_hot);
-                    continue;
-                }
-                const int k0 = ((int)threadIdx.x - (int)c.rot) & (kTileThreads - 1);
-                if (k0 >= c.n) continue;                       // no target of this class here
-                switch (c.len) {
-                case 1: tile_cls<1>(k0, c.n, 1, dc, e, sc, sents, out, tk, s_hot); break;
-                case 2: tile_cls<2>(k0, c.n, 2, dc, e, sc, sents, out, tk, s_hot); break;
-                case 3: tile_cls<3>(k0, c.n, 3, dc, e, sc, sents, out, tk, s_hot); break;
-                default: tile_cls<4>(k0, c.n, 4, dc, e, sc, sents, out, tk, s_hot); break;
-                }
-            }
-        }
+        tile_reduce(blob, sc, tid, out, tk, s_hot);
         TILE_TRACE(3 + 2 * it);
         if (kBuf == 1) __syncthreads();                         // B0: slots free for the next tile
         stage = sn;
@@ -1459,47 +1559,9 @@ __global__ void __launch_bounds__(kTileThreads, tile_ctas(kForm)) k_tile(TileK t
         step(t, rb, ra);
         t += G;
     }
-    if (tk.n_side) {
-        __syncthreads();
-        for (int h = tid; h < tk.n_hot; h += kTileThreads) {
-            double v = 0.0;
-#pragma unroll
-            for (int q = 0; q < kHotPieces; q++) v += s_hot[h * kHotPieces + q];   // piece order
-            tk.part[tk.hot_base + (int64_t)h * G + blockIdx.x] = v;
-        }
-        if (tk.side_inline) {
-            __threadfence();
-            __syncthreads();
-            if (tid == 0) s_last = atomicAdd(tk.done, 1u) == (unsigned)G - 1;
-            __syncthreads();
-            TILE_TRACE_TAIL(kTraceSlots - 2);
-            if (s_last) {
-                __threadfence();
-                // hot targets (one part per CTA): a warp each, fixed lane
-                // stride, eight loads in flight per lane, fixed shuffle tree
-                for (int h = warp; h < tk.n_hot; h += kTileThreads >> 5) {
-                    const double *pp = tk.part + tk.hot_base + (int64_t)h * G;
-                    double u = 0.0;
-                    for (int q0 = 0; q0 < G; q0 += 256) {
-                        double a[8];
-#pragma unroll
-                        for (int r = 0; r < 8; r++) {
-                            const int q = q0 + r * 32 + lane;
-                            a[r] = q < G ? __ldcg(pp + q) : 0.0;
-                        }
-#pragma unroll
-                        for (int r = 0; r < 8; r++) u += a[r];
-                    }
-                    u = warp_sum(u);
-                    if (lane == 0) *s_hot_dst[h] = s_hot_pre[h] + u;
-                }
-                for (int32_t sid = warp; sid < tk.n_side; sid += kTileThreads >> 5)
-                    if (__ldg(tk.sd_part + 2 * sid) < tk.hot_base || tk.n_hot == 0) side_finish(tk, P, sid, lane);
-                if (tid == 0) *tk.done = 0;
-            }
-        }
-    }
+    tile_finish<kTrace>(tk, P, s_hot, s_hot_dst, s_hot_pre, &s_last);
     TILE_TRACE_TAIL(kTraceSlots - 1);
+#undef s_stage
 }
 
 __global__ void __launch_bounds__(256) k_side_final(TileK tk, CallK P)

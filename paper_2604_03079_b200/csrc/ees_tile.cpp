@@ -109,23 +109,26 @@ bool build_tile_host(int form, int64_t N, int32_t n_nodes, int32_t n, int64_t nn
         for (int p = 0; p < NPAIR + 4; p++)
             if (listed_c(i, p)) tcnt[p < NPAIR ? rec[i].s[p] : nnz + rec[i].t[p - NPAIR]]++;
     // distinct target lengths of the tile being formed (class headers)
-    int32_t max_len = 1;
-    for (int64_t g = 0; g < nnz + n; g++) max_len = std::max(max_len, tcnt[g]);
-    std::vector<int32_t> len_tile((size_t)max_len + 1, -1);
+    // class keys: lengths 1..4, then 4 + group size (<= 36)
+    std::vector<int32_t> len_tile(64, -1);
     auto tgt_bytes = [&](int32_t L, int32_t tile) -> int64_t {
         if (L <= 0) return 0;
-        int64_t e = 4 + 2 * (int64_t)L;
-        if (len_tile[L] != tile) {
-            len_tile[L] = tile;
+        int64_t e = 4 + 2 * (int64_t)L + (L > kShortMax ? 4 : 0);   // dst, entries, group meta
+        const int32_t key = L > kShortMax ? kShortMax + cls_group(L) : L;   // class of this length
+        if (len_tile[key] != tile) {
+            len_tile[key] = tile;
             e += (int64_t)sizeof(TileCls);
         }
         return e;
     };
     hh_len_bytes = [&](int32_t g, int32_t tile) -> int64_t {
         const int32_t L = tcnt[g];
-        if (L <= 0 || len_tile[L] == tile) return 0;
-        len_tile[L] = tile;
-        return (int64_t)sizeof(TileCls);
+        if (L <= 0) return 0;
+        const int32_t key = L > kShortMax ? kShortMax + cls_group(L) : L;
+        int64_t e = L > kShortMax ? 4 : 0;                       // group meta word (owned case)
+        if (len_tile[key] == tile) return e;
+        len_tile[key] = tile;
+        return e + (int64_t)sizeof(TileCls);
     };
     auto row_bytes = [&](int32_t r, int32_t tile) {       // the row's CSR entries and its b row
         int64_t e = tgt_bytes(tcnt[nnz + r], tile);
@@ -306,6 +309,7 @@ bool build_tile_host(int form, int64_t N, int32_t n_nodes, int32_t n, int64_t nn
     std::vector<TileCls> cls;
     std::vector<int32_t> dsts;
     std::vector<uint16_t> ents;
+    std::vector<uint32_t> meta;
     auto emit_tile = [&](int32_t tt, TileOut &o) -> bool {
         // owned targets, ascending
         gids.clear();
@@ -385,32 +389,55 @@ bool build_tile_host(int form, int64_t N, int32_t n_nodes, int32_t n, int64_t nn
         }
         const int32_t n_sent = (int32_t)sents.size();
         o.listed += (int64_t)con.size() + (int64_t)side.size();
-        // classes: one per distinct length, longest first; targets in list order
-        std::stable_sort(tg.begin(), tg.end(), [](const Tgt &a, const Tgt &b) { return a.len > b.len; });
+        // classes: group classes (L > 4, by lane-group size, largest first),
+        // then one per short length 4..1; targets in list order
+        auto cls_key = [](int32_t L) { return L > kShortMax ? 100 + cls_group(L) : L; };
+        std::stable_sort(tg.begin(), tg.end(),
+                         [&](const Tgt &a, const Tgt &b) { return cls_key(a.len) > cls_key(b.len); });
         cls.clear();
         dsts.clear();
         ents.clear();
+        meta.clear();
         int64_t cum = 0;
         for (size_t k = 0; k < tg.size();) {
             size_t e = k;
-            while (e < tg.size() && tg[e].len == tg[k].len) e++;
-            const int32_t L = tg[k].len, nc = (int32_t)(e - k);
-            if (L > 65535 || nc > 65535 || ents.size() > 65535) return false;
+            const int key = cls_key(tg[k].len);
+            while (e < tg.size() && cls_key(tg[e].len) == key) e++;
+            const int32_t nc = (int32_t)(e - k);
+            if (nc > 65535 || ents.size() > 65535 || dsts.size() > 65535 || meta.size() > 65535) return false;
             TileCls tc;
             std::memset(&tc, 0, sizeof(tc));
-            tc.len = (uint16_t)L;
             tc.n = (uint16_t)nc;
             tc.ent = (uint16_t)ents.size();
             tc.dst = (uint16_t)dsts.size();
-            const int64_t gs = cls_group(L), ng = kTileThreads / gs;
-            tc.rot = (uint16_t)((cum / gs) % ng);
-            cls.push_back(tc);
-            for (size_t q = k; q < e; q++) dsts.push_back(tg[q].dst);
-            for (int32_t p = 0; p < L; p++)
+            auto entry = [&](const Tgt &t2, int32_t p) {
+                return (uint16_t)(8 * (t2.is_side ? side[t2.beg + p].second : con[t2.beg + p].second));
+            };
+            int64_t gs = 1;
+            if (key > 100) {                                  // group class
+                gs = cls_group(tg[k].len);
+                int lg = 0;
+                while ((1 << lg) < gs) lg++;
+                tc.len = 0;
+                tc.lg = (uint16_t)lg;
+                tc.meta = (uint16_t)meta.size();
                 for (size_t q = k; q < e; q++) {
                     const Tgt &t2 = tg[q];
-                    ents.push_back((uint16_t)(8 * (t2.is_side ? side[t2.beg + p].second : con[t2.beg + p].second)));
+                    if (ents.size() > 65535 || t2.len > 65535) return false;
+                    meta.push_back((uint32_t)ents.size() | ((uint32_t)t2.len << 16));
+                    for (int32_t p = 0; p < t2.len; p++) ents.push_back(entry(t2, p));
+                    dsts.push_back(t2.dst);
                 }
+            } else {
+                const int32_t L = tg[k].len;
+                tc.len = (uint16_t)L;
+                for (size_t q = k; q < e; q++) dsts.push_back(tg[q].dst);
+                for (int32_t p = 0; p < L; p++)
+                    for (size_t q = k; q < e; q++) ents.push_back(entry(tg[q], p));
+            }
+            const int64_t ng = kTileThreads / gs;
+            tc.rot = (uint16_t)((cum / gs) % ng);
+            cls.push_back(tc);
             cum += (int64_t)nc * gs;          // lanes occupied
             k = e;
         }
@@ -427,7 +454,8 @@ bool build_tile_host(int form, int64_t N, int32_t n_nodes, int32_t n, int64_t nn
         const size_t items_bytes = pad16((size_t)ni * kItemBlobBytes);
         hdr.off_side = (uint32_t)(hdr.off_items + items_bytes);
         hdr.off_dst = (uint32_t)pad16(hdr.off_side + sizeof(SideEnt) * sents.size());
-        hdr.off_ent = (uint32_t)pad16(hdr.off_dst + 4 * dsts.size());
+        hdr.off_meta = (uint32_t)(hdr.off_dst + 4 * dsts.size());
+        hdr.off_ent = (uint32_t)pad16(hdr.off_meta + 4 * meta.size());
         const size_t bytes = pad16(hdr.off_ent + 2 * ents.size());
         if (bytes > (size_t)kStageMax) return false;
         hdr.bytes = (uint32_t)bytes;
@@ -457,6 +485,7 @@ bool build_tile_host(int form, int64_t N, int32_t n_nodes, int32_t n, int64_t nn
         }
         if (!sents.empty()) std::memcpy(bp + hdr.off_side, sents.data(), sizeof(SideEnt) * sents.size());
         if (!dsts.empty()) std::memcpy(bp + hdr.off_dst, dsts.data(), 4 * dsts.size());
+        if (!meta.empty()) std::memcpy(bp + hdr.off_meta, meta.data(), 4 * meta.size());
         if (!ents.empty()) std::memcpy(bp + hdr.off_ent, ents.data(), 2 * ents.size());
         o.n_own = n_own;
         o.n_sent = n_sent;

@@ -107,6 +107,42 @@ def test_parity_full_size(cuda_ok, cfg):
     ctx.close()
 
 
+@pytest.mark.slow
+@pytest.mark.parametrize("cfg", [2, 4])
+def test_parity_full_size_color_high_c(cuda_ok, cfg):
+    """The colour-phased variants at full size where C is in the thousands
+    (cfg2 C = 2,052, cfg4 C = 4,088; one launch per colour): COLOR and
+    COLOR_BUF under the default rule, every entry against the oracle."""
+    nl = netgen.config(cfg)
+    ref = reference(nl, key=("full", cfg))
+    ctx = ctx_for(nl, variant="color")
+    assert ctx.stats()["n_colors"] > 2000
+    for v in ("color", "color_buf"):
+        A, b = gpu_run(ctx, nl, v)
+        assert_parity(ref, A, b, f"cfg{cfg} full {v}")
+    ctx.close()
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("cfg", [0, 1])
+def test_parity_full_size_paper_rule(cuda_ok, cfg):
+    """The paper-literal conflict rule (every shared non-ground node,
+    VDD included) at full size: cfg0 C = 1,001, cfg1 C = 101,001 colour
+    phases; colouring bit-equal to the oracle's and conflict-free, every
+    variant within tolerance."""
+    nl = netgen.config(cfg)
+    ref = reference(nl, key=("full", cfg))
+    ctx = ctx_for(nl, variant="color", rule="paper")
+    col, C = ctx.colors()
+    ocol, oC = oracle.greedy_color(nl, "paper")
+    assert C == oC and np.array_equal(col, ocol)
+    assert oracle.color_violations(nl, col, C, "paper") == 0
+    for v in VARIANTS:
+        A, b = gpu_run(ctx, nl, v)
+        assert_parity(ref, A, b, f"cfg{cfg} full paper-rule {v}")
+    ctx.close()
+
+
 # ---------------------------------------------------------------- colour sweep (B5)
 @pytest.mark.parametrize("ct", [1, 2, 7, 64, 333])
 def test_parity_synth(cuda_ok, ct):
