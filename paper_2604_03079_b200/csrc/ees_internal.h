@@ -169,7 +169,10 @@ static_assert(8 * kScSlots < 65536, "entry byte offsets must fit 16 bits");
 // with cls_group(L) lanes per target (about four entries per lane, at most a
 // warp).  Measured (profiles/r02_ab.md): one thread for L = 5 beats two on
 // cfg2; lane groups for L > 6 beat one thread on cfg3.
-constexpr int kShortMax = 6;
+#ifndef EES_SHORT_MAX
+#define EES_SHORT_MAX 6
+#endif
+constexpr int kShortMax = EES_SHORT_MAX;
 __host__ __device__ constexpr int cls_group(int L)
 {
     return L <= kShortMax ? 1 : L <= 8 ? 2 : L <= 16 ? 4 : L <= 32 ? 8 : L <= 64 ? 16 : 32;

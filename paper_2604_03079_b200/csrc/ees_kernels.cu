@@ -1392,30 +1392,25 @@ __device__ __forceinline__ void tile_reduce(const unsigned char *blob, const uns
     const SideEnt *sents = reinterpret_cast<const SideEnt *>(blob + h->off_side);
     const uint32_t *meta = reinterpret_cast<const uint32_t *>(blob + h->off_meta);
     const int ncl = h->n_cls;
-    int ci = 0;
-    for (; ci < ncl && cls[ci].len == 0; ci++)                // group classes (warp-uniform)
-        tile_cls_group(cls[ci], r, dst + cls[ci].dst, meta + cls[ci].meta, ent, sc, sents, out, tk, s_hot);
-    if (ci >= ncl) return;
-    // short classes, walked as one list: thread r takes short targets q =
-    // r - rot, +kTileThreads, ... (rot: lanes the group classes used), and
-    // advances through the classes as q passes their ends
-    TileCls c = cls[ci];
-    int qb = 0;                                               // first short index of class ci
-    for (int q = (r - (int)c.rot) & (kTileThreads - 1);; q += kTileThreads) {
-        while (q >= qb + (int)c.n) {
-            qb += c.n;
-            if (++ci >= ncl) return;
-            c = cls[ci];
-        }
-        const int k = q - qb;
+    for (int ci = 0; ci < ncl; ci++) {
+        const TileCls c = cls[ci];
         const uint16_t *e = ent + c.ent;
         const int32_t *dc = dst + c.dst;
+        if (c.len == 0) {                              // group class (warp-uniform)
+            tile_cls_group(c, r, dc, meta + c.meta, ent, sc, sents, out, tk, s_hot);
+            continue;
+        }
+        // short class: targets k = r - rot, +kTileThreads, ... (rot continues the
+        // lane position from the classes before, so the threads' loads stay even)
+        const int n = c.n;
+        const int k0 = (r - (int)c.rot) & (kTileThreads - 1);
+        if (k0 >= n) continue;                         // no target of this class here
         switch (c.len) {
-        case 1: tile_one<1>(k, c.n, 1, dc, e, sc, sents, out, tk, s_hot); break;
-        case 2: tile_one<2>(k, c.n, 2, dc, e, sc, sents, out, tk, s_hot); break;
-        case 3: tile_one<3>(k, c.n, 3, dc, e, sc, sents, out, tk, s_hot); break;
-        case 4: tile_one<4>(k, c.n, 4, dc, e, sc, sents, out, tk, s_hot); break;
-        default: tile_one<0>(k, c.n, c.len, dc, e, sc, sents, out, tk, s_hot); break;
+        case 1: for (int k = k0; k < n; k += kTileThreads) tile_one<1>(k, n, 1, dc, e, sc, sents, out, tk, s_hot); break;
+        case 2: for (int k = k0; k < n; k += kTileThreads) tile_one<2>(k, n, 2, dc, e, sc, sents, out, tk, s_hot); break;
+        case 3: for (int k = k0; k < n; k += kTileThreads) tile_one<3>(k, n, 3, dc, e, sc, sents, out, tk, s_hot); break;
+        case 4: for (int k = k0; k < n; k += kTileThreads) tile_one<4>(k, n, 4, dc, e, sc, sents, out, tk, s_hot); break;
+        default: for (int k = k0; k < n; k += kTileThreads) tile_one<0>(k, n, c.len, dc, e, sc, sents, out, tk, s_hot); break;
         }
     }
 }

@@ -65,7 +65,7 @@ def main(src, dst):
     os.makedirs(os.path.dirname(dst) or ".", exist_ok=True)
     lines = bench_lines(src)
     md = ["# bench + ncu summary", "", f"source: `{src}`", ""]
-    md.append("| file | config | variant | FET/s | ms/step | kernel ms | roofline frac | frac of same-size stream | e2e FET/s |")
+    md.append("| file | config | variant | FET/s | ms/step | kernel ms | roofline frac | frac of stream probe | e2e FET/s |")
     md.append("|---|---|---|---|---|---|---|---|---|")
     for j in lines:
         r = j.get("roofline", {})
@@ -74,6 +74,11 @@ def main(src, dst):
                   f"{j['value']:.3e} | {j['ms_per_step']:.4f} | {r.get('kernel_ms', 0):.4f} | "
                   f"{r.get('frac', 0):.3f} | {(r.get('stream_ref') or {}).get('frac', float('nan')):.3f} | "
                   f"{e.get('value', 0):.3e} |")
+        for name, pc in (j.get("per_config") or {}).items():
+            pr = pc.get("roofline", {})
+            md.append(f"| {j['_file']} per_config | {name} | {pc.get('variant')} | {pc['value']:.3e} | "
+                      f"{pc['ms_per_step']:.4f} | {pr.get('kernel_ms', 0):.4f} | {pr.get('frac', 0):.3f} | "
+                      f"{pc.get('stream_ref_frac', float('nan')):.3f} | |")
     md.append("")
     reps = sorted(glob.glob(os.path.join(src, "*.ncu-rep")))
     ncu = {}
@@ -88,7 +93,7 @@ def main(src, dst):
                     md.append(f"  - {k}: {d[k]}")
         md.append("")
     open(dst + ".md", "w").write("\n".join(md) + "\n")
-    update_traffic(ncu)
+    update_traffic(ncu, src, os.path.basename(dst))
     json.dump({"bench": lines, "ncu": ncu}, open(dst + ".json", "w"), indent=1)
     print(dst + ".md")
 
@@ -101,12 +106,19 @@ def _bytes(v):
     return float(num) * _UNIT[unit]
 
 
-def update_traffic(ncu):
+def update_traffic(ncu, src, profile):
     """profiles/traffic.json: DRAM read+write bytes per launch of the dominant
     kernel, from `ncu --set full` captures named prof_c<cfg>_<variant>.ncu-rep
-    (bench.py reports it as roofline.traffic)."""
+    (bench.py reports it as roofline.traffic), tagged with the profile name
+    and the hash of the kernel sources the capture ran on (src_hash.txt
+    written by the GPU script; bench.py drops a figure whose hash differs)."""
     path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "profiles", "traffic.json")
     d = json.load(open(path)) if os.path.exists(path) else {}
+    hf = os.path.join(src, "src_hash.txt")
+    if not os.path.exists(hf):
+        print("no src_hash.txt in", src, "- traffic.json not updated")
+        return
+    h = open(hf).read().strip()
     for rep, rows in ncu.items():
         m = re.match(r"prof_c(\d)_(\w+?)\.ncu-rep", rep)
         if not m or not rows:
@@ -114,8 +126,9 @@ def update_traffic(ncu):
         r = rows[0]
         if "dram__bytes_read.sum" not in r:
             continue
-        d.setdefault(f"cfg{m.group(1)}", {})[m.group(2)] = _bytes(r["dram__bytes_read.sum"]) + \
-            _bytes(r["dram__bytes_write.sum"])
+        d.setdefault(f"cfg{m.group(1)}", {})[m.group(2)] = {
+            "bytes": _bytes(r["dram__bytes_read.sum"]) + _bytes(r["dram__bytes_write.sum"]),
+            "profile": f"{profile} ({rep})", "src_hash": h}
     json.dump(d, open(path, "w"), indent=1, sort_keys=True)
 
 

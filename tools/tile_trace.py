@@ -36,16 +36,14 @@ def main():
         return "p10 %.2f p50 %.2f p90 %.2f max %.2f us" % tuple(np.percentile(a, [10, 50, 90, 100]) / 1e3)
     print(" start     ", q(rel[:, 0]))
     print(" staged    ", q(rel[:, 1]))
-    for i in range(4):
-        s = 2 + 4 * i
-        ok = (tr[:, s] > 0) & (tr[:, s - 1 if i == 0 else s - 1] > 0)
+    for i in range(6):
+        s = 2 + 2 * i                      # slots: 2+2i evaluated (+ next gathers), 3+2i reduced
+        prev = tr[:, 1] if i == 0 else tr[:, s - 1]
+        ok = (tr[:, s] > 0) & (prev > 0) & (tr[:, s + 1] > 0)
         if not ok.any():
             break
-        prev = tr[:, 1] if i == 0 else tr[:, s - 1]
-        print(f" tile{i}: eval+gather {q(np.where(ok, tr[:, s] - prev, -1))}")
-        print(f"        B1+sums {q(np.where(ok, tr[:, s + 1] - tr[:, s], -1))}")
-        print(f"        B2+fix+B3 {q(np.where(ok, tr[:, s + 2] - tr[:, s + 1], -1))}")
-        print(f"        write {q(np.where(ok, tr[:, s + 3] - tr[:, s + 2], -1))}")
+        print(f" tile{i}: (B0+) eval+gather {q(np.where(ok, tr[:, s] - prev, -1))}")
+        print(f"        B1+reduce+RED {q(np.where(ok, tr[:, s + 1] - tr[:, s], -1))}")
     print(" ticket    ", q(rel[:, 62]), "(side targets finished by the last CTA)" if (tr[:, 62] > 0).any()
           else "(none: no inline side finish)")
     print(" end       ", q(rel[:, 63]))
