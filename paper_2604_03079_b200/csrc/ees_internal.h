@@ -138,8 +138,13 @@ struct GatherK {
 // Contributions of a FET whose source and bulk are one node (every PMOS of the
 // inverter configs) are merged at evaluation (DB into DS, BD into SD, BB into
 // SS, J[B] into J[S]) and the merged-away slots are not listed.
-constexpr int kTileItems = 128;      // max items (FET copies) per tile = threads per CTA
-constexpr int kTileThreads = 128;
+#ifndef EES_TILE_ITEMS
+#define EES_TILE_ITEMS 128
+#endif
+constexpr int kTileItems = EES_TILE_ITEMS;   // max items (FET copies) per tile = threads per CTA
+constexpr int kTileThreads = kTileItems;
+constexpr int kLogTileThreads = kTileThreads == 128 ? 7 : kTileThreads == 64 ? 6 : kTileThreads == 256 ? 8 : -1;
+static_assert(kLogTileThreads > 0, "tile width must be 64, 128 or 256 threads");
 constexpr int kHeavyDeg = 64;        // nodes with more incident FETs are heavy
 constexpr int kMaxCls = 15;          // distinct target lengths per tile
 constexpr int kSidePiece = 4;        // side-target entries per piece (an unrolled class)
@@ -147,7 +152,7 @@ constexpr int kHotPieces = 24;       // pieces of one hot target per tile
 // TILE forms (chosen at setup from the FET copy factor, ees_host.cpp):
 // stage bytes (one tile blob), item bytes in the blob, shared-memory slot
 // buffers (2: one barrier per tile), CTAs per SM
-__host__ __device__ constexpr int stage_max(int form) { return form ? 7680 : 11264; }
+__host__ __device__ constexpr int stage_max(int form) { return (form ? 7680 : 11264) * kTileItems / 128; }
 __host__ __device__ constexpr int item_blob_bytes(int form) { return form ? 16 : 49; }
 #ifndef EES_TILE_BUF1
 #define EES_TILE_BUF1 1
@@ -156,7 +161,10 @@ __host__ __device__ constexpr int item_blob_bytes(int form) { return form ? 16 :
 #define EES_TILE_BUF0 1
 #endif
 __host__ __device__ constexpr int tile_bufs(int form) { return form ? EES_TILE_BUF1 : EES_TILE_BUF0; }
-__host__ __device__ constexpr int tile_ctas(int form) { return form ? (tile_bufs(1) == 2 ? 4 : 5) : (tile_bufs(0) == 2 ? 3 : 4); }
+__host__ __device__ constexpr int tile_ctas(int form)
+{
+    return (form ? (tile_bufs(1) == 2 ? 4 : 5) : (tile_bufs(0) == 2 ? 3 : 4)) * 128 / kTileItems;
+}
 
 constexpr int kStages = 3;           // TMA pipeline depth (blobs in flight per CTA)
 constexpr int kScSlots = 16 * kTileItems + 2;   // contribution slots per buffer (+16-byte pad)

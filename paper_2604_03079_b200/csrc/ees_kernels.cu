@@ -1276,8 +1276,7 @@ __device__ __forceinline__ void tile_cls_group(const TileCls c, int r, const int
                                                double *s_hot)
 {
     const int n = c.n, lg = c.lg, gs = 1 << lg;
-    static_assert(kTileThreads == 128, "lgn assumes 128 threads");
-    const int lgn = 7 - lg;                               // log2(kTileThreads / gs)
+    const int lgn = kLogTileThreads - lg;                 // log2(kTileThreads / gs)
     const int gi = r >> lg, lj = r & (gs - 1);
     const int k0 = (gi - (int)c.rot) & ((1 << lgn) - 1);
     const int mine = k0 < n ? ((n - 1 - k0) >> lgn) + 1 : 0;
