@@ -158,6 +158,9 @@ typedef struct {
     int32_t gather_form;                    /* EES_GATHER: 0 compact buffer + index lists, 1 target-ordered */
     int32_t n_color_side_targets;           /* EES_CONFLICT_HYBRID: entries summed after the colours */
     int64_t n_color_side_contributions;     /* their contributions (scratch slots) */
+    int32_t atomic_form;                    /* EES_ATOMIC: 0 one RED per contribution, 1 one RED per
+                                               run of equal entries in a warp (timed at setup) */
+    int32_t reserved0;
 } ees_stats_t;
 
 /* Build everything that depends only on topology ("constructs the FET

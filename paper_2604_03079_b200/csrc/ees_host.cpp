@@ -73,6 +73,7 @@ struct ees_ctx {
     int64_t *d_color_ptr = nullptr;
     double *coop_partials = nullptr;
     int atomic_grid = 1;
+    int atomic_agg = 1;                   // ATOMIC: warp run aggregation (timed at setup)
     int32_t variant = EES_ATOMIC;
     int32_t launches = 0;
     int32_t work = 1;                     // S:229 work multiplier
@@ -434,7 +435,7 @@ ees_status enqueue(ees_ctx *c, int32_t variant, const double *x, double h, doubl
     cudaError_t e = cudaSuccess;
     if (variant == EES_ATOMIC) {
         PhaseMark m(c, st, 0, timed);
-        e = launch_atomic(c->L_atomic.k(), call, c->atomic_grid, st);
+        e = launch_atomic(c->L_atomic.k(), call, c->atomic_grid, c->atomic_agg != 0, st);
         nl = c->n_dev ? 1 : 0;
     } else if (variant == EES_COLOR && c->hybrid) {
         const DevK dv = c->L_colorh.k();
@@ -1043,7 +1044,8 @@ ees_status autotune(ees_ctx *c, bool full)
     // layout override (ees.h): force the COLOR form instead of timing both
     const char *mode = (c->setup_flags & EES_SETUP_COLOR_LAUNCH) ? "launch"
                        : (c->setup_flags & EES_SETUP_COLOR_COOP) ? "coop" : nullptr;
-    for (int32_t v = EES_COLOR; v <= (full ? EES_COLOR_BUF : EES_COLOR) && rc == EES_OK; v++) {
+    for (int32_t v = EES_COLOR; v <= EES_COLOR_BUF && rc == EES_OK; v++) {
+        if (!full && v != c->variant) continue;          // an explicit variant: its forms only
         double ms;
         if (v == EES_COLOR_BUF) {
             if (c->n_colors > 512) { c->st.tune_ms[v] = -1; continue; }
@@ -1055,6 +1057,16 @@ ees_status autotune(ees_ctx *c, bool full)
         } else if (v == EES_COLOR && mode && (!std::strcmp(mode, "launch") || !std::strcmp(mode, "coop"))) {
             c->color_coop = !std::strcmp(mode, "coop") && c->coop_grid > 0;
             ms = time_variant(v);
+        } else if (v == EES_ATOMIC) {
+            // both ATOMIC forms: plain REDs, and one RED per run of equal entries
+            c->atomic_agg = 0;
+            ms = time_variant(v);
+            if (rc == EES_OK) {
+                c->atomic_agg = 1;
+                const double ms2 = time_variant(v);
+                if (ms2 < ms) ms = ms2;
+                else c->atomic_agg = 0;
+            }
         } else if (v == EES_COLOR) {
             // colour phasing pays one barrier per colour: past 512 colours it is
             // launch/barrier-bound by construction, not worth timing
@@ -1178,7 +1190,7 @@ ees_status setup_impl(const ees_desc *d, ees_ctx *c)
         TRY(autotune(c, true));
     } else {
         c->variant = d->variant;
-        if (d->variant == EES_COLOR) TRY(autotune(c, false));   // pick the COLOR form
+        if (d->variant == EES_COLOR || d->variant == EES_ATOMIC) TRY(autotune(c, false));   // pick its form
     }
     c->st.setup_s = now_s() - t0;
     return EES_OK;
@@ -1373,6 +1385,7 @@ ees_status ees_stats(const ees_ctx *c, ees_stats_t *out)
     out->variant_chosen = c->variant;
     out->n_rail_entries = c->n_rail_entries;
     out->launches_per_call = c->launches;
+    out->atomic_form = c->atomic_agg;
     return EES_OK;
 }
 

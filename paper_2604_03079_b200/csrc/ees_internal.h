@@ -195,7 +195,7 @@ struct TileCls {
                                      // groups per CTA (kTileThreads / gs)
     uint16_t lg;                     // group classes: log2 of the group size gs
     uint16_t meta;                   // group classes: index of the first target's meta[] word
-    uint16_t pad;
+    uint16_t side;                   // short classes: 1 = side pieces (destinations < 0), 0 = owned
 };
 static_assert(sizeof(TileCls) == 16, "TileCls layout");
 
@@ -294,7 +294,7 @@ cudaError_t launch_stream_probe(const void *src, int64_t read_bytes, void *dst, 
                                 double *sink, cudaStream_t st);
 int tile_blocks_per_sm(int form);
 cudaError_t launch_tile(const TileK &tk, const CallK &call, int grid, cudaStream_t st, int *n_launches);
-cudaError_t launch_atomic(const DevK &dv, const CallK &call, int grid, cudaStream_t st);
+cudaError_t launch_atomic(const DevK &dv, const CallK &call, int grid, bool agg, cudaStream_t st);
 cudaError_t launch_color(const DevK &dv, const CallK &call, int64_t begin, int64_t count,
                          double *partials, cudaStream_t st);
 int color_coop_blocks_per_sm();

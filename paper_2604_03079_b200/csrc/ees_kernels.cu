@@ -192,7 +192,9 @@ __device__ __forceinline__ void merge_source_bulk(const int4 &T, Stamp &st, int3
 // (one shuffle + vote) whether a lane repeats its left neighbour's entry; if
 // so, a segmented warp scan sums each run of equal entries and only the run's
 // last lane issues the RED -- one same-address RED per run instead of one per
-// lane (the L2 serialises same-address atomics, P:31's lock analogue).
+// lane (the L2 serialises same-address atomics, P:31's lock analogue).  The
+// scan costs instructions where runs are short and the kernel is latency
+// bound (cfg1), so setup times both forms (kAgg) and keeps the faster.
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void red_run(double *base, int32_t k, double v, int lane)
 {
@@ -216,8 +218,11 @@ __device__ __forceinline__ void red_run(double *base, int32_t k, double v, int l
     }
 }
 
-template <bool kRep>
-__global__ void __launch_bounds__(kBlock, 4) k_atomic(DevK dv, CallK P)
+#ifndef EES_ATOMIC_MINB
+#define EES_ATOMIC_MINB 4          // resident 256-thread blocks per SM the register budget targets
+#endif
+template <bool kRep, bool kAgg>
+__global__ void __launch_bounds__(kBlock, EES_ATOMIC_MINB) k_atomic(DevK dv, CallK P)
 {
     __shared__ CardK s_cards[EES_MAX_MODELS];
     __shared__ double s_railx[EES_MAX_RAILS];
@@ -267,10 +272,19 @@ __global__ void __launch_bounds__(kBlock, 4) k_atomic(DevK dv, CallK P)
 #pragma unroll
             for (int a = 0; a < 4; a++) st.j[a] = 0.0;
         }
+        if (kAgg) {
 #pragma unroll
-        for (int p = 0; p < NPAIR; p++) red_run(P.A, slot[p], st.y[p], lane);
+            for (int p = 0; p < NPAIR; p++) red_run(P.A, slot[p], st.y[p], lane);
 #pragma unroll
-        for (int a = 0; a < 4; a++) red_run(P.b, tc[a], st.j[a], lane);
+            for (int a = 0; a < 4; a++) red_run(P.b, tc[a], st.j[a], lane);
+        } else {
+#pragma unroll
+            for (int p = 0; p < NPAIR; p++)
+                if (slot[p] >= 0) atomicAdd(P.A + slot[p], st.y[p]);
+#pragma unroll
+            for (int a = 0; a < 4; a++)
+                if (tc[a] >= 0) atomicAdd(P.b + tc[a], st.j[a]);
+        }
         if (P.n_rail_entries) rail_accumulate(P, slot, tc, st, valid, s_acc);
     }
     if (P.n_rail_entries) {
@@ -885,16 +899,22 @@ static size_t rail_smem(const CallK &P) { return sizeof(double) * (kBlock / 32) 
 int atomic_blocks_per_sm()
 {
     int nb = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_atomic<false>, kBlock,
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_atomic<false, true>, kBlock,
                                                   sizeof(double) * (kBlock / 32) * kMaxRailEntries);
     return nb > 0 ? nb : 1;
 }
 
-cudaError_t launch_atomic(const DevK &dv, const CallK &call, int grid, cudaStream_t st)
+cudaError_t launch_atomic(const DevK &dv, const CallK &call, int grid, bool agg, cudaStream_t st)
 {
     if (dv.N == 0) return cudaSuccess;
-    if (call.work > 1) k_atomic<true><<<grid, kBlock, rail_smem(call), st>>>(dv, call);
-    else k_atomic<false><<<grid, kBlock, rail_smem(call), st>>>(dv, call);
+    const size_t sm = rail_smem(call);
+    if (call.work > 1) {
+        if (agg) k_atomic<true, true><<<grid, kBlock, sm, st>>>(dv, call);
+        else k_atomic<true, false><<<grid, kBlock, sm, st>>>(dv, call);
+    } else {
+        if (agg) k_atomic<false, true><<<grid, kBlock, sm, st>>>(dv, call);
+        else k_atomic<false, false><<<grid, kBlock, sm, st>>>(dv, call);
+    }
     return cudaPeekAtLastError();
 }
 
@@ -1248,7 +1268,7 @@ __device__ __forceinline__ void tile_put(const SideEnt *sents, const TileOut &o,
 // One target k of a short class: entries [len][n] (byte offsets into the
 // slot buffer), summed in list order; L > 0 the length at compile time
 // (unrolled), L = 0 at run time (len <= kShortMax).
-template <int L>
+template <int L, bool kSide>
 __device__ __forceinline__ void tile_one(int k, int n, int len, const int32_t *dst, const uint16_t *ent,
                                          const unsigned char *sc, const SideEnt *sents, const TileOut &o,
                                          const TileK &tk, double *s_hot)
@@ -1262,7 +1282,8 @@ __device__ __forceinline__ void tile_one(int k, int n, int len, const int32_t *d
 #pragma unroll 2
         for (int p = 1; p < len; p++) v += *reinterpret_cast<const double *>(sc + ent[p * n + k]);
     }
-    tile_put(sents, o, tk, s_hot, g, v);
+    if (kSide) tile_put(sents, o, tk, s_hot, g, v);           // a side piece
+    else red_add((g < o.nnz ? o.A : o.Bm) + g, v);            // an owned target: one RED
 }
 
 // A group class (targets of L > kShortMax with one group size gs = cls_group(L)): a
@@ -1404,13 +1425,25 @@ __device__ __forceinline__ void tile_reduce(const unsigned char *blob, const uns
         const int n = c.n;
         const int k0 = (r - (int)c.rot) & (kTileThreads - 1);
         if (k0 >= n) continue;                         // no target of this class here
-        switch (c.len) {
-        case 1: for (int k = k0; k < n; k += kTileThreads) tile_one<1>(k, n, 1, dc, e, sc, sents, out, tk, s_hot); break;
-        case 2: for (int k = k0; k < n; k += kTileThreads) tile_one<2>(k, n, 2, dc, e, sc, sents, out, tk, s_hot); break;
-        case 3: for (int k = k0; k < n; k += kTileThreads) tile_one<3>(k, n, 3, dc, e, sc, sents, out, tk, s_hot); break;
-        case 4: for (int k = k0; k < n; k += kTileThreads) tile_one<4>(k, n, 4, dc, e, sc, sents, out, tk, s_hot); break;
-        default: for (int k = k0; k < n; k += kTileThreads) tile_one<0>(k, n, c.len, dc, e, sc, sents, out, tk, s_hot); break;
+#define TILE_ONE(L, S) for (int k = k0; k < n; k += kTileThreads) tile_one<L, S>(k, n, c.len, dc, e, sc, sents, out, tk, s_hot)
+        if (c.side) {                                  // side pieces (lengths 1 .. kSidePiece)
+            switch (c.len) {
+            case 1: TILE_ONE(1, true); break;
+            case 2: TILE_ONE(2, true); break;
+            case 3: TILE_ONE(3, true); break;
+            case 4: TILE_ONE(4, true); break;
+            default: TILE_ONE(0, true); break;
+            }
+        } else {
+            switch (c.len) {
+            case 1: TILE_ONE(1, false); break;
+            case 2: TILE_ONE(2, false); break;
+            case 3: TILE_ONE(3, false); break;
+            case 4: TILE_ONE(4, false); break;
+            default: TILE_ONE(0, false); break;
+            }
         }
+#undef TILE_ONE
     }
 }
 

@@ -389,11 +389,14 @@ bool build_tile_host(int form, int64_t N, int32_t n_nodes, int32_t n, int64_t nn
         }
         const int32_t n_sent = (int32_t)sents.size();
         o.listed += (int64_t)con.size() + (int64_t)side.size();
-        // classes: group classes (L > 4, by lane-group size, largest first),
-        // then one per short length 4..1; targets in list order
-        auto cls_key = [](int32_t L) { return L > kShortMax ? 100 + cls_group(L) : L; };
-        std::stable_sort(tg.begin(), tg.end(),
-                         [&](const Tgt &a, const Tgt &b) { return cls_key(a.len) > cls_key(b.len); });
+        // classes: group classes (L > kShortMax, by lane-group size, largest
+        // first), then short side classes (pieces, one per length), then short
+        // owned classes (one per length, their threads never branch to a side
+        // entry); targets in list order within a class
+        auto cls_key = [](const Tgt &t2) {
+            return t2.len > kShortMax ? 100 + cls_group(t2.len) : (t2.is_side ? 50 : 0) + t2.len;
+        };
+        std::stable_sort(tg.begin(), tg.end(), [&](const Tgt &a, const Tgt &b) { return cls_key(a) > cls_key(b); });
         cls.clear();
         dsts.clear();
         ents.clear();
@@ -401,8 +404,8 @@ bool build_tile_host(int form, int64_t N, int32_t n_nodes, int32_t n, int64_t nn
         int64_t cum = 0;
         for (size_t k = 0; k < tg.size();) {
             size_t e = k;
-            const int key = cls_key(tg[k].len);
-            while (e < tg.size() && cls_key(tg[e].len) == key) e++;
+            const int key = cls_key(tg[k]);
+            while (e < tg.size() && cls_key(tg[e]) == key) e++;
             const int32_t nc = (int32_t)(e - k);
             if (nc > 65535 || ents.size() > 65535 || dsts.size() > 65535 || meta.size() > 65535) return false;
             TileCls tc;
@@ -431,6 +434,7 @@ bool build_tile_host(int form, int64_t N, int32_t n_nodes, int32_t n, int64_t nn
             } else {
                 const int32_t L = tg[k].len;
                 tc.len = (uint16_t)L;
+                tc.side = (uint16_t)(key > 50 ? 1 : 0);
                 for (size_t q = k; q < e; q++) dsts.push_back(tg[q].dst);
                 for (int32_t p = 0; p < L; p++)
                     for (size_t q = k; q < e; q++) ents.push_back(entry(tg[q], p));

@@ -5,6 +5,9 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>
 if [ "${RUN_TESTS:-1}" = 1 ]; then
 timeout 2400 python -m pytest tests -m gpu -q --timeout 900 > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $O/rc.txt
 fi
+if [ "${DEFAULT_BENCH:-0}" = 1 ]; then
+timeout 900 python bench.py --steps 20 --warmup 5 --no-cpu-baseline > $O/bench_default.log 2>&1; echo "bench default rc=$?" >> $O/rc.txt
+fi
 B="python bench.py --no-cpu-baseline --no-e2e --per-config none --steps 30"
 for c in 4 2 3; do
   timeout 300 $B --config $c --variant tile > $O/bench_c${c}_tile.log 2>&1; echo "bench c$c rc=$?" >> $O/rc.txt
