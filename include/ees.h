@@ -256,9 +256,9 @@ ees_status ees_race_probe(ees_ctx *ctx, const int32_t *color, int64_t *n_conflic
 
 /* Debug: one EES_TILE call that also records %globaltimer stamps (ns) per
  * CTA into trace [n_ctas][64] (host, cap entries): slot 0 start, 1 first tile
- * staged, per tile i < 15: 2+4i evaluated (and the next tile's gathers
- * issued), 3+4i segment sums done, 4+4i carries fixed up, 5+4i owned entries
- * stored; 62 ticket taken, 63 end.  Synchronous. */
+ * staged, per tile i < 30: 2+2i evaluated (and the next tile's gathers
+ * issued), 3+2i reduced and written; 62 past the grid barrier before the side
+ * sums (side targets only), 63 end.  Synchronous. */
 ees_status ees_tile_trace(ees_ctx *ctx, const double *x, double h, double *A_vals, double *b,
                           ees_stream stream, uint64_t *trace, int64_t cap, int32_t *n_ctas);
 

@@ -978,11 +978,9 @@ ees_status build_tile(const ees_desc *d, ees_ctx *c, const std::vector<int32_t> 
     TRY(up(&k.sd_part, th.sd_part));
     TRY(up(&k.hot_gid, th.hot_gid));
     k.n_side = th.n_side;
-    k.side_inline = th.n_parts <= kSideInlineParts;
     k.n_hot = th.n_hot;
     k.hot_base = th.hot_base;
-    TRY(dalloc(c, &k.done, 1));
-    if (cudaMemset(k.done, 0, sizeof(uint32_t)) != cudaSuccess) return EES_ECUDA;
+    TRY(dalloc(c, &k.hot_pre, (size_t)std::max(1, th.n_hot)));
     TRY(dalloc(c, &k.part, (size_t)th.n_parts));
     // persistent CTAs: no more than tiles (the hot parts are laid out for
     // `grid` CTAs; k_tile sums the first gridDim.x of them)

@@ -148,11 +148,17 @@ static_assert(kLogTileThreads > 0, "tile width must be 64, 128 or 256 threads");
 constexpr int kHeavyDeg = 64;        // nodes with more incident FETs are heavy
 constexpr int kMaxCls = 15;          // distinct target lengths per tile
 constexpr int kSidePiece = 4;        // side-target entries per piece (an unrolled class)
-constexpr int kHotPieces = 24;       // pieces of one hot target per tile
+#ifndef EES_HOT_PIECES
+#define EES_HOT_PIECES 24
+#endif
+constexpr int kHotPieces = EES_HOT_PIECES;   // pieces of one hot target per tile
 // TILE forms (chosen at setup from the FET copy factor, ees_host.cpp):
 // stage bytes (one tile blob), item bytes in the blob, shared-memory slot
 // buffers (2: one barrier per tile), CTAs per SM
-__host__ __device__ constexpr int stage_max(int form) { return (form ? 7680 : 11264) * kTileItems / 128; }
+#ifndef EES_STAGE1
+#define EES_STAGE1 7680
+#endif
+__host__ __device__ constexpr int stage_max(int form) { return (form ? EES_STAGE1 : 11264) * kTileItems / 128; }
 __host__ __device__ constexpr int item_blob_bytes(int form) { return form ? 16 : 49; }
 #ifndef EES_TILE_BUF1
 #define EES_TILE_BUF1 1
@@ -163,13 +169,18 @@ __host__ __device__ constexpr int item_blob_bytes(int form) { return form ? 16 :
 __host__ __device__ constexpr int tile_bufs(int form) { return form ? EES_TILE_BUF1 : EES_TILE_BUF0; }
 __host__ __device__ constexpr int tile_ctas(int form)
 {
-    return (form ? (tile_bufs(1) == 2 ? 4 : 5) : (tile_bufs(0) == 2 ? 3 : 4)) * 128 / kTileItems;
+#ifndef EES_TILE_CTAS1
+#define EES_TILE_CTAS1 5
+#endif
+    return (form ? (tile_bufs(1) == 2 ? 4 : EES_TILE_CTAS1) : (tile_bufs(0) == 2 ? 3 : 4)) * 128 / kTileItems;
 }
 
 constexpr int kStages = 3;           // TMA pipeline depth (blobs in flight per CTA)
 constexpr int kScSlots = 16 * kTileItems + 2;   // contribution slots per buffer (+16-byte pad)
-constexpr int64_t kSideInlineParts = 8192;   // up to this many parts: last CTA finalises
-constexpr int kMaxHot = 16;          // side targets pre-reduced per CTA (rails): parts = CTAs, not tiles
+#ifndef EES_MAX_HOT
+#define EES_MAX_HOT 16
+#endif
+constexpr int kMaxHot = EES_MAX_HOT;  // side targets pre-reduced per CTA (rails): parts = CTAs, not tiles
 static_assert(8 * kScSlots < 65536, "entry byte offsets must fit 16 bits");
 
 // Targets of up to kShortMax contributions form short classes (one per exact
@@ -195,7 +206,7 @@ struct TileCls {
                                      // groups per CTA (kTileThreads / gs)
     uint16_t lg;                     // group classes: log2 of the group size gs
     uint16_t meta;                   // group classes: index of the first target's meta[] word
-    uint16_t side;                   // short classes: 1 = side pieces (destinations < 0), 0 = owned
+    uint16_t pad;
 };
 static_assert(sizeof(TileCls) == 16, "TileCls layout");
 
@@ -221,7 +232,7 @@ struct TileK {
     const int64_t *blob_off;       // [T+1] byte offsets into blob
     const uint8_t *blob;
     int32_t n_side;
-    int32_t side_inline;           // 1: the last CTA finalises side targets; 0: k_side_final
+    int32_t pad0;
     int32_t n_hot;                 // hot side targets: CTA b's part at part[hot_base + h*grid + b]
     int64_t hot_base;
     const int32_t *sd_gid;         // [n_side] global target
@@ -230,7 +241,7 @@ struct TileK {
     const double *item_beta;       // [n_tiles * kTileItems]
     const double *item_v0;         // [n_tiles * kTileItems][3]
     const uint8_t *item_model;     // [n_tiles * kTileItems]
-    uint32_t *done;                // CTA completion ticket, self-resetting
+    double *hot_pre;               // [n_hot] old values of the hot targets (read by CTA 0)
     double *part;                  // [n_side_entries]
     unsigned long long *trace;     // debug: [grid][kTraceSlots] %globaltimer stamps, or null
 };

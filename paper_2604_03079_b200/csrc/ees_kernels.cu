@@ -1161,7 +1161,7 @@ cudaError_t launch_count_conflicts(const int32_t *cnt, int64_t n, unsigned long 
 //           the CTA's running sum in shared memory (tile order);
 //   (B0)    with one slot buffer, a barrier before the next evaluation.
 // After the last tile, hot partials are stored per CTA, and side targets are
-// summed in part order by the last CTA (few parts) or k_side_final.
+// summed in part order by the warps of the whole grid after a grid barrier.
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void *p)
 {
@@ -1241,7 +1241,11 @@ __device__ __forceinline__ void tile_gather(const unsigned char *blob, int32_t t
 // FP64 reduction without a result (RED.E.ADD.F64): fire and forget
 __device__ __forceinline__ void red_add(double *p, double v)
 {
+#ifdef EES_DIAG_STORE            // diagnostic A/B only (wrong sums): a plain store instead
+    *p = v;
+#else
     asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+#endif
 }
 
 // Destination of one target (ees_internal.h): g >= 0 the global target --
@@ -1268,7 +1272,7 @@ __device__ __forceinline__ void tile_put(const SideEnt *sents, const TileOut &o,
 // One target k of a short class: entries [len][n] (byte offsets into the
 // slot buffer), summed in list order; L > 0 the length at compile time
 // (unrolled), L = 0 at run time (len <= kShortMax).
-template <int L, bool kSide>
+template <int L>
 __device__ __forceinline__ void tile_one(int k, int n, int len, const int32_t *dst, const uint16_t *ent,
                                          const unsigned char *sc, const SideEnt *sents, const TileOut &o,
                                          const TileK &tk, double *s_hot)
@@ -1282,8 +1286,7 @@ __device__ __forceinline__ void tile_one(int k, int n, int len, const int32_t *d
 #pragma unroll 2
         for (int p = 1; p < len; p++) v += *reinterpret_cast<const double *>(sc + ent[p * n + k]);
     }
-    if (kSide) tile_put(sents, o, tk, s_hot, g, v);           // a side piece
-    else red_add((g < o.nnz ? o.A : o.Bm) + g, v);            // an owned target: one RED
+    tile_put(sents, o, tk, s_hot, g, v);
 }
 
 // A group class (targets of L > kShortMax with one group size gs = cls_group(L)): a
@@ -1405,6 +1408,9 @@ __device__ __forceinline__ void tile_eval_item(const unsigned char *blob, const 
 __device__ __forceinline__ void tile_reduce(const unsigned char *blob, const unsigned char *sc, int r,
                                             const TileOut &out, const TileK &tk, double *s_hot)
 {
+#ifdef EES_DIAG_NOREDUCE         // diagnostic A/B only (no stamps): evaluation alone
+    return;
+#endif
     const TileHdr *h = reinterpret_cast<const TileHdr *>(blob);
     const TileCls *cls = reinterpret_cast<const TileCls *>(blob + sizeof(TileHdr));
     const int32_t *dst = reinterpret_cast<const int32_t *>(blob + h->off_dst);
@@ -1425,34 +1431,25 @@ __device__ __forceinline__ void tile_reduce(const unsigned char *blob, const uns
         const int n = c.n;
         const int k0 = (r - (int)c.rot) & (kTileThreads - 1);
         if (k0 >= n) continue;                         // no target of this class here
-#define TILE_ONE(L, S) for (int k = k0; k < n; k += kTileThreads) tile_one<L, S>(k, n, c.len, dc, e, sc, sents, out, tk, s_hot)
-        if (c.side) {                                  // side pieces (lengths 1 .. kSidePiece)
-            switch (c.len) {
-            case 1: TILE_ONE(1, true); break;
-            case 2: TILE_ONE(2, true); break;
-            case 3: TILE_ONE(3, true); break;
-            case 4: TILE_ONE(4, true); break;
-            default: TILE_ONE(0, true); break;
-            }
-        } else {
-            switch (c.len) {
-            case 1: TILE_ONE(1, false); break;
-            case 2: TILE_ONE(2, false); break;
-            case 3: TILE_ONE(3, false); break;
-            case 4: TILE_ONE(4, false); break;
-            default: TILE_ONE(0, false); break;
-            }
+#define TILE_ONE(L) for (int k = k0; k < n; k += kTileThreads) tile_one<L>(k, n, c.len, dc, e, sc, sents, out, tk, s_hot)
+        switch (c.len) {
+        case 1: TILE_ONE(1); break;
+        case 2: TILE_ONE(2); break;
+        case 3: TILE_ONE(3); break;
+        case 4: TILE_ONE(4); break;
+        default: TILE_ONE(0); break;
         }
 #undef TILE_ONE
     }
 }
 
-// After the last tile (all threads of the CTA): hot partials per CTA, then
-// the side targets summed in part order by the last CTA (ticket) unless
-// k_side_final does it.
+// After the last tile (all threads of the CTA): hot partials per CTA; then,
+// after a grid-wide barrier (the kernel is launched cooperatively: its grid
+// is the co-resident persistent grid), every warp of the grid sums a fixed
+// share of the side targets, each in part order (fixed lane stride, fixed
+// shuffle tree): deterministic, and no second launch or single finishing CTA.
 template <bool kTrace>
-__device__ __forceinline__ void tile_finish(const TileK &tk, const CallK &P, const double *s_hot,
-                                            double *const *s_hot_dst, const double *s_hot_pre, int *s_last)
+__device__ __forceinline__ void tile_finish(const TileK &tk, const CallK &P, const double *s_hot)
 {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nt = blockDim.x;
     const int32_t G = gridDim.x;
@@ -1464,18 +1461,14 @@ __device__ __forceinline__ void tile_finish(const TileK &tk, const CallK &P, con
         for (int q = 0; q < kHotPieces; q++) v += s_hot[h * kHotPieces + q];   // piece order
         tk.part[tk.hot_base + (int64_t)h * G + blockIdx.x] = v;
     }
-    if (!tk.side_inline) return;
     __threadfence();
-    __syncthreads();
-    if (tid == 0) *s_last = atomicAdd(tk.done, 1u) == (unsigned)G - 1;
-    __syncthreads();
+    cg::this_grid().sync();
     TILE_TRACE_TAIL(kTraceSlots - 2);
-    if (!*s_last) return;
-    __threadfence();
-    // hot targets (one part per CTA): a warp each, fixed lane stride, eight
-    // loads in flight per lane, fixed shuffle tree
-    for (int h = warp; h < tk.n_hot; h += nt >> 5) {
-        const double *pp = tk.part + tk.hot_base + (int64_t)h * G;
+    const int nw = nt >> 5;
+    const int64_t gw = (int64_t)blockIdx.x * nw + warp, n_gw = (int64_t)G * nw;
+    // hot targets (one part per CTA) first: warps 0 .. n_hot-1 of the grid
+    for (int64_t h = gw; h < tk.n_hot; h += n_gw) {
+        const double *pp = tk.part + tk.hot_base + h * G;
         double u = 0.0;
         for (int q0 = 0; q0 < G; q0 += 256) {
             double a[8];
@@ -1488,11 +1481,14 @@ __device__ __forceinline__ void tile_finish(const TileK &tk, const CallK &P, con
             for (int r = 0; r < 8; r++) u += a[r];
         }
         u = warp_sum(u);
-        if (lane == 0) *s_hot_dst[h] = s_hot_pre[h] + u;
+        if (lane == 0) {
+            const int32_t g = tk.hot_gid[h];
+            double *d = g < tk.nnz ? P.A + g : P.b + (g - tk.nnz);
+            *d = __ldcg(tk.hot_pre + h) + u;
+        }
     }
-    for (int32_t sid = warp; sid < tk.n_side; sid += nt >> 5)
-        if (__ldg(tk.sd_part + 2 * sid) < tk.hot_base || tk.n_hot == 0) side_finish(tk, P, sid, lane);
-    if (tid == 0) *tk.done = 0;
+    for (int64_t sid = gw; sid < tk.n_side; sid += n_gw)
+        if (__ldg(tk.sd_part + 2 * sid) < tk.hot_base || tk.n_hot == 0) side_finish(tk, P, (int32_t)sid, lane);
 }
 
 // TILE kernel prologue: hot targets, card copy, mbarriers and the first
@@ -1501,17 +1497,13 @@ __device__ __forceinline__ void tile_finish(const TileK &tk, const CallK &P, con
     extern __shared__ __align__(16) unsigned char smem[];                                        \
     __shared__ CardK s_cards[EES_MAX_MODELS];                                                    \
     __shared__ __align__(8) uint64_t s_bar[NSTAGES];                                             \
-    __shared__ double s_hot[kMaxHot * kHotPieces], s_hot_pre[kMaxHot];                           \
-    __shared__ double *s_hot_dst[kMaxHot];                                                       \
-    __shared__ int s_last;                                                                       \
+    __shared__ double s_hot[kMaxHot * kHotPieces];                                               \
     const int tid = threadIdx.x;                                                                 \
     const int32_t G = gridDim.x;                                                                 \
     for (int k = tid; k < kMaxHot * kHotPieces; k += (NT)) s_hot[k] = 0.0;                       \
-    if (tid < tk.n_hot) {            /* hot side targets: only the finisher writes them */       \
-        const int32_t g = tk.hot_gid[tid];                                                       \
-        double *d = g < tk.nnz ? P.A + g : P.b + (g - tk.nnz);                                   \
-        s_hot_dst[tid] = d;                                                                      \
-        s_hot_pre[tid] = *d;                                                                     \
+    if (tid < tk.n_hot && blockIdx.x == 0) {  /* hot targets' old values (written after the  */  \
+        const int32_t g = tk.hot_gid[tid];       /* grid barrier only)                         */  \
+        tk.hot_pre[tid] = g < tk.nnz ? P.A[g] : P.b[g - tk.nnz];                                 \
     }                                                                                            \
     auto issue = [&](int32_t tile, int stage) {                                                  \
         const int64_t off = tk.blob_off[tile];                                                   \
@@ -1579,23 +1571,28 @@ __global__ void __launch_bounds__(kTileThreads, tile_ctas(kForm)) k_tile(TileK t
         stage = sn;
         it++;
     };
-    for (int32_t t = t0; t < tk.n_tiles;) {
-        step(t, ra, rb);
-        t += G;
-        if (t >= tk.n_tiles) break;
-        step(t, rb, ra);
-        t += G;
+#ifndef EES_TILE_UNROLL2
+#define EES_TILE_UNROLL2 1
+#endif
+    if (EES_TILE_UNROLL2) {
+        for (int32_t t = t0; t < tk.n_tiles;) {
+            step(t, ra, rb);
+            t += G;
+            if (t >= tk.n_tiles) break;
+            step(t, rb, ra);
+            t += G;
+        }
+    } else {                            // one copy of the loop body (half the code), one register copy
+        for (int32_t t = t0; t < tk.n_tiles; t += G) {
+            step(t, ra, rb);
+            ra = rb;
+        }
     }
-    tile_finish<kTrace>(tk, P, s_hot, s_hot_dst, s_hot_pre, &s_last);
+    tile_finish<kTrace>(tk, P, s_hot);
     TILE_TRACE_TAIL(kTraceSlots - 1);
 #undef s_stage
 }
 
-__global__ void __launch_bounds__(256) k_side_final(TileK tk, CallK P)
-{
-    const int32_t sid = (int32_t)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
-    if (sid < tk.n_side) side_finish(tk, P, sid, threadIdx.x & 31);
-}
 
 template <int kForm>
 static int tile_bps()
@@ -1604,36 +1601,41 @@ static int tile_bps()
     cudaFuncSetAttribute(k_tile<false, false, kForm>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaFuncSetAttribute(k_tile<true, false, kForm>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaFuncSetAttribute(k_tile<false, true, kForm>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    int nb = 0, nb2 = 0;
+    // one grid serves every instantiation (the hot-part layout, and the
+    // cooperative launch needs it co-resident): the smallest occupancy
+    int nb = 0, nb2 = 0, nb3 = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_tile<false, false, kForm>, kTileThreads, smem);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb2, k_tile<false, true, kForm>, kTileThreads, smem);
-    nb = nb2 > 0 && nb2 < nb ? nb2 : nb;      // one grid (the hot-part layout) serves both
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb3, k_tile<true, false, kForm>, kTileThreads, smem);
+    nb = std::min(nb, std::min(nb2 > 0 ? nb2 : nb, nb3 > 0 ? nb3 : nb));
     return nb > 0 ? nb : 1;
 }
 
 int tile_blocks_per_sm(int form) { return form == 1 ? tile_bps<1>() : tile_bps<0>(); }
 
+// Cooperative launch when side targets need the grid barrier (the grid is
+// the co-resident persistent grid: SMs x tile_blocks_per_sm, capped by tiles).
 template <int kForm>
-static void launch_tile_form(const TileK &tk, const CallK &call, int grid, cudaStream_t st)
+static cudaError_t launch_tile_form(const TileK &tk, const CallK &call, int grid, cudaStream_t st)
 {
     constexpr size_t smem = tile_smem<kForm>();
-    if (tk.trace) k_tile<true, false, kForm><<<grid, kTileThreads, smem, st>>>(tk, call);
-    else if (call.work > 1) k_tile<false, true, kForm><<<grid, kTileThreads, smem, st>>>(tk, call);
-    else k_tile<false, false, kForm><<<grid, kTileThreads, smem, st>>>(tk, call);
+    const void *fn = tk.trace ? (const void *)k_tile<true, false, kForm>
+                     : call.work > 1 ? (const void *)k_tile<false, true, kForm>
+                                     : (const void *)k_tile<false, false, kForm>;
+    TileK a0 = tk;
+    CallK a1 = call;
+    void *args[] = {&a0, &a1};
+    if (tk.n_side) return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kTileThreads), args, smem, st);
+    return cudaLaunchKernel(fn, dim3(grid), dim3(kTileThreads), args, smem, st);
 }
 
 cudaError_t launch_tile(const TileK &tk, const CallK &call, int grid, cudaStream_t st, int *n_launches)
 {
     *n_launches = 0;
     if (tk.n_tiles == 0) return cudaSuccess;
-    if (tk.form == 1) launch_tile_form<1>(tk, call, grid, st);
-    else launch_tile_form<0>(tk, call, grid, st);
+    const cudaError_t e = tk.form == 1 ? launch_tile_form<1>(tk, call, grid, st) : launch_tile_form<0>(tk, call, grid, st);
     *n_launches = 1;
-    if (tk.n_side && !tk.side_inline) {
-        k_side_final<<<(unsigned)((tk.n_side * 32 + 255) / 256), 256, 0, st>>>(tk, call);
-        *n_launches = 2;
-    }
-    return cudaPeekAtLastError();
+    return e == cudaSuccess ? cudaPeekAtLastError() : e;
 }
 
 }  // namespace ees

@@ -390,12 +390,10 @@ bool build_tile_host(int form, int64_t N, int32_t n_nodes, int32_t n, int64_t nn
         const int32_t n_sent = (int32_t)sents.size();
         o.listed += (int64_t)con.size() + (int64_t)side.size();
         // classes: group classes (L > kShortMax, by lane-group size, largest
-        // first), then short side classes (pieces, one per length), then short
-        // owned classes (one per length, their threads never branch to a side
-        // entry); targets in list order within a class
-        auto cls_key = [](const Tgt &t2) {
-            return t2.len > kShortMax ? 100 + cls_group(t2.len) : (t2.is_side ? 50 : 0) + t2.len;
-        };
+        // first), then one per short length (owned targets and side pieces
+        // together: separate side classes measured slower, profiles/r02_ab.md);
+        // targets in list order within a class
+        auto cls_key = [](const Tgt &t2) { return t2.len > kShortMax ? 100 + cls_group(t2.len) : t2.len; };
         std::stable_sort(tg.begin(), tg.end(), [&](const Tgt &a, const Tgt &b) { return cls_key(a) > cls_key(b); });
         cls.clear();
         dsts.clear();
@@ -434,7 +432,6 @@ bool build_tile_host(int form, int64_t N, int32_t n_nodes, int32_t n, int64_t nn
             } else {
                 const int32_t L = tg[k].len;
                 tc.len = (uint16_t)L;
-                tc.side = (uint16_t)(key > 50 ? 1 : 0);
                 for (size_t q = k; q < e; q++) dsts.push_back(tg[q].dst);
                 for (int32_t p = 0; p < L; p++)
                     for (size_t q = k; q < e; q++) ents.push_back(entry(tg[q], p));

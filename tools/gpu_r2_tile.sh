@@ -9,12 +9,12 @@ if [ "${DEFAULT_BENCH:-0}" = 1 ]; then
 timeout 900 python bench.py --steps 20 --warmup 5 --no-cpu-baseline > $O/bench_default.log 2>&1; echo "bench default rc=$?" >> $O/rc.txt
 fi
 B="python bench.py --no-cpu-baseline --no-e2e --per-config none --steps 30"
-for c in 4 2 3; do
+for c in ${MAIN_CFGS:-4 2 3}; do
   timeout 300 $B --config $c --variant tile > $O/bench_c${c}_tile.log 2>&1; echo "bench c$c rc=$?" >> $O/rc.txt
   timeout 300 $B --config $c --variant atomic > $O/bench_c${c}_atomic.log 2>&1; echo "bench c$c atomic rc=$?" >> $O/rc.txt
 done
 for t in ${AB_TREES}; do
-  for c in 4 2 3; do (cd ab_$t && timeout 300 $B --config $c --variant tile > ../$O/ab_${t}_c${c}_tile.log 2>&1); echo "ab $t c$c rc=$?" >> $O/rc.txt; done
+  for c in ${AB_CFGS:-4 2 3}; do (cd ab_$t && timeout 300 $B --config $c --variant tile > ../$O/ab_${t}_c${c}_tile.log 2>&1); echo "ab $t c$c rc=$?" >> $O/rc.txt; done
 done
 for c in ${NCU_CFGS:-4}; do
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_tile" -s 3 -c 1 -o $O/prof_c${c}_tile python bench.py --config $c --steps 2 --warmup 3 --no-cpu-baseline --no-e2e --per-config '' --variant tile > $O/ncu_c${c}.log 2>&1; echo "ncu c$c rc=$?" >> $O/rc.txt

@@ -44,8 +44,8 @@ def main():
             break
         print(f" tile{i}: (B0+) eval+gather {q(np.where(ok, tr[:, s] - prev, -1))}")
         print(f"        B1+reduce+RED {q(np.where(ok, tr[:, s + 1] - tr[:, s], -1))}")
-    print(" ticket    ", q(rel[:, 62]), "(side targets finished by the last CTA)" if (tr[:, 62] > 0).any()
-          else "(none: no inline side finish)")
+    print(" grid sync ", q(rel[:, 62]), "(then the side targets, summed by the whole grid)" if (tr[:, 62] > 0).any()
+          else "(none: no side targets)")
     print(" end       ", q(rel[:, 63]))
 
 
