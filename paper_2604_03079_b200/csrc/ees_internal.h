@@ -215,7 +215,9 @@ struct TileHdr {
     uint32_t bytes;                  // blob size, multiple of 16
     uint32_t off_items, off_side, off_dst, off_ent;   // byte offsets of the sections
     uint32_t off_meta;
-    uint32_t pad1[8];
+    uint16_t n_full;                 // items [n_full, n_items) list gate-row contributions only
+    uint16_t pad0;
+    uint32_t pad1[7];
 };
 static_assert(sizeof(TileHdr) == 64, "TileHdr layout");
 

@@ -1223,18 +1223,23 @@ __device__ __forceinline__ void tile_gather(const unsigned char *blob, int32_t t
     const TileHdr *h = reinterpret_cast<const TileHdr *>(blob);
     R.VD = R.VG = R.VS = 0.0;
     if (tid < h->n_items) {
+        const bool full = tid < h->n_full;            // gate-row items: caps only (no x, no beta)
         if (kForm == 1) {
             const int64_t q = (int64_t)tile * kTileItems + tid;
-            R.beta = __ldg(tk.item_beta + q);
             R.v0a = __ldg(tk.item_v0 + 3 * q);
             R.v0b = __ldg(tk.item_v0 + 3 * q + 1);
-            R.v0c = __ldg(tk.item_v0 + 3 * q + 2);
             R.model = __ldg(tk.item_model + q);
+            if (full) {
+                R.beta = __ldg(tk.item_beta + q);
+                R.v0c = __ldg(tk.item_v0 + 3 * q + 2);
+            }
         }
-        const int4 T = reinterpret_cast<const int4 *>(blob + h->off_items)[tid];
-        R.VD = T.x >= 0 ? __ldg(P.x + T.x) : 0.0;
-        R.VG = T.y >= 0 ? __ldg(P.x + T.y) : 0.0;
-        R.VS = T.z >= 0 ? __ldg(P.x + T.z) : 0.0;
+        if (full) {
+            const int4 T = reinterpret_cast<const int4 *>(blob + h->off_items)[tid];
+            R.VD = T.x >= 0 ? __ldg(P.x + T.x) : 0.0;
+            R.VG = T.y >= 0 ? __ldg(P.x + T.y) : 0.0;
+            R.VS = T.z >= 0 ? __ldg(P.x + T.z) : 0.0;
+        }
     }
 }
 
@@ -1380,6 +1385,19 @@ __device__ __forceinline__ void tile_eval_item(const unsigned char *blob, const 
 {
     const TileHdr *h = reinterpret_cast<const TileHdr *>(blob);
     const int ni = h->n_items;
+    if (it >= h->n_full) {
+        // gate-row item: only GD, GG, GS and J[G] are listed -- the BE
+        // companions of cgs (G,S) and cgd (G,D), eval_fet1's gate row
+        const CardK &cd = s_cards[kForm == 1 ? cur.model : blob[h->off_items + 48 * ni + it]];
+        const double v0gs = kForm == 1 ? cur.v0a : reinterpret_cast<const double *>(blob + h->off_items + 24 * ni)[it];
+        const double v0gd = kForm == 1 ? cur.v0b : reinterpret_cast<const double *>(blob + h->off_items + 32 * ni)[it];
+        const double g1 = cd.gcgs, g2 = cd.gcgd;
+        scd[GD * kTileItems + it] = -g2;
+        scd[GG * kTileItems + it] = g1 + g2;
+        scd[GS * kTileItems + it] = -g1;
+        scd[(NPAIR + 1) * kTileItems + it] = g1 * v0gs + g2 * v0gd;
+        return;
+    }
     Stamp st;
     if (kForm == 1) {
         eval_fet<kRep>(s_cards[cur.model], cur.beta, P.gmin, cur.VD, cur.VG, cur.VS, cur.v0a, cur.v0b, cur.v0c, st,
@@ -1505,12 +1523,12 @@ __device__ __forceinline__ void tile_finish(const TileK &tk, const CallK &P, con
         const int32_t g = tk.hot_gid[tid];       /* grid barrier only)                         */  \
         tk.hot_pre[tid] = g < tk.nnz ? P.A[g] : P.b[g - tk.nnz];                                 \
     }                                                                                            \
-    auto issue = [&](int32_t tile, int stage) {                                                  \
-        const int64_t off = tk.blob_off[tile];                                                   \
-        const uint32_t bytes = (uint32_t)(tk.blob_off[tile + 1] - off);                          \
+    auto issue_at = [&](int64_t off, int64_t end, int stage) {                                   \
+        const uint32_t bytes = (uint32_t)(end - off);                                            \
         mbar_expect_tx(&s_bar[stage], bytes);                                                    \
         tma_bulk_g2s(s_stage + (size_t)stage * kStage, tk.blob + off, bytes, &s_bar[stage]);     \
     };                                                                                           \
+    auto issue = [&](int32_t tile, int stage) { issue_at(tk.blob_off[tile], tk.blob_off[tile + 1], stage); }; \
     TileOut out;                                                                                 \
     out.A = P.A;                                                                                 \
     out.Bm = P.b - tk.nnz;                                                                       \
@@ -1549,6 +1567,14 @@ __global__ void __launch_bounds__(kTileThreads, tile_ctas(kForm)) k_tile(TileK t
     auto step = [&](int32_t t, const TileRegs &cur, TileRegs &nxt) {
         const unsigned char *blob = s_stage + (size_t)stage * kStage;
         unsigned char *sc = s_c + (kBuf == 2 ? (size_t)(it & 1) * 8 * kScSlots : 0);
+        // the blob this iteration's refill (at B1) will fetch: its offsets are
+        // loaded now, so warp 0 does not wait on global memory after B1
+        const int32_t tr = t - G + kStages * G;
+        int64_t rf_off = 0, rf_end = 0;
+        if (tid == 0 && it > 0 && tr < tk.n_tiles) {
+            rf_off = __ldg(tk.blob_off + tr);
+            rf_end = __ldg(tk.blob_off + tr + 1);
+        }
         if (tid < reinterpret_cast<const TileHdr *>(blob)->n_items)
             tile_eval_item<kRep, kForm>(blob, cur, tid, reinterpret_cast<double *>(sc), s_cards, P);
         // next tile: its blob was issued >= one tile ago; start its gathers now
@@ -1561,10 +1587,8 @@ __global__ void __launch_bounds__(kTileThreads, tile_ctas(kForm)) k_tile(TileK t
         }
         TILE_TRACE(2 + 2 * it);
         __syncthreads();                                        // B1
-        if (tid == 0 && it > 0) {
-            const int32_t tr = t - G + kStages * G;             // refill the stage of tile t-G
-            if (tr < tk.n_tiles) issue(tr, stage == 0 ? kStages - 1 : stage - 1);
-        }
+        if (tid == 0 && it > 0 && tr < tk.n_tiles)              // refill the stage of tile t-G
+            issue_at(rf_off, rf_end, stage == 0 ? kStages - 1 : stage - 1);
         tile_reduce(blob, sc, tid, out, tk, s_hot);
         TILE_TRACE(3 + 2 * it);
         if (kBuf == 1) __syncthreads();                         // B0: slots free for the next tile

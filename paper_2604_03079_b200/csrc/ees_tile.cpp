@@ -326,6 +326,29 @@ bool build_tile_host(int form, int64_t N, int32_t n_nodes, int32_t n, int64_t nn
         side.clear();
         const int32_t q0 = out_item_ptr[tt];
         const int32_t ni = out_item_ptr[tt + 1] - q0;
+        // the contributions of FET i this tile lists: owned by it, or (heavy x
+        // heavy) side contributions of its home tile
+        auto in_tile = [&](int32_t i, int p) -> bool {
+            if (!listed_c(i, p)) return false;
+            const DevRec &dr = rec[i];
+            const int32_t r = p < NPAIR ? dr.t[pair_row(p)] : dr.t[p - NPAIR];
+            const int32_t c = p < NPAIR ? dr.t[pair_col(p)] : r;
+            if (!heavy[r] || !heavy[c]) return (!heavy[r] ? tile_of_row[r] : tile_of_row[c]) == tt;
+            return home[i] == tt;
+        };
+        // gate-row items (every listed contribution in the gate row: GD, GG,
+        // GS, J[G] -- capacitor companions only, no channel evaluation, no x)
+        // go last, so whole warps take the short path
+        int32_t n_full = ni;
+        {
+            auto gate_only = [&](int32_t i) {
+                for (int p = 0; p < NPAIR + 4; p++)
+                    if (in_tile(i, p) && p != GD && p != GG && p != GS && p != NPAIR + 1) return false;
+                return true;
+            };
+            int32_t *it0 = item_dev.data() + q0;
+            n_full = (int32_t)(std::stable_partition(it0, it0 + ni, [&](int32_t i) { return !gate_only(i); }) - it0);
+        }
         for (int32_t q = q0; q < out_item_ptr[tt + 1]; q++) {
             const int32_t i = item_dev[q];
             const int32_t loc = q - q0;
@@ -447,6 +470,7 @@ bool build_tile_host(int form, int64_t N, int32_t n_nodes, int32_t n, int64_t nn
         TileHdr hdr;
         std::memset(&hdr, 0, sizeof(hdr));
         hdr.n_items = (uint16_t)ni;
+        hdr.n_full = (uint16_t)n_full;
         hdr.n_cls = (uint16_t)cls.size();
         hdr.n_sent = (uint16_t)n_sent;
         hdr.n_tgt = (uint16_t)tg.size();
