@@ -149,7 +149,7 @@ typedef struct {
     double setup_s;                         /* wall time of ees_setup */
     double setup_pattern_s, setup_color_s;  /* parts of it */
     int32_t n_tiles, n_heavy_nodes, n_side_targets;   /* EES_TILE structure */
-    int32_t tile_blob_max;                  /* largest per-tile blob (bytes) */
+    int32_t tile_blob_max;                  /* largest per-tile head + program (bytes) */
     int64_t n_tile_items;                   /* device copies over all tiles (>= n_dev) */
     double tune_ms[6];                      /* EES_AUTO: measured ms per call of
                                                [_, COLOR, ATOMIC, GATHER, TILE, COLOR_BUF] */
@@ -160,7 +160,8 @@ typedef struct {
     int64_t n_color_side_contributions;     /* their contributions (scratch slots) */
     int32_t atomic_form;                    /* EES_ATOMIC: 0 one RED per contribution, 1 one RED per
                                                run of equal entries in a warp (timed at setup) */
-    int32_t reserved0;
+    int32_t n_tile_programs;                /* EES_TILE: distinct reduction programs (tiles of equal
+                                               structure share one) */
 } ees_stats_t;
 
 /* Build everything that depends only on topology ("constructs the FET

@@ -960,6 +960,7 @@ ees_status build_tile(const ees_desc *d, ees_ctx *c, const std::vector<int32_t> 
     c->st.n_side_targets = th.n_side;
     c->st.n_tile_items = th.n_items;
     c->st.tile_blob_max = th.blob_max;
+    c->st.n_tile_programs = th.n_progs;
     if (c->host_only) return EES_OK;
     TileK &k = c->tk;
     k.form = form;
@@ -969,8 +970,13 @@ ees_status build_tile(const ees_desc *d, ees_ctx *c, const std::vector<int32_t> 
         using T = typename std::remove_reference<decltype(vec)>::type::value_type;
         return upload(c, const_cast<T **>(dst), vec.data(), vec.size());
     };
-    TRY(up(&k.blob_off, th.blob_off));
+    {
+        const uint32_t *td = nullptr;
+        TRY(up(&td, th.tdesc));
+        k.tdesc = reinterpret_cast<const uint4 *>(td);
+    }
     TRY(up(&k.blob, th.blob));
+    TRY(up(&k.prog, th.prog));
     TRY(up(&k.item_beta, th.item_beta));
     TRY(up(&k.item_v0, th.item_v0));
     TRY(up(&k.item_model, th.item_model));

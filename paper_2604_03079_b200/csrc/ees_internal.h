@@ -119,22 +119,30 @@ struct GatherK {
 // and part (plain store), or, for the hot side targets (rails), a running
 // sum per CTA and piece index in shared memory, in tile order.  Classes are
 // processed back to back by the CTA's threads with the lane position
-// continuing across classes (cls[c].rot), so the threads' loads stay even.  Everything a tile needs except x
-// (and, in form 1, the item data) is one 16-byte-aligned blob that a TMA bulk
-// copy (cp.async.bulk + mbarrier) brings into shared memory, kStages tiles
-// ahead:
-//   TileHdr (64 B) | TileCls[n_cls] (16 B each)
-//   items:  form 0: term int4[ni] | beta f64[ni] | v0 f64[3][ni] | model u8[ni]
-//           form 1: term int4[ni]; beta, v0[3], model in tile-order HBM arrays
-//           (kTileItems slots per tile) loaded one tile ahead into registers
-//   side:   SideEnt[n_sent]
-//   dst:    int32[n_tgt]: per class, the destinations of its targets (>= 0:
-//           global target g = A index, or nnz + b row; < 0: side entry -1-dst)
-//   meta:   u32[n_grp]: targets of group classes (L > 4): first entry (low 16
-//           bits, u16 index in ent[]) | length << 16
-//   ent:    u16: per short class c, entries [L_c][n_c] (k-major: lanes of a
-//           warp read consecutive u16); group classes: each target's entries
-//           contiguous (the lanes of its group read consecutive u16)
+// continuing across classes (cls[c].rot), so the threads' loads stay even.
+// Everything a tile needs except x (and, in form 1, the item data) is its
+// HEAD (per tile) and its PROGRAM (shared by structurally equal tiles), which
+// two TMA bulk copies (cp.async.bulk + one mbarrier) bring into one shared-
+// memory stage, kStages tiles ahead (program right after the head):
+//   head:    TileHdr (64 B: counts, sizes, offsets, kTileBases destination
+//            bases)
+//            items: form 0: term int4[ni] | beta f64[ni] | v0 f64[3][ni] | model u8[ni]
+//                   form 1: term int4[ni]; beta, v0[3], model in tile-order HBM
+//                   arrays (kTileItems slots per tile) loaded one tile ahead
+//            side:  SideEnt[n_sent]
+//   program: ProgHdr (16 B) | TileCls[n_cls] (16 B each)
+//            dst:  int32[n_tgt]: per class, the destinations of its targets
+//                  (>= 0: global target g = base[dst >> 28] + (dst & 0x0FFFFFFF),
+//                  g an A index or nnz + b row; < 0: side entry -1-dst of the head)
+//            meta: u32[n_grp]: targets of group classes: first entry (low 16
+//                  bits, u16 index in ent[]) | length << 16
+//            ent:  u16: per short class c, entries [L_c][n_c] (k-major: lanes
+//                  of a warp read consecutive u16); group classes: each
+//                  target's entries contiguous
+// The bases are the first target of each cluster of the tile's owned targets
+// (its rows' CSR block, its b rows, each heavy row's slice), so tiles of the
+// same structure have byte-identical programs; the builder stores each
+// distinct program once (cfg4: the inverter-chain and hub-load tiles).
 // Contributions of a FET whose source and bulk are one node (every PMOS of the
 // inverter configs) are merged at evaluation (DB into DS, BD into SD, BB into
 // SS, J[B] into J[S]) and the merged-away slots are not listed.
@@ -210,16 +218,27 @@ struct TileCls {
 };
 static_assert(sizeof(TileCls) == 16, "TileCls layout");
 
+// Per-tile head (streamed: one per tile) and the tile's reduction program
+// (shared by every tile with the same program bytes: owned destinations are
+// coded relative to the head's bases, so the programs of structurally equal
+// tiles -- inverter chains, hub loads -- are one copy, L2-resident).
+constexpr int kTileBases = 8;            // dst code >= 0: base[code >> 28] + (code & 0x0FFFFFFF)
 struct TileHdr {
-    uint16_t n_items, n_cls, n_sent, n_tgt;
-    uint32_t bytes;                  // blob size, multiple of 16
-    uint32_t off_items, off_side, off_dst, off_ent;   // byte offsets of the sections
-    uint32_t off_meta;
-    uint16_t n_full;                 // items [n_full, n_items) list gate-row contributions only
-    uint16_t pad0;
-    uint32_t pad1[7];
+    uint16_t n_items, n_full, n_sent, pad0;
+    uint32_t head_bytes;             // head size (multiple of 16): the program follows it in the stage
+    uint32_t prog_bytes;             // program size (multiple of 16)
+    uint32_t off_items, off_side;    // byte offsets of the head's sections
+    int32_t base[kTileBases];        // owned-destination bases (global target ids)
+    uint32_t pad1[2];
 };
 static_assert(sizeof(TileHdr) == 64, "TileHdr layout");
+
+struct ProgHdr {
+    uint16_t n_cls, n_tgt;
+    uint16_t off_dst, off_meta, off_ent;   // byte offsets from the program start
+    uint16_t pad[3];
+};
+static_assert(sizeof(ProgHdr) == 16, "ProgHdr layout");
 
 struct SideEnt {
     int32_t sid;                     // side target
@@ -231,8 +250,9 @@ struct TileK {
     int32_t form;                  // 0: whole items in the blob; 1: items' data in HBM arrays
     int32_t n_tiles;
     int64_t nnz;
-    const int64_t *blob_off;       // [T+1] byte offsets into blob
-    const uint8_t *blob;
+    const uint4 *tdesc;            // [T] head offset / 16, head bytes, program offset / 16, program bytes
+    const uint8_t *blob;           // the heads
+    const uint8_t *prog;           // the distinct programs
     int32_t n_side;
     int32_t pad0;
     int32_t n_hot;                 // hot side targets: CTA b's part at part[hot_base + h*grid + b]
@@ -258,10 +278,13 @@ struct TileHost {
     int64_t n_items = 0, n_owned = 0, n_side_entries = 0;
     int64_t n_parts = 0, hot_base = 0;
     int64_t n_listed = 0, n_padded = 0;    // list entries, and with class padding
-    int32_t blob_max = 0, n_hot = 0;
+    int32_t blob_max = 0, n_hot = 0;       // largest head + program
     int32_t grid = 1;                      // persistent CTAs the hot-part layout is made for
-    std::vector<int64_t> blob_off;
-    std::vector<uint8_t> blob;
+    int32_t n_progs = 0;                   // distinct programs
+    std::vector<int64_t> blob_off;         // [T+1] head offsets
+    std::vector<uint8_t> blob;             // heads
+    std::vector<uint8_t> prog;             // distinct programs
+    std::vector<uint32_t> tdesc;           // [T][4] (TileK::tdesc)
     std::vector<double> item_beta, item_v0;
     std::vector<uint8_t> item_model;
     std::vector<int32_t> sd_gid, sd_part, hot_gid;

@@ -674,7 +674,7 @@ __global__ void __launch_bounds__(kBlock) k_accept_soa(const int4 *term, int64_t
 
 __global__ void __launch_bounds__(kTileThreads) k_accept_tile(TileK tk, CallK P, double *item_v0)
 {
-    unsigned char *b = const_cast<unsigned char *>(tk.blob) + tk.blob_off[blockIdx.x];
+    unsigned char *b = const_cast<unsigned char *>(tk.blob) + 16 * (size_t)tk.tdesc[blockIdx.x].x;
     const TileHdr *h = reinterpret_cast<const TileHdr *>(b);
     const int ni = h->n_items;
     const int4 *term = reinterpret_cast<const int4 *>(b + h->off_items);
@@ -1260,12 +1260,14 @@ __device__ __forceinline__ void red_add(double *p, double v)
 struct TileOut {
     double *A, *Bm;            // A, and b - nnz (so that b row r is Bm + nnz + r)
     int32_t nnz;
+    const int32_t *base;       // the staged head's destination bases (shared memory)
 };
 
 __device__ __forceinline__ void tile_put(const SideEnt *sents, const TileOut &o, const TileK &tk, double *s_hot,
-                                         int32_t g, double v)
+                                         int32_t g, double v)     // g: the program's destination code
 {
     if (g >= 0) {
+        g = o.base[g >> 28] + (g & 0x0FFFFFFF);
         red_add((g < o.nnz ? o.A : o.Bm) + g, v);
     } else {
         const SideEnt se = sents[-1 - g];
@@ -1424,18 +1426,22 @@ __device__ __forceinline__ void tile_eval_item(const unsigned char *blob, const 
 // The reduction program of one staged tile, run by kTileThreads threads with
 // thread index r (0 .. kTileThreads-1; whole warps).
 __device__ __forceinline__ void tile_reduce(const unsigned char *blob, const unsigned char *sc, int r,
-                                            const TileOut &out, const TileK &tk, double *s_hot)
+                                            const TileOut &out0, const TileK &tk, double *s_hot)
 {
 #ifdef EES_DIAG_NOREDUCE         // diagnostic A/B only (no stamps): evaluation alone
     return;
 #endif
     const TileHdr *h = reinterpret_cast<const TileHdr *>(blob);
-    const TileCls *cls = reinterpret_cast<const TileCls *>(blob + sizeof(TileHdr));
-    const int32_t *dst = reinterpret_cast<const int32_t *>(blob + h->off_dst);
-    const uint16_t *ent = reinterpret_cast<const uint16_t *>(blob + h->off_ent);
+    const unsigned char *prog = blob + h->head_bytes;
+    const ProgHdr *ph = reinterpret_cast<const ProgHdr *>(prog);
+    const TileCls *cls = reinterpret_cast<const TileCls *>(prog + sizeof(ProgHdr));
+    const int32_t *dst = reinterpret_cast<const int32_t *>(prog + ph->off_dst);
+    const uint16_t *ent = reinterpret_cast<const uint16_t *>(prog + ph->off_ent);
+    const uint32_t *meta = reinterpret_cast<const uint32_t *>(prog + ph->off_meta);
     const SideEnt *sents = reinterpret_cast<const SideEnt *>(blob + h->off_side);
-    const uint32_t *meta = reinterpret_cast<const uint32_t *>(blob + h->off_meta);
-    const int ncl = h->n_cls;
+    TileOut out = out0;
+    out.base = h->base;
+    const int ncl = ph->n_cls;
     for (int ci = 0; ci < ncl; ci++) {
         const TileCls c = cls[ci];
         const uint16_t *e = ent + c.ent;
@@ -1523,16 +1529,18 @@ __device__ __forceinline__ void tile_finish(const TileK &tk, const CallK &P, con
         const int32_t g = tk.hot_gid[tid];       /* grid barrier only)                         */  \
         tk.hot_pre[tid] = g < tk.nnz ? P.A[g] : P.b[g - tk.nnz];                                 \
     }                                                                                            \
-    auto issue_at = [&](int64_t off, int64_t end, int stage) {                                   \
-        const uint32_t bytes = (uint32_t)(end - off);                                            \
-        mbar_expect_tx(&s_bar[stage], bytes);                                                    \
-        tma_bulk_g2s(s_stage + (size_t)stage * kStage, tk.blob + off, bytes, &s_bar[stage]);     \
+    auto issue_at = [&](uint4 d, int stage) {   /* head, then the program right after it */     \
+        unsigned char *sd = s_stage + (size_t)stage * kStage;                                    \
+        mbar_expect_tx(&s_bar[stage], d.y + d.w);                                                \
+        tma_bulk_g2s(sd, tk.blob + 16 * (size_t)d.x, d.y, &s_bar[stage]);                       \
+        tma_bulk_g2s(sd + d.y, tk.prog + 16 * (size_t)d.z, d.w, &s_bar[stage]);                 \
     };                                                                                           \
-    auto issue = [&](int32_t tile, int stage) { issue_at(tk.blob_off[tile], tk.blob_off[tile + 1], stage); }; \
+    auto issue = [&](int32_t tile, int stage) { issue_at(__ldg(tk.tdesc + tile), stage); };     \
     TileOut out;                                                                                 \
     out.A = P.A;                                                                                 \
     out.Bm = P.b - tk.nnz;                                                                       \
     out.nnz = (int32_t)tk.nnz;                    /* < 2^31 (setup) */                           \
+    out.base = nullptr;                           /* set per tile (tile_reduce) */               \
     const int32_t t0 = blockIdx.x;                                                               \
     if (tid == 0) {                                                                              \
         for (int k = 0; k < (NSTAGES); k++) mbar_init(&s_bar[k], 1);                             \
@@ -1570,11 +1578,8 @@ __global__ void __launch_bounds__(kTileThreads, tile_ctas(kForm)) k_tile(TileK t
         // the blob this iteration's refill (at B1) will fetch: its offsets are
         // loaded now, so warp 0 does not wait on global memory after B1
         const int32_t tr = t - G + kStages * G;
-        int64_t rf_off = 0, rf_end = 0;
-        if (tid == 0 && it > 0 && tr < tk.n_tiles) {
-            rf_off = __ldg(tk.blob_off + tr);
-            rf_end = __ldg(tk.blob_off + tr + 1);
-        }
+        uint4 rf = make_uint4(0, 0, 0, 0);
+        if (tid == 0 && it > 0 && tr < tk.n_tiles) rf = __ldg(tk.tdesc + tr);
         if (tid < reinterpret_cast<const TileHdr *>(blob)->n_items)
             tile_eval_item<kRep, kForm>(blob, cur, tid, reinterpret_cast<double *>(sc), s_cards, P);
         // next tile: its blob was issued >= one tile ago; start its gathers now
@@ -1588,7 +1593,7 @@ __global__ void __launch_bounds__(kTileThreads, tile_ctas(kForm)) k_tile(TileK t
         TILE_TRACE(2 + 2 * it);
         __syncthreads();                                        // B1
         if (tid == 0 && it > 0 && tr < tk.n_tiles)              // refill the stage of tile t-G
-            issue_at(rf_off, rf_end, stage == 0 ? kStages - 1 : stage - 1);
+            issue_at(rf, stage == 0 ? kStages - 1 : stage - 1);
         tile_reduce(blob, sc, tid, out, tk, s_hot);
         TILE_TRACE(3 + 2 * it);
         if (kBuf == 1) __syncthreads();                         // B0: slots free for the next tile

@@ -15,6 +15,7 @@
 #include <cstring>
 #include <functional>
 #include <numeric>
+#include <unordered_map>
 #include <vector>
 
 #include "ees_internal.h"
@@ -34,8 +35,10 @@ constexpr int32_t kSide = -2;
 // entry + 2 B per entry, whose lengths (1..kSidePiece) take at most
 // kSidePiece class headers per tile (reserved in kBlobFixed) -> 12 B per
 // distinct target + 2 + 12 / kSidePiece = 5 B per contribution covers both.
-// Fixed: header + five section paddings + the side-piece class headers.
-constexpr int64_t kBlobFixed = (int64_t)sizeof(TileHdr) + 5 * 16 + kSidePiece * (int64_t)sizeof(TileCls);
+// Fixed: head and program headers + six section paddings + the side-piece
+// class headers.
+constexpr int64_t kBlobFixed = (int64_t)sizeof(TileHdr) + (int64_t)sizeof(ProgHdr) + 6 * 16 +
+                               kSidePiece * (int64_t)sizeof(TileCls);
 constexpr int64_t kHHTarget = 12, kHHContrib = 5;
 size_t pad16(size_t x) { return (x + 15) & ~(size_t)15; }
 }  // namespace
@@ -282,7 +285,8 @@ bool build_tile_host(int form, int64_t N, int32_t n_nodes, int32_t n, int64_t nn
     // their global target for now), then concatenated in tile order, where
     // side ids are numbered by first appearance (the serial order).
     struct TileOut {
-        std::vector<uint8_t> blob;
+        std::vector<uint8_t> blob, prog;     // head, program
+        uint64_t hash = 0;                   // of the program bytes
         int64_t listed = 0, L = 0, padded = 0;
         int32_t n_own = 0, n_sent = 0;
         bool ok = true;
@@ -310,6 +314,7 @@ bool build_tile_host(int form, int64_t N, int32_t n_nodes, int32_t n, int64_t nn
     std::vector<int32_t> dsts;
     std::vector<uint16_t> ents;
     std::vector<uint32_t> meta;
+    std::vector<int32_t> owned_g;
     auto emit_tile = [&](int32_t tt, TileOut &o) -> bool {
         // owned targets, ascending
         gids.clear();
@@ -466,31 +471,85 @@ bool build_tile_host(int form, int64_t N, int32_t n_nodes, int32_t n, int64_t nn
             k = e;
         }
         if (ents.size() > 65536) return false;
-        // emit the blob
+        // destination bases: the first target of each cluster of the owned
+        // targets (ascending; a new cluster after a gap > kGap), so equal tile
+        // structures give equal codes; more than kTileBases clusters: the
+        // fixed bases s << 28 (codes = global targets)
+        int32_t bases[kTileBases];
+        {
+            constexpr int32_t kGap = 4096, kSpan = 1 << 28;
+            int nb = 0;
+            bool fixed = false;
+            int32_t prev = -1;
+            owned_g.clear();
+            for (const Tgt &t2 : tg)
+                if (!t2.is_side) owned_g.push_back(t2.dst);
+            std::sort(owned_g.begin(), owned_g.end());
+            for (const int32_t g : owned_g) {
+                if (nb == 0 || g - prev > kGap || g - bases[nb - 1] >= kSpan) {
+                    if (nb == kTileBases) { fixed = true; break; }
+                    bases[nb++] = g;
+                }
+                prev = g;
+            }
+            if (fixed) {
+                for (int q = 0; q < kTileBases; q++) bases[q] = q * kSpan;
+                nb = kTileBases;
+            }
+            for (int q = nb; q < kTileBases; q++) bases[q] = INT32_MAX;
+            for (int32_t &d : dsts) {
+                if (d < 0) continue;
+                int q = 0;
+                while (q + 1 < kTileBases && bases[q + 1] <= d) q++;
+                const int32_t off = d - bases[q];
+                if (off < 0 || off >= kSpan) return false;
+                d = (q << 28) | off;
+            }
+        }
+        // emit the head (per tile) and the program (shared by equal tiles)
+        ProgHdr ph;
+        std::memset(&ph, 0, sizeof(ph));
+        ph.n_cls = (uint16_t)cls.size();
+        ph.n_tgt = (uint16_t)tg.size();
+        if (tg.size() > 65535 || n_sent > 65535) return false;
+        const size_t off_dst = pad16(sizeof(ProgHdr) + sizeof(TileCls) * cls.size());
+        const size_t off_meta = off_dst + 4 * dsts.size();
+        const size_t off_ent = pad16(off_meta + 4 * meta.size());
+        const size_t pbytes = pad16(off_ent + 2 * ents.size());
+        if (pbytes > 65535) return false;
+        ph.off_dst = (uint16_t)off_dst;
+        ph.off_meta = (uint16_t)off_meta;
+        ph.off_ent = (uint16_t)off_ent;
+        o.prog.assign(pbytes, 0);
+        uint8_t *pp = o.prog.data();
+        std::memcpy(pp, &ph, sizeof(ph));
+        if (!cls.empty()) std::memcpy(pp + sizeof(ProgHdr), cls.data(), sizeof(TileCls) * cls.size());
+        if (!dsts.empty()) std::memcpy(pp + off_dst, dsts.data(), 4 * dsts.size());
+        if (!meta.empty()) std::memcpy(pp + off_meta, meta.data(), 4 * meta.size());
+        if (!ents.empty()) std::memcpy(pp + off_ent, ents.data(), 2 * ents.size());
+        uint64_t hsh = 1469598103934665603ull;            // FNV-1a
+        for (size_t q = 0; q < pbytes; q++) hsh = (hsh ^ pp[q]) * 1099511628211ull;
+        o.hash = hsh;
+
         TileHdr hdr;
         std::memset(&hdr, 0, sizeof(hdr));
         hdr.n_items = (uint16_t)ni;
         hdr.n_full = (uint16_t)n_full;
-        hdr.n_cls = (uint16_t)cls.size();
         hdr.n_sent = (uint16_t)n_sent;
-        hdr.n_tgt = (uint16_t)tg.size();
-        if (tg.size() > 65535 || n_sent > 65535) return false;
-        hdr.off_items = (uint32_t)pad16(sizeof(TileHdr) + sizeof(TileCls) * cls.size());
+        for (int q = 0; q < kTileBases; q++) hdr.base[q] = bases[q];
+        hdr.off_items = (uint32_t)sizeof(TileHdr);
         const size_t items_bytes = pad16((size_t)ni * kItemBlobBytes);
         hdr.off_side = (uint32_t)(hdr.off_items + items_bytes);
-        hdr.off_dst = (uint32_t)pad16(hdr.off_side + sizeof(SideEnt) * sents.size());
-        hdr.off_meta = (uint32_t)(hdr.off_dst + 4 * dsts.size());
-        hdr.off_ent = (uint32_t)pad16(hdr.off_meta + 4 * meta.size());
-        const size_t bytes = pad16(hdr.off_ent + 2 * ents.size());
-        if (bytes > (size_t)kStageMax) return false;
-        hdr.bytes = (uint32_t)bytes;
+        const size_t bytes = pad16(hdr.off_side + sizeof(SideEnt) * sents.size());
+        if (bytes + pbytes > (size_t)kStageMax) return false;
+        hdr.head_bytes = (uint32_t)bytes;
+        hdr.prog_bytes = (uint32_t)pbytes;
         o.blob.assign(bytes, 0);
         uint8_t *bp = o.blob.data();
         std::memcpy(bp, &hdr, sizeof(hdr));
-        if (!cls.empty()) std::memcpy(bp + sizeof(TileHdr), cls.data(), sizeof(TileCls) * cls.size());
         uint8_t *it = bp + hdr.off_items;
         int4 *term = reinterpret_cast<int4 *>(it);
-        // form 0: beta, v0, model follow the terms in the blob; form 1: they
+        // form 0: beta, v0, model follow the terms in the head; form 1: they
         // live in tile-order arrays, kTileItems slots per tile (v0 per item)
         const size_t ib = (size_t)tt * kTileItems;     // form 1 arrays: preallocated, disjoint per tile
         double *bt = form == 1 ? out.item_beta.data() + ib : reinterpret_cast<double *>(it + 16 * (size_t)ni);
@@ -509,9 +568,6 @@ bool build_tile_host(int form, int64_t N, int32_t n_nodes, int32_t n, int64_t nn
             md[q] = (uint8_t)model[i];
         }
         if (!sents.empty()) std::memcpy(bp + hdr.off_side, sents.data(), sizeof(SideEnt) * sents.size());
-        if (!dsts.empty()) std::memcpy(bp + hdr.off_dst, dsts.data(), 4 * dsts.size());
-        if (!meta.empty()) std::memcpy(bp + hdr.off_meta, meta.data(), 4 * meta.size());
-        if (!ents.empty()) std::memcpy(bp + hdr.off_ent, ents.data(), 2 * ents.size());
         o.n_own = n_own;
         o.n_sent = n_sent;
         o.L = (int64_t)con.size() + (int64_t)side.size();
@@ -537,18 +593,44 @@ bool build_tile_host(int form, int64_t N, int32_t n_nodes, int32_t n, int64_t nn
     for (int32_t tt = 0; tt < T; tt++) {
         const TileOut &o = tout[tt];
         out.blob_off[tt + 1] = out.blob_off[tt] + (int64_t)o.blob.size();
-        out.blob_max = std::max(out.blob_max, (int32_t)o.blob.size());
+        out.blob_max = std::max(out.blob_max, (int32_t)(o.blob.size() + o.prog.size()));
         out.n_owned += o.n_own;
         out.n_side_entries += o.n_sent;
         out.n_listed += o.L;
         out.n_padded += o.padded;
         listed += o.listed;
     }
+    // distinct programs, numbered by first appearance (tile order)
+    std::vector<int64_t> prog_off((size_t)T, -1);
+    {
+        std::unordered_map<uint64_t, std::vector<int32_t>> by_hash;   // hash -> first tiles
+        for (int32_t tt = 0; tt < T; tt++) {
+            const TileOut &o = tout[tt];
+            std::vector<int32_t> &same = by_hash[o.hash];
+            for (int32_t u : same)
+                if (tout[u].prog == o.prog) { prog_off[tt] = prog_off[u]; break; }
+            if (prog_off[tt] >= 0) continue;
+            prog_off[tt] = (int64_t)out.prog.size();
+            out.prog.insert(out.prog.end(), o.prog.begin(), o.prog.end());
+            same.push_back(tt);
+            out.n_progs++;
+        }
+    }
+    if (out.blob_off[T] / 16 > (int64_t)UINT32_MAX || (int64_t)out.prog.size() / 16 > (int64_t)UINT32_MAX)
+        return false;
+    out.tdesc.resize(4 * (size_t)T);
+    for (int32_t tt = 0; tt < T; tt++) {
+        out.tdesc[4 * tt] = (uint32_t)(out.blob_off[tt] / 16);
+        out.tdesc[4 * tt + 1] = (uint32_t)tout[tt].blob.size();
+        out.tdesc[4 * tt + 2] = (uint32_t)(prog_off[tt] / 16);
+        out.tdesc[4 * tt + 3] = (uint32_t)tout[tt].prog.size();
+    }
     out.blob.resize((size_t)out.blob_off[T]);
 #pragma omp parallel for schedule(dynamic, 256)
     for (int32_t tt = 0; tt < T; tt++) {
         if (!tout[tt].blob.empty()) std::memcpy(out.blob.data() + out.blob_off[tt], tout[tt].blob.data(), tout[tt].blob.size());
         std::vector<uint8_t>().swap(tout[tt].blob);
+        std::vector<uint8_t>().swap(tout[tt].prog);
     }
     for (int32_t tt = 0; tt < T; tt++) {
         uint8_t *bp = out.blob.data() + out.blob_off[tt];
