@@ -102,47 +102,60 @@ struct GatherK {
 // tiles (heavy x heavy: rails, hub diagonals) is a SIDE target, to which the
 // tile contributes one part.
 //
-// The tile's reduction program lists its targets by contribution count
-// ("length class"): short class c holds n_c targets of exactly L_c <= 4
-// contributions, a group class the targets of lengths 4 gs/2 < L <= 4 gs
-// (gs = cls_group(L) lanes per target);
-// each as a 32-bit destination and L_c entries (byte offsets of the
-// contributions in the tile's shared-memory slots).  A thread sums one target
-// in list order (fixed-length unrolled loops for L <= 4; a longer target is
-// summed by a group of cls_group(L) lanes, each a fixed strided subset, then
-// a fixed shuffle tree) and adds the sum to
-// its destination with ONE reduction (RED.ADD.F64): every owned target is
-// written by exactly one thread in exactly one CTA, so A_vals[k] + sum is
-// formed once and the result equals a plain read-modify-write (deterministic;
-// the SM loads no old value).  A side target's contributions in the tile are
-// cut into pieces of at most kSidePiece entries, each its own program target
-// and part (plain store), or, for the hot side targets (rails), a running
-// sum per CTA and piece index in shared memory, in tile order.  Classes are
-// processed back to back by the CTA's threads with the lane position
-// continuing across classes (cls[c].rot), so the threads' loads stay even.
+// The tile's reduction program (TILE v4).  Short targets (at most kOpMax
+// contributions; every target on the inverter / SRAM / hub structures) are
+// an OP STREAM: each thread runs its own sequence of pair-ops, one u32 each
+// (two u16 byte offsets of contributions in the tile's shared-memory slot
+// buffer; bit 0 of the second = "emit"): the thread adds both entries to its
+// running sum and, on "emit", adds the sum to the next destination of its own
+// destination list with ONE reduction (RED.ADD.F64) and restarts the sum at
+// 0.  A target of L contributions is ceil(L/2) consecutive pair-ops of one
+// thread (odd L: the last pair's second entry is the zero slot).  Every owned
+// target is written by exactly one thread of exactly one CTA, once per call,
+// so A_vals[k] + sum is formed once -- the same IEEE addition as a plain
+// read-modify-write (deterministic; the SM loads no old value).  The builder
+// balances the targets over the threads (longest first, least-loaded thread)
+// and orders the threads' sequences by length (thread 0 the longest), so op
+// step s is stored as one contiguous row of the threads that still have an op
+// there (row offsets orow[]): no padding, conflict-free 4-byte loads.
+// Longer owned targets form GROUP classes (one per lane-group size gs =
+// cls_group(L)): gs lanes per target, lane j summing the target's entries j,
+// j+gs, ... in four fixed partial sums, then a fixed xor-shuffle tree.  A
+// side target's contributions in the tile are cut into pieces of at most
+// kSidePiece entries, each its own part (plain store), or, for the hot side
+// targets (rails), a running sum per CTA and piece index in shared memory, in
+// tile order; the pieces form a second op stream (thread order reversed, so
+// they fall on the warps the owned stream loads least) whose destinations are
+// the head's side entries.
 // Everything a tile needs except x (and, in form 1, the item data) is its
 // HEAD (per tile) and its PROGRAM (shared by structurally equal tiles), which
 // two TMA bulk copies (cp.async.bulk + one mbarrier) bring into one shared-
 // memory stage, kStages tiles ahead (program right after the head):
-//   head:    TileHdr (64 B: counts, sizes, offsets, kTileBases destination
+//   head:    TileHdr (96 B: counts, sizes, offsets, kTileBases destination
 //            bases)
 //            items: form 0: term int4[ni] | beta f64[ni] | v0 f64[3][ni] | model u8[ni]
 //                   form 1: term int4[ni]; beta, v0[3], model in tile-order HBM
 //                   arrays (kTileItems slots per tile) loaded one tile ahead
 //            side:  SideEnt[n_sent]
-//   program: ProgHdr (16 B) | TileCls[n_cls] (16 B each)
-//            dst:  int32[n_tgt]: per class, the destinations of its targets
-//                  (>= 0: global target g = base[dst >> 28] + (dst & 0x0FFFFFFF),
-//                  g an A index or nnz + b row; < 0: side entry -1-dst of the head)
-//            meta: u32[n_grp]: targets of group classes: first entry (low 16
-//                  bits, u16 index in ent[]) | length << 16
-//            ent:  u16: per short class c, entries [L_c][n_c] (k-major: lanes
-//                  of a warp read consecutive u16); group classes: each
-//                  target's entries contiguous
-// The bases are the first target of each cluster of the tile's owned targets
-// (its rows' CSR block, its b rows, each heavy row's slice), so tiles of the
-// same structure have byte-identical programs; the builder stores each
-// distinct program once (cfg4: the inverter-chain and hub-load tiles).
+//   program: ProgHdr (32 B)
+//            owned op stream: orow u16[n_ostep+1] | ops u32[..] | ostart
+//                  u16[orow[1]] (first destination of each thread with ops;
+//                  a thread's step count is the rows it falls in) |
+//                  odst u32[..] (destination codes, per thread contiguous)
+//            side op stream:  srow | sops | sstart | sdst u16[..] (side entries)
+//            group classes:   TileCls[n_cls] | dst u32[..] | meta u32[..]
+//                  (first entry | length << 16) | ent u16[..] (each target's
+//                  entries contiguous)
+// A destination code d is base[d >> 28] + (d & 0x0FFFFFFF): the 16 bases are
+// global targets (an A index, or nnz + a b row), each the first target of a
+// cluster of the tile's owned targets (its rows' CSR block, its b rows, each
+// heavy row's slice; a cluster never straddles nnz), so tiles of the same
+// structure have byte-identical programs; the builder stores each distinct
+// program once (cfg4: the inverter-chain and hub-load tiles).  The kernel
+// turns the bases into 16 pointers per tile (A + g, or b + g - nnz), so a
+// destination costs a shift, a mask and one shared-memory load.  With more
+// than 16 clusters the bases are fixed: 8 chunks of 2^28 entries of A, then 8
+// of b.
 // Contributions of a FET whose source and bulk are one node (every PMOS of the
 // inverter configs) are merged at evaluation (DB into DS, BD into SD, BB into
 // SS, J[B] into J[S]) and the merged-away slots are not listed.
@@ -155,7 +168,12 @@ constexpr int kLogTileThreads = kTileThreads == 128 ? 7 : kTileThreads == 64 ? 6
 static_assert(kLogTileThreads > 0, "tile width must be 64, 128 or 256 threads");
 constexpr int kHeavyDeg = 64;        // nodes with more incident FETs are heavy
 constexpr int kMaxCls = 15;          // distinct target lengths per tile
-constexpr int kSidePiece = 4;        // side-target entries per piece (an unrolled class)
+constexpr int kSidePiece = 4;        // side-target entries per piece (two pair-ops)
+#ifndef EES_OP_MAX
+#define EES_OP_MAX 8
+#endif
+constexpr int kOpMax = EES_OP_MAX;   // owned targets of up to kOpMax contributions: op stream
+constexpr uint32_t kNoEmit = 0xFFFFFFFFu;
 #ifndef EES_HOT_PIECES
 #define EES_HOT_PIECES 24
 #endif
@@ -164,7 +182,7 @@ constexpr int kHotPieces = EES_HOT_PIECES;   // pieces of one hot target per til
 // stage bytes (one tile blob), item bytes in the blob, shared-memory slot
 // buffers (2: one barrier per tile), CTAs per SM
 #ifndef EES_STAGE1
-#define EES_STAGE1 7680
+#define EES_STAGE1 8320              // about the largest stage that keeps 5 CTAs per SM (228 KB)
 #endif
 __host__ __device__ constexpr int stage_max(int form) { return (form ? EES_STAGE1 : 11264) * kTileItems / 128; }
 __host__ __device__ constexpr int item_blob_bytes(int form) { return form ? 16 : 49; }
@@ -185,60 +203,53 @@ __host__ __device__ constexpr int tile_ctas(int form)
 
 constexpr int kStages = 3;           // TMA pipeline depth (blobs in flight per CTA)
 constexpr int kScSlots = 16 * kTileItems + 2;   // contribution slots per buffer (+16-byte pad)
+constexpr int kZeroSlotByte = 8 * 16 * kTileItems; // the pad's first slot holds 0.0 (odd-length targets)
 #ifndef EES_MAX_HOT
 #define EES_MAX_HOT 16
 #endif
 constexpr int kMaxHot = EES_MAX_HOT;  // side targets pre-reduced per CTA (rails): parts = CTAs, not tiles
 static_assert(8 * kScSlots < 65536, "entry byte offsets must fit 16 bits");
 
-// Targets of up to kShortMax contributions form short classes (one per exact
-// length, entries k-major, one thread per target); longer ones group classes
-// with cls_group(L) lanes per target (about four entries per lane, at most a
-// warp).  Measured (profiles/r02_ab.md): one thread for L = 5 beats two on
-// cfg2; lane groups for L > 6 beat one thread on cfg3.
-#ifndef EES_SHORT_MAX
-#define EES_SHORT_MAX 6
-#endif
-constexpr int kShortMax = EES_SHORT_MAX;
+// Owned targets longer than kOpMax form group classes with cls_group(L)
+// lanes per target (about four entries per lane, at most a warp).
 __host__ __device__ constexpr int cls_group(int L)
 {
-    return L <= kShortMax ? 1 : L <= 8 ? 2 : L <= 16 ? 4 : L <= 32 ? 8 : L <= 64 ? 16 : 32;
+    return L <= 16 ? 4 : L <= 32 ? 8 : L <= 64 ? 16 : 32;
 }
 
 struct TileCls {
-    uint16_t len;                    // contributions per target (1..kShortMax); 0: a group class
+    uint16_t len;                    // 0 (group class)
     uint16_t n;                      // targets
     uint16_t ent;                    // u16 index of the class's first entry in ent[]
     uint16_t dst;                    // index of the class's first destination in dst[]
     uint16_t rot;                    // lane groups (of gs lanes) used before the class, mod the
                                      // groups per CTA (kTileThreads / gs)
-    uint16_t lg;                     // group classes: log2 of the group size gs
-    uint16_t meta;                   // group classes: index of the first target's meta[] word
+    uint16_t lg;                     // log2 of the group size gs
+    uint16_t meta;                   // index of the first target's meta[] word
     uint16_t pad;
 };
 static_assert(sizeof(TileCls) == 16, "TileCls layout");
 
 // Per-tile head (streamed: one per tile) and the tile's reduction program
-// (shared by every tile with the same program bytes: owned destinations are
-// coded relative to the head's bases, so the programs of structurally equal
-// tiles -- inverter chains, hub loads -- are one copy, L2-resident).
-constexpr int kTileBases = 8;            // dst code >= 0: base[code >> 28] + (code & 0x0FFFFFFF)
+// (shared by every tile with the same program bytes).
+constexpr int kTileBases = 16;           // dst code: base[code >> 28] + (code & 0x0FFFFFFF)
 struct TileHdr {
     uint16_t n_items, n_full, n_sent, pad0;
     uint32_t head_bytes;             // head size (multiple of 16): the program follows it in the stage
     uint32_t prog_bytes;             // program size (multiple of 16)
     uint32_t off_items, off_side;    // byte offsets of the head's sections
-    int32_t base[kTileBases];        // owned-destination bases (global target ids)
+    int32_t base[kTileBases];        // destination bases (global target ids)
     uint32_t pad1[2];
 };
-static_assert(sizeof(TileHdr) == 64, "TileHdr layout");
+static_assert(sizeof(TileHdr) == 96, "TileHdr layout");
 
 struct ProgHdr {
-    uint16_t n_cls, n_tgt;
-    uint16_t off_dst, off_meta, off_ent;   // byte offsets from the program start
-    uint16_t pad[3];
+    uint16_t n_ostep, off_orow, off_ops, off_ostart, off_odst;   // owned op stream
+    uint16_t n_sstep, off_srow, off_sops, off_sstart, off_sdst;  // side op stream
+    uint16_t n_cls, off_cls, off_dst, off_meta, off_ent;         // group classes
+    uint16_t pad;
 };
-static_assert(sizeof(ProgHdr) == 16, "ProgHdr layout");
+static_assert(sizeof(ProgHdr) == 32, "ProgHdr layout");
 
 struct SideEnt {
     int32_t sid;                     // side target

@@ -1253,58 +1253,40 @@ __device__ __forceinline__ void red_add(double *p, double v)
 #endif
 }
 
-// Destination of one target (ees_internal.h): g >= 0 the global target --
-// one RED, the entry's only addition this call; g < 0 a side piece -- its
-// part slot (plain store, ordered by the ticket) or the CTA's running sum of
-// a hot target's piece index (one writer per tile).
+// Output of the reduction: the tile's destination pointers (one per base,
+// ees_internal.h: A + g or b + g - nnz, set per tile from the staged head).
 struct TileOut {
     double *A, *Bm;            // A, and b - nnz (so that b row r is Bm + nnz + r)
     int32_t nnz;
-    const int32_t *base;       // the staged head's destination bases (shared memory)
+    double *const *bptr;       // shared memory: [kTileBases]
 };
 
-__device__ __forceinline__ void tile_put(const SideEnt *sents, const TileOut &o, const TileK &tk, double *s_hot,
-                                         int32_t g, double v)     // g: the program's destination code
+__device__ __forceinline__ double *tile_dst(const TileOut &o, uint32_t d)
 {
-    if (g >= 0) {
-        g = o.base[g >> 28] + (g & 0x0FFFFFFF);
-        red_add((g < o.nnz ? o.A : o.Bm) + g, v);
-    } else {
-        const SideEnt se = sents[-1 - g];
-        if (se.slot >= 0) tk.part[se.slot] = v;
-        else s_hot[-1 - se.slot] += v;
-    }
+    return o.bptr[d >> 28] + (d & 0x0FFFFFFFu);
 }
 
-// One target k of a short class: entries [len][n] (byte offsets into the
-// slot buffer), summed in list order; L > 0 the length at compile time
-// (unrolled), L = 0 at run time (len <= kShortMax).
-template <int L>
-__device__ __forceinline__ void tile_one(int k, int n, int len, const int32_t *dst, const uint16_t *ent,
-                                         const unsigned char *sc, const SideEnt *sents, const TileOut &o,
-                                         const TileK &tk, double *s_hot)
+__device__ __forceinline__ double sc_ld(const unsigned char *sc, uint32_t byte)
 {
-    const int32_t g = dst[k];
-    double v = *reinterpret_cast<const double *>(sc + ent[k]);
-    if (L > 0) {
-#pragma unroll
-        for (int p = 1; p < L; p++) v += *reinterpret_cast<const double *>(sc + ent[p * n + k]);
-    } else {
-#pragma unroll 2
-        for (int p = 1; p < len; p++) v += *reinterpret_cast<const double *>(sc + ent[p * n + k]);
-    }
-    tile_put(sents, o, tk, s_hot, g, v);
+    return *reinterpret_cast<const double *>(sc + byte);
 }
 
-// A group class (targets of L > kShortMax with one group size gs = cls_group(L)): a
-// group of gs lanes per target, lane j summing the target's entries j, j+gs,
-// ... in four fixed partial sums, then a fixed xor shuffle tree within the
-// group; the group's first lane puts the sum.  All
+// The steps of sequence j in an op stream: the rows it falls in (sequences
+// are ordered longest first, so row s holds sequences 0 .. rows[s+1]-rows[s]-1).
+__device__ __forceinline__ int op_steps(const uint16_t *row, int n_step, int j)
+{
+    int c = 0;
+    while (c < n_step && j < (int)row[c + 1] - (int)row[c]) c++;
+    return c;
+}
+
+// A group class (owned targets longer than kOpMax, group size gs =
+// cls_group(L)): a group of gs lanes per target, lane j summing the target's
+// entries j, j+gs, ... in four fixed partial sums, then a fixed xor shuffle
+// tree within the group; the group's first lane adds the sum (one RED).  All
 // lanes of a warp run the same number of iterations (shuffles need them).
-__device__ __forceinline__ void tile_cls_group(const TileCls c, int r, const int32_t *dst, const uint32_t *meta,
-                                               const uint16_t *ent, const unsigned char *sc,
-                                               const SideEnt *sents, const TileOut &o, const TileK &tk,
-                                               double *s_hot)
+__device__ __forceinline__ void tile_cls_group(const TileCls c, int r, const uint32_t *dst, const uint32_t *meta,
+                                               const uint16_t *ent, const unsigned char *sc, const TileOut &o)
 {
     const int n = c.n, lg = c.lg, gs = 1 << lg;
     const int lgn = kLogTileThreads - lg;                 // log2(kTileThreads / gs)
@@ -1322,20 +1304,19 @@ __device__ __forceinline__ void tile_cls_group(const TileCls c, int r, const int
             const uint32_t m = meta[k];
             const uint16_t *e = ent + (m & 0xFFFFu);
             const int L = (int)(m >> 16);
-            auto val = [&](int p) { return *reinterpret_cast<const double *>(sc + e[p]); };
             double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
             int p = lj;
             for (; p + 3 * gs < L; p += 4 * gs) {
-                s0 += val(p);
-                s1 += val(p + gs);
-                s2 += val(p + 2 * gs);
-                s3 += val(p + 3 * gs);
+                s0 += sc_ld(sc, e[p]);
+                s1 += sc_ld(sc, e[p + gs]);
+                s2 += sc_ld(sc, e[p + 2 * gs]);
+                s3 += sc_ld(sc, e[p + 3 * gs]);
             }
-            for (; p < L; p += gs) s0 += val(p);
+            for (; p < L; p += gs) s0 += sc_ld(sc, e[p]);
             s = (s0 + s1) + (s2 + s3);
         }
         for (int off = gs >> 1; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-        if (act && lj == 0) tile_put(sents, o, tk, s_hot, dst[k], s);
+        if (act && lj == 0) red_add(tile_dst(o, dst[k]), s);
     }
 }
 
@@ -1424,9 +1405,10 @@ __device__ __forceinline__ void tile_eval_item(const unsigned char *blob, const 
 }
 
 // The reduction program of one staged tile, run by kTileThreads threads with
-// thread index r (0 .. kTileThreads-1; whole warps).
+// thread index r (0 .. kTileThreads-1; whole warps): the owned op stream,
+// the group classes, then the side op stream (ees_internal.h).
 __device__ __forceinline__ void tile_reduce(const unsigned char *blob, const unsigned char *sc, int r,
-                                            const TileOut &out0, const TileK &tk, double *s_hot)
+                                            const TileOut &out, const TileK &tk, double *s_hot)
 {
 #ifdef EES_DIAG_NOREDUCE         // diagnostic A/B only (no stamps): evaluation alone
     return;
@@ -1434,36 +1416,64 @@ __device__ __forceinline__ void tile_reduce(const unsigned char *blob, const uns
     const TileHdr *h = reinterpret_cast<const TileHdr *>(blob);
     const unsigned char *prog = blob + h->head_bytes;
     const ProgHdr *ph = reinterpret_cast<const ProgHdr *>(prog);
-    const TileCls *cls = reinterpret_cast<const TileCls *>(prog + sizeof(ProgHdr));
-    const int32_t *dst = reinterpret_cast<const int32_t *>(prog + ph->off_dst);
-    const uint16_t *ent = reinterpret_cast<const uint16_t *>(prog + ph->off_ent);
-    const uint32_t *meta = reinterpret_cast<const uint32_t *>(prog + ph->off_meta);
-    const SideEnt *sents = reinterpret_cast<const SideEnt *>(blob + h->off_side);
-    TileOut out = out0;
-    out.base = h->base;
-    const int ncl = ph->n_cls;
-    for (int ci = 0; ci < ncl; ci++) {
-        const TileCls c = cls[ci];
-        const uint16_t *e = ent + c.ent;
-        const int32_t *dc = dst + c.dst;
-        if (c.len == 0) {                              // group class (warp-uniform)
-            tile_cls_group(c, r, dc, meta + c.meta, ent, sc, sents, out, tk, s_hot);
-            continue;
+    {
+        // owned op stream: pair-ops of this thread's sequence, one RED per target
+        const uint16_t *row = reinterpret_cast<const uint16_t *>(prog + ph->off_orow);
+        const uint32_t *ops = reinterpret_cast<const uint32_t *>(prog + ph->off_ops);
+        const int ns = op_steps(row, ph->n_ostep, r);
+        if (ns > 0) {
+            const uint32_t *dst = reinterpret_cast<const uint32_t *>(prog + ph->off_odst) +
+                                  reinterpret_cast<const uint16_t *>(prog + ph->off_ostart)[r];
+            double acc = 0.0;
+#pragma unroll 2
+            for (int st = 0; st < ns; st++) {
+                const uint32_t w = ops[row[st] + r];
+                acc += sc_ld(sc, w & 0xFFFFu);
+                acc += sc_ld(sc, (w >> 16) & 0xFFF8u);
+                if (w & 0x10000u) {                       // emit: the target is complete
+                    red_add(tile_dst(out, *dst++), acc);
+                    acc = 0.0;
+                }
+            }
         }
-        // short class: targets k = r - rot, +kTileThreads, ... (rot continues the
-        // lane position from the classes before, so the threads' loads stay even)
-        const int n = c.n;
-        const int k0 = (r - (int)c.rot) & (kTileThreads - 1);
-        if (k0 >= n) continue;                         // no target of this class here
-#define TILE_ONE(L) for (int k = k0; k < n; k += kTileThreads) tile_one<L>(k, n, c.len, dc, e, sc, sents, out, tk, s_hot)
-        switch (c.len) {
-        case 1: TILE_ONE(1); break;
-        case 2: TILE_ONE(2); break;
-        case 3: TILE_ONE(3); break;
-        case 4: TILE_ONE(4); break;
-        default: TILE_ONE(0); break;
+    }
+    {
+        // group classes (targets longer than kOpMax)
+        const int ncl = ph->n_cls;
+        const TileCls *cls = reinterpret_cast<const TileCls *>(prog + ph->off_cls);
+        const uint32_t *dst = reinterpret_cast<const uint32_t *>(prog + ph->off_dst);
+        const uint32_t *meta = reinterpret_cast<const uint32_t *>(prog + ph->off_meta);
+        const uint16_t *ent = reinterpret_cast<const uint16_t *>(prog + ph->off_ent);
+        for (int ci = 0; ci < ncl; ci++) {
+            const TileCls c = cls[ci];
+            tile_cls_group(c, r, dst + c.dst, meta + c.meta, ent, sc, out);
         }
-#undef TILE_ONE
+    }
+    {
+        // side op stream (sequences in reversed thread order): each piece's sum
+        // is its part (plain store) or adds to the CTA's running sum of a hot
+        // target's piece (one writer per tile)
+        const int j = kTileThreads - 1 - r;
+        const uint16_t *row = reinterpret_cast<const uint16_t *>(prog + ph->off_srow);
+        const uint32_t *ops = reinterpret_cast<const uint32_t *>(prog + ph->off_sops);
+        const int ns = op_steps(row, ph->n_sstep, j);
+        if (ns > 0) {
+            const SideEnt *sents = reinterpret_cast<const SideEnt *>(blob + h->off_side);
+            const uint16_t *dst = reinterpret_cast<const uint16_t *>(prog + ph->off_sdst) +
+                                  reinterpret_cast<const uint16_t *>(prog + ph->off_sstart)[j];
+            double acc = 0.0;
+            for (int st = 0; st < ns; st++) {
+                const uint32_t w = ops[row[st] + j];
+                acc += sc_ld(sc, w & 0xFFFFu);
+                acc += sc_ld(sc, (w >> 16) & 0xFFF8u);
+                if (w & 0x10000u) {
+                    const SideEnt se = sents[*dst++];
+                    if (se.slot >= 0) tk.part[se.slot] = acc;
+                    else s_hot[-1 - se.slot] += acc;
+                    acc = 0.0;
+                }
+            }
+        }
     }
 }
 
@@ -1536,11 +1546,12 @@ __device__ __forceinline__ void tile_finish(const TileK &tk, const CallK &P, con
         tma_bulk_g2s(sd + d.y, tk.prog + 16 * (size_t)d.z, d.w, &s_bar[stage]);                 \
     };                                                                                           \
     auto issue = [&](int32_t tile, int stage) { issue_at(__ldg(tk.tdesc + tile), stage); };     \
+    __shared__ double *s_bptr[2 * kTileBases];    /* two tiles (a second slot buffer has no B0) */ \
     TileOut out;                                                                                 \
     out.A = P.A;                                                                                 \
     out.Bm = P.b - tk.nnz;                                                                       \
     out.nnz = (int32_t)tk.nnz;                    /* < 2^31 (setup) */                           \
-    out.base = nullptr;                           /* set per tile (tile_reduce) */               \
+    out.bptr = s_bptr;                            /* per tile: s_bptr + (it & 1) * kTileBases */ \
     const int32_t t0 = blockIdx.x;                                                               \
     if (tid == 0) {                                                                              \
         for (int k = 0; k < (NSTAGES); k++) mbar_init(&s_bar[k], 1);                             \
@@ -1561,6 +1572,7 @@ __global__ void __launch_bounds__(kTileThreads, tile_ctas(kForm)) k_tile(TileK t
 #define s_stage (smem + sizeof(double) * kScSlots * kBuf)
     TILE_PROLOGUE(kTileThreads, kStages);
     unsigned char *s_c = smem;                                           // [kBuf][kScSlots] doubles
+    if (tid < kBuf) reinterpret_cast<double *>(s_c + (size_t)tid * 8 * kScSlots)[16 * kTileItems] = 0.0;  // zero slot
     uint32_t parity = 0;                 // bit k: phase of s_bar[k]
     int it = 0;
     int stage = 0;
@@ -1580,6 +1592,12 @@ __global__ void __launch_bounds__(kTileThreads, tile_ctas(kForm)) k_tile(TileK t
         const int32_t tr = t - G + kStages * G;
         uint4 rf = make_uint4(0, 0, 0, 0);
         if (tid == 0 && it > 0 && tr < tk.n_tiles) rf = __ldg(tk.tdesc + tr);
+        TileOut o = out;
+        o.bptr = s_bptr + (it & 1) * kTileBases;
+        if (tid < kTileBases) {                 // this tile's destination pointers (read after B1)
+            const int32_t g = reinterpret_cast<const TileHdr *>(blob)->base[tid];
+            s_bptr[(it & 1) * kTileBases + tid] = g < out.nnz ? out.A + g : out.Bm + g;
+        }
         if (tid < reinterpret_cast<const TileHdr *>(blob)->n_items)
             tile_eval_item<kRep, kForm>(blob, cur, tid, reinterpret_cast<double *>(sc), s_cards, P);
         // next tile: its blob was issued >= one tile ago; start its gathers now
@@ -1594,7 +1612,7 @@ __global__ void __launch_bounds__(kTileThreads, tile_ctas(kForm)) k_tile(TileK t
         __syncthreads();                                        // B1
         if (tid == 0 && it > 0 && tr < tk.n_tiles)              // refill the stage of tile t-G
             issue_at(rf, stage == 0 ? kStages - 1 : stage - 1);
-        tile_reduce(blob, sc, tid, out, tk, s_hot);
+        tile_reduce(blob, sc, tid, o, tk, s_hot);
         TILE_TRACE(3 + 2 * it);
         if (kBuf == 1) __syncthreads();                         // B0: slots free for the next tile
         stage = sn;

@@ -26,19 +26,21 @@ namespace {
 constexpr int32_t kUnset = -1;
 constexpr int32_t kSide = -2;
 // Upper bound of a tile's blob while it is being formed.  Owned targets are
-// counted exactly: a target with L contributions costs a 4 B destination and
-// 2 B per entry; each distinct length in the tile costs an 8 B class header.
-// Items cost item_blob_bytes(form).  Heavy x heavy targets (owned by their
-// home tile, or side) are bounded: owned, a target with c contributions costs
-// 4 + 2c B and the class header of length c (counted like an owned target's);
-// side, at most ceil(c / kSidePiece) pieces of 4 B destination + 8 B side
-// entry + 2 B per entry, whose lengths (1..kSidePiece) take at most
-// kSidePiece class headers per tile (reserved in kBlobFixed) -> 12 B per
-// distinct target + 2 + 12 / kSidePiece = 5 B per contribution covers both.
-// Fixed: head and program headers + six section paddings + the side-piece
-// class headers.
-constexpr int64_t kBlobFixed = (int64_t)sizeof(TileHdr) + (int64_t)sizeof(ProgHdr) + 6 * 16 +
-                               kSidePiece * (int64_t)sizeof(TileCls);
+// counted exactly: a target with L <= kOpMax contributions costs ceil(L/2)
+// 4 B pair-ops and a 4 B destination; a longer one a 4 B destination, 2 B per
+// entry, a 4 B meta word and, if its lane-group size is new in the tile, a
+// 16 B class header.  Items cost item_blob_bytes(form).  Heavy x heavy
+// targets (owned by their home tile, or side) are bounded: owned, as above
+// (<= 12 + 2c B for c contributions, plus meta and class header); side, at
+// most ceil(c / kSidePiece) pieces of 4 B per pair-op, a 2 B destination and
+// an 8 B side entry -> 2c + 12 ceil(c/4) <= 12 + 5c B: kHHTarget = 12 B per
+// distinct target and kHHContrib = 5 B per contribution cover both.  Fixed:
+// head and program headers, the two streams' per-sequence start words and row
+// offsets (a tile lists at most 16 kTileItems contributions, so a stream has
+// at most 16 + 3 steps: balanced, targets of <= 4 pair-ops), fourteen section
+// paddings.
+constexpr int64_t kBlobFixed = (int64_t)sizeof(TileHdr) + (int64_t)sizeof(ProgHdr) + 14 * 16 +
+                               2 * 2 * kTileThreads + 2 * 2 * 21;
 constexpr int64_t kHHTarget = 12, kHHContrib = 5;
 size_t pad16(size_t x) { return (x + 15) & ~(size_t)15; }
 }  // namespace
@@ -111,13 +113,13 @@ bool build_tile_host(int form, int64_t N, int32_t n_nodes, int32_t n, int64_t nn
     for (int64_t i = 0; i < N; i++)
         for (int p = 0; p < NPAIR + 4; p++)
             if (listed_c(i, p)) tcnt[p < NPAIR ? rec[i].s[p] : nnz + rec[i].t[p - NPAIR]]++;
-    // distinct target lengths of the tile being formed (class headers)
-    // class keys: lengths 1..4, then 4 + group size (<= 36)
+    // lane-group sizes (group classes) of the tile being formed (class headers)
     std::vector<int32_t> len_tile(64, -1);
     auto tgt_bytes = [&](int32_t L, int32_t tile) -> int64_t {
         if (L <= 0) return 0;
-        int64_t e = 4 + 2 * (int64_t)L + (L > kShortMax ? 4 : 0);   // dst, entries, group meta
-        const int32_t key = L > kShortMax ? kShortMax + cls_group(L) : L;   // class of this length
+        if (L <= kOpMax) return 4 + 4 * (int64_t)((L + 1) / 2);     // destination, pair-ops
+        int64_t e = 4 + 2 * (int64_t)L + 4;                         // destination, entries, meta
+        const int32_t key = cls_group(L);
         if (len_tile[key] != tile) {
             len_tile[key] = tile;
             e += (int64_t)sizeof(TileCls);
@@ -126,12 +128,11 @@ bool build_tile_host(int form, int64_t N, int32_t n_nodes, int32_t n, int64_t nn
     };
     hh_len_bytes = [&](int32_t g, int32_t tile) -> int64_t {
         const int32_t L = tcnt[g];
-        if (L <= 0) return 0;
-        const int32_t key = L > kShortMax ? kShortMax + cls_group(L) : L;
-        int64_t e = L > kShortMax ? 4 : 0;                       // group meta word (owned case)
-        if (len_tile[key] == tile) return e;
+        if (L <= kOpMax) return 0;
+        const int32_t key = cls_group(L);
+        if (len_tile[key] == tile) return 4;                     // group meta word (owned case)
         len_tile[key] = tile;
-        return e + (int64_t)sizeof(TileCls);
+        return 4 + (int64_t)sizeof(TileCls);
     };
     auto row_bytes = [&](int32_t r, int32_t tile) {       // the row's CSR entries and its b row
         int64_t e = tgt_bytes(tcnt[nnz + r], tile);
@@ -417,116 +418,214 @@ bool build_tile_host(int form, int64_t N, int32_t n_nodes, int32_t n, int64_t nn
         }
         const int32_t n_sent = (int32_t)sents.size();
         o.listed += (int64_t)con.size() + (int64_t)side.size();
-        // classes: group classes (L > kShortMax, by lane-group size, largest
-        // first), then one per short length (owned targets and side pieces
-        // together: separate side classes measured slower, profiles/r02_ab.md);
-        // targets in list order within a class
-        auto cls_key = [](const Tgt &t2) { return t2.len > kShortMax ? 100 + cls_group(t2.len) : t2.len; };
-        std::stable_sort(tg.begin(), tg.end(), [&](const Tgt &a, const Tgt &b) { return cls_key(a) > cls_key(b); });
-        cls.clear();
-        dsts.clear();
-        ents.clear();
-        meta.clear();
-        int64_t cum = 0;
-        for (size_t k = 0; k < tg.size();) {
-            size_t e = k;
-            const int key = cls_key(tg[k]);
-            while (e < tg.size() && cls_key(tg[e]) == key) e++;
-            const int32_t nc = (int32_t)(e - k);
-            if (nc > 65535 || ents.size() > 65535 || dsts.size() > 65535 || meta.size() > 65535) return false;
-            TileCls tc;
-            std::memset(&tc, 0, sizeof(tc));
-            tc.n = (uint16_t)nc;
-            tc.ent = (uint16_t)ents.size();
-            tc.dst = (uint16_t)dsts.size();
-            auto entry = [&](const Tgt &t2, int32_t p) {
-                return (uint16_t)(8 * (t2.is_side ? side[t2.beg + p].second : con[t2.beg + p].second));
-            };
-            int64_t gs = 1;
-            if (key > 100) {                                  // group class
-                gs = cls_group(tg[k].len);
-                int lg = 0;
-                while ((1 << lg) < gs) lg++;
-                tc.len = 0;
-                tc.lg = (uint16_t)lg;
-                tc.meta = (uint16_t)meta.size();
-                for (size_t q = k; q < e; q++) {
-                    const Tgt &t2 = tg[q];
-                    if (ents.size() > 65535 || t2.len > 65535) return false;
-                    meta.push_back((uint32_t)ents.size() | ((uint32_t)t2.len << 16));
-                    for (int32_t p = 0; p < t2.len; p++) ents.push_back(entry(t2, p));
-                    dsts.push_back(t2.dst);
-                }
-            } else {
-                const int32_t L = tg[k].len;
-                tc.len = (uint16_t)L;
-                for (size_t q = k; q < e; q++) dsts.push_back(tg[q].dst);
-                for (int32_t p = 0; p < L; p++)
-                    for (size_t q = k; q < e; q++) ents.push_back(entry(tg[q], p));
-            }
-            const int64_t ng = kTileThreads / gs;
-            tc.rot = (uint16_t)((cum / gs) % ng);
-            cls.push_back(tc);
-            cum += (int64_t)nc * gs;          // lanes occupied
-            k = e;
-        }
-        if (ents.size() > 65536) return false;
-        // destination bases: the first target of each cluster of the owned
-        // targets (ascending; a new cluster after a gap > kGap), so equal tile
-        // structures give equal codes; more than kTileBases clusters: the
-        // fixed bases s << 28 (codes = global targets)
+        auto entry = [&](const Tgt &t2, int32_t p) {
+            return (uint16_t)(8 * (t2.is_side ? side[t2.beg + p].second : con[t2.beg + p].second));
+        };
+        // ---- destination bases: the first target of each cluster of the owned
+        // targets (ascending; a new cluster after a gap > kGap and at nnz, so
+        // a cluster is all A or all b), so equal tile structures give equal
+        // codes; more than kTileBases clusters: fixed bases (8 chunks of A,
+        // 8 of b)
         int32_t bases[kTileBases];
+        bool fixed = false;
         {
             constexpr int32_t kGap = 4096, kSpan = 1 << 28;
             int nb = 0;
-            bool fixed = false;
             int32_t prev = -1;
             owned_g.clear();
             for (const Tgt &t2 : tg)
                 if (!t2.is_side) owned_g.push_back(t2.dst);
             std::sort(owned_g.begin(), owned_g.end());
             for (const int32_t g : owned_g) {
-                if (nb == 0 || g - prev > kGap || g - bases[nb - 1] >= kSpan) {
+                if (nb == 0 || g - prev > kGap || g - bases[nb - 1] >= kSpan - 1 ||
+                    (g >= nnz && bases[nb - 1] < nnz)) {
                     if (nb == kTileBases) { fixed = true; break; }
                     bases[nb++] = g;
                 }
                 prev = g;
             }
             if (fixed) {
-                for (int q = 0; q < kTileBases; q++) bases[q] = q * kSpan;
-                nb = kTileBases;
+                for (int q = 0; q < 8; q++) {
+                    bases[q] = (int32_t)std::min<int64_t>((int64_t)q * kSpan, INT32_MAX);
+                    bases[8 + q] = (int32_t)std::min<int64_t>(nnz + (int64_t)q * kSpan, INT32_MAX);
+                }
+            } else {
+                for (int q = nb; q < kTileBases; q++) bases[q] = INT32_MAX;
             }
-            for (int q = nb; q < kTileBases; q++) bases[q] = INT32_MAX;
-            for (int32_t &d : dsts) {
-                if (d < 0) continue;
-                int q = 0;
-                while (q + 1 < kTileBases && bases[q + 1] <= d) q++;
-                const int32_t off = d - bases[q];
-                if (off < 0 || off >= kSpan) return false;
-                d = (q << 28) | off;
+        }
+        auto code_of = [&](int32_t g) -> uint32_t {
+            if (fixed) {
+                const int64_t r = g < nnz ? (int64_t)g : (int64_t)g - nnz;
+                const int q = (int)(r >> 28) + (g < nnz ? 0 : 8);
+                return ((uint32_t)q << 28) | (uint32_t)(r & 0x0FFFFFFF);
             }
+            int q = 0;
+            while (q + 1 < kTileBases && bases[q + 1] <= g) q++;      // clusters never straddle nnz
+            return ((uint32_t)q << 28) | (uint32_t)(g - bases[q]);
+        };
+        for (int32_t g : owned_g) {             // every owned target must be codable
+            const uint32_t c = code_of(g);
+            const int q = (int)(c >> 28);
+            if ((int64_t)bases[q] + (c & 0x0FFFFFFF) != (int64_t)g) return false;
+        }
+        // ---- op streams: owned targets of <= kOpMax entries (and the side
+        // pieces, a stream of their own) as per-thread sequences of pair-ops
+        struct Stream {
+            std::vector<uint16_t> row;           // [n_step + 1] row offsets
+            std::vector<uint32_t> ops;           // pair words, step-major rows
+            std::vector<uint16_t> start;         // per sequence with ops: its first emission
+            std::vector<uint32_t> dst;           // destination per emission
+            int32_t n_step = 0;
+        };
+        auto build_stream = [&](const std::vector<int32_t> &tl, Stream &S) -> bool {
+            // longest first onto the least-loaded sequence (ties: lower index)
+            std::vector<int32_t> order(tl);
+            std::stable_sort(order.begin(), order.end(),
+                             [&](int32_t a, int32_t b) { return tg[a].len > tg[b].len; });
+            std::vector<std::vector<int32_t>> seq(kTileThreads);
+            std::vector<int32_t> load(kTileThreads, 0);
+            for (int32_t k : order) {
+                int best = 0;
+                for (int r = 1; r < kTileThreads; r++)
+                    if (load[r] < load[best]) best = r;
+                seq[best].push_back(k);
+                load[best] += (tg[k].len + 1) / 2;
+            }
+            // sequences by length, longest first: step s is a contiguous row
+            std::vector<int32_t> perm(kTileThreads);
+            std::iota(perm.begin(), perm.end(), 0);
+            std::stable_sort(perm.begin(), perm.end(), [&](int32_t a, int32_t b) { return load[a] > load[b]; });
+            S.n_step = load[perm[0]];
+            if (S.n_step > 20) return false;                  // the byte bound's row reserve
+            std::vector<std::vector<uint32_t>> words(kTileThreads);
+            S.start.clear();
+            S.dst.clear();
+            for (int j = 0; j < kTileThreads; j++) {
+                const int32_t r = perm[j];
+                if (S.dst.size() > 65535) return false;
+                if (load[r] > 0) S.start.push_back((uint16_t)S.dst.size());   // sequences with ops
+                for (int32_t k : seq[r]) {
+                    const Tgt &t2 = tg[k];
+                    for (int32_t p = 0; p < t2.len; p += 2) {
+                        const uint16_t ea = entry(t2, p);
+                        uint16_t eb = p + 1 < t2.len ? entry(t2, p + 1) : (uint16_t)kZeroSlotByte;
+                        if (p + 2 >= t2.len) eb |= 1;                      // emit after this pair
+                        words[j].push_back((uint32_t)ea | ((uint32_t)eb << 16));
+                    }
+                    S.dst.push_back(t2.is_side ? (uint32_t)(-1 - t2.dst) : code_of(t2.dst));
+                }
+            }
+            S.row.assign(1, 0);
+            S.ops.clear();
+            for (int32_t st = 0; st < S.n_step; st++) {
+                for (int j = 0; j < kTileThreads && (int32_t)words[j].size() > st; j++) S.ops.push_back(words[j][st]);
+                if (S.ops.size() > 65535) return false;
+                S.row.push_back((uint16_t)S.ops.size());
+            }
+            return true;
+        };
+        std::vector<int32_t> own_short, own_long, side_tl;
+        for (int32_t k = 0; k < (int32_t)tg.size(); k++) {
+            if (tg[k].is_side) side_tl.push_back(k);
+            else if (tg[k].len <= kOpMax) own_short.push_back(k);
+            else own_long.push_back(k);
+        }
+        Stream so, ss;
+        if (!build_stream(own_short, so) || !build_stream(side_tl, ss)) return false;
+        // ---- group classes: owned targets longer than kOpMax, one class per
+        // lane-group size (largest first), targets in list order
+        cls.clear();
+        dsts.clear();
+        ents.clear();
+        meta.clear();
+        {
+            std::stable_sort(own_long.begin(), own_long.end(), [&](int32_t a, int32_t b) {
+                return cls_group(tg[a].len) > cls_group(tg[b].len);
+            });
+            int64_t cum = 0;
+            for (size_t k = 0; k < own_long.size();) {
+                const int gs = cls_group(tg[own_long[k]].len);
+                size_t e = k;
+                while (e < own_long.size() && cls_group(tg[own_long[e]].len) == gs) e++;
+                if (e - k > 65535 || ents.size() > 65535 || dsts.size() > 65535 || meta.size() > 65535) return false;
+                TileCls tc;
+                std::memset(&tc, 0, sizeof(tc));
+                tc.n = (uint16_t)(e - k);
+                tc.ent = (uint16_t)ents.size();
+                tc.dst = (uint16_t)dsts.size();
+                int lg = 0;
+                while ((1 << lg) < gs) lg++;
+                tc.lg = (uint16_t)lg;
+                tc.meta = (uint16_t)meta.size();
+                for (size_t q = k; q < e; q++) {
+                    const Tgt &t2 = tg[own_long[q]];
+                    if (ents.size() > 65535 || t2.len > 65535) return false;
+                    meta.push_back((uint32_t)ents.size() | ((uint32_t)t2.len << 16));
+                    for (int32_t p = 0; p < t2.len; p++) ents.push_back(entry(t2, p));
+                    dsts.push_back((int32_t)code_of(t2.dst));
+                }
+                const int64_t ng = kTileThreads / gs;
+                tc.rot = (uint16_t)((cum / gs) % ng);
+                cls.push_back(tc);
+                cum += (int64_t)tc.n * gs;
+                k = e;
+            }
+            if (ents.size() > 65536) return false;
         }
         // emit the head (per tile) and the program (shared by equal tiles)
         ProgHdr ph;
         std::memset(&ph, 0, sizeof(ph));
-        ph.n_cls = (uint16_t)cls.size();
-        ph.n_tgt = (uint16_t)tg.size();
-        if (tg.size() > 65535 || n_sent > 65535) return false;
-        const size_t off_dst = pad16(sizeof(ProgHdr) + sizeof(TileCls) * cls.size());
-        const size_t off_meta = off_dst + 4 * dsts.size();
-        const size_t off_ent = pad16(off_meta + 4 * meta.size());
-        const size_t pbytes = pad16(off_ent + 2 * ents.size());
+        size_t off = sizeof(ProgHdr);
+        auto place = [&](size_t bytes) {
+            const size_t at = off;
+            off = pad16(off + bytes);
+            return at;
+        };
+        const size_t o_orow = place(2 * so.row.size()), o_ops = place(4 * so.ops.size()),
+                     o_ost = place(2 * so.start.size()), o_odst = place(4 * so.dst.size());
+        const size_t o_srow = place(2 * ss.row.size()), o_sops = place(4 * ss.ops.size()),
+                     o_sst = place(2 * ss.start.size()), o_sdst = place(2 * ss.dst.size());
+        const size_t o_cls = place(sizeof(TileCls) * cls.size()), o_dst = place(4 * dsts.size()),
+                     o_meta = place(4 * meta.size()), o_ent = place(2 * ents.size());
+        const size_t pbytes = off;
         if (pbytes > 65535) return false;
-        ph.off_dst = (uint16_t)off_dst;
-        ph.off_meta = (uint16_t)off_meta;
-        ph.off_ent = (uint16_t)off_ent;
+        ph.n_ostep = (uint16_t)so.n_step;
+        ph.off_orow = (uint16_t)o_orow;
+        ph.off_ops = (uint16_t)o_ops;
+        ph.off_ostart = (uint16_t)o_ost;
+        ph.off_odst = (uint16_t)o_odst;
+        ph.n_sstep = (uint16_t)ss.n_step;
+        ph.off_srow = (uint16_t)o_srow;
+        ph.off_sops = (uint16_t)o_sops;
+        ph.off_sstart = (uint16_t)o_sst;
+        ph.off_sdst = (uint16_t)o_sdst;
+        ph.n_cls = (uint16_t)cls.size();
+        ph.off_cls = (uint16_t)o_cls;
+        ph.off_dst = (uint16_t)o_dst;
+        ph.off_meta = (uint16_t)o_meta;
+        ph.off_ent = (uint16_t)o_ent;
         o.prog.assign(pbytes, 0);
         uint8_t *pp = o.prog.data();
         std::memcpy(pp, &ph, sizeof(ph));
-        if (!cls.empty()) std::memcpy(pp + sizeof(ProgHdr), cls.data(), sizeof(TileCls) * cls.size());
-        if (!dsts.empty()) std::memcpy(pp + off_dst, dsts.data(), 4 * dsts.size());
-        if (!meta.empty()) std::memcpy(pp + off_meta, meta.data(), 4 * meta.size());
-        if (!ents.empty()) std::memcpy(pp + off_ent, ents.data(), 2 * ents.size());
+        auto put = [&](size_t at, const void *src, size_t bytes) {
+            if (bytes) std::memcpy(pp + at, src, bytes);
+        };
+        put(o_orow, so.row.data(), 2 * so.row.size());
+        put(o_ops, so.ops.data(), 4 * so.ops.size());
+        put(o_ost, so.start.data(), 2 * so.start.size());
+        put(o_odst, so.dst.data(), 4 * so.dst.size());
+        put(o_srow, ss.row.data(), 2 * ss.row.size());
+        put(o_sops, ss.ops.data(), 4 * ss.ops.size());
+        put(o_sst, ss.start.data(), 2 * ss.start.size());
+        for (size_t q = 0; q < ss.dst.size(); q++) {
+            if (ss.dst[q] > 65535) return false;
+            const uint16_t v = (uint16_t)ss.dst[q];
+            std::memcpy(pp + o_sdst + 2 * q, &v, 2);
+        }
+        put(o_cls, cls.data(), sizeof(TileCls) * cls.size());
+        put(o_dst, dsts.data(), 4 * dsts.size());
+        put(o_meta, meta.data(), 4 * meta.size());
+        put(o_ent, ents.data(), 2 * ents.size());
         uint64_t hsh = 1469598103934665603ull;            // FNV-1a
         for (size_t q = 0; q < pbytes; q++) hsh = (hsh ^ pp[q]) * 1099511628211ull;
         o.hash = hsh;
@@ -571,7 +670,7 @@ bool build_tile_host(int form, int64_t N, int32_t n_nodes, int32_t n, int64_t nn
         o.n_own = n_own;
         o.n_sent = n_sent;
         o.L = (int64_t)con.size() + (int64_t)side.size();
-        o.padded = o.L;
+        o.padded = 2 * (int64_t)(so.ops.size() + ss.ops.size()) + (int64_t)ents.size();
         return true;
     };
 #pragma omp for schedule(dynamic, 64)
