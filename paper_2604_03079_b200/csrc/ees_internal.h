@@ -138,10 +138,10 @@ struct GatherK {
 //                   arrays (kTileItems slots per tile) loaded one tile ahead
 //            side:  SideEnt[n_sent]
 //   program: ProgHdr (32 B)
-//            owned op stream: orow u16[n_ostep+1] | ops u32[..] | ostart
-//                  u16[orow[1]] (first destination of each thread with ops;
-//                  a thread's step count is the rows it falls in) |
-//                  odst u32[..] (destination codes, per thread contiguous)
+//            owned op stream: orow u16[steps] (row offsets) | ops u32[..] |
+//                  ostart u16[n_oseq] (per sequence with ops: its first
+//                  destination | its step count << kSeqStartBits) |
+//                  odst u32[..] (destination codes, per sequence contiguous)
 //            side op stream:  srow | sops | sstart | sdst u16[..] (side entries)
 //            group classes:   TileCls[n_cls] | dst u32[..] | meta u32[..]
 //                  (first entry | length << 16) | ent u16[..] (each target's
@@ -244,11 +244,12 @@ struct TileHdr {
 static_assert(sizeof(TileHdr) == 96, "TileHdr layout");
 
 struct ProgHdr {
-    uint16_t n_ostep, off_orow, off_ops, off_ostart, off_odst;   // owned op stream
-    uint16_t n_sstep, off_srow, off_sops, off_sstart, off_sdst;  // side op stream
+    uint16_t n_oseq, off_orow, off_ops, off_ostart, off_odst;    // owned op stream
+    uint16_t n_sseq, off_srow, off_sops, off_sstart, off_sdst;   // side op stream
     uint16_t n_cls, off_cls, off_dst, off_meta, off_ent;         // group classes
     uint16_t pad;
 };
+constexpr int kSeqStartBits = 11;        // sequence word: first destination | steps << 11
 static_assert(sizeof(ProgHdr) == 32, "ProgHdr layout");
 
 struct SideEnt {

@@ -1258,26 +1258,33 @@ __device__ __forceinline__ void red_add(double *p, double v)
 struct TileOut {
     double *A, *Bm;            // A, and b - nnz (so that b row r is Bm + nnz + r)
     int32_t nnz;
-    double *const *bptr;       // shared memory: [kTileBases]
+    uint32_t bptr;             // shared-memory address of the tile's [kTileBases] pointers
 };
 
+// destination d: pointer base[d >> 28] plus d's low 28 bits
 __device__ __forceinline__ double *tile_dst(const TileOut &o, uint32_t d)
 {
-    return o.bptr[d >> 28] + (d & 0x0FFFFFFFu);
+    uint64_t p, a;
+    asm volatile("ld.shared.u64 %0, [%1];" : "=l"(p) : "r"(o.bptr + ((d >> 25) & 0x78u)));
+    asm("mad.wide.u32 %0, %1, 8, %2;" : "=l"(a) : "r"(d & 0x0FFFFFFFu), "l"(p));   // one IMAD.WIDE.U32
+    return reinterpret_cast<double *>(a);
+}
+
+// RED under a predicate (no branch around it)
+__device__ __forceinline__ void red_add_if(uint32_t pred, double *p, double v)
+{
+#ifdef EES_DIAG_STORE
+    if (pred) *p = v;
+#else
+    asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %2, 0;\n @q red.global.add.f64 [%0], %1;\n}" ::"l"(p), "d"(v),
+                 "r"(pred)
+                 : "memory");
+#endif
 }
 
 __device__ __forceinline__ double sc_ld(const unsigned char *sc, uint32_t byte)
 {
     return *reinterpret_cast<const double *>(sc + byte);
-}
-
-// The steps of sequence j in an op stream: the rows it falls in (sequences
-// are ordered longest first, so row s holds sequences 0 .. rows[s+1]-rows[s]-1).
-__device__ __forceinline__ int op_steps(const uint16_t *row, int n_step, int j)
-{
-    int c = 0;
-    while (c < n_step && j < (int)row[c + 1] - (int)row[c]) c++;
-    return c;
 }
 
 // A group class (owned targets longer than kOpMax, group size gs =
@@ -1316,7 +1323,7 @@ __device__ __forceinline__ void tile_cls_group(const TileCls c, int r, const uin
             s = (s0 + s1) + (s2 + s3);
         }
         for (int off = gs >> 1; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-        if (act && lj == 0) red_add(tile_dst(o, dst[k]), s);
+        if (act && lj == 0) red_add(tile_dst(o, dst[k]), s);   // (o.bptr: shared address)
     }
 }
 
@@ -1418,22 +1425,26 @@ __device__ __forceinline__ void tile_reduce(const unsigned char *blob, const uns
     const ProgHdr *ph = reinterpret_cast<const ProgHdr *>(prog);
     {
         // owned op stream: pair-ops of this thread's sequence, one RED per target
-        const uint16_t *row = reinterpret_cast<const uint16_t *>(prog + ph->off_orow);
-        const uint32_t *ops = reinterpret_cast<const uint32_t *>(prog + ph->off_ops);
-        const int ns = op_steps(row, ph->n_ostep, r);
-        if (ns > 0) {
+        // (the last pair of a sequence always emits, so the destination read
+        // ahead of an emit is always the sequence's own)
+        if (r < ph->n_oseq) {
+            const uint16_t *row = reinterpret_cast<const uint16_t *>(prog + ph->off_orow);
+            const uint32_t *ops = reinterpret_cast<const uint32_t *>(prog + ph->off_ops) + r;
+            const uint32_t sw = reinterpret_cast<const uint16_t *>(prog + ph->off_ostart)[r];
+            const int ns = (int)(sw >> kSeqStartBits);
             const uint32_t *dst = reinterpret_cast<const uint32_t *>(prog + ph->off_odst) +
-                                  reinterpret_cast<const uint16_t *>(prog + ph->off_ostart)[r];
+                                  (sw & ((1u << kSeqStartBits) - 1));
             double acc = 0.0;
 #pragma unroll 2
             for (int st = 0; st < ns; st++) {
-                const uint32_t w = ops[row[st] + r];
+                const uint32_t w = ops[row[st]];
                 acc += sc_ld(sc, w & 0xFFFFu);
                 acc += sc_ld(sc, (w >> 16) & 0xFFF8u);
-                if (w & 0x10000u) {                       // emit: the target is complete
-                    red_add(tile_dst(out, *dst++), acc);
-                    acc = 0.0;
-                }
+                const uint32_t em = (w >> 16) & 1u;       // the target is complete
+                const uint32_t d = *dst;
+                dst += em;
+                red_add_if(em, tile_dst(out, d), acc);
+                acc = em ? 0.0 : acc;
             }
         }
     }
@@ -1454,16 +1465,17 @@ __device__ __forceinline__ void tile_reduce(const unsigned char *blob, const uns
         // is its part (plain store) or adds to the CTA's running sum of a hot
         // target's piece (one writer per tile)
         const int j = kTileThreads - 1 - r;
-        const uint16_t *row = reinterpret_cast<const uint16_t *>(prog + ph->off_srow);
-        const uint32_t *ops = reinterpret_cast<const uint32_t *>(prog + ph->off_sops);
-        const int ns = op_steps(row, ph->n_sstep, j);
-        if (ns > 0) {
+        if (j < ph->n_sseq) {
             const SideEnt *sents = reinterpret_cast<const SideEnt *>(blob + h->off_side);
+            const uint16_t *row = reinterpret_cast<const uint16_t *>(prog + ph->off_srow);
+            const uint32_t *ops = reinterpret_cast<const uint32_t *>(prog + ph->off_sops) + j;
+            const uint32_t sw = reinterpret_cast<const uint16_t *>(prog + ph->off_sstart)[j];
+            const int ns = (int)(sw >> kSeqStartBits);
             const uint16_t *dst = reinterpret_cast<const uint16_t *>(prog + ph->off_sdst) +
-                                  reinterpret_cast<const uint16_t *>(prog + ph->off_sstart)[j];
+                                  (sw & ((1u << kSeqStartBits) - 1));
             double acc = 0.0;
             for (int st = 0; st < ns; st++) {
-                const uint32_t w = ops[row[st] + j];
+                const uint32_t w = ops[row[st]];
                 acc += sc_ld(sc, w & 0xFFFFu);
                 acc += sc_ld(sc, (w >> 16) & 0xFFF8u);
                 if (w & 0x10000u) {
@@ -1551,7 +1563,7 @@ __device__ __forceinline__ void tile_finish(const TileK &tk, const CallK &P, con
     out.A = P.A;                                                                                 \
     out.Bm = P.b - tk.nnz;                                                                       \
     out.nnz = (int32_t)tk.nnz;                    /* < 2^31 (setup) */                           \
-    out.bptr = s_bptr;                            /* per tile: s_bptr + (it & 1) * kTileBases */ \
+    out.bptr = 0;                                 /* per tile: s_bptr + (it & 1) * kTileBases */ \
     const int32_t t0 = blockIdx.x;                                                               \
     if (tid == 0) {                                                                              \
         for (int k = 0; k < (NSTAGES); k++) mbar_init(&s_bar[k], 1);                             \
@@ -1593,7 +1605,7 @@ __global__ void __launch_bounds__(kTileThreads, tile_ctas(kForm)) k_tile(TileK t
         uint4 rf = make_uint4(0, 0, 0, 0);
         if (tid == 0 && it > 0 && tr < tk.n_tiles) rf = __ldg(tk.tdesc + tr);
         TileOut o = out;
-        o.bptr = s_bptr + (it & 1) * kTileBases;
+        o.bptr = smem_u32(s_bptr + (it & 1) * kTileBases);
         if (tid < kTileBases) {                 // this tile's destination pointers (read after B1)
             const int32_t g = reinterpret_cast<const TileHdr *>(blob)->base[tid];
             s_bptr[(it & 1) * kTileBases + tid] = g < out.nnz ? out.A + g : out.Bm + g;

@@ -471,9 +471,9 @@ bool build_tile_host(int form, int64_t N, int32_t n_nodes, int32_t n, int64_t nn
         // ---- op streams: owned targets of <= kOpMax entries (and the side
         // pieces, a stream of their own) as per-thread sequences of pair-ops
         struct Stream {
-            std::vector<uint16_t> row;           // [n_step + 1] row offsets
+            std::vector<uint16_t> row;           // [n_step] row offsets
             std::vector<uint32_t> ops;           // pair words, step-major rows
-            std::vector<uint16_t> start;         // per sequence with ops: its first emission
+            std::vector<uint16_t> start;         // per sequence with ops: first emission | steps << 11
             std::vector<uint32_t> dst;           // destination per emission
             int32_t n_step = 0;
         };
@@ -503,7 +503,10 @@ bool build_tile_host(int form, int64_t N, int32_t n_nodes, int32_t n, int64_t nn
             for (int j = 0; j < kTileThreads; j++) {
                 const int32_t r = perm[j];
                 if (S.dst.size() > 65535) return false;
-                if (load[r] > 0) S.start.push_back((uint16_t)S.dst.size());   // sequences with ops
+                if (load[r] > 0) {                              // sequences with ops
+                    if (S.dst.size() >= (1u << kSeqStartBits) || load[r] >= (1 << (16 - kSeqStartBits))) return false;
+                    S.start.push_back((uint16_t)(S.dst.size() | ((size_t)load[r] << kSeqStartBits)));
+                }
                 for (int32_t k : seq[r]) {
                     const Tgt &t2 = tg[k];
                     for (int32_t p = 0; p < t2.len; p += 2) {
@@ -515,12 +518,12 @@ bool build_tile_host(int form, int64_t N, int32_t n_nodes, int32_t n, int64_t nn
                     S.dst.push_back(t2.is_side ? (uint32_t)(-1 - t2.dst) : code_of(t2.dst));
                 }
             }
-            S.row.assign(1, 0);
+            S.row.clear();
             S.ops.clear();
             for (int32_t st = 0; st < S.n_step; st++) {
+                S.row.push_back((uint16_t)S.ops.size());
                 for (int j = 0; j < kTileThreads && (int32_t)words[j].size() > st; j++) S.ops.push_back(words[j][st]);
                 if (S.ops.size() > 65535) return false;
-                S.row.push_back((uint16_t)S.ops.size());
             }
             return true;
         };
@@ -589,12 +592,12 @@ bool build_tile_host(int form, int64_t N, int32_t n_nodes, int32_t n, int64_t nn
                      o_meta = place(4 * meta.size()), o_ent = place(2 * ents.size());
         const size_t pbytes = off;
         if (pbytes > 65535) return false;
-        ph.n_ostep = (uint16_t)so.n_step;
+        ph.n_oseq = (uint16_t)so.start.size();
         ph.off_orow = (uint16_t)o_orow;
         ph.off_ops = (uint16_t)o_ops;
         ph.off_ostart = (uint16_t)o_ost;
         ph.off_odst = (uint16_t)o_odst;
-        ph.n_sstep = (uint16_t)ss.n_step;
+        ph.n_sseq = (uint16_t)ss.start.size();
         ph.off_srow = (uint16_t)o_srow;
         ph.off_sops = (uint16_t)o_sops;
         ph.off_sstart = (uint16_t)o_sst;
