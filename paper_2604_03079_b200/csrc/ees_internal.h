@@ -103,30 +103,30 @@ struct GatherK {
 // tile contributes one part.
 //
 // The tile's reduction program (TILE v4).  Short targets (at most kOpMax
-// contributions; every target on the inverter / SRAM / hub structures) are
-// an OP STREAM: each thread runs its own sequence of pair-ops, one u32 each
-// (two u16 byte offsets of contributions in the tile's shared-memory slot
-// buffer; bit 0 of the second = "emit"): the thread adds both entries to its
-// running sum and, on "emit", adds the sum to the next destination of its own
-// destination list with ONE reduction (RED.ADD.F64) and restarts the sum at
-// 0.  A target of L contributions is ceil(L/2) consecutive pair-ops of one
-// thread (odd L: the last pair's second entry is the zero slot).  Every owned
-// target is written by exactly one thread of exactly one CTA, once per call,
-// so A_vals[k] + sum is formed once -- the same IEEE addition as a plain
-// read-modify-write (deterministic; the SM loads no old value).  The builder
-// balances the targets over the threads (longest first, least-loaded thread)
-// and orders the threads' sequences by length (thread 0 the longest), so op
-// step s is stored as one contiguous row of the threads that still have an op
-// there (row offsets orow[]): no padding, conflict-free 4-byte loads.
-// Longer owned targets form GROUP classes (one per lane-group size gs =
-// cls_group(L)): gs lanes per target, lane j summing the target's entries j,
-// j+gs, ... in four fixed partial sums, then a fixed xor-shuffle tree.  A
-// side target's contributions in the tile are cut into pieces of at most
-// kSidePiece entries, each its own part (plain store), or, for the hot side
-// targets (rails), a running sum per CTA and piece index in shared memory, in
-// tile order; the pieces form a second op stream (thread order reversed, so
-// they fall on the warps the owned stream loads least) whose destinations are
-// the head's side entries.
+// contributions; every owned target on the inverter / SRAM / hub structures)
+// are an OP STREAM: each thread runs its own sequence of pair-ops, one u32
+// each (two u16 byte offsets of contributions in the tile's shared-memory
+// slot buffer; bit 2 of the first = kEmitBit, "emit"): the thread adds both
+// entries to its running sum and, on "emit", adds the sum to the next
+// destination of its own destination list with ONE reduction (RED.ADD.F64)
+// and restarts the sum at 0.  A target of L contributions is ceil(L/2)
+// consecutive pair-ops of one thread (odd L: the last pair's second entry is
+// the zero slot).  Every owned target is written by exactly one thread of
+// exactly one CTA, once per call, so A_vals[k] + sum is formed once -- the
+// same IEEE addition as a plain read-modify-write (deterministic; the SM
+// loads no old value).  The builder balances the targets over the threads
+// (longest first, least-loaded thread) and orders the threads' sequences by
+// length (thread 0 the longest), so op step s is stored as one contiguous row
+// of the threads that still have an op there (row offsets orow[]): no
+// padding, conflict-free 4-byte loads.  Longer targets form GROUP classes
+// (one per kind and lane-group size gs = cls_group(L)): gs lanes per target,
+// lane j summing the target's entries j, j+gs, ... in four fixed partial
+// sums, then a fixed xor-shuffle tree.  A side target's contributions in the
+// tile are one target of the tile (a second op stream, thread order reversed
+// so it falls on the warps the owned stream loads least, or a side group
+// class) whose sum is the tile's part (plain store) or, for the hot side
+// targets (rails), adds to the CTA's running sum in shared memory, in tile
+// order.
 // Everything a tile needs except x (and, in form 1, the item data) is its
 // HEAD (per tile) and its PROGRAM (shared by structurally equal tiles), which
 // two TMA bulk copies (cp.async.bulk + one mbarrier) bring into one shared-
@@ -168,21 +168,25 @@ constexpr int kLogTileThreads = kTileThreads == 128 ? 7 : kTileThreads == 64 ? 6
 static_assert(kLogTileThreads > 0, "tile width must be 64, 128 or 256 threads");
 constexpr int kHeavyDeg = 64;        // nodes with more incident FETs are heavy
 constexpr int kMaxCls = 15;          // distinct target lengths per tile
-constexpr int kSidePiece = 4;        // side-target entries per piece (two pair-ops)
+#ifndef EES_SIDE_PIECE
+#define EES_SIDE_PIECE (1 << 30)
+#endif
+constexpr int kSidePiece = EES_SIDE_PIECE;   // side-target entries per piece: whole (one part per tile)
+constexpr uint32_t kEmitBit = 4;     // pair-op word: bit 2 of the first entry = emit after this pair
 #ifndef EES_OP_MAX
 #define EES_OP_MAX 8
 #endif
 constexpr int kOpMax = EES_OP_MAX;   // owned targets of up to kOpMax contributions: op stream
 constexpr uint32_t kNoEmit = 0xFFFFFFFFu;
 #ifndef EES_HOT_PIECES
-#define EES_HOT_PIECES 24
+#define EES_HOT_PIECES 1
 #endif
 constexpr int kHotPieces = EES_HOT_PIECES;   // pieces of one hot target per tile
 // TILE forms (chosen at setup from the FET copy factor, ees_host.cpp):
 // stage bytes (one tile blob), item bytes in the blob, shared-memory slot
 // buffers (2: one barrier per tile), CTAs per SM
 #ifndef EES_STAGE1
-#define EES_STAGE1 8320              // about the largest stage that keeps 5 CTAs per SM (228 KB)
+#define EES_STAGE1 9344              // about the largest stage that keeps 5 CTAs per SM (228 KB)
 #endif
 __host__ __device__ constexpr int stage_max(int form) { return (form ? EES_STAGE1 : 11264) * kTileItems / 128; }
 __host__ __device__ constexpr int item_blob_bytes(int form) { return form ? 16 : 49; }
@@ -226,7 +230,7 @@ struct TileCls {
                                      // groups per CTA (kTileThreads / gs)
     uint16_t lg;                     // log2 of the group size gs
     uint16_t meta;                   // index of the first target's meta[] word
-    uint16_t pad;
+    uint16_t side;                   // 1: side targets (dst = side entry index)
 };
 static_assert(sizeof(TileCls) == 16, "TileCls layout");
 

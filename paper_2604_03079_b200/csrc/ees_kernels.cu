@@ -1287,13 +1287,44 @@ __device__ __forceinline__ double sc_ld(const unsigned char *sc, uint32_t byte)
     return *reinterpret_cast<const double *>(sc + byte);
 }
 
+__device__ __forceinline__ double lds_f64(uint32_t a)
+{
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+    return v;
+}
+
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a)
+{
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+
+__device__ __forceinline__ uint32_t lds_u16(uint32_t a)
+{
+    uint16_t v;
+    asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
+    return v;
+}
+
+// A side target's part for this tile: its part slot (plain store) or the
+// CTA's running sum of a hot target (one writer per tile, tiles in order).
+__device__ __forceinline__ void side_put(const SideEnt *sents, uint32_t e, const TileK &tk, double *s_hot, double v)
+{
+    const SideEnt se = sents[e];
+    if (se.slot >= 0) tk.part[se.slot] = v;
+    else s_hot[-1 - se.slot] += v;
+}
+
 // A group class (owned targets longer than kOpMax, group size gs =
 // cls_group(L)): a group of gs lanes per target, lane j summing the target's
 // entries j, j+gs, ... in four fixed partial sums, then a fixed xor shuffle
 // tree within the group; the group's first lane adds the sum (one RED).  All
 // lanes of a warp run the same number of iterations (shuffles need them).
 __device__ __forceinline__ void tile_cls_group(const TileCls c, int r, const uint32_t *dst, const uint32_t *meta,
-                                               const uint16_t *ent, const unsigned char *sc, const TileOut &o)
+                                               const uint16_t *ent, const unsigned char *sc, const TileOut &o,
+                                               const SideEnt *sents, const TileK &tk, double *s_hot)
 {
     const int n = c.n, lg = c.lg, gs = 1 << lg;
     const int lgn = kLogTileThreads - lg;                 // log2(kTileThreads / gs)
@@ -1323,7 +1354,10 @@ __device__ __forceinline__ void tile_cls_group(const TileCls c, int r, const uin
             s = (s0 + s1) + (s2 + s3);
         }
         for (int off = gs >> 1; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-        if (act && lj == 0) red_add(tile_dst(o, dst[k]), s);   // (o.bptr: shared address)
+        if (act && lj == 0) {
+            if (c.side) side_put(sents, dst[k], tk, s_hot, s);    // (warp-uniform)
+            else red_add(tile_dst(o, dst[k]), s);
+        }
     }
 }
 
@@ -1428,21 +1462,21 @@ __device__ __forceinline__ void tile_reduce(const unsigned char *blob, const uns
         // (the last pair of a sequence always emits, so the destination read
         // ahead of an emit is always the sequence's own)
         if (r < ph->n_oseq) {
-            const uint16_t *row = reinterpret_cast<const uint16_t *>(prog + ph->off_orow);
-            const uint32_t *ops = reinterpret_cast<const uint32_t *>(prog + ph->off_ops) + r;
-            const uint32_t sw = reinterpret_cast<const uint16_t *>(prog + ph->off_ostart)[r];
+            const uint32_t p32 = smem_u32(prog), sc32 = smem_u32(sc);
+            const uint32_t sw = lds_u16(p32 + ph->off_ostart + 2 * r);
             const int ns = (int)(sw >> kSeqStartBits);
-            const uint32_t *dst = reinterpret_cast<const uint32_t *>(prog + ph->off_odst) +
-                                  (sw & ((1u << kSeqStartBits) - 1));
+            uint32_t row = p32 + ph->off_orow;                               // u16 row offsets
+            const uint32_t ops = p32 + ph->off_ops + 4 * r;
+            uint32_t dst = p32 + ph->off_odst + 4 * (sw & ((1u << kSeqStartBits) - 1));
             double acc = 0.0;
 #pragma unroll 2
-            for (int st = 0; st < ns; st++) {
-                const uint32_t w = ops[row[st]];
-                acc += sc_ld(sc, w & 0xFFFFu);
-                acc += sc_ld(sc, (w >> 16) & 0xFFF8u);
-                const uint32_t em = (w >> 16) & 1u;       // the target is complete
-                const uint32_t d = *dst;
-                dst += em;
+            for (int st = 0; st < ns; st++, row += 2) {
+                const uint32_t w = lds_u32(ops + 4 * lds_u16(row));
+                acc += lds_f64(sc32 + (w & 0xFFF8u));
+                acc += lds_f64(sc32 + (w >> 16));
+                const uint32_t em = w & kEmitBit;              // the target is complete
+                const uint32_t d = lds_u32(dst);
+                dst += em;                                     // kEmitBit = 4: one destination
                 red_add_if(em, tile_dst(out, d), acc);
                 acc = em ? 0.0 : acc;
             }
@@ -1455,9 +1489,10 @@ __device__ __forceinline__ void tile_reduce(const unsigned char *blob, const uns
         const uint32_t *dst = reinterpret_cast<const uint32_t *>(prog + ph->off_dst);
         const uint32_t *meta = reinterpret_cast<const uint32_t *>(prog + ph->off_meta);
         const uint16_t *ent = reinterpret_cast<const uint16_t *>(prog + ph->off_ent);
+        const SideEnt *sents = reinterpret_cast<const SideEnt *>(blob + h->off_side);
         for (int ci = 0; ci < ncl; ci++) {
             const TileCls c = cls[ci];
-            tile_cls_group(c, r, dst + c.dst, meta + c.meta, ent, sc, out);
+            tile_cls_group(c, r, dst + c.dst, meta + c.meta, ent, sc, out, sents, tk, s_hot);
         }
     }
     {
@@ -1467,21 +1502,20 @@ __device__ __forceinline__ void tile_reduce(const unsigned char *blob, const uns
         const int j = kTileThreads - 1 - r;
         if (j < ph->n_sseq) {
             const SideEnt *sents = reinterpret_cast<const SideEnt *>(blob + h->off_side);
-            const uint16_t *row = reinterpret_cast<const uint16_t *>(prog + ph->off_srow);
-            const uint32_t *ops = reinterpret_cast<const uint32_t *>(prog + ph->off_sops) + j;
-            const uint32_t sw = reinterpret_cast<const uint16_t *>(prog + ph->off_sstart)[j];
+            const uint32_t p32 = smem_u32(prog), sc32 = smem_u32(sc);
+            const uint32_t sw = lds_u16(p32 + ph->off_sstart + 2 * j);
             const int ns = (int)(sw >> kSeqStartBits);
-            const uint16_t *dst = reinterpret_cast<const uint16_t *>(prog + ph->off_sdst) +
-                                  (sw & ((1u << kSeqStartBits) - 1));
+            uint32_t row = p32 + ph->off_srow;
+            const uint32_t ops = p32 + ph->off_sops + 4 * j;
+            uint32_t dst = p32 + ph->off_sdst + 2 * (sw & ((1u << kSeqStartBits) - 1));
             double acc = 0.0;
-            for (int st = 0; st < ns; st++) {
-                const uint32_t w = ops[row[st]];
-                acc += sc_ld(sc, w & 0xFFFFu);
-                acc += sc_ld(sc, (w >> 16) & 0xFFF8u);
-                if (w & 0x10000u) {
-                    const SideEnt se = sents[*dst++];
-                    if (se.slot >= 0) tk.part[se.slot] = acc;
-                    else s_hot[-1 - se.slot] += acc;
+            for (int st = 0; st < ns; st++, row += 2) {
+                const uint32_t w = lds_u32(ops + 4 * lds_u16(row));
+                acc += lds_f64(sc32 + (w & 0xFFF8u));
+                acc += lds_f64(sc32 + (w >> 16));
+                if (w & kEmitBit) {
+                    side_put(sents, lds_u16(dst), tk, s_hot, acc);
+                    dst += 2;
                     acc = 0.0;
                 }
             }

@@ -32,8 +32,9 @@ constexpr int32_t kSide = -2;
 // 16 B class header.  Items cost item_blob_bytes(form).  Heavy x heavy
 // targets (owned by their home tile, or side) are bounded: owned, as above
 // (<= 12 + 2c B for c contributions, plus meta and class header); side, at
-// most ceil(c / kSidePiece) pieces of 4 B per pair-op, a 2 B destination and
-// an 8 B side entry -> 2c + 12 ceil(c/4) <= 12 + 5c B: kHHTarget = 12 B per
+// one target per tile: c <= kOpMax, ceil(c/2) 4 B pair-ops, a 2 B destination
+// and an 8 B side entry (<= 2c + 12 B); longer, a group-class target (<= 2c +
+// 32 B with its class header, <= 12 + 5c for c > kOpMax): kHHTarget = 12 B per
 // distinct target and kHHContrib = 5 B per contribution cover both.  Fixed:
 // head and program headers, the two streams' per-sequence start words and row
 // offsets (a tile lists at most 16 kTileItems contributions, so a stream has
@@ -510,9 +511,9 @@ bool build_tile_host(int form, int64_t N, int32_t n_nodes, int32_t n, int64_t nn
                 for (int32_t k : seq[r]) {
                     const Tgt &t2 = tg[k];
                     for (int32_t p = 0; p < t2.len; p += 2) {
-                        const uint16_t ea = entry(t2, p);
-                        uint16_t eb = p + 1 < t2.len ? entry(t2, p + 1) : (uint16_t)kZeroSlotByte;
-                        if (p + 2 >= t2.len) eb |= 1;                      // emit after this pair
+                        uint16_t ea = entry(t2, p);
+                        const uint16_t eb = p + 1 < t2.len ? entry(t2, p + 1) : (uint16_t)kZeroSlotByte;
+                        if (p + 2 >= t2.len) ea |= kEmitBit;               // emit after this pair
                         words[j].push_back((uint32_t)ea | ((uint32_t)eb << 16));
                     }
                     S.dst.push_back(t2.is_side ? (uint32_t)(-1 - t2.dst) : code_of(t2.dst));
@@ -527,29 +528,30 @@ bool build_tile_host(int form, int64_t N, int32_t n_nodes, int32_t n, int64_t nn
             }
             return true;
         };
-        std::vector<int32_t> own_short, own_long, side_tl;
+        std::vector<int32_t> own_short, own_long, side_tl;     // own_long: owned, then side
         for (int32_t k = 0; k < (int32_t)tg.size(); k++) {
-            if (tg[k].is_side) side_tl.push_back(k);
-            else if (tg[k].len <= kOpMax) own_short.push_back(k);
-            else own_long.push_back(k);
+            if (tg[k].len > kOpMax) own_long.push_back(k);
+            else if (tg[k].is_side) side_tl.push_back(k);
+            else own_short.push_back(k);
         }
         Stream so, ss;
         if (!build_stream(own_short, so) || !build_stream(side_tl, ss)) return false;
-        // ---- group classes: owned targets longer than kOpMax, one class per
-        // lane-group size (largest first), targets in list order
+        // ---- group classes: targets longer than kOpMax, one class per kind
+        // (owned, then side) and lane-group size (largest first), targets in
+        // list order
         cls.clear();
         dsts.clear();
         ents.clear();
         meta.clear();
         {
-            std::stable_sort(own_long.begin(), own_long.end(), [&](int32_t a, int32_t b) {
-                return cls_group(tg[a].len) > cls_group(tg[b].len);
-            });
+            auto gkey = [&](int32_t k) { return (tg[k].is_side ? 0 : 64) + cls_group(tg[k].len); };
+            std::stable_sort(own_long.begin(), own_long.end(), [&](int32_t a, int32_t b) { return gkey(a) > gkey(b); });
             int64_t cum = 0;
             for (size_t k = 0; k < own_long.size();) {
                 const int gs = cls_group(tg[own_long[k]].len);
+                const int key = gkey(own_long[k]);
                 size_t e = k;
-                while (e < own_long.size() && cls_group(tg[own_long[e]].len) == gs) e++;
+                while (e < own_long.size() && gkey(own_long[e]) == key) e++;
                 if (e - k > 65535 || ents.size() > 65535 || dsts.size() > 65535 || meta.size() > 65535) return false;
                 TileCls tc;
                 std::memset(&tc, 0, sizeof(tc));
@@ -560,12 +562,13 @@ bool build_tile_host(int form, int64_t N, int32_t n_nodes, int32_t n, int64_t nn
                 while ((1 << lg) < gs) lg++;
                 tc.lg = (uint16_t)lg;
                 tc.meta = (uint16_t)meta.size();
+                tc.side = tg[own_long[k]].is_side ? 1 : 0;
                 for (size_t q = k; q < e; q++) {
                     const Tgt &t2 = tg[own_long[q]];
                     if (ents.size() > 65535 || t2.len > 65535) return false;
                     meta.push_back((uint32_t)ents.size() | ((uint32_t)t2.len << 16));
                     for (int32_t p = 0; p < t2.len; p++) ents.push_back(entry(t2, p));
-                    dsts.push_back((int32_t)code_of(t2.dst));
+                    dsts.push_back(t2.is_side ? -1 - t2.dst : (int32_t)code_of(t2.dst));   // side: entry index
                 }
                 const int64_t ng = kTileThreads / gs;
                 tc.rot = (uint16_t)((cum / gs) % ng);
