@@ -122,11 +122,13 @@ struct GatherK {
 // (one per kind and lane-group size gs = cls_group(L)): gs lanes per target,
 // lane j summing the target's entries j, j+gs, ... in four fixed partial
 // sums, then a fixed xor-shuffle tree.  A side target's contributions in the
-// tile are one target of the tile (a second op stream, thread order reversed
-// so it falls on the warps the owned stream loads least, or a side group
-// class) whose sum is the tile's part (plain store) or, for the hot side
-// targets (rails), adds to the CTA's running sum in shared memory, in tile
-// order.
+// tile are cut into pieces of at most kSidePiece entries, each a target of
+// the tile (a second op stream, thread order reversed so it falls on the
+// warps the owned stream loads least; a side group class if longer than
+// kOpMax) whose sum is its part (plain store) or, for the hot side targets
+// (rails), adds to the CTA's running sum of its piece index in shared memory,
+// in tile order.  (Whole side targets in group classes measured slower:
+// profiles/r02_ab.md.)
 // Everything a tile needs except x (and, in form 1, the item data) is its
 // HEAD (per tile) and its PROGRAM (shared by structurally equal tiles), which
 // two TMA bulk copies (cp.async.bulk + one mbarrier) bring into one shared-
@@ -169,9 +171,9 @@ static_assert(kLogTileThreads > 0, "tile width must be 64, 128 or 256 threads");
 constexpr int kHeavyDeg = 64;        // nodes with more incident FETs are heavy
 constexpr int kMaxCls = 15;          // distinct target lengths per tile
 #ifndef EES_SIDE_PIECE
-#define EES_SIDE_PIECE (1 << 30)
+#define EES_SIDE_PIECE 4
 #endif
-constexpr int kSidePiece = EES_SIDE_PIECE;   // side-target entries per piece: whole (one part per tile)
+constexpr int kSidePiece = EES_SIDE_PIECE;   // side-target entries per piece (one part each)
 constexpr uint32_t kEmitBit = 4;     // pair-op word: bit 2 of the first entry = emit after this pair
 #ifndef EES_OP_MAX
 #define EES_OP_MAX 8
@@ -179,14 +181,15 @@ constexpr uint32_t kEmitBit = 4;     // pair-op word: bit 2 of the first entry =
 constexpr int kOpMax = EES_OP_MAX;   // owned targets of up to kOpMax contributions: op stream
 constexpr uint32_t kNoEmit = 0xFFFFFFFFu;
 #ifndef EES_HOT_PIECES
-#define EES_HOT_PIECES 1
+#define EES_HOT_PIECES 24
 #endif
 constexpr int kHotPieces = EES_HOT_PIECES;   // pieces of one hot target per tile
 // TILE forms (chosen at setup from the FET copy factor, ees_host.cpp):
 // stage bytes (one tile blob), item bytes in the blob, shared-memory slot
 // buffers (2: one barrier per tile), CTAs per SM
 #ifndef EES_STAGE1
-#define EES_STAGE1 9344              // about the largest stage that keeps 5 CTAs per SM (228 KB)
+#define EES_STAGE1 8336              // about the largest stage that keeps 5 CTAs per SM (228 KB; the
+                                     // shared-memory allocation granularity is 256 B)
 #endif
 __host__ __device__ constexpr int stage_max(int form) { return (form ? EES_STAGE1 : 11264) * kTileItems / 128; }
 __host__ __device__ constexpr int item_blob_bytes(int form) { return form ? 16 : 49; }

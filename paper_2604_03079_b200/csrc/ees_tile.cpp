@@ -32,9 +32,10 @@ constexpr int32_t kSide = -2;
 // 16 B class header.  Items cost item_blob_bytes(form).  Heavy x heavy
 // targets (owned by their home tile, or side) are bounded: owned, as above
 // (<= 12 + 2c B for c contributions, plus meta and class header); side, at
-// one target per tile: c <= kOpMax, ceil(c/2) 4 B pair-ops, a 2 B destination
-// and an 8 B side entry (<= 2c + 12 B); longer, a group-class target (<= 2c +
-// 32 B with its class header, <= 12 + 5c for c > kOpMax): kHHTarget = 12 B per
+// pieces of <= kSidePiece entries, each ceil(c'/2) 4 B pair-ops, a 2 B
+// destination and an 8 B side entry (<= 2c' + 12 B) if c' <= kOpMax, else a
+// group-class target (<= 2c' + 32 B with its class header): with kSidePiece
+// = 4, <= 2c + 12 ceil(c/4) <= 12 + 5c B in all: kHHTarget = 12 B per
 // distinct target and kHHContrib = 5 B per contribution cover both.  Fixed:
 // head and program headers, the two streams' per-sequence start words and row
 // offsets (a tile lists at most 16 kTileItems contributions, so a stream has
