@@ -39,10 +39,11 @@ constexpr int32_t kSide = -2;
 // distinct target and kHHContrib = 5 B per contribution cover both.  Fixed:
 // head and program headers, the two streams' per-sequence start words and row
 // offsets (a tile lists at most 16 kTileItems contributions, so a stream has
-// at most 16 + 3 steps: balanced, targets of <= 4 pair-ops), fourteen section
+// at most 16 + ceil(kOpMax/2) steps: balanced, longest first), fourteen section
 // paddings.
+constexpr int32_t kMaxSteps = 16 + (kOpMax + 1) / 2;
 constexpr int64_t kBlobFixed = (int64_t)sizeof(TileHdr) + (int64_t)sizeof(ProgHdr) + 14 * 16 +
-                               2 * 2 * kTileThreads + 2 * 2 * 21;
+                               2 * 2 * kTileThreads + 2 * 2 * (kMaxSteps + 1);
 constexpr int64_t kHHTarget = 12, kHHContrib = 5;
 size_t pad16(size_t x) { return (x + 15) & ~(size_t)15; }
 }  // namespace
@@ -498,7 +499,7 @@ bool build_tile_host(int form, int64_t N, int32_t n_nodes, int32_t n, int64_t nn
             std::iota(perm.begin(), perm.end(), 0);
             std::stable_sort(perm.begin(), perm.end(), [&](int32_t a, int32_t b) { return load[a] > load[b]; });
             S.n_step = load[perm[0]];
-            if (S.n_step > 20) return false;                  // the byte bound's row reserve
+            if (S.n_step > kMaxSteps) return false;           // the byte bound's row reserve
             std::vector<std::vector<uint32_t>> words(kTileThreads);
             S.start.clear();
             S.dst.clear();
