@@ -176,7 +176,7 @@ constexpr int kMaxCls = 15;          // distinct target lengths per tile
 constexpr int kSidePiece = EES_SIDE_PIECE;   // side-target entries per piece (one part each)
 constexpr uint32_t kEmitBit = 4;     // pair-op word: bit 2 of the first entry = emit after this pair
 #ifndef EES_OP_MAX
-#define EES_OP_MAX 16
+#define EES_OP_MAX 32
 #endif
 constexpr int kOpMax = EES_OP_MAX;   // owned targets of up to kOpMax contributions: op stream
 constexpr uint32_t kNoEmit = 0xFFFFFFFFu;
