@@ -188,11 +188,13 @@ constexpr int kHotPieces = EES_HOT_PIECES;   // pieces of one hot target per til
 // stage bytes (one tile blob), item bytes in the blob, shared-memory slot
 // buffers (2: one barrier per tile), CTAs per SM
 #ifndef EES_STAGE1
-#define EES_STAGE1 8336              // about the largest stage that keeps 5 CTAs per SM (228 KB; the
+#define EES_STAGE1 9024              // about the largest stage that keeps 5 CTAs per SM (228 KB; the
                                      // shared-memory allocation granularity is 256 B)
 #endif
 __host__ __device__ constexpr int stage_max(int form) { return (form ? EES_STAGE1 : 11264) * kTileItems / 128; }
-__host__ __device__ constexpr int item_blob_bytes(int form) { return form ? 16 : 49; }
+// bytes per item in the head and program: form 0 the whole item; form 1 the
+// terms (head) and the item's 16 contribution positions (program, TILE v5)
+__host__ __device__ constexpr int item_blob_bytes(int form) { return form ? 16 + 32 : 49; }
 #ifndef EES_TILE_BUF1
 #define EES_TILE_BUF1 1
 #endif
@@ -209,7 +211,16 @@ __host__ __device__ constexpr int tile_ctas(int form)
 }
 
 constexpr int kStages = 3;           // TMA pipeline depth (blobs in flight per CTA)
-constexpr int kScSlots = 16 * kTileItems + 2;   // contribution slots per buffer (+16-byte pad)
+constexpr int kScSlots = 16 * kTileItems + 2;   // form 0: contribution slots per buffer (+16-byte pad)
+#ifndef EES_SC_ROWS
+#define EES_SC_ROWS 7
+#endif
+constexpr int kScRows = EES_SC_ROWS;             // form 1: pair rows (of kTileItems pairs) per tile
+static_assert(kScRows <= 8, "row masks are 8 bits");
+// contribution slots (doubles) of the form's slot buffer; form 1: kScRows rows
+// of kTileItems 16-byte pairs, then the trash slot and a pad
+__host__ __device__ constexpr int sc_slots(int form) { return form ? kScRows * 2 * kTileItems + 2 : kScSlots; }
+constexpr int kTrashByte1 = 8 * kScRows * 2 * kTileItems;   // form 1: unlisted contributions land here
 constexpr int kZeroSlotByte = 8 * 16 * kTileItems; // the pad's first slot holds 0.0 (odd-length targets)
 #ifndef EES_MAX_HOT
 #define EES_MAX_HOT 16
@@ -257,6 +268,32 @@ struct ProgHdr {
     uint16_t pad;
 };
 constexpr int kSeqStartBits = 11;        // sequence word: first destination | steps << 11
+
+// TILE v5 (form 1) program: the contribution POSITIONS replace the op words.
+// Each item's 16 contributions are stored by the evaluating thread straight
+// into their place in the pair rows: thread j's pair of row s is the 16 bytes
+// at (s * kTileItems + j) * 16 of the slot buffer (a conflict-free LDS.128 at
+// a compile-time offset), so the reduction reads no program entry per pair.
+// The slot buffer is all zero between tiles (the reduction zeroes every pair
+// it reads; padding halves are never written), so an odd target's second
+// half reads 0.  Per thread one sequence word: first destination (11 bits) |
+// pair rows used << 11 (4 bits) | emit mask << 16 (bit s: the pair of row s
+// completes a target) | side mask << 24 (bit s: that target is a side piece,
+// its destination a side entry).  Owned targets longer than kOpMax1 are group
+// classes whose entries are contiguous in a group area after the rows.
+//   program: ProgHdr5 | pos u16[ni][16] (byte offset of each contribution in
+//            the slot buffer; kTrashByte1 if not listed) | oseq u32[kTileItems]
+//            | odst u32[..] (destination code, or side entry index) |
+//            TileCls[n_cls] | dst u32[..] | meta u32[..] (first slot after
+//            the group base | length << 16)
+struct ProgHdr5 {
+    uint16_t n_rows, off_pos, off_oseq, off_odst;
+    uint16_t n_cls, off_cls, off_dst, off_meta;
+    uint16_t gbase;                      // first slot (double index) of the group area
+    uint16_t pad[7];
+};
+static_assert(sizeof(ProgHdr5) == 32, "ProgHdr5 layout");
+constexpr int kOpMax1 = 8;               // form 1: owned targets of <= 8 contributions in the rows
 static_assert(sizeof(ProgHdr) == 32, "ProgHdr layout");
 
 struct SideEnt {

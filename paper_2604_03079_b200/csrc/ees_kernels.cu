@@ -1204,7 +1204,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase)
 template <int kForm>
 constexpr size_t tile_smem()
 {
-    return sizeof(double) * kScSlots * tile_bufs(kForm) + kStages * (size_t)stage_max(kForm);
+    return sizeof(double) * sc_slots(kForm) * tile_bufs(kForm) + kStages * (size_t)stage_max(kForm);
 }
 
 // What a thread gathers from global memory one tile ahead: its item's node
@@ -1403,6 +1403,19 @@ __device__ __forceinline__ unsigned long long globaltimer()
 
 // Evaluate item `it` of a staged tile and store its 16 contributions at
 // slots p*kTileItems + it of the slot buffer (ees_internal.h).
+__device__ __forceinline__ void sts_f64(uint32_t a, double v)
+{
+    asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
+}
+
+// form 1: item it's 16 contribution positions in the staged program
+__device__ __forceinline__ const uint4 *tile_pos(const unsigned char *blob, int it)
+{
+    const TileHdr *h = reinterpret_cast<const TileHdr *>(blob);
+    const unsigned char *prog = blob + h->head_bytes;
+    return reinterpret_cast<const uint4 *>(prog + reinterpret_cast<const ProgHdr5 *>(prog)->off_pos + 32 * it);
+}
+
 template <bool kRep, int kForm>
 __device__ __forceinline__ void tile_eval_item(const unsigned char *blob, const TileRegs &cur, int it, double *scd,
                                                const CardK *s_cards, const CallK &P)
@@ -1416,6 +1429,18 @@ __device__ __forceinline__ void tile_eval_item(const unsigned char *blob, const 
         const double v0gs = kForm == 1 ? cur.v0a : reinterpret_cast<const double *>(blob + h->off_items + 24 * ni)[it];
         const double v0gd = kForm == 1 ? cur.v0b : reinterpret_cast<const double *>(blob + h->off_items + 32 * ni)[it];
         const double g1 = cd.gcgs, g2 = cd.gcgd;
+        if (kForm == 1) {
+            const uint32_t sc32 = smem_u32(scd);
+            const uint4 *pp = tile_pos(blob, it);
+            const uint4 pa = pp[0], pb = pp[1];
+            const uint32_t w[8] = {pa.x, pa.y, pa.z, pa.w, pb.x, pb.y, pb.z, pb.w};
+            auto at = [&](int q) { return sc32 + (q & 1 ? w[q >> 1] >> 16 : w[q >> 1] & 0xFFFFu); };
+            sts_f64(at(GD), -g2);
+            sts_f64(at(GG), g1 + g2);
+            sts_f64(at(GS), -g1);
+            sts_f64(at(NPAIR + 1), g1 * v0gs + g2 * v0gd);
+            return;
+        }
         scd[GD * kTileItems + it] = -g2;
         scd[GG * kTileItems + it] = g1 + g2;
         scd[GS * kTileItems + it] = -g1;
@@ -1439,10 +1464,113 @@ __device__ __forceinline__ void tile_eval_item(const unsigned char *blob, const 
         st.y[SS] += st.y[BB];
         st.j[2] += st.j[3];
     }
+    if (kForm == 1) {                     // v5: each contribution straight to its pair slot
+        const uint32_t sc32 = smem_u32(scd);
+        const uint4 *pp = tile_pos(blob, it);
+        const uint4 pa = pp[0], pb = pp[1];
+        const uint32_t w[8] = {pa.x, pa.y, pa.z, pa.w, pb.x, pb.y, pb.z, pb.w};
+#pragma unroll
+        for (int p = 0; p < 16; p++) {
+            const uint32_t off = p & 1 ? w[p >> 1] >> 16 : w[p >> 1] & 0xFFFFu;
+            sts_f64(sc32 + off, p < NPAIR ? st.y[p] : st.j[p - NPAIR]);
+        }
+        return;
+    }
 #pragma unroll
     for (int p = 0; p < NPAIR; p++) scd[p * kTileItems + it] = st.y[p];
 #pragma unroll
     for (int a = 0; a < 4; a++) scd[(NPAIR + a) * kTileItems + it] = st.j[a];
+}
+
+// TILE v5 (form 1, ees_internal.h ProgHdr5): thread r's pair of row s is
+// the 16 bytes at (s * kTileItems + r) * 16 of the slot buffer; it reads and
+// zeroes them (the buffer is all zero between tiles), adds both halves to its
+// running sum and, where the row's emit bit is set, adds the sum to its next
+// destination (one RED; a side piece's sum is its part).
+__device__ __forceinline__ void tile_grp5(const TileCls c, int r, const uint32_t *dst, const uint32_t *meta,
+                                          uint32_t g32, const TileOut &o)
+{
+    const int n = c.n, lg = c.lg, gs = 1 << lg;
+    const int lgn = kLogTileThreads - lg;
+    const int gi = r >> lg, lj = r & (gs - 1);
+    const int k0 = (gi - (int)c.rot) & ((1 << lgn) - 1);
+    const int mine = k0 < n ? ((n - 1 - k0) >> lgn) + 1 : 0;
+    const int iters = __reduce_max_sync(0xffffffffu, mine);
+    for (int it = 0; it < iters; it++) {
+        const int k = k0 + (it << lgn);
+        const bool act = k < n;
+        double s = 0.0;
+        if (act) {
+            const uint32_t m = meta[k];
+            const uint32_t e = g32 + 8 * (m & 0xFFFFu);       // the target's first entry
+            const int L = (int)(m >> 16);
+            double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+            int p = lj;
+            auto take = [&](int q) {
+                const double v = lds_f64(e + 8 * q);
+                sts_f64(e + 8 * q, 0.0);
+                return v;
+            };
+            for (; p + 3 * gs < L; p += 4 * gs) {
+                s0 += take(p);
+                s1 += take(p + gs);
+                s2 += take(p + 2 * gs);
+                s3 += take(p + 3 * gs);
+            }
+            for (; p < L; p += gs) s0 += take(p);
+            s = (s0 + s1) + (s2 + s3);
+        }
+        for (int off = gs >> 1; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+        if (act && lj == 0) red_add(tile_dst(o, dst[k]), s);
+    }
+}
+
+__device__ __forceinline__ void tile_reduce5(const unsigned char *blob, const unsigned char *sc, int r,
+                                             const TileOut &out, const TileK &tk, double *s_hot)
+{
+#ifdef EES_DIAG_NOREDUCE
+    return;
+#endif
+    const TileHdr *h = reinterpret_cast<const TileHdr *>(blob);
+    const unsigned char *prog = blob + h->head_bytes;
+    const ProgHdr5 *ph = reinterpret_cast<const ProgHdr5 *>(prog);
+    const uint32_t p32 = smem_u32(prog), sc32 = smem_u32(sc);
+    {
+        const uint32_t w = lds_u32(p32 + ph->off_oseq + 4 * r);
+        const int ns = (int)((w >> kSeqStartBits) & 15u);
+        uint32_t dst = p32 + ph->off_odst + 4 * (w & ((1u << kSeqStartBits) - 1));
+        const uint32_t a = sc32 + 16 * r;
+        const SideEnt *sents = reinterpret_cast<const SideEnt *>(blob + h->off_side);
+        double acc = 0.0;
+#pragma unroll
+        for (int st = 0; st < kScRows; st++) {
+            if (st < ns) {
+                double v0, v1;
+                const uint32_t q = a + st * 16 * kTileItems;
+                asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v0), "=d"(v1) : "r"(q));
+                asm volatile("st.shared.v2.f64 [%0], {%1, %1};" ::"r"(q), "d"(0.0) : "memory");
+                acc += v0;
+                acc += v1;
+                if ((w >> (16 + st)) & 1u) {                     // the target is complete
+                    const uint32_t d = lds_u32(dst);
+                    dst += 4;
+                    if ((w >> (24 + st)) & 1u) side_put(sents, d, tk, s_hot, acc);
+                    else red_add(tile_dst(out, d), acc);
+                    acc = 0.0;
+                }
+            }
+        }
+    }
+    const int ncl = ph->n_cls;
+    if (ncl) {
+        const TileCls *cls = reinterpret_cast<const TileCls *>(prog + ph->off_cls);
+        const uint32_t *dst = reinterpret_cast<const uint32_t *>(prog + ph->off_dst);
+        const uint32_t *meta = reinterpret_cast<const uint32_t *>(prog + ph->off_meta);
+        for (int ci = 0; ci < ncl; ci++) {
+            const TileCls c = cls[ci];
+            tile_grp5(c, r, dst + c.dst, meta + c.meta, sc32 + 8 * ph->gbase, out);
+        }
+    }
 }
 
 // The reduction program of one staged tile, run by kTileThreads threads with
@@ -1615,10 +1743,15 @@ __global__ void __launch_bounds__(kTileThreads, tile_ctas(kForm)) k_tile(TileK t
 {
     constexpr int kBuf = tile_bufs(kForm);
     constexpr int kStage = stage_max(kForm);
-#define s_stage (smem + sizeof(double) * kScSlots * kBuf)
+#define s_stage (smem + sizeof(double) * sc_slots(kForm) * kBuf)
     TILE_PROLOGUE(kTileThreads, kStages);
     unsigned char *s_c = smem;                                           // [kBuf][kScSlots] doubles
-    if (tid < kBuf) reinterpret_cast<double *>(s_c + (size_t)tid * 8 * kScSlots)[16 * kTileItems] = 0.0;  // zero slot
+    if (kForm == 1) {                    // v5: the slot buffer is all zero between tiles
+        for (int k = tid; k < kBuf * sc_slots(kForm); k += kTileThreads) reinterpret_cast<double *>(s_c)[k] = 0.0;
+        __syncthreads();
+    } else if (tid < kBuf) {
+        reinterpret_cast<double *>(s_c + (size_t)tid * 8 * kScSlots)[16 * kTileItems] = 0.0;   // zero slot
+    }
     uint32_t parity = 0;                 // bit k: phase of s_bar[k]
     int it = 0;
     int stage = 0;
@@ -1632,7 +1765,7 @@ __global__ void __launch_bounds__(kTileThreads, tile_ctas(kForm)) k_tile(TileK t
     // one tile; the two register sets alternate (no copies between tiles)
     auto step = [&](int32_t t, const TileRegs &cur, TileRegs &nxt) {
         const unsigned char *blob = s_stage + (size_t)stage * kStage;
-        unsigned char *sc = s_c + (kBuf == 2 ? (size_t)(it & 1) * 8 * kScSlots : 0);
+        unsigned char *sc = s_c + (kBuf == 2 ? (size_t)(it & 1) * 8 * sc_slots(kForm) : 0);
         // the blob this iteration's refill (at B1) will fetch: its offsets are
         // loaded now, so warp 0 does not wait on global memory after B1
         const int32_t tr = t - G + kStages * G;
@@ -1658,7 +1791,8 @@ __global__ void __launch_bounds__(kTileThreads, tile_ctas(kForm)) k_tile(TileK t
         __syncthreads();                                        // B1
         if (tid == 0 && it > 0 && tr < tk.n_tiles)              // refill the stage of tile t-G
             issue_at(rf, stage == 0 ? kStages - 1 : stage - 1);
-        tile_reduce(blob, sc, tid, o, tk, s_hot);
+        if (kForm == 1) tile_reduce5(blob, sc, tid, o, tk, s_hot);
+        else tile_reduce(blob, sc, tid, o, tk, s_hot);
         TILE_TRACE(3 + 2 * it);
         if (kBuf == 1) __syncthreads();                         // B0: slots free for the next tile
         stage = sn;

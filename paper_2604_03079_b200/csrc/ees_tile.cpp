@@ -42,9 +42,9 @@ constexpr int32_t kSide = -2;
 // at most 16 + ceil(kOpMax/2) steps: balanced, longest first), fourteen section
 // paddings.
 constexpr int32_t kMaxSteps = 16 + (kOpMax + 1) / 2;
-constexpr int64_t kBlobFixed = (int64_t)sizeof(TileHdr) + (int64_t)sizeof(ProgHdr) + 14 * 16 +
+constexpr int64_t kBlobFixed0 = (int64_t)sizeof(TileHdr) + (int64_t)sizeof(ProgHdr) + 14 * 16 +
                                2 * 2 * kTileThreads + 2 * 2 * (kMaxSteps + 1);
-constexpr int64_t kHHTarget = 12, kHHContrib = 5;
+constexpr int64_t kHHTarget = 12, kHHContrib0 = 5;
 size_t pad16(size_t x) { return (x + 15) & ~(size_t)15; }
 }  // namespace
 
@@ -56,6 +56,15 @@ bool build_tile_host(int form, int64_t N, int32_t n_nodes, int32_t n, int64_t nn
                      TileHost &out)
 {
     const int64_t kStageMax = stage_max(form), kItemBlobBytes = item_blob_bytes(form);
+    // form 1 (v5): a side piece of <= 4 entries costs a 4 B destination and an
+    // 8 B side entry (<= 3c + 12 B for c contributions); an owned heavy x heavy
+    // target a 4 B destination (+ meta and class header if long, hh_len_bytes)
+    const int64_t kHHContrib = form == 1 ? 3 : kHHContrib0;
+    // form 1 (v5): head and program headers, the per-thread sequence words,
+    // seven section paddings
+    const int64_t kBlobFixed = form == 1 ? (int64_t)sizeof(TileHdr) + (int64_t)sizeof(ProgHdr5) + 4 * kTileThreads +
+                                               10 * 16
+                                         : kBlobFixed0;
     // a device's 12 slots and 4 terminals in one 64-byte record: the builder
     // visits devices in row order (random in netlist order on scattered
     // topologies), so one cache line per visit instead of sixteen
@@ -91,6 +100,7 @@ bool build_tile_host(int form, int64_t N, int32_t n_nodes, int32_t n, int64_t nn
     // plus the class header of their length if it would be new, as owned)
     std::vector<int32_t> hh_seen((size_t)(nnz + n), -1);
     std::function<int64_t(int32_t, int32_t)> hh_len_bytes;      // set below (needs tcnt)
+    int64_t hh_nd = 0;                                           // distinct new targets (hh_new)
     auto hh_new = [&](int64_t i, int32_t tile) {
         int64_t k = 0;
         for (int p = 0; p < NPAIR; p++) {
@@ -98,6 +108,7 @@ bool build_tile_host(int form, int64_t N, int32_t n_nodes, int32_t n, int64_t nn
             if (s2 >= 0 && heavy[rec[i].t[pair_row(p)]] && heavy[rec[i].t[pair_col(p)]] && hh_seen[s2] != tile) {
                 hh_seen[s2] = tile;
                 k += kHHTarget + hh_len_bytes(s2, tile);
+                hh_nd++;
             }
         }
         for (int a = 0; a < 4; a++) {
@@ -105,6 +116,7 @@ bool build_tile_host(int form, int64_t N, int32_t n_nodes, int32_t n, int64_t nn
             if (r >= 0 && heavy[r] && hh_seen[nnz + r] != tile) {
                 hh_seen[nnz + r] = tile;
                 k += kHHTarget + hh_len_bytes((int32_t)(nnz + r), tile);
+                hh_nd++;
             }
         }
         return k;
@@ -120,7 +132,8 @@ bool build_tile_host(int form, int64_t N, int32_t n_nodes, int32_t n, int64_t nn
     std::vector<int32_t> len_tile(64, -1);
     auto tgt_bytes = [&](int32_t L, int32_t tile) -> int64_t {
         if (L <= 0) return 0;
-        if (L <= kOpMax) return 4 + 4 * (int64_t)((L + 1) / 2);     // destination, pair-ops
+        if (form == 1 && L <= kOpMax1) return 4;                     // v5: destination (positions per item)
+        if (form == 0 && L <= kOpMax) return 4 + 4 * (int64_t)((L + 1) / 2);     // destination, pair-ops
         int64_t e = 4 + 2 * (int64_t)L + 4;                         // destination, entries, meta
         const int32_t key = cls_group(L);
         if (len_tile[key] != tile) {
@@ -131,7 +144,7 @@ bool build_tile_host(int form, int64_t N, int32_t n_nodes, int32_t n, int64_t nn
     };
     hh_len_bytes = [&](int32_t g, int32_t tile) -> int64_t {
         const int32_t L = tcnt[g];
-        if (L <= kOpMax) return 0;
+        if (L <= (form == 1 ? kOpMax1 : kOpMax)) return 0;
         const int32_t key = cls_group(L);
         if (len_tile[key] == tile) return 4;                     // group meta word (owned case)
         len_tile[key] = tile;
@@ -152,6 +165,40 @@ bool build_tile_host(int form, int64_t N, int32_t n_nodes, int32_t n, int64_t nn
         return k;
     };
 
+    // form 1 (TILE v5): the tile's pair rows.  Owned targets of L <= kOpMax1
+    // contributions take ceil(L/2) pairs of one thread (a chain), longer ones
+    // L slots of the group area.  A heavy x heavy target with c contributions
+    // in the tile takes at most c/2 + 1 pairs (side pieces of <= 4 entries;
+    // owned, a chain) or c group slots (< c/2 + 1 pairs' 2 slots each): counted
+    // as half a pair per contribution and one pair per distinct target.
+    // Longest-first balancing gives at most floor(P / kTileItems) + (longest
+    // chain) rows, which with the group area must fit the kScRows rows of the
+    // slot buffer.  (P is kept in half pairs.)
+    int64_t tP = 0, tG = 0;
+    int32_t tPM = 0;
+    auto tgt_pairs = [&](int32_t L, int64_t &P, int32_t &PM, int64_t &G) {
+        if (L <= 0) return;
+        if (L <= kOpMax1) {
+            P += 2 * ((L + 1) / 2);
+            PM = std::max(PM, (L + 1) / 2);
+        } else {
+            G += L;
+        }
+    };
+    auto hh_pm = [&](int64_t i) {                // longest chain a heavy x heavy target of FET i can need
+        int32_t m = 0;
+        auto one = [&](int64_t g) { m = std::max(m, tcnt[g] <= kOpMax1 ? (tcnt[g] + 1) / 2 : 2); };
+        for (int p = 0; p < NPAIR; p++)
+            if (rec[i].s[p] >= 0 && heavy[rec[i].t[pair_row(p)]] && heavy[rec[i].t[pair_col(p)]]) one(rec[i].s[p]);
+        for (int a = 0; a < 4; a++)
+            if (rec[i].t[a] >= 0 && heavy[rec[i].t[a]]) one(nnz + rec[i].t[a]);
+        return m;
+    };
+    auto rows_over = [&](int64_t P, int32_t PM, int64_t G) {
+        if (form != 1) return false;
+        const int64_t rows = (P + 1) / 2 / kTileItems + PM;
+        return rows > kScRows || rows * 2 * kTileItems + G > (int64_t)kScRows * 2 * kTileItems;
+    };
     auto close_tile = [&]() {
         std::sort(cur.begin(), cur.end());
         item_dev.insert(item_dev.end(), cur.begin(), cur.end());
@@ -159,6 +206,8 @@ bool build_tile_host(int form, int64_t N, int32_t n_nodes, int32_t n, int64_t nn
         tile_rows_ptr.push_back((int32_t)tile_rows.size());
         cur.clear();
         bytes = kBlobFixed;
+        tP = tG = 0;
+        tPM = 0;
         t++;
     };
     for (bool done = false; !done;) {
@@ -200,6 +249,8 @@ bool build_tile_host(int form, int64_t N, int32_t n_nodes, int32_t n, int64_t nn
     item_dev.clear();
     t = 0;
     bytes = kBlobFixed;
+    tP = tG = 0;
+    tPM = 0;
     last_row = -2;
     std::fill(hh_seen.begin(), hh_seen.end(), -1);
     std::fill(len_tile.begin(), len_tile.end(), -1);
@@ -211,16 +262,31 @@ bool build_tile_host(int form, int64_t N, int32_t n_nodes, int32_t n, int64_t nn
         for (int pass = 0; pass < 2; pass++) {
             int32_t fresh = 0;
             int64_t add_bytes = row_bytes(v, t);
-            for (int32_t k = hs_ptr[v]; k < hs_ptr[v + 1]; k++) add_bytes += tgt_bytes(tcnt[hs_k[k]], t);
+            int64_t aP = tP, aG = tG;
+            int32_t aPM = tPM;
+            tgt_pairs(tcnt[nnz + v], aP, aPM, aG);
+            for (int32_t k = row_ptr[v]; k < row_ptr[v + 1]; k++) tgt_pairs(tcnt[k], aP, aPM, aG);
+            for (int32_t k = hs_ptr[v]; k < hs_ptr[v + 1]; k++) {
+                add_bytes += tgt_bytes(tcnt[hs_k[k]], t);
+                tgt_pairs(tcnt[hs_k[k]], aP, aPM, aG);
+            }
             for (int64_t k = iptr[v]; k < iptr[v + 1]; k++) {
                 const int32_t i = idev[k];
                 if (mark[i] != t) {
                     fresh++;
                     add_bytes += kItemBlobBytes;
                 }
-                if (home[i] < 0) add_bytes += hh_new(i, t) + kHHContrib * hh_count(i);
+                if (home[i] < 0) {
+                    hh_nd = 0;
+                    add_bytes += hh_new(i, t) + kHHContrib * hh_count(i);
+                    if (form == 1) {
+                        aP += hh_count(i) + 2 * hh_nd;
+                        aPM = std::max(aPM, hh_pm(i));
+                    }
+                }
             }
-            const bool over = (int64_t)cur.size() + fresh > kTileItems || bytes + add_bytes > kStageMax;
+            const bool over = (int64_t)cur.size() + fresh > kTileItems || bytes + add_bytes > kStageMax ||
+                              rows_over(aP, aPM, aG);
             if (over && pass == 0 && !cur.empty()) {
                 close_tile();
                 continue;
@@ -230,6 +296,9 @@ bool build_tile_host(int form, int64_t N, int32_t n_nodes, int32_t n, int64_t nn
                 done = false;
             }
             bytes += add_bytes;
+            tP = aP;
+            tG = aG;
+            tPM = aPM;
             break;
         }
         if (!done) break;
@@ -251,10 +320,15 @@ bool build_tile_host(int form, int64_t N, int32_t n_nodes, int32_t n, int64_t nn
     for (int64_t i = 0; i < N; i++)
         if (home[i] < 0) {
             const int64_t add_bytes = kItemBlobBytes + (kHHTarget + (int64_t)sizeof(TileCls) + kHHContrib) * hh_count(i);
-            if (!cur.empty() && ((int64_t)cur.size() + 1 > kTileItems || bytes + add_bytes > kStageMax))
+            const int64_t aP = tP + (form == 1 ? 3 * hh_count(i) : 0);      // (each distinct at most once)
+            const int32_t aPM = std::max(tPM, form == 1 ? hh_pm(i) : 0);
+            if (!cur.empty() && ((int64_t)cur.size() + 1 > kTileItems || bytes + add_bytes > kStageMax ||
+                                 rows_over(aP, aPM, tG)))
                 close_tile();
             home[i] = t;
             bytes += add_bytes;
+            tP += form == 1 ? 3 * hh_count(i) : 0;
+            tPM = std::max(tPM, form == 1 ? hh_pm(i) : 0);
             cur.push_back((int32_t)i);
         }
     if (!cur.empty()) close_tile();
@@ -471,172 +545,297 @@ bool build_tile_host(int form, int64_t N, int32_t n_nodes, int32_t n, int64_t nn
             const int q = (int)(c >> 28);
             if ((int64_t)bases[q] + (c & 0x0FFFFFFF) != (int64_t)g) return false;
         }
-        // ---- op streams: owned targets of <= kOpMax entries (and the side
-        // pieces, a stream of their own) as per-thread sequences of pair-ops
-        struct Stream {
-            std::vector<uint16_t> row;           // [n_step] row offsets
-            std::vector<uint32_t> ops;           // pair words, step-major rows
-            std::vector<uint16_t> start;         // per sequence with ops: first emission | steps << 11
-            std::vector<uint32_t> dst;           // destination per emission
-            int32_t n_step = 0;
-        };
-        auto build_stream = [&](const std::vector<int32_t> &tl, Stream &S) -> bool {
-            // longest first onto the least-loaded sequence (ties: lower index)
-            std::vector<int32_t> order(tl);
-            std::stable_sort(order.begin(), order.end(),
-                             [&](int32_t a, int32_t b) { return tg[a].len > tg[b].len; });
+        if (form == 1) {
+            // ---- TILE v5 program (ees_internal.h ProgHdr5): pair rows, positions
+            std::vector<int32_t> opt, lng;            // row targets; long owned targets (group area)
+            for (int32_t k = 0; k < (int32_t)tg.size(); k++) {
+                if (!tg[k].is_side && tg[k].len > kOpMax1) lng.push_back(k);
+                else opt.push_back(k);
+            }
+            std::stable_sort(opt.begin(), opt.end(), [&](int32_t a, int32_t b) { return tg[a].len > tg[b].len; });
             std::vector<std::vector<int32_t>> seq(kTileThreads);
             std::vector<int32_t> load(kTileThreads, 0);
-            for (int32_t k : order) {
+            for (int32_t k : opt) {                    // longest first onto the least-loaded thread
                 int best = 0;
                 for (int r = 1; r < kTileThreads; r++)
                     if (load[r] < load[best]) best = r;
                 seq[best].push_back(k);
                 load[best] += (tg[k].len + 1) / 2;
             }
-            // sequences by length, longest first: step s is a contiguous row
-            std::vector<int32_t> perm(kTileThreads);
-            std::iota(perm.begin(), perm.end(), 0);
-            std::stable_sort(perm.begin(), perm.end(), [&](int32_t a, int32_t b) { return load[a] > load[b]; });
-            S.n_step = load[perm[0]];
-            if (S.n_step > kMaxSteps) return false;           // the byte bound's row reserve
-            std::vector<std::vector<uint32_t>> words(kTileThreads);
-            S.start.clear();
-            S.dst.clear();
+            const int32_t n_rows = *std::max_element(load.begin(), load.end());
+            int64_t G = 0;
+            for (int32_t k : lng) G += tg[k].len;
+            if (n_rows > kScRows || (int64_t)n_rows * 2 * kTileThreads + G > (int64_t)kScRows * 2 * kTileThreads)
+                return false;
+            const int32_t gbase = n_rows * 2 * kTileThreads;           // first group slot
+            std::vector<uint16_t> pos((size_t)ni * 16, (uint16_t)kTrashByte1);
+            auto place = [&](const Tgt &t2, int32_t p, int32_t slot_index) {
+                const uint16_t cs = t2.is_side ? side[t2.beg + p].second : con[t2.beg + p].second;
+                const int32_t pc = cs / kTileItems, loc = cs % kTileItems;   // contribution (p, item)
+                pos[(size_t)loc * 16 + pc] = (uint16_t)(8 * slot_index);
+            };
+            std::vector<uint32_t> oseq(kTileThreads, 0), odst;
             for (int j = 0; j < kTileThreads; j++) {
-                const int32_t r = perm[j];
-                if (S.dst.size() > 65535) return false;
-                if (load[r] > 0) {                              // sequences with ops
-                    if (S.dst.size() >= (1u << kSeqStartBits) || load[r] >= (1 << (16 - kSeqStartBits))) return false;
-                    S.start.push_back((uint16_t)(S.dst.size() | ((size_t)load[r] << kSeqStartBits)));
-                }
-                for (int32_t k : seq[r]) {
+                const uint32_t start = (uint32_t)odst.size();
+                if (start >= (1u << kSeqStartBits)) return false;
+                uint32_t em = 0, sm = 0;
+                int32_t st = 0;
+                for (int32_t k : seq[j]) {
                     const Tgt &t2 = tg[k];
-                    for (int32_t p = 0; p < t2.len; p += 2) {
-                        uint16_t ea = entry(t2, p);
-                        const uint16_t eb = p + 1 < t2.len ? entry(t2, p + 1) : (uint16_t)kZeroSlotByte;
-                        if (p + 2 >= t2.len) ea |= kEmitBit;               // emit after this pair
-                        words[j].push_back((uint32_t)ea | ((uint32_t)eb << 16));
+                    for (int32_t p = 0; p < t2.len; p += 2, st++) {
+                        const int32_t slot = 2 * (st * kTileThreads + j);
+                        place(t2, p, slot);
+                        if (p + 1 < t2.len) place(t2, p + 1, slot + 1);
+                        if (p + 2 >= t2.len) {
+                            em |= 1u << st;
+                            if (t2.is_side) sm |= 1u << st;
+                        }
                     }
-                    S.dst.push_back(t2.is_side ? (uint32_t)(-1 - t2.dst) : code_of(t2.dst));
+                    odst.push_back(t2.is_side ? (uint32_t)(-1 - t2.dst) : code_of(t2.dst));
+                }
+                oseq[j] = start | ((uint32_t)st << kSeqStartBits) | (em << 16) | (sm << 24);
+            }
+            // group classes (owned targets longer than kOpMax1), entries contiguous
+            cls.clear();
+            dsts.clear();
+            meta.clear();
+            {
+                std::stable_sort(lng.begin(), lng.end(), [&](int32_t a, int32_t b) {
+                    return cls_group(tg[a].len) > cls_group(tg[b].len);
+                });
+                int64_t cum = 0, off = 0;
+                for (size_t k = 0; k < lng.size();) {
+                    const int gs = cls_group(tg[lng[k]].len);
+                    size_t e = k;
+                    while (e < lng.size() && cls_group(tg[lng[e]].len) == gs) e++;
+                    TileCls tc;
+                    std::memset(&tc, 0, sizeof(tc));
+                    tc.n = (uint16_t)(e - k);
+                    tc.dst = (uint16_t)dsts.size();
+                    int lg = 0;
+                    while ((1 << lg) < gs) lg++;
+                    tc.lg = (uint16_t)lg;
+                    tc.meta = (uint16_t)meta.size();
+                    for (size_t q = k; q < e; q++) {
+                        const Tgt &t2 = tg[lng[q]];
+                        meta.push_back((uint32_t)off | ((uint32_t)t2.len << 16));
+                        for (int32_t p = 0; p < t2.len; p++) place(t2, p, gbase + (int32_t)off + p);
+                        off += t2.len;
+                        dsts.push_back((int32_t)code_of(t2.dst));
+                    }
+                    tc.rot = (uint16_t)((cum / gs) % (kTileThreads / gs));
+                    cls.push_back(tc);
+                    cum += (int64_t)tc.n * gs;
+                    k = e;
                 }
             }
-            S.row.clear();
-            S.ops.clear();
-            for (int32_t st = 0; st < S.n_step; st++) {
-                S.row.push_back((uint16_t)S.ops.size());
-                for (int j = 0; j < kTileThreads && (int32_t)words[j].size() > st; j++) S.ops.push_back(words[j][st]);
-                if (S.ops.size() > 65535) return false;
-            }
-            return true;
-        };
-        std::vector<int32_t> own_short, own_long, side_tl;     // own_long: owned, then side
-        for (int32_t k = 0; k < (int32_t)tg.size(); k++) {
-            if (tg[k].len > kOpMax) own_long.push_back(k);
-            else if (tg[k].is_side) side_tl.push_back(k);
-            else own_short.push_back(k);
-        }
-        Stream so, ss;
-        if (!build_stream(own_short, so) || !build_stream(side_tl, ss)) return false;
-        // ---- group classes: targets longer than kOpMax, one class per kind
-        // (owned, then side) and lane-group size (largest first), targets in
-        // list order
-        cls.clear();
-        dsts.clear();
-        ents.clear();
-        meta.clear();
-        {
-            auto gkey = [&](int32_t k) { return (tg[k].is_side ? 0 : 64) + cls_group(tg[k].len); };
-            std::stable_sort(own_long.begin(), own_long.end(), [&](int32_t a, int32_t b) { return gkey(a) > gkey(b); });
-            int64_t cum = 0;
-            for (size_t k = 0; k < own_long.size();) {
-                const int gs = cls_group(tg[own_long[k]].len);
-                const int key = gkey(own_long[k]);
-                size_t e = k;
-                while (e < own_long.size() && gkey(own_long[e]) == key) e++;
-                if (e - k > 65535 || ents.size() > 65535 || dsts.size() > 65535 || meta.size() > 65535) return false;
-                TileCls tc;
-                std::memset(&tc, 0, sizeof(tc));
-                tc.n = (uint16_t)(e - k);
-                tc.ent = (uint16_t)ents.size();
-                tc.dst = (uint16_t)dsts.size();
-                int lg = 0;
-                while ((1 << lg) < gs) lg++;
-                tc.lg = (uint16_t)lg;
-                tc.meta = (uint16_t)meta.size();
-                tc.side = tg[own_long[k]].is_side ? 1 : 0;
-                for (size_t q = k; q < e; q++) {
-                    const Tgt &t2 = tg[own_long[q]];
-                    if (ents.size() > 65535 || t2.len > 65535) return false;
-                    meta.push_back((uint32_t)ents.size() | ((uint32_t)t2.len << 16));
-                    for (int32_t p = 0; p < t2.len; p++) ents.push_back(entry(t2, p));
-                    dsts.push_back(t2.is_side ? -1 - t2.dst : (int32_t)code_of(t2.dst));   // side: entry index
+            ProgHdr5 ph;
+            std::memset(&ph, 0, sizeof(ph));
+            size_t off = sizeof(ProgHdr5);
+            auto place_sec = [&](size_t bytes) {
+                const size_t at = off;
+                off = pad16(off + bytes);
+                return at;
+            };
+            const size_t o_pos = place_sec(2 * pos.size()), o_oseq = place_sec(4 * oseq.size()),
+                         o_odst = place_sec(4 * odst.size()), o_cls = place_sec(sizeof(TileCls) * cls.size()),
+                         o_dst = place_sec(4 * dsts.size()), o_meta = place_sec(4 * meta.size());
+            const size_t pbytes = off;
+            if (pbytes > 65535 || gbase > 65535) return false;
+            ph.n_rows = (uint16_t)n_rows;
+            ph.off_pos = (uint16_t)o_pos;
+            ph.off_oseq = (uint16_t)o_oseq;
+            ph.off_odst = (uint16_t)o_odst;
+            ph.n_cls = (uint16_t)cls.size();
+            ph.off_cls = (uint16_t)o_cls;
+            ph.off_dst = (uint16_t)o_dst;
+            ph.off_meta = (uint16_t)o_meta;
+            ph.gbase = (uint16_t)gbase;
+            o.prog.assign(pbytes, 0);
+            uint8_t *pp = o.prog.data();
+            std::memcpy(pp, &ph, sizeof(ph));
+            auto put = [&](size_t at, const void *src, size_t bytes) {
+                if (bytes) std::memcpy(pp + at, src, bytes);
+            };
+            put(o_pos, pos.data(), 2 * pos.size());
+            put(o_oseq, oseq.data(), 4 * oseq.size());
+            put(o_odst, odst.data(), 4 * odst.size());
+            put(o_cls, cls.data(), sizeof(TileCls) * cls.size());
+            put(o_dst, dsts.data(), 4 * dsts.size());
+            put(o_meta, meta.data(), 4 * meta.size());
+            uint64_t hsh = 1469598103934665603ull;            // FNV-1a
+            for (size_t q = 0; q < pbytes; q++) hsh = (hsh ^ pp[q]) * 1099511628211ull;
+            o.hash = hsh;
+            o.padded = 2 * (int64_t)n_rows * kTileThreads;
+        } else {
+            // ---- op streams: owned targets of <= kOpMax entries (and the side
+            // pieces, a stream of their own) as per-thread sequences of pair-ops
+            struct Stream {
+                std::vector<uint16_t> row;           // [n_step] row offsets
+                std::vector<uint32_t> ops;           // pair words, step-major rows
+                std::vector<uint16_t> start;         // per sequence with ops: first emission | steps << 11
+                std::vector<uint32_t> dst;           // destination per emission
+                int32_t n_step = 0;
+            };
+            auto build_stream = [&](const std::vector<int32_t> &tl, Stream &S) -> bool {
+                // longest first onto the least-loaded sequence (ties: lower index)
+                std::vector<int32_t> order(tl);
+                std::stable_sort(order.begin(), order.end(),
+                                 [&](int32_t a, int32_t b) { return tg[a].len > tg[b].len; });
+                std::vector<std::vector<int32_t>> seq(kTileThreads);
+                std::vector<int32_t> load(kTileThreads, 0);
+                for (int32_t k : order) {
+                    int best = 0;
+                    for (int r = 1; r < kTileThreads; r++)
+                        if (load[r] < load[best]) best = r;
+                    seq[best].push_back(k);
+                    load[best] += (tg[k].len + 1) / 2;
                 }
-                const int64_t ng = kTileThreads / gs;
-                tc.rot = (uint16_t)((cum / gs) % ng);
-                cls.push_back(tc);
-                cum += (int64_t)tc.n * gs;
-                k = e;
+                // sequences by length, longest first: step s is a contiguous row
+                std::vector<int32_t> perm(kTileThreads);
+                std::iota(perm.begin(), perm.end(), 0);
+                std::stable_sort(perm.begin(), perm.end(), [&](int32_t a, int32_t b) { return load[a] > load[b]; });
+                S.n_step = load[perm[0]];
+                if (S.n_step > kMaxSteps) return false;           // the byte bound's row reserve
+                std::vector<std::vector<uint32_t>> words(kTileThreads);
+                S.start.clear();
+                S.dst.clear();
+                for (int j = 0; j < kTileThreads; j++) {
+                    const int32_t r = perm[j];
+                    if (S.dst.size() > 65535) return false;
+                    if (load[r] > 0) {                              // sequences with ops
+                        if (S.dst.size() >= (1u << kSeqStartBits) || load[r] >= (1 << (16 - kSeqStartBits))) return false;
+                        S.start.push_back((uint16_t)(S.dst.size() | ((size_t)load[r] << kSeqStartBits)));
+                    }
+                    for (int32_t k : seq[r]) {
+                        const Tgt &t2 = tg[k];
+                        for (int32_t p = 0; p < t2.len; p += 2) {
+                            uint16_t ea = entry(t2, p);
+                            const uint16_t eb = p + 1 < t2.len ? entry(t2, p + 1) : (uint16_t)kZeroSlotByte;
+                            if (p + 2 >= t2.len) ea |= kEmitBit;               // emit after this pair
+                            words[j].push_back((uint32_t)ea | ((uint32_t)eb << 16));
+                        }
+                        S.dst.push_back(t2.is_side ? (uint32_t)(-1 - t2.dst) : code_of(t2.dst));
+                    }
+                }
+                S.row.clear();
+                S.ops.clear();
+                for (int32_t st = 0; st < S.n_step; st++) {
+                    S.row.push_back((uint16_t)S.ops.size());
+                    for (int j = 0; j < kTileThreads && (int32_t)words[j].size() > st; j++) S.ops.push_back(words[j][st]);
+                    if (S.ops.size() > 65535) return false;
+                }
+                return true;
+            };
+            std::vector<int32_t> own_short, own_long, side_tl;     // own_long: owned, then side
+            for (int32_t k = 0; k < (int32_t)tg.size(); k++) {
+                if (tg[k].len > kOpMax) own_long.push_back(k);
+                else if (tg[k].is_side) side_tl.push_back(k);
+                else own_short.push_back(k);
             }
-            if (ents.size() > 65536) return false;
+            Stream so, ss;
+            if (!build_stream(own_short, so) || !build_stream(side_tl, ss)) return false;
+            // ---- group classes: targets longer than kOpMax, one class per kind
+            // (owned, then side) and lane-group size (largest first), targets in
+            // list order
+            cls.clear();
+            dsts.clear();
+            ents.clear();
+            meta.clear();
+            {
+                auto gkey = [&](int32_t k) { return (tg[k].is_side ? 0 : 64) + cls_group(tg[k].len); };
+                std::stable_sort(own_long.begin(), own_long.end(), [&](int32_t a, int32_t b) { return gkey(a) > gkey(b); });
+                int64_t cum = 0;
+                for (size_t k = 0; k < own_long.size();) {
+                    const int gs = cls_group(tg[own_long[k]].len);
+                    const int key = gkey(own_long[k]);
+                    size_t e = k;
+                    while (e < own_long.size() && gkey(own_long[e]) == key) e++;
+                    if (e - k > 65535 || ents.size() > 65535 || dsts.size() > 65535 || meta.size() > 65535) return false;
+                    TileCls tc;
+                    std::memset(&tc, 0, sizeof(tc));
+                    tc.n = (uint16_t)(e - k);
+                    tc.ent = (uint16_t)ents.size();
+                    tc.dst = (uint16_t)dsts.size();
+                    int lg = 0;
+                    while ((1 << lg) < gs) lg++;
+                    tc.lg = (uint16_t)lg;
+                    tc.meta = (uint16_t)meta.size();
+                    tc.side = tg[own_long[k]].is_side ? 1 : 0;
+                    for (size_t q = k; q < e; q++) {
+                        const Tgt &t2 = tg[own_long[q]];
+                        if (ents.size() > 65535 || t2.len > 65535) return false;
+                        meta.push_back((uint32_t)ents.size() | ((uint32_t)t2.len << 16));
+                        for (int32_t p = 0; p < t2.len; p++) ents.push_back(entry(t2, p));
+                        dsts.push_back(t2.is_side ? -1 - t2.dst : (int32_t)code_of(t2.dst));   // side: entry index
+                    }
+                    const int64_t ng = kTileThreads / gs;
+                    tc.rot = (uint16_t)((cum / gs) % ng);
+                    cls.push_back(tc);
+                    cum += (int64_t)tc.n * gs;
+                    k = e;
+                }
+                if (ents.size() > 65536) return false;
+            }
+            // emit the head (per tile) and the program (shared by equal tiles)
+            ProgHdr ph;
+            std::memset(&ph, 0, sizeof(ph));
+            size_t off = sizeof(ProgHdr);
+            auto place = [&](size_t bytes) {
+                const size_t at = off;
+                off = pad16(off + bytes);
+                return at;
+            };
+            const size_t o_orow = place(2 * so.row.size()), o_ops = place(4 * so.ops.size()),
+                         o_ost = place(2 * so.start.size()), o_odst = place(4 * so.dst.size());
+            const size_t o_srow = place(2 * ss.row.size()), o_sops = place(4 * ss.ops.size()),
+                         o_sst = place(2 * ss.start.size()), o_sdst = place(2 * ss.dst.size());
+            const size_t o_cls = place(sizeof(TileCls) * cls.size()), o_dst = place(4 * dsts.size()),
+                         o_meta = place(4 * meta.size()), o_ent = place(2 * ents.size());
+            const size_t pbytes = off;
+            if (pbytes > 65535) return false;
+            ph.n_oseq = (uint16_t)so.start.size();
+            ph.off_orow = (uint16_t)o_orow;
+            ph.off_ops = (uint16_t)o_ops;
+            ph.off_ostart = (uint16_t)o_ost;
+            ph.off_odst = (uint16_t)o_odst;
+            ph.n_sseq = (uint16_t)ss.start.size();
+            ph.off_srow = (uint16_t)o_srow;
+            ph.off_sops = (uint16_t)o_sops;
+            ph.off_sstart = (uint16_t)o_sst;
+            ph.off_sdst = (uint16_t)o_sdst;
+            ph.n_cls = (uint16_t)cls.size();
+            ph.off_cls = (uint16_t)o_cls;
+            ph.off_dst = (uint16_t)o_dst;
+            ph.off_meta = (uint16_t)o_meta;
+            ph.off_ent = (uint16_t)o_ent;
+            o.prog.assign(pbytes, 0);
+            uint8_t *pp = o.prog.data();
+            std::memcpy(pp, &ph, sizeof(ph));
+            auto put = [&](size_t at, const void *src, size_t bytes) {
+                if (bytes) std::memcpy(pp + at, src, bytes);
+            };
+            put(o_orow, so.row.data(), 2 * so.row.size());
+            put(o_ops, so.ops.data(), 4 * so.ops.size());
+            put(o_ost, so.start.data(), 2 * so.start.size());
+            put(o_odst, so.dst.data(), 4 * so.dst.size());
+            put(o_srow, ss.row.data(), 2 * ss.row.size());
+            put(o_sops, ss.ops.data(), 4 * ss.ops.size());
+            put(o_sst, ss.start.data(), 2 * ss.start.size());
+            for (size_t q = 0; q < ss.dst.size(); q++) {
+                if (ss.dst[q] > 65535) return false;
+                const uint16_t v = (uint16_t)ss.dst[q];
+                std::memcpy(pp + o_sdst + 2 * q, &v, 2);
+            }
+            put(o_cls, cls.data(), sizeof(TileCls) * cls.size());
+            put(o_dst, dsts.data(), 4 * dsts.size());
+            put(o_meta, meta.data(), 4 * meta.size());
+            put(o_ent, ents.data(), 2 * ents.size());
+            uint64_t hsh = 1469598103934665603ull;            // FNV-1a
+            for (size_t q = 0; q < pbytes; q++) hsh = (hsh ^ pp[q]) * 1099511628211ull;
+            o.hash = hsh;
+            o.padded = 2 * (int64_t)(so.ops.size() + ss.ops.size()) + (int64_t)ents.size();
         }
-        // emit the head (per tile) and the program (shared by equal tiles)
-        ProgHdr ph;
-        std::memset(&ph, 0, sizeof(ph));
-        size_t off = sizeof(ProgHdr);
-        auto place = [&](size_t bytes) {
-            const size_t at = off;
-            off = pad16(off + bytes);
-            return at;
-        };
-        const size_t o_orow = place(2 * so.row.size()), o_ops = place(4 * so.ops.size()),
-                     o_ost = place(2 * so.start.size()), o_odst = place(4 * so.dst.size());
-        const size_t o_srow = place(2 * ss.row.size()), o_sops = place(4 * ss.ops.size()),
-                     o_sst = place(2 * ss.start.size()), o_sdst = place(2 * ss.dst.size());
-        const size_t o_cls = place(sizeof(TileCls) * cls.size()), o_dst = place(4 * dsts.size()),
-                     o_meta = place(4 * meta.size()), o_ent = place(2 * ents.size());
-        const size_t pbytes = off;
-        if (pbytes > 65535) return false;
-        ph.n_oseq = (uint16_t)so.start.size();
-        ph.off_orow = (uint16_t)o_orow;
-        ph.off_ops = (uint16_t)o_ops;
-        ph.off_ostart = (uint16_t)o_ost;
-        ph.off_odst = (uint16_t)o_odst;
-        ph.n_sseq = (uint16_t)ss.start.size();
-        ph.off_srow = (uint16_t)o_srow;
-        ph.off_sops = (uint16_t)o_sops;
-        ph.off_sstart = (uint16_t)o_sst;
-        ph.off_sdst = (uint16_t)o_sdst;
-        ph.n_cls = (uint16_t)cls.size();
-        ph.off_cls = (uint16_t)o_cls;
-        ph.off_dst = (uint16_t)o_dst;
-        ph.off_meta = (uint16_t)o_meta;
-        ph.off_ent = (uint16_t)o_ent;
-        o.prog.assign(pbytes, 0);
-        uint8_t *pp = o.prog.data();
-        std::memcpy(pp, &ph, sizeof(ph));
-        auto put = [&](size_t at, const void *src, size_t bytes) {
-            if (bytes) std::memcpy(pp + at, src, bytes);
-        };
-        put(o_orow, so.row.data(), 2 * so.row.size());
-        put(o_ops, so.ops.data(), 4 * so.ops.size());
-        put(o_ost, so.start.data(), 2 * so.start.size());
-        put(o_odst, so.dst.data(), 4 * so.dst.size());
-        put(o_srow, ss.row.data(), 2 * ss.row.size());
-        put(o_sops, ss.ops.data(), 4 * ss.ops.size());
-        put(o_sst, ss.start.data(), 2 * ss.start.size());
-        for (size_t q = 0; q < ss.dst.size(); q++) {
-            if (ss.dst[q] > 65535) return false;
-            const uint16_t v = (uint16_t)ss.dst[q];
-            std::memcpy(pp + o_sdst + 2 * q, &v, 2);
-        }
-        put(o_cls, cls.data(), sizeof(TileCls) * cls.size());
-        put(o_dst, dsts.data(), 4 * dsts.size());
-        put(o_meta, meta.data(), 4 * meta.size());
-        put(o_ent, ents.data(), 2 * ents.size());
-        uint64_t hsh = 1469598103934665603ull;            // FNV-1a
-        for (size_t q = 0; q < pbytes; q++) hsh = (hsh ^ pp[q]) * 1099511628211ull;
-        o.hash = hsh;
 
         TileHdr hdr;
         std::memset(&hdr, 0, sizeof(hdr));
@@ -645,9 +844,10 @@ bool build_tile_host(int form, int64_t N, int32_t n_nodes, int32_t n, int64_t nn
         hdr.n_sent = (uint16_t)n_sent;
         for (int q = 0; q < kTileBases; q++) hdr.base[q] = bases[q];
         hdr.off_items = (uint32_t)sizeof(TileHdr);
-        const size_t items_bytes = pad16((size_t)ni * kItemBlobBytes);
+        const size_t items_bytes = pad16((size_t)ni * (form == 1 ? 16 : kItemBlobBytes));   // form 1: terms
         hdr.off_side = (uint32_t)(hdr.off_items + items_bytes);
         const size_t bytes = pad16(hdr.off_side + sizeof(SideEnt) * sents.size());
+        const size_t pbytes = o.prog.size();
         if (bytes + pbytes > (size_t)kStageMax) return false;
         hdr.head_bytes = (uint32_t)bytes;
         hdr.prog_bytes = (uint32_t)pbytes;
@@ -678,7 +878,6 @@ bool build_tile_host(int form, int64_t N, int32_t n_nodes, int32_t n, int64_t nn
         o.n_own = n_own;
         o.n_sent = n_sent;
         o.L = (int64_t)con.size() + (int64_t)side.size();
-        o.padded = 2 * (int64_t)(so.ops.size() + ss.ops.size()) + (int64_t)ents.size();
         return true;
     };
 #pragma omp for schedule(dynamic, 64)
