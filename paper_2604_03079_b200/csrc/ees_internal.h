@@ -210,7 +210,10 @@ __host__ __device__ constexpr int tile_ctas(int form)
     return (form ? (tile_bufs(1) == 2 ? 4 : EES_TILE_CTAS1) : (tile_bufs(0) == 2 ? 3 : 4)) * 128 / kTileItems;
 }
 
-constexpr int kStages = 3;           // TMA pipeline depth (blobs in flight per CTA)
+#ifndef EES_STAGES
+#define EES_STAGES 3
+#endif
+constexpr int kStages = EES_STAGES;  // TMA pipeline depth (blobs in flight per CTA)
 constexpr int kScSlots = 16 * kTileItems + 2;   // form 0: contribution slots per buffer (+16-byte pad)
 #ifndef EES_SC_ROWS
 #define EES_SC_ROWS 7

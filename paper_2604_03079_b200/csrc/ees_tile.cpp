@@ -48,8 +48,13 @@ constexpr int64_t kHHTarget = 12, kHHContrib0 = 5;
 size_t pad16(size_t x) { return (x + 15) & ~(size_t)15; }
 }  // namespace
 
-bool build_tile_host(int form, int64_t N, int32_t n_nodes, int32_t n, int64_t nnz, const int32_t *const TT[4],
-                     const int32_t *raw_slot, const std::vector<int64_t> &iptr,
+namespace {
+// strict: the form-1 row bound is the guaranteed one (longest-first
+// balancing: floor(P / kTileItems) + longest chain); otherwise the expected
+// one (ceil(P / kTileItems) + 1), and build_tile_host falls back to strict if
+// a tile's rows do not fit.
+bool build_tile_impl(int form, bool strict, int64_t N, int32_t n_nodes, int32_t n, int64_t nnz,
+                     const int32_t *const TT[4], const int32_t *raw_slot, const std::vector<int64_t> &iptr,
                      const std::vector<int32_t> &idev, const std::vector<int32_t> &rails,
                      const std::vector<int32_t> &row_ptr, const std::vector<int32_t> &col_idx,
                      const double *beta, const double *vprev, const int32_t *model, int32_t grid,
@@ -196,7 +201,8 @@ bool build_tile_host(int form, int64_t N, int32_t n_nodes, int32_t n, int64_t nn
     };
     auto rows_over = [&](int64_t P, int32_t PM, int64_t G) {
         if (form != 1) return false;
-        const int64_t rows = (P + 1) / 2 / kTileItems + PM;
+        const int64_t pairs = (P + 1) / 2;
+        const int64_t rows = strict ? pairs / kTileItems + PM : (pairs + kTileItems - 1) / kTileItems + (PM > 1);
         return rows > kScRows || rows * 2 * kTileItems + G > (int64_t)kScRows * 2 * kTileItems;
     };
     auto close_tile = [&]() {
@@ -1045,6 +1051,23 @@ bool build_tile_host(int form, int64_t N, int32_t n_nodes, int32_t n, int64_t nn
     }
     out.n_items = (int64_t)item_dev.size();
     return true;
+}
+}  // namespace
+
+bool build_tile_host(int form, int64_t N, int32_t n_nodes, int32_t n, int64_t nnz, const int32_t *const TT[4],
+                     const int32_t *raw_slot, const std::vector<int64_t> &iptr,
+                     const std::vector<int32_t> &idev, const std::vector<int32_t> &rails,
+                     const std::vector<int32_t> &row_ptr, const std::vector<int32_t> &col_idx,
+                     const double *beta, const double *vprev, const int32_t *model, int32_t grid,
+                     TileHost &out)
+{
+    if (build_tile_impl(form, false, N, n_nodes, n, nnz, TT, raw_slot, iptr, idev, rails, row_ptr, col_idx, beta,
+                        vprev, model, grid, out))
+        return true;
+    if (form != 1) return false;
+    out = TileHost();
+    return build_tile_impl(form, true, N, n_nodes, n, nnz, TT, raw_slot, iptr, idev, rails, row_ptr, col_idx, beta,
+                           vprev, model, grid, out);
 }
 
 }  // namespace ees
