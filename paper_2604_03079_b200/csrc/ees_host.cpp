@@ -988,6 +988,8 @@ ees_status build_tile(const ees_desc *d, ees_ctx *c, const std::vector<int32_t> 
     k.hot_base = th.hot_base;
     TRY(dalloc(c, &k.hot_pre, (size_t)std::max(1, th.n_hot)));
     TRY(dalloc(c, &k.part, (size_t)th.n_parts));
+    TRY(dalloc(c, &k.gbar, 2));
+    if (cudaMemset(k.gbar, 0, 2 * sizeof(unsigned int)) != cudaSuccess) return EES_ECUDA;
     // persistent CTAs: no more than tiles (the hot parts are laid out for
     // `grid` CTAs; k_tile sums the first gridDim.x of them)
     c->tile_grid = th.grid;

@@ -324,6 +324,7 @@ struct TileK {
     const uint8_t *item_model;     // [n_tiles * kTileItems]
     double *hot_pre;               // [n_hot] old values of the hot targets (read by CTA 0)
     double *part;                  // [n_side_entries]
+    unsigned int *gbar;            // [2] grid barrier: arrivals, generation (zero at setup)
     unsigned long long *trace;     // debug: [grid][kTraceSlots] %globaltimer stamps, or null
 };
 constexpr int kTraceSlots = 64;

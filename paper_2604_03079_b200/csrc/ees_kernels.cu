@@ -1464,7 +1464,7 @@ __device__ __forceinline__ void tile_eval_item(const unsigned char *blob, const 
         st.y[SS] += st.y[BB];
         st.j[2] += st.j[3];
     }
-    if (kForm == 1) {                     // v5: each contribution straight to its pair slot
+    if constexpr (kForm == 1) {           // v5: each contribution straight to its pair slot
         const uint32_t sc32 = smem_u32(scd);
         const uint4 *pp = tile_pos(blob, it);
         const uint4 pa = pp[0], pb = pp[1];
@@ -1474,12 +1474,12 @@ __device__ __forceinline__ void tile_eval_item(const unsigned char *blob, const 
             const uint32_t off = p & 1 ? w[p >> 1] >> 16 : w[p >> 1] & 0xFFFFu;
             sts_f64(sc32 + off, p < NPAIR ? st.y[p] : st.j[p - NPAIR]);
         }
-        return;
+    } else {
+#pragma unroll
+        for (int p = 0; p < NPAIR; p++) scd[p * kTileItems + it] = st.y[p];
+#pragma unroll
+        for (int a = 0; a < 4; a++) scd[(NPAIR + a) * kTileItems + it] = st.j[a];
     }
-#pragma unroll
-    for (int p = 0; p < NPAIR; p++) scd[p * kTileItems + it] = st.y[p];
-#pragma unroll
-    for (int a = 0; a < 4; a++) scd[(NPAIR + a) * kTileItems + it] = st.j[a];
 }
 
 // TILE v5 (form 1, ees_internal.h ProgHdr5): thread r's pair of row s is
@@ -1651,6 +1651,30 @@ __device__ __forceinline__ void tile_reduce(const unsigned char *blob, const uns
     }
 }
 
+// Grid-wide barrier of the co-resident (cooperatively launched) grid: one
+// thread per CTA arrives on a counter and, unless last, polls the generation
+// word with a back-off sleep (the cooperative-groups barrier spins, and its
+// polling warps take issue slots from the CTAs still working on the same SM);
+// the last arrival resets the counter and advances the generation.
+__device__ __forceinline__ void grid_barrier(unsigned int *bar, unsigned int nblocks)
+{
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile unsigned int *gen = bar + 1;
+        const unsigned int g0 = *gen;
+        __threadfence();                                   // this CTA's writes before its arrival
+        if (atomicAdd(bar, 1u) == nblocks - 1) {
+            bar[0] = 0;
+            __threadfence();
+            atomicAdd(bar + 1, 1u);                         // release
+        } else {
+            while (*gen == g0) __nanosleep(256);
+        }
+        __threadfence();                                   // acquire: the others' writes after
+    }
+    __syncthreads();
+}
+
 // After the last tile (all threads of the CTA): hot partials per CTA; then,
 // after a grid-wide barrier (the kernel is launched cooperatively: its grid
 // is the co-resident persistent grid), every warp of the grid sums a fixed
@@ -1669,8 +1693,7 @@ __device__ __forceinline__ void tile_finish(const TileK &tk, const CallK &P, con
         for (int q = 0; q < kHotPieces; q++) v += s_hot[h * kHotPieces + q];   // piece order
         tk.part[tk.hot_base + (int64_t)h * G + blockIdx.x] = v;
     }
-    __threadfence();
-    cg::this_grid().sync();
+    grid_barrier(tk.gbar, G);
     TILE_TRACE_TAIL(kTraceSlots - 2);
     const int nw = nt >> 5;
     const int64_t gw = (int64_t)blockIdx.x * nw + warp, n_gw = (int64_t)G * nw;
