@@ -181,14 +181,14 @@ constexpr uint32_t kEmitBit = 4;     // pair-op word: bit 2 of the first entry =
 constexpr int kOpMax = EES_OP_MAX;   // owned targets of up to kOpMax contributions: op stream
 constexpr uint32_t kNoEmit = 0xFFFFFFFFu;
 #ifndef EES_HOT_PIECES
-#define EES_HOT_PIECES 24
+#define EES_HOT_PIECES 16
 #endif
 constexpr int kHotPieces = EES_HOT_PIECES;   // pieces of one hot target per tile
 // TILE forms (chosen at setup from the FET copy factor, ees_host.cpp):
 // stage bytes (one tile blob), item bytes in the blob, shared-memory slot
 // buffers (2: one barrier per tile), CTAs per SM
 #ifndef EES_STAGE1
-#define EES_STAGE1 9024              // about the largest stage that keeps 5 CTAs per SM (228 KB; the
+#define EES_STAGE1 9360              // about the largest stage that keeps 5 CTAs per SM (228 KB; the
                                      // shared-memory allocation granularity is 256 B)
 #endif
 __host__ __device__ constexpr int stage_max(int form) { return (form ? EES_STAGE1 : 11264) * kTileItems / 128; }
