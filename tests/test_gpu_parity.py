@@ -547,3 +547,36 @@ def test_tile_results_independent_of_setup_threads(cuda_ok):
     assert_parity(reference(nl), A, b, "cfg4@0.02 tile")
     assert hashlib.sha256(A.tobytes() + b.tobytes()).hexdigest() == digests[0]
     ctx.close()
+
+
+def _form_nets():
+    ms = netgen.bench_models()
+    yield netgen.ring_oscillators(20, 101, fanout=4)          # targets of 10 contributions (group classes)
+    yield netgen.gen_synth(6000, 300)                           # heavy cliques: side pieces, hot sums
+    yield netgen.full_adder_28t(8)
+    yield netgen.config(2, 0.01)
+    yield netgen.config(3, 0.01)
+    yield netgen.config(4, 0.01)
+    rng = np.random.Generator(np.random.PCG64(91))
+    for k in range(3):
+        N = int(rng.integers(500, 4000)); nn = int(rng.integers(20, N // 4))
+        T = rng.integers(-1, nn, size=(N, 4))
+        yield netgen.custom(f"rand{k}", nn, [tuple(t) for t in T], [int(v) for v in rng.integers(0, 2, N)], ms,
+                            rails=[int(rng.integers(0, nn))])
+
+
+@pytest.mark.parametrize("form", [0, 1])
+def test_tile_forms_parity(cuda_ok, form):
+    """Both TILE program formats (form 0: op streams over the evaluation's
+    p-major slots; form 1: contribution positions into pair rows, group
+    area) on structures that exercise short and long owned targets, side
+    pieces and hot sums, whatever form setup would choose."""
+    for nl in _form_nets():
+        ref = reference(nl)
+        ctx = ctx_for(nl, variant="tile", tile_form=form)
+        assert ctx.stats()["tile_form"] == form
+        assert_parity(ref, *gpu_run(ctx, nl), f"{nl.name} tile form {form}")
+        A1, b1 = gpu_run(ctx, nl)
+        A2, b2 = gpu_run(ctx, nl)
+        assert np.array_equal(A1, A2) and np.array_equal(b1, b2), f"{nl.name} form {form} not deterministic"
+        ctx.close()
