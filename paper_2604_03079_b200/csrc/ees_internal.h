@@ -100,9 +100,10 @@ struct GatherK {
 // rows, heavy-row slices (h, c) of its light columns c, and heavy x heavy
 // targets whose contributors all live in it; a target shared by several
 // tiles (heavy x heavy: rails, hub diagonals) is a SIDE target, to which the
-// tile contributes one part.
+// tile contributes one part.  (That slot layout is form 0's; form 1 stores
+// each contribution straight into its pair row, TILE v5 below ProgHdr5.)
 //
-// The tile's reduction program (TILE v4).  Short targets (at most kOpMax
+// The tile's reduction program, form 0 (TILE v4).  Short targets (at most kOpMax
 // contributions; every owned target on the inverter / SRAM / hub structures)
 // are an OP STREAM: each thread runs its own sequence of pair-ops, one u32
 // each (two u16 byte offsets of contributions in the tile's shared-memory
@@ -139,7 +140,7 @@ struct GatherK {
 //                   form 1: term int4[ni]; beta, v0[3], model in tile-order HBM
 //                   arrays (kTileItems slots per tile) loaded one tile ahead
 //            side:  SideEnt[n_sent]
-//   program: ProgHdr (32 B)
+//   program: ProgHdr (32 B; form 0 -- form 1: ProgHdr5)
 //            owned op stream: orow u16[steps] (row offsets) | ops u32[..] |
 //                  ostart u16[n_oseq] (per sequence with ops: its first
 //                  destination | its step count << kSeqStartBits) |
@@ -169,7 +170,6 @@ constexpr int kTileThreads = kTileItems;
 constexpr int kLogTileThreads = kTileThreads == 128 ? 7 : kTileThreads == 64 ? 6 : kTileThreads == 256 ? 8 : -1;
 static_assert(kLogTileThreads > 0, "tile width must be 64, 128 or 256 threads");
 constexpr int kHeavyDeg = 64;        // nodes with more incident FETs are heavy
-constexpr int kMaxCls = 15;          // distinct target lengths per tile
 #ifndef EES_SIDE_PIECE
 #define EES_SIDE_PIECE 4
 #endif
