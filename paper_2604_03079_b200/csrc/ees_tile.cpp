@@ -601,6 +601,23 @@ bool build_tile_impl(int form, bool strict, int64_t N, int32_t n_nodes, int32_t 
                 }
                 oseq[j] = start | ((uint32_t)st << kSeqStartBits) | (em << 16) | (sm << 24);
             }
+            // self-check of the pair rows: every listed contribution has its own
+            // slot, no slot holds two, and no thread's pairs pass its step count
+            {
+                std::vector<uint8_t> used((size_t)n_rows * 2 * kTileThreads, 0);
+                int64_t placed = 0;
+                for (size_t q = 0; q < pos.size(); q++) {
+                    if (pos[q] == (uint16_t)kTrashByte1) continue;
+                    const int32_t sl = pos[q] / 8;
+                    if (sl >= n_rows * 2 * kTileThreads || used[(size_t)sl]++) return false;
+                    const int32_t row = sl / (2 * kTileThreads), j = (sl / 2) % kTileThreads;
+                    if (row >= (int32_t)((oseq[(size_t)j] >> kSeqStartBits) & 15u)) return false;
+                    placed++;
+                }
+                int64_t in_rows = 0;
+                for (int32_t k : opt) in_rows += tg[k].len;
+                if (placed != in_rows) return false;
+            }
             // group classes (owned targets longer than kOpMax1), entries contiguous
             cls.clear();
             dsts.clear();
