@@ -984,6 +984,8 @@ ees_status build_tile(const ees_desc *d, ees_ctx *c, const std::vector<int32_t> 
     TRY(up(&k.sd_part, th.sd_part));
     TRY(up(&k.hot_gid, th.hot_gid));
     k.n_side = th.n_side;
+    k.n_side_big = th.n_side_big;
+    k.n_side_cold = th.n_side_cold;
     k.n_hot = th.n_hot;
     k.hot_base = th.hot_base;
     TRY(dalloc(c, &k.hot_pre, (size_t)std::max(1, th.n_hot)));

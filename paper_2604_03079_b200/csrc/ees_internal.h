@@ -312,8 +312,9 @@ struct TileK {
     const uint4 *tdesc;            // [T] head offset / 16, head bytes, program offset / 16, program bytes
     const uint8_t *blob;           // the heads
     const uint8_t *prog;           // the distinct programs
-    int32_t n_side;
-    int32_t pad0;
+    int32_t n_side;                // side targets, ordered: cold with > 8 parts | cold <= 8 | hot
+    int32_t n_side_big;            // cold side targets with more than 8 parts (summed by a warp each)
+    int32_t n_side_cold;           // cold side targets (the rest of them summed by a thread each)
     int32_t n_hot;                 // hot side targets: CTA b's part at part[hot_base + h*grid + b]
     int64_t hot_base;
     const int32_t *sd_gid;         // [n_side] global target
@@ -334,7 +335,7 @@ constexpr int kTraceSlots = 64;
 #include <vector>
 namespace ees {
 struct TileHost {
-    int32_t n_tiles = 0, n_heavy = 0, n_side = 0;
+    int32_t n_tiles = 0, n_heavy = 0, n_side = 0, n_side_big = 0, n_side_cold = 0;
     int64_t n_items = 0, n_owned = 0, n_side_entries = 0;
     int64_t n_parts = 0, hot_base = 0;
     int64_t n_listed = 0, n_padded = 0;    // list entries, and with class padding

@@ -1718,8 +1718,23 @@ __device__ __forceinline__ void tile_finish(const TileK &tk, const CallK &P, con
             *d = __ldcg(tk.hot_pre + h) + u;
         }
     }
-    for (int64_t sid = gw; sid < tk.n_side; sid += n_gw)
-        if (__ldg(tk.sd_part + 2 * sid) < tk.hot_base || tk.n_hot == 0) side_finish(tk, P, (int32_t)sid, lane);
+    // cold side targets: those of at most 8 parts one per thread (parts in
+    // order), the rest one per warp (side_finish) -- one round of latency for
+    // the many small ones (cfg2's bit lines, cfg4's hub loads)
+    const int64_t gt = (int64_t)blockIdx.x * nt + tid, n_gt = (int64_t)G * nt;
+    for (int64_t sid = tk.n_side_big + gt; sid < tk.n_side_cold; sid += n_gt) {
+        const int32_t q0 = __ldg(tk.sd_part + 2 * sid), q1 = __ldg(tk.sd_part + 2 * sid + 1);
+        double a[8];
+#pragma unroll
+        for (int r = 0; r < 8; r++) a[r] = q0 + r < q1 ? __ldcg(tk.part + q0 + r) : 0.0;
+        double u = a[0];
+#pragma unroll
+        for (int r = 1; r < 8; r++) u += a[r];
+        const int32_t g = __ldg(tk.sd_gid + sid);
+        double *dst = g < tk.nnz ? P.A + g : P.b + (g - tk.nnz);
+        *dst = *dst + u;
+    }
+    for (int64_t sid = gw; sid < tk.n_side_big; sid += n_gw) side_finish(tk, P, (int32_t)sid, lane);
 }
 
 // TILE kernel prologue: hot targets, card copy, mbarriers and the first

@@ -1066,6 +1066,28 @@ bool build_tile_impl(int form, bool strict, int64_t N, int32_t n_nodes, int32_t 
             }
         }
     }
+    // side-target order for the finishing phase: cold targets with more than
+    // 8 parts, the other cold ones, then the hot ones (the heads' side
+    // entries carry part slots, not these ids)
+    {
+        std::vector<int32_t> ord;
+        for (int pass = 0; pass < 3; pass++)
+            for (int32_t s2 = 0; s2 < out.n_side; s2++) {
+                const bool hot = hot_of[s2] >= 0, big = part_hi[s2] - part_lo[s2] > 8;
+                if ((pass == 0 && !hot && big) || (pass == 1 && !hot && !big) || (pass == 2 && hot))
+                    ord.push_back(s2);
+                if (pass == 0 && !hot && big) out.n_side_big++;
+                if (pass < 2 && !hot && (pass == 0) == big) out.n_side_cold++;
+            }
+        std::vector<int32_t> gid((size_t)out.n_side), part(2 * (size_t)out.n_side);
+        for (int32_t k = 0; k < out.n_side; k++) {
+            gid[k] = out.sd_gid[ord[k]];
+            part[2 * k] = part_lo[ord[k]];
+            part[2 * k + 1] = part_hi[ord[k]];
+        }
+        out.sd_gid.swap(gid);
+        out.sd_part.swap(part);
+    }
     out.n_items = (int64_t)item_dev.size();
     return true;
 }
