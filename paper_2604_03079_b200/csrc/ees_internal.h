@@ -213,7 +213,17 @@ __host__ __device__ constexpr int tile_ctas(int form)
 #ifndef EES_STAGES
 #define EES_STAGES 3
 #endif
-constexpr int kStages = EES_STAGES;  // TMA pipeline depth (blobs in flight per CTA)
+constexpr int kStages = EES_STAGES;  // TMA pipeline depth (blobs in flight per CTA), form 0
+#ifndef EES_STAGES1
+#define EES_STAGES1 EES_STAGES
+#endif
+__host__ __device__ constexpr int tile_stages(int form) { return form ? EES_STAGES1 : kStages; }
+// EES_LATE_GATHER: a tile's successor is gathered after B1 (into the same
+// registers the evaluation just consumed) and a stage is refilled after B0;
+// fewer registers and stages, shorter latency cover for the gathers
+#ifndef EES_LATE_GATHER
+#define EES_LATE_GATHER 0
+#endif
 constexpr int kScSlots = 16 * kTileItems + 2;   // form 0: contribution slots per buffer (+16-byte pad)
 #ifndef EES_SC_ROWS
 #define EES_SC_ROWS 7

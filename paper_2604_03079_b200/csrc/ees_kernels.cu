@@ -1204,7 +1204,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase)
 template <int kForm>
 constexpr size_t tile_smem()
 {
-    return sizeof(double) * sc_slots(kForm) * tile_bufs(kForm) + kStages * (size_t)stage_max(kForm);
+    return sizeof(double) * sc_slots(kForm) * tile_bufs(kForm) + tile_stages(kForm) * (size_t)stage_max(kForm);
 }
 
 // What a thread gathers from global memory one tile ahead: its item's node
@@ -1782,7 +1782,8 @@ __global__ void __launch_bounds__(kTileThreads, tile_ctas(kForm)) k_tile(TileK t
     constexpr int kBuf = tile_bufs(kForm);
     constexpr int kStage = stage_max(kForm);
 #define s_stage (smem + sizeof(double) * sc_slots(kForm) * kBuf)
-    TILE_PROLOGUE(kTileThreads, kStages);
+    constexpr int kStg = tile_stages(kForm);
+    TILE_PROLOGUE(kTileThreads, kStg);
     unsigned char *s_c = smem;                                           // [kBuf][kScSlots] doubles
     if (kForm == 1) {                    // v5: the slot buffer is all zero between tiles
         for (int k = tid; k < kBuf * sc_slots(kForm); k += kTileThreads) reinterpret_cast<double *>(s_c)[k] = 0.0;
@@ -1793,6 +1794,46 @@ __global__ void __launch_bounds__(kTileThreads, tile_ctas(kForm)) k_tile(TileK t
     uint32_t parity = 0;                 // bit k: phase of s_bar[k]
     int it = 0;
     int stage = 0;
+#if EES_LATE_GATHER
+    TileRegs R;
+    if (t0 < tk.n_tiles) {
+        mbar_wait(&s_bar[0], 0);
+        parity ^= 1u;
+        tile_gather<kForm>(s_stage, t0, tk, P, R);
+    }
+    TILE_TRACE(1);
+    for (int32_t t = t0; t < tk.n_tiles; t += G) {
+        const unsigned char *blob = s_stage + (size_t)stage * kStage;
+        unsigned char *sc = s_c + (kBuf == 2 ? (size_t)(it & 1) * 8 * sc_slots(kForm) : 0);
+        const int32_t tr = t + kStg * G;              // the refill of this tile's stage (after B0)
+        uint4 rf = make_uint4(0, 0, 0, 0);
+        if (tid == 0 && tr < tk.n_tiles) rf = __ldg(tk.tdesc + tr);
+        TileOut o = out;
+        o.bptr = smem_u32(s_bptr + (it & 1) * kTileBases);
+        if (tid < kTileBases) {
+            const int32_t g = reinterpret_cast<const TileHdr *>(blob)->base[tid];
+            s_bptr[(it & 1) * kTileBases + tid] = g < out.nnz ? out.A + g : out.Bm + g;
+        }
+        if (tid < reinterpret_cast<const TileHdr *>(blob)->n_items)
+            tile_eval_item<kRep, kForm>(blob, R, tid, reinterpret_cast<double *>(sc), s_cards, P);
+        TILE_TRACE(2 + 2 * it);
+        __syncthreads();                                        // B1
+        const int32_t tn = t + G;
+        const int sn = stage + 1 == kStg ? 0 : stage + 1;
+        if (tn < tk.n_tiles) {                                  // next tile's gathers hide behind the reduction
+            mbar_wait(&s_bar[sn], (parity >> sn) & 1u);
+            parity ^= 1u << sn;
+            tile_gather<kForm>(s_stage + (size_t)sn * kStage, tn, tk, P, R);
+        }
+        if (kForm == 1) tile_reduce5(blob, sc, tid, o, tk, s_hot);
+        else tile_reduce(blob, sc, tid, o, tk, s_hot);
+        TILE_TRACE(3 + 2 * it);
+        __syncthreads();                                        // B0
+        if (tid == 0 && tr < tk.n_tiles) issue_at(rf, stage);  // this tile's stage is free
+        stage = sn;
+        it++;
+    }
+#else
     TileRegs ra, rb;
     if (t0 < tk.n_tiles) {
         mbar_wait(&s_bar[0], 0);
@@ -1806,7 +1847,7 @@ __global__ void __launch_bounds__(kTileThreads, tile_ctas(kForm)) k_tile(TileK t
         unsigned char *sc = s_c + (kBuf == 2 ? (size_t)(it & 1) * 8 * sc_slots(kForm) : 0);
         // the blob this iteration's refill (at B1) will fetch: its offsets are
         // loaded now, so warp 0 does not wait on global memory after B1
-        const int32_t tr = t - G + kStages * G;
+        const int32_t tr = t - G + kStg * G;
         uint4 rf = make_uint4(0, 0, 0, 0);
         if (tid == 0 && it > 0 && tr < tk.n_tiles) rf = __ldg(tk.tdesc + tr);
         TileOut o = out;
@@ -1819,7 +1860,7 @@ __global__ void __launch_bounds__(kTileThreads, tile_ctas(kForm)) k_tile(TileK t
             tile_eval_item<kRep, kForm>(blob, cur, tid, reinterpret_cast<double *>(sc), s_cards, P);
         // next tile: its blob was issued >= one tile ago; start its gathers now
         const int32_t tn = t + G;
-        const int sn = stage + 1 == kStages ? 0 : stage + 1;
+        const int sn = stage + 1 == kStg ? 0 : stage + 1;
         if (tn < tk.n_tiles) {
             mbar_wait(&s_bar[sn], (parity >> sn) & 1u);
             parity ^= 1u << sn;
@@ -1828,7 +1869,7 @@ __global__ void __launch_bounds__(kTileThreads, tile_ctas(kForm)) k_tile(TileK t
         TILE_TRACE(2 + 2 * it);
         __syncthreads();                                        // B1
         if (tid == 0 && it > 0 && tr < tk.n_tiles)              // refill the stage of tile t-G
-            issue_at(rf, stage == 0 ? kStages - 1 : stage - 1);
+            issue_at(rf, stage == 0 ? kStg - 1 : stage - 1);
         if (kForm == 1) tile_reduce5(blob, sc, tid, o, tk, s_hot);
         else tile_reduce(blob, sc, tid, o, tk, s_hot);
         TILE_TRACE(3 + 2 * it);
@@ -1853,6 +1894,7 @@ __global__ void __launch_bounds__(kTileThreads, tile_ctas(kForm)) k_tile(TileK t
             ra = rb;
         }
     }
+#endif
     tile_finish<kTrace>(tk, P, s_hot);
     TILE_TRACE_TAIL(kTraceSlots - 1);
 #undef s_stage
