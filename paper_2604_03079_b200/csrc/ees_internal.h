@@ -221,6 +221,9 @@ __host__ __device__ constexpr int tile_stages(int form) { return form ? EES_STAG
 // EES_LATE_GATHER: a tile's successor is gathered after B1 (into the same
 // registers the evaluation just consumed) and a stage is refilled after B0;
 // fewer registers and stages, shorter latency cover for the gathers
+#ifndef EES_A_PREFETCH
+#define EES_A_PREFETCH 1               // bulk L2 prefetch of the next tile's CSR block of A
+#endif
 #ifndef EES_LATE_GATHER
 #define EES_LATE_GATHER 0
 #endif
@@ -229,7 +232,11 @@ constexpr int kScSlots = 16 * kTileItems + 2;   // form 0: contribution slots pe
 #define EES_SC_ROWS 7
 #endif
 constexpr int kScRows = EES_SC_ROWS;             // form 1: pair rows (of kTileItems pairs) per tile
-static_assert(kScRows <= 8, "row masks are 8 bits");
+static_assert(kScRows <= 7, "row masks are 7 bits");
+// form 1 sequence word: first destination (11 bits) | emit mask << 11 | side
+// mask << 18 | pad mask << 25 (bit s of each: the thread's pair of row s);
+// a sequence's rows end with its last emit (every sequence ends a target)
+constexpr int kSeqEmit = 11, kSeqSide = 18, kSeqPad = 25;
 // contribution slots (doubles) of the form's slot buffer; form 1: kScRows rows
 // of kTileItems 16-byte pairs, then the trash slot and a pad
 __host__ __device__ constexpr int sc_slots(int form) { return form ? kScRows * 2 * kTileItems + 2 : kScSlots; }
@@ -270,7 +277,7 @@ struct TileHdr {
     uint32_t prog_bytes;             // program size (multiple of 16)
     uint32_t off_items, off_side;    // byte offsets of the head's sections
     int32_t base[kTileBases];        // destination bases (global target ids)
-    uint32_t pad1[2];
+    int32_t a_lo, a_n;               // the tile rows' CSR block of A: [a_lo, a_lo + a_n) (L2 prefetch)
 };
 static_assert(sizeof(TileHdr) == 96, "TileHdr layout");
 
@@ -287,12 +294,11 @@ constexpr int kSeqStartBits = 11;        // sequence word: first destination | s
 // into their place in the pair rows: thread j's pair of row s is the 16 bytes
 // at (s * kTileItems + j) * 16 of the slot buffer (a conflict-free LDS.128 at
 // a compile-time offset), so the reduction reads no program entry per pair.
-// The slot buffer is all zero between tiles (the reduction zeroes every pair
-// it reads; padding halves are never written), so an odd target's second
-// half reads 0.  Per thread one sequence word: first destination (11 bits) |
-// pair rows used << 11 (4 bits) | emit mask << 16 (bit s: the pair of row s
-// completes a target) | side mask << 24 (bit s: that target is a side piece,
-// its destination a side entry).  Owned targets longer than kOpMax1 are group
+// An odd target's last pair has no second contribution: that half is never
+// written and its pad bit tells the reduction to skip it.  Per thread one
+// sequence word: first destination (11 bits) | emit mask << 11 (bit s: the
+// pair of row s completes a target) | side mask << 18 (that target is a side
+// piece, its destination a side entry) | pad mask << 25.  Owned targets longer than kOpMax1 are group
 // classes whose entries are contiguous in a group area after the rows.
 //   program: ProgHdr5 | pos u16[ni][16] (byte offset of each contribution in
 //            the slot buffer; kTrashByte1 if not listed) | oseq u32[kTileItems]

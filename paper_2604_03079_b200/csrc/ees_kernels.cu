@@ -1188,6 +1188,17 @@ __device__ __forceinline__ void tma_bulk_g2s(void *dst, const void *src, uint32_
                  : "memory");
 }
 
+// bulk L2 prefetch of a tile's CSR block of A (its REDs then find the sectors in L2)
+__device__ __forceinline__ void l2_prefetch_block(const double *A, int32_t lo, int32_t n)
+{
+#if EES_A_PREFETCH
+    if (n <= 0) return;
+    const uintptr_t a0 = reinterpret_cast<uintptr_t>(A + lo) & ~(uintptr_t)15;
+    const uintptr_t a1 = (reinterpret_cast<uintptr_t>(A + lo + n) + 15) & ~(uintptr_t)15;
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"((uint32_t)(a1 - a0)) : "memory");
+#endif
+}
+
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase)
 {
     asm volatile(
@@ -1483,10 +1494,10 @@ __device__ __forceinline__ void tile_eval_item(const unsigned char *blob, const 
 }
 
 // TILE v5 (form 1, ees_internal.h ProgHdr5): thread r's pair of row s is
-// the 16 bytes at (s * kTileItems + r) * 16 of the slot buffer; it reads and
-// zeroes them (the buffer is all zero between tiles), adds both halves to its
-// running sum and, where the row's emit bit is set, adds the sum to its next
-// destination (one RED; a side piece's sum is its part).
+// the 16 bytes at (s * kTileItems + r) * 16 of the slot buffer; it reads
+// them (one LDS.128), adds both halves to its running sum (one where the pad
+// bit marks an odd target's last pair) and, where the row's emit bit is set,
+// adds the sum to its next destination (one RED; a side piece's sum is its part).
 __device__ __forceinline__ void tile_grp5(const TileCls c, int r, const uint32_t *dst, const uint32_t *meta,
                                           uint32_t g32, const TileOut &o)
 {
@@ -1506,11 +1517,7 @@ __device__ __forceinline__ void tile_grp5(const TileCls c, int r, const uint32_t
             const int L = (int)(m >> 16);
             double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
             int p = lj;
-            auto take = [&](int q) {
-                const double v = lds_f64(e + 8 * q);
-                sts_f64(e + 8 * q, 0.0);
-                return v;
-            };
+            auto take = [&](int q) { return lds_f64(e + 8 * q); };
             for (; p + 3 * gs < L; p += 4 * gs) {
                 s0 += take(p);
                 s1 += take(p + gs);
@@ -1537,10 +1544,11 @@ __device__ __forceinline__ void tile_reduce5(const unsigned char *blob, const un
     const uint32_t p32 = smem_u32(prog), sc32 = smem_u32(sc);
     {
         const uint32_t w = lds_u32(p32 + ph->off_oseq + 4 * r);
-        const int ns = (int)((w >> kSeqStartBits) & 15u);
+        const uint32_t em = (w >> kSeqEmit) & 0x7Fu;
+        const int ns = em ? 32 - __clz(em) : 0;                // rows end with the last emit
         uint32_t dst = p32 + ph->off_odst + 4 * (w & ((1u << kSeqStartBits) - 1));
-        const uint32_t a = sc32 + 16 * r;
         const SideEnt *sents = reinterpret_cast<const SideEnt *>(blob + h->off_side);
+        const uint32_t a = sc32 + 16 * r;
         double acc = 0.0;
 #pragma unroll
         for (int st = 0; st < kScRows; st++) {
@@ -1548,13 +1556,12 @@ __device__ __forceinline__ void tile_reduce5(const unsigned char *blob, const un
                 double v0, v1;
                 const uint32_t q = a + st * 16 * kTileItems;
                 asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v0), "=d"(v1) : "r"(q));
-                asm volatile("st.shared.v2.f64 [%0], {%1, %1};" ::"r"(q), "d"(0.0) : "memory");
                 acc += v0;
-                acc += v1;
-                if ((w >> (16 + st)) & 1u) {                     // the target is complete
+                if (!((w >> (kSeqPad + st)) & 1u)) acc += v1;   // an odd target's last pair: one half
+                if ((em >> st) & 1u) {                           // the target is complete
                     const uint32_t d = lds_u32(dst);
                     dst += 4;
-                    if ((w >> (24 + st)) & 1u) side_put(sents, d, tk, s_hot, acc);
+                    if ((w >> (kSeqSide + st)) & 1u) side_put(sents, d, tk, s_hot, acc);
                     else red_add(tile_dst(out, d), acc);
                     acc = 0.0;
                 }
@@ -1785,10 +1792,7 @@ __global__ void __launch_bounds__(kTileThreads, tile_ctas(kForm)) k_tile(TileK t
     constexpr int kStg = tile_stages(kForm);
     TILE_PROLOGUE(kTileThreads, kStg);
     unsigned char *s_c = smem;                                           // [kBuf][kScSlots] doubles
-    if (kForm == 1) {                    // v5: the slot buffer is all zero between tiles
-        for (int k = tid; k < kBuf * sc_slots(kForm); k += kTileThreads) reinterpret_cast<double *>(s_c)[k] = 0.0;
-        __syncthreads();
-    } else if (tid < kBuf) {
+    if (kForm == 0 && tid < kBuf) {
         reinterpret_cast<double *>(s_c + (size_t)tid * 8 * kScSlots)[16 * kTileItems] = 0.0;   // zero slot
     }
     uint32_t parity = 0;                 // bit k: phase of s_bar[k]
@@ -1865,6 +1869,10 @@ __global__ void __launch_bounds__(kTileThreads, tile_ctas(kForm)) k_tile(TileK t
             mbar_wait(&s_bar[sn], (parity >> sn) & 1u);
             parity ^= 1u << sn;
             tile_gather<kForm>(s_stage + (size_t)sn * kStage, tn, tk, P, nxt);
+            if (tid == 32) {                                    // warp 1: the next tile's A block into L2
+                const TileHdr *hn = reinterpret_cast<const TileHdr *>(s_stage + (size_t)sn * kStage);
+                l2_prefetch_block(P.A, hn->a_lo, hn->a_n);
+            }
         }
         TILE_TRACE(2 + 2 * it);
         __syncthreads();                                        // B1

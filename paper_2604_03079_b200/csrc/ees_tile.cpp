@@ -584,7 +584,7 @@ bool build_tile_impl(int form, bool strict, int64_t N, int32_t n_nodes, int32_t 
             for (int j = 0; j < kTileThreads; j++) {
                 const uint32_t start = (uint32_t)odst.size();
                 if (start >= (1u << kSeqStartBits)) return false;
-                uint32_t em = 0, sm = 0;
+                uint32_t em = 0, sm = 0, pm = 0;
                 int32_t st = 0;
                 for (int32_t k : seq[j]) {
                     const Tgt &t2 = tg[k];
@@ -592,6 +592,7 @@ bool build_tile_impl(int form, bool strict, int64_t N, int32_t n_nodes, int32_t 
                         const int32_t slot = 2 * (st * kTileThreads + j);
                         place(t2, p, slot);
                         if (p + 1 < t2.len) place(t2, p + 1, slot + 1);
+                        else pm |= 1u << st;                        // odd target: no second half
                         if (p + 2 >= t2.len) {
                             em |= 1u << st;
                             if (t2.is_side) sm |= 1u << st;
@@ -599,7 +600,7 @@ bool build_tile_impl(int form, bool strict, int64_t N, int32_t n_nodes, int32_t 
                     }
                     odst.push_back(t2.is_side ? (uint32_t)(-1 - t2.dst) : code_of(t2.dst));
                 }
-                oseq[j] = start | ((uint32_t)st << kSeqStartBits) | (em << 16) | (sm << 24);
+                oseq[j] = start | (em << kSeqEmit) | (sm << kSeqSide) | (pm << kSeqPad);
             }
             // self-check of the pair rows: every listed contribution has its own
             // slot, no slot holds two, and no thread's pairs pass its step count
@@ -611,7 +612,8 @@ bool build_tile_impl(int form, bool strict, int64_t N, int32_t n_nodes, int32_t 
                     const int32_t sl = pos[q] / 8;
                     if (sl >= n_rows * 2 * kTileThreads || used[(size_t)sl]++) return false;
                     const int32_t row = sl / (2 * kTileThreads), j = (sl / 2) % kTileThreads;
-                    if (row >= (int32_t)((oseq[(size_t)j] >> kSeqStartBits) & 15u)) return false;
+                    const uint32_t emj = (oseq[(size_t)j] >> kSeqEmit) & 0x7Fu;
+                    if (row >= (emj ? 32 - __builtin_clz(emj) : 0)) return false;
                     placed++;
                 }
                 int64_t in_rows = 0;
@@ -866,6 +868,11 @@ bool build_tile_impl(int form, bool strict, int64_t N, int32_t n_nodes, int32_t 
         hdr.n_full = (uint16_t)n_full;
         hdr.n_sent = (uint16_t)n_sent;
         for (int q = 0; q < kTileBases; q++) hdr.base[q] = bases[q];
+        if (tile_rows_ptr[tt + 1] > tile_rows_ptr[tt]) {
+            const int32_t r0 = tile_rows[tile_rows_ptr[tt]], r1 = tile_rows[tile_rows_ptr[tt + 1] - 1];
+            hdr.a_lo = row_ptr[r0];
+            hdr.a_n = row_ptr[r1 + 1] - row_ptr[r0];
+        }
         hdr.off_items = (uint32_t)sizeof(TileHdr);
         const size_t items_bytes = pad16((size_t)ni * (form == 1 ? 16 : kItemBlobBytes));   // form 1: terms
         hdr.off_side = (uint32_t)(hdr.off_items + items_bytes);
