@@ -162,6 +162,10 @@ typedef struct {
                                                run of equal entries in a warp (timed at setup) */
     int32_t n_tile_programs;                /* EES_TILE: distinct reduction programs (tiles of equal
                                                structure share one) */
+    int64_t tile_store_waves;               /* EES_TILE form 1: the builder's estimate of the shared-
+                                               memory wavefronts of the evaluation's STS.64 per call
+                                               (bank model: 16 bank pairs per half-warp store) */
+    int64_t tile_store_waves_naive;         /* the same without the bank-aware lane placement */
 } ees_stats_t;
 
 /* Build everything that depends only on topology ("constructs the FET

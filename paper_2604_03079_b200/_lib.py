@@ -52,7 +52,8 @@ class ees_stats_t(C.Structure):
                 ("tile_blob_max", i32), ("n_tile_items", i64), ("tune_ms", f64 * 6),
                 ("n_excluded_nodes", i32), ("tile_form", i32), ("gather_form", i32),
                 ("n_color_side_targets", i32),
-                ("n_color_side_contributions", i64), ("atomic_form", i32), ("n_tile_programs", i32)]
+                ("n_color_side_contributions", i64), ("atomic_form", i32), ("n_tile_programs", i32),
+                ("tile_store_waves", i64), ("tile_store_waves_naive", i64)]
 
 
 lib = C.CDLL(LIB_PATH)

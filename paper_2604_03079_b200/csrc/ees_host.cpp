@@ -961,6 +961,8 @@ ees_status build_tile(const ees_desc *d, ees_ctx *c, const std::vector<int32_t> 
     c->st.n_tile_items = th.n_items;
     c->st.tile_blob_max = th.blob_max;
     c->st.n_tile_programs = th.n_progs;
+    c->st.tile_store_waves = th.st_waves;
+    c->st.tile_store_waves_naive = th.st_waves0;
     if (c->host_only) return EES_OK;
     TileK &k = c->tk;
     k.form = form;

@@ -300,7 +300,7 @@ constexpr int kSeqStartBits = 11;        // sequence word: first destination | s
 // pair of row s completes a target) | side mask << 18 (that target is a side
 // piece, its destination a side entry) | pad mask << 25.  Owned targets longer than kOpMax1 are group
 // classes whose entries are contiguous in a group area after the rows.
-//   program: ProgHdr5 | pos u16[ni][16] (byte offset of each contribution in
+//   program: ProgHdr5 | pos u16[2][ni][8] (byte offset of each contribution in
 //            the slot buffer; kTrashByte1 if not listed) | oseq u32[kTileItems]
 //            | odst u32[..] (destination code, or side entry index) |
 //            TileCls[n_cls] | dst u32[..] | meta u32[..] (first slot after
@@ -358,6 +358,7 @@ struct TileHost {
     int32_t blob_max = 0, n_hot = 0;       // largest head + program
     int32_t grid = 1;                      // persistent CTAs the hot-part layout is made for
     int32_t n_progs = 0;                   // distinct programs
+    int64_t st_waves0 = 0, st_waves = 0;   // form 1: estimated evaluation STS wavefronts per call
     std::vector<int64_t> blob_off;         // [T+1] head offsets
     std::vector<uint8_t> blob;             // heads
     std::vector<uint8_t> prog;             // distinct programs

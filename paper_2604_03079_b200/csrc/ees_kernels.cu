@@ -1224,6 +1224,7 @@ struct TileRegs {
     double VD, VG, VS;
     double beta, v0a, v0b, v0c;
     int model;
+    int tied;                  // source tied to bulk (terms z == w, not ground)
 };
 
 template <int kForm>
@@ -1233,6 +1234,7 @@ __device__ __forceinline__ void tile_gather(const unsigned char *blob, int32_t t
     const int tid = threadIdx.x;
     const TileHdr *h = reinterpret_cast<const TileHdr *>(blob);
     R.VD = R.VG = R.VS = 0.0;
+    R.tied = 0;
     if (tid < h->n_items) {
         const bool full = tid < h->n_full;            // gate-row items: caps only (no x, no beta)
         if (kForm == 1) {
@@ -1250,6 +1252,7 @@ __device__ __forceinline__ void tile_gather(const unsigned char *blob, int32_t t
             R.VD = T.x >= 0 ? __ldg(P.x + T.x) : 0.0;
             R.VG = T.y >= 0 ? __ldg(P.x + T.y) : 0.0;
             R.VS = T.z >= 0 ? __ldg(P.x + T.z) : 0.0;
+            R.tied = T.z == T.w && T.z != -1;
         }
     }
 }
@@ -1420,11 +1423,14 @@ __device__ __forceinline__ void sts_f64(uint32_t a, double v)
 }
 
 // form 1: item it's 16 contribution positions in the staged program
-__device__ __forceinline__ const uint4 *tile_pos(const unsigned char *blob, int it)
+// (ees_internal.h: [2][ni] uint4, two conflict-free LDS.128)
+__device__ __forceinline__ void tile_pos(const unsigned char *blob, int it, uint4 &pa, uint4 &pb)
 {
     const TileHdr *h = reinterpret_cast<const TileHdr *>(blob);
     const unsigned char *prog = blob + h->head_bytes;
-    return reinterpret_cast<const uint4 *>(prog + reinterpret_cast<const ProgHdr5 *>(prog)->off_pos + 32 * it);
+    const uint4 *pp = reinterpret_cast<const uint4 *>(prog + reinterpret_cast<const ProgHdr5 *>(prog)->off_pos);
+    pa = pp[it];
+    pb = pp[h->n_items + it];
 }
 
 template <bool kRep, int kForm>
@@ -1442,8 +1448,8 @@ __device__ __forceinline__ void tile_eval_item(const unsigned char *blob, const 
         const double g1 = cd.gcgs, g2 = cd.gcgd;
         if (kForm == 1) {
             const uint32_t sc32 = smem_u32(scd);
-            const uint4 *pp = tile_pos(blob, it);
-            const uint4 pa = pp[0], pb = pp[1];
+            uint4 pa, pb;
+            tile_pos(blob, it, pa, pb);
             const uint32_t w[8] = {pa.x, pa.y, pa.z, pa.w, pb.x, pb.y, pb.z, pb.w};
             auto at = [&](int q) { return sc32 + (q & 1 ? w[q >> 1] >> 16 : w[q >> 1] & 0xFFFFu); };
             sts_f64(at(GD), -g2);
@@ -1468,8 +1474,7 @@ __device__ __forceinline__ void tile_eval_item(const unsigned char *blob, const 
         eval_fet<kRep>(s_cards[md[it]], bt[it], P.gmin, cur.VD, cur.VG, cur.VS, bt[ni + it], bt[2 * ni + it],
                        bt[3 * ni + it], st, P.work);
     }
-    const int4 T = reinterpret_cast<const int4 *>(blob + h->off_items)[it];
-    if (T.z == T.w && T.z != -1) {        // source tied to bulk: one entry each (ees_internal.h)
+    if (cur.tied) {                       // source tied to bulk: one entry each (ees_internal.h)
         st.y[DS] += st.y[DB];
         st.y[SD] += st.y[BD];
         st.y[SS] += st.y[BB];
@@ -1477,8 +1482,8 @@ __device__ __forceinline__ void tile_eval_item(const unsigned char *blob, const 
     }
     if constexpr (kForm == 1) {           // v5: each contribution straight to its pair slot
         const uint32_t sc32 = smem_u32(scd);
-        const uint4 *pp = tile_pos(blob, it);
-        const uint4 pa = pp[0], pb = pp[1];
+        uint4 pa, pb;
+        tile_pos(blob, it, pa, pb);
         const uint32_t w[8] = {pa.x, pa.y, pa.z, pa.w, pb.x, pb.y, pb.z, pb.w};
 #pragma unroll
         for (int p = 0; p < 16; p++) {

@@ -14,11 +14,26 @@
 #include <algorithm>
 #include <cstring>
 #include <functional>
+#include <iterator>
 #include <numeric>
 #include <unordered_map>
 #include <vector>
 
 #include "ees_internal.h"
+
+// build-time A/B knobs of the TILE builder (tools/ab_tree.sh)
+#ifndef EES_BANK_ORDER
+#define EES_BANK_ORDER 0
+#endif
+#ifndef EES_PIECE_INTERLEAVE
+#define EES_PIECE_INTERLEAVE 1
+#endif
+#ifndef EES_BANK_GREEDY
+#define EES_BANK_GREEDY 0
+#endif
+#ifndef EES_BANK_SWAP
+#define EES_BANK_SWAP 1          // passes of lane swaps (0: none)
+#endif
 
 namespace ees {
 
@@ -372,6 +387,7 @@ bool build_tile_impl(int form, bool strict, int64_t N, int32_t n_nodes, int32_t 
         std::vector<uint8_t> blob, prog;     // head, program
         uint64_t hash = 0;                   // of the program bytes
         int64_t listed = 0, L = 0, padded = 0;
+        int64_t st_waves0 = 0, st_waves = 0;  // form 1: estimated STS wavefronts (identity / placed)
         int32_t n_own = 0, n_sent = 0;
         bool ok = true;
     };
@@ -384,7 +400,7 @@ bool build_tile_impl(int form, bool strict, int64_t N, int32_t n_nodes, int32_t 
     bool all_ok = true;
 #pragma omp parallel
     {
-    std::vector<std::pair<int32_t, uint16_t>> con, side;
+    std::vector<std::pair<int32_t, uint16_t>> con, side, piece_tmp;
     std::vector<int32_t> gids;
     std::vector<SideEnt> sents;
     // one target of the program: destination, its entries con/side[beg, beg+len)
@@ -489,13 +505,33 @@ bool build_tile_impl(int form, bool strict, int64_t N, int32_t n_nodes, int32_t 
             const int32_t g = side[k].first;
             size_t e = k;
             while (e < side.size() && side[e].first == g) e++;
+#if EES_PIECE_INTERLEAVE
+            // piece q takes entries q, q + P, q + 2P, ... (P pieces): a piece's
+            // entries come from items far apart, so its two pair rows do not
+            // receive stores of the same half-warp into the same bank pair
+            {
+                const size_t n = e - k, P = (n + kSidePiece - 1) / kSidePiece;
+                if (P > 1) {
+                    piece_tmp.assign(side.begin() + (std::ptrdiff_t)k, side.begin() + (std::ptrdiff_t)e);
+                    size_t at = k;
+                    for (size_t q = 0; q < P; q++)
+                        for (size_t m = q; m < n; m += P) side[at++] = piece_tmp[m];
+                }
+            }
+            for (size_t p0 = k, q = 0, n = e - k, P = (n + kSidePiece - 1) / kSidePiece; p0 < e; q++) {
+                const size_t p1 = p0 + (n - q + P - 1) / P;   // piece q holds ceil((n - q) / P) entries
+#else
             for (size_t p0 = k; p0 < e; p0 += kSidePiece) {
                 const size_t p1 = std::min(e, p0 + (size_t)kSidePiece);
+#endif
                 SideEnt se;
                 se.sid = g;             // global target; numbered after the concatenation
                 se.slot = -1;
                 tg.push_back(Tgt{-1 - (int32_t)sents.size(), (int32_t)p0, (int32_t)(p1 - p0), true});
                 sents.push_back(se);
+#if EES_PIECE_INTERLEAVE
+                p0 = p1;
+#endif
             }
             k = e;
         }
@@ -574,24 +610,292 @@ bool build_tile_impl(int form, bool strict, int64_t N, int32_t n_nodes, int32_t 
             if (n_rows > kScRows || (int64_t)n_rows * 2 * kTileThreads + G > (int64_t)kScRows * 2 * kTileThreads)
                 return false;
             const int32_t gbase = n_rows * 2 * kTileThreads;           // first group slot
+            // pos: [2][ni] uint4 -- item `it`'s positions of contributions 0-7
+            // at 16*it, of 8-15 at 16*(ni + it) (two conflict-free LDS.128)
             std::vector<uint16_t> pos((size_t)ni * 16, (uint16_t)kTrashByte1);
-            auto place = [&](const Tgt &t2, int32_t p, int32_t slot_index) {
-                const uint16_t cs = t2.is_side ? side[t2.beg + p].second : con[t2.beg + p].second;
-                const int32_t pc = cs / kTileItems, loc = cs % kTileItems;   // contribution (p, item)
-                pos[(size_t)loc * 16 + pc] = (uint16_t)(8 * slot_index);
+            auto pos_at = [&](int32_t loc, int32_t pc) -> uint16_t & {
+                return pos[((size_t)(pc >> 3) * ni + loc) * 8 + (pc & 7)];
             };
+            auto code_at = [&](const Tgt &t2, int32_t p) -> uint16_t {
+                return t2.is_side ? side[t2.beg + p].second : con[t2.beg + p].second;
+            };
+            auto place = [&](const Tgt &t2, int32_t p, int32_t slot_index) {
+                const uint16_t cs = code_at(t2, p);
+                pos_at(cs % kTileItems, cs / kTileItems) = (uint16_t)(8 * slot_index);   // (item, p)
+            };
+            // ---- bank-aware placement of the evaluation's stores.  Thread j's
+            // pair of row s sits at byte 16 (s kTileItems + j): its two halves
+            // are the 8-byte bank pairs 2 (j mod 8) and 2 (j mod 8) + 1.  A
+            // half-warp's STS.64 of contribution p (items 16w' .. 16w'+15)
+            // takes as many shared-memory wavefronts as its busiest bank pair
+            // holds distinct addresses.  Within each warp the 32 sequences are
+            // permuted onto the lanes (the warp's set of RED addresses, hence
+            // their coalescing, is unchanged) and the two halves of each full
+            // pair are oriented, greedily, to spread every such store over the
+            // 16 bank pairs.  (The order of a target's additions changes with
+            // an orientation; it stays fixed per program: deterministic.)
+            std::vector<int32_t> perm(kTileThreads);        // thread j runs sequence perm[j]
+            std::vector<uint8_t> flip(tg.size(), 0);         // bit q: pair q of the target swapped
+            {
+                const int32_t n_full_items = n_full;
+                auto key_of = [&](uint16_t cs) {              // (half-warp of items, contribution, item kind)
+                    const int32_t pc = cs / kTileItems, loc = cs % kTileItems;
+                    return ((loc >> 4) * 16 + pc) * 2 + (loc >= n_full_items ? 1 : 0);
+                };
+                constexpr int kKeys = (kTileItems / 16) * 16 * 2;
+                std::vector<uint8_t> in_rows((size_t)ni * 16, 0);      // 1 rows, 2 group area
+                for (int32_t k = 0; k < (int32_t)tg.size(); k++)
+                    for (int32_t p = 0; p < tg[k].len; p++) {
+                        const uint16_t cs = code_at(tg[k], p);
+                        in_rows[(size_t)(cs % kTileItems) * 16 + cs / kTileItems] =
+                            (!tg[k].is_side && tg[k].len > kOpMax1) ? 2 : 1;
+                    }
+                // stores that do not go to the rows: the trash slot (bank pair
+                // 0, one address) and the group area (ignored here)
+                std::vector<uint16_t> base_cnt((size_t)kKeys * 16, 0);
+                for (int32_t loc = 0; loc < ni; loc++) {
+                    const bool full = loc < n_full_items;
+                    for (int pc = 0; pc < 16; pc++) {
+                        if (!full && pc != GD && pc != GG && pc != GS && pc != NPAIR + 1) continue;
+                        if (in_rows[(size_t)loc * 16 + pc]) continue;
+                        const int key = key_of((uint16_t)(pc * kTileItems + loc));
+                        base_cnt[(size_t)key * 16] = 1;                          // trash: one address
+                    }
+                }
+                auto waves = [&](const std::vector<uint16_t> &cnt) {
+                    int64_t w = 0;
+                    for (int key = 0; key < kKeys; key++) {
+                        int m = 0;
+                        for (int b = 0; b < 16; b++) m = std::max(m, (int)cnt[(size_t)key * 16 + b]);
+                        w += m;
+                    }
+                    return w;
+                };
+                // identity placement (the estimate without this step)
+                {
+                    std::vector<uint16_t> cnt = base_cnt;
+                    for (int j = 0; j < kTileThreads; j++)
+                        for (int32_t k : seq[j])
+                            for (int32_t p = 0; p < tg[k].len; p++)
+                                cnt[(size_t)key_of(code_at(tg[k], p)) * 16 + 2 * (j & 7) + (p & 1)]++;
+                    o.st_waves0 = waves(cnt);
+                }
+                std::vector<uint16_t> cnt = base_cnt;
+                std::vector<uint16_t> mx(kKeys, 0);                 // per key: its busiest bank pair
+                for (int key = 0; key < kKeys; key++)
+                    for (int b = 0; b < 16; b++) mx[key] = std::max(mx[key], cnt[(size_t)key * 16 + b]);
+                // place sequence s in class c: each full pair oriented by the
+                // smaller increase of sum-of-max (then of the counts it meets);
+                // returns (increase, counts met); commit = keep the increments
+                std::vector<std::pair<int, int>> undo;             // (key*16+b, old max of key)
+                auto apply = [&](int s, int c, bool commit, int64_t &dmax, int64_t &prox) {
+                    dmax = 0;
+                    prox = 0;
+                    undo.clear();
+                    auto inc = [&](int key, int b) {
+                        const size_t q = (size_t)key * 16 + b;
+                        undo.emplace_back((int)q, (int)mx[key]);
+                        prox += cnt[q];
+                        if (++cnt[q] > mx[key]) { mx[key] = cnt[q]; dmax++; }
+                    };
+                    auto gain = [&](int key, int b) { return cnt[(size_t)key * 16 + b] + 1 > mx[key] ? 1 : 0; };
+                    for (int32_t k : seq[s]) {
+                        const Tgt &t2 = tg[k];
+                        for (int32_t p = 0; p < t2.len; p += 2) {
+                            const int ka = key_of(code_at(t2, p));
+                            if (p + 1 < t2.len) {
+                                const int kb = key_of(code_at(t2, p + 1));
+                                int keep, swp;
+                                if (ka == kb) {
+                                    keep = swp = 0;
+                                } else {
+                                    keep = 2 * (gain(ka, 2 * c) + gain(kb, 2 * c + 1)) * 64 +
+                                           cnt[(size_t)ka * 16 + 2 * c] + cnt[(size_t)kb * 16 + 2 * c + 1];
+                                    swp = 2 * (gain(ka, 2 * c + 1) + gain(kb, 2 * c)) * 64 +
+                                          cnt[(size_t)ka * 16 + 2 * c + 1] + cnt[(size_t)kb * 16 + 2 * c];
+                                }
+                                if (swp < keep) {
+                                    if (commit) flip[(size_t)k] |= (uint8_t)(1u << (p >> 1));
+                                    inc(ka, 2 * c + 1);
+                                    inc(kb, 2 * c);
+                                } else {
+                                    inc(ka, 2 * c);
+                                    inc(kb, 2 * c + 1);
+                                }
+                            } else {
+                                inc(ka, 2 * c);
+                            }
+                        }
+                    }
+                    if (!commit)
+                        for (size_t u = undo.size(); u-- > 0;) {
+                            cnt[(size_t)undo[u].first]--;
+                            mx[undo[u].first / 16] = (uint16_t)undo[u].second;
+                        }
+                };
+#if EES_BANK_GREEDY
+                for (int w = 0; w < kTileThreads / 32; w++) {
+                    int order[32], cap[8], n_c[32];
+                    for (int l = 0; l < 32; l++) {
+                        order[l] = 32 * w + l;
+                        n_c[l] = 0;
+                        for (int32_t k : seq[32 * w + l]) n_c[l] += tg[k].len;
+                    }
+                    for (int c = 0; c < 8; c++) cap[c] = 4;
+                    if (EES_BANK_ORDER) std::stable_sort(order, order + 32, [&](int a, int b) { return n_c[a - 32 * w] > n_c[b - 32 * w]; });
+                    int lane_used[32] = {0};
+                    for (int oi = 0; oi < 32; oi++) {
+                        const int s = order[oi];
+                        int best_c = -1;
+                        int64_t best_d = INT64_MAX, best_p = INT64_MAX;
+                        for (int c0 = 0; c0 < 8; c0++) {
+                            const int c = ((s & 7) + c0) & 7;           // ties: the sequence's own class
+                            if (!cap[c]) continue;
+                            int64_t d, pr;
+                            apply(s, c, false, d, pr);
+                            if (d < best_d) { best_d = d; best_p = pr; best_c = c; }
+                        }
+                        int64_t d, pr;
+                        apply(s, best_c, true, d, pr);
+                        cap[best_c]--;
+                        int lane = best_c;
+                        while (lane_used[lane]) lane += 8;
+                        lane_used[lane] = 1;
+                        perm[32 * w + lane] = s;
+                    }
+                }
+#else
+                // identity lane placement; then hill-climb the orientation of
+                // each full pair (two halves swapped) on the exact sum of maxima
+                for (int j = 0; j < kTileThreads; j++) perm[j] = j;
+                for (int j = 0; j < kTileThreads; j++)
+                    for (int32_t k : seq[j])
+                        for (int32_t p = 0; p < tg[k].len; p++)
+                            if (p + 1 < tg[k].len || (p & 1)) {
+                                const size_t q = (size_t)key_of(code_at(tg[k], p)) * 16 + 2 * (j & 7) + (p & 1);
+                                mx[q / 16] = std::max(mx[q / 16], ++cnt[q]);
+                            } else {
+                                const size_t q = (size_t)key_of(code_at(tg[k], p)) * 16 + 2 * (j & 7);
+                                mx[q / 16] = std::max(mx[q / 16], ++cnt[q]);
+                            }
+                auto kmax = [&](int key) {
+                    uint16_t m = 0;
+                    for (int b = 0; b < 16; b++) m = std::max(m, cnt[(size_t)key * 16 + b]);
+                    return m;
+                };
+                for (int pass = 0; pass < 4; pass++) {
+                    bool any = false;
+                    for (int j = 0; j < kTileThreads; j++) {
+                        const int c = j & 7;
+                        for (int32_t k : seq[j])
+                            for (int32_t p = 0; p + 1 < tg[k].len; p += 2) {
+                                const int ka = key_of(code_at(tg[k], p)), kb = key_of(code_at(tg[k], p + 1));
+                                if (ka == kb) continue;
+                                const bool sw = (flip[(size_t)k] >> (p >> 1)) & 1u;
+                                const size_t qa = (size_t)ka * 16 + 2 * c + (sw ? 1 : 0);
+                                const size_t qb = (size_t)kb * 16 + 2 * c + (sw ? 0 : 1);
+                                const size_t ra = (size_t)ka * 16 + 2 * c + (sw ? 0 : 1);
+                                const size_t rb = (size_t)kb * 16 + 2 * c + (sw ? 1 : 0);
+                                const int before = mx[ka] + mx[kb];
+                                cnt[qa]--; cnt[qb]--; cnt[ra]++; cnt[rb]++;
+                                const uint16_t na = kmax(ka), nb = kmax(kb);
+                                if (na + nb < before) {
+                                    mx[ka] = na; mx[kb] = nb;
+                                    flip[(size_t)k] ^= (uint8_t)(1u << (p >> 1));
+                                    any = true;
+                                } else {
+                                    cnt[qa]++; cnt[qb]++; cnt[ra]--; cnt[rb]--;
+                                }
+                            }
+                    }
+                    if (!any) break;
+                }
+#if EES_BANK_SWAP
+                // lane swaps inside a warp (the warp's RED set is unchanged): a
+                // sequence with a store in a key's busiest bank pair tries each
+                // lane of another class; the first swap that lowers the sum of
+                // maxima over the keys the two touch is kept
+                {
+                    std::vector<std::vector<int>> skeys(kTileThreads);
+                    for (int s = 0; s < kTileThreads; s++) {
+                        for (int32_t k : seq[s])
+                            for (int32_t p = 0; p < tg[k].len; p++) skeys[s].push_back(key_of(code_at(tg[k], p)));
+                        std::sort(skeys[s].begin(), skeys[s].end());
+                        skeys[s].erase(std::unique(skeys[s].begin(), skeys[s].end()), skeys[s].end());
+                    }
+                    auto add_seq = [&](int s, int c, int sign) {
+                        for (int32_t k : seq[s]) {
+                            const Tgt &t2 = tg[k];
+                            for (int32_t p = 0; p < t2.len; p += 2) {
+                                const int ka = key_of(code_at(t2, p));
+                                const bool sw = (flip[(size_t)k] >> (p >> 1)) & 1u;
+                                cnt[(size_t)ka * 16 + 2 * c + (sw ? 1 : 0)] += sign;
+                                if (p + 1 < t2.len)
+                                    cnt[(size_t)key_of(code_at(t2, p + 1)) * 16 + 2 * c + (sw ? 0 : 1)] += sign;
+                            }
+                        }
+                    };
+                    auto conflicted = [&](int s, int c) {
+                        for (int32_t k : seq[s]) {
+                            const Tgt &t2 = tg[k];
+                            for (int32_t p = 0; p < t2.len; p++) {
+                                const int key = key_of(code_at(t2, p));
+                                const bool sw = (flip[(size_t)k] >> (p >> 1)) & 1u;
+                                const int h = (p + 1 < t2.len || (p & 1)) ? ((p & 1) ^ (sw ? 1 : 0)) : 0;
+                                const uint16_t v = cnt[(size_t)key * 16 + 2 * c + h];
+                                if (v >= 2 && v == mx[key]) return true;
+                            }
+                        }
+                        return false;
+                    };
+                    std::vector<int> touched;
+                    for (int pass = 0; pass < EES_BANK_SWAP; pass++) {
+                        bool moved = false;
+                        for (int w = 0; w < kTileThreads / 32; w++)
+                            for (int la = 0; la < 32; la++) {
+                                const int ja = 32 * w + la, ca = la & 7;
+                                if (!conflicted(perm[ja], ca)) continue;
+                                for (int lb = 0; lb < 32; lb++) {
+                                    const int jb = 32 * w + lb, cb = lb & 7;
+                                    if (cb == ca) continue;
+                                    const int a = perm[ja], b = perm[jb];
+                                    touched.clear();
+                                    std::set_union(skeys[a].begin(), skeys[a].end(), skeys[b].begin(), skeys[b].end(),
+                                                   std::back_inserter(touched));
+                                    int before = 0;
+                                    for (int key : touched) before += mx[key];
+                                    add_seq(a, ca, -1); add_seq(b, cb, -1); add_seq(a, cb, 1); add_seq(b, ca, 1);
+                                    int after = 0;
+                                    for (int key : touched) after += kmax(key);
+                                    if (after < before) {
+                                        for (int key : touched) mx[key] = kmax(key);
+                                        std::swap(perm[ja], perm[jb]);
+                                        moved = true;
+                                        break;
+                                    }
+                                    add_seq(a, cb, -1); add_seq(b, ca, -1); add_seq(a, ca, 1); add_seq(b, cb, 1);
+                                }
+                            }
+                        if (!moved) break;
+                    }
+                }
+#endif
+#endif
+                o.st_waves = waves(cnt);
+            }
             std::vector<uint32_t> oseq(kTileThreads, 0), odst;
             for (int j = 0; j < kTileThreads; j++) {
                 const uint32_t start = (uint32_t)odst.size();
                 if (start >= (1u << kSeqStartBits)) return false;
                 uint32_t em = 0, sm = 0, pm = 0;
                 int32_t st = 0;
-                for (int32_t k : seq[j]) {
+                for (int32_t k : seq[perm[j]]) {
                     const Tgt &t2 = tg[k];
                     for (int32_t p = 0; p < t2.len; p += 2, st++) {
                         const int32_t slot = 2 * (st * kTileThreads + j);
-                        place(t2, p, slot);
-                        if (p + 1 < t2.len) place(t2, p + 1, slot + 1);
+                        const bool sw = (flip[(size_t)k] >> (p >> 1)) & 1u;
+                        place(t2, p, slot + (sw ? 1 : 0));
+                        if (p + 1 < t2.len) place(t2, p + 1, sw ? slot : slot + 1);
                         else pm |= 1u << st;                        // odd target: no second half
                         if (p + 2 >= t2.len) {
                             em |= 1u << st;
@@ -934,6 +1238,8 @@ bool build_tile_impl(int form, bool strict, int64_t N, int32_t n_nodes, int32_t 
         out.n_side_entries += o.n_sent;
         out.n_listed += o.L;
         out.n_padded += o.padded;
+        out.st_waves0 += o.st_waves0;
+        out.st_waves += o.st_waves;
         listed += o.listed;
     }
     // distinct programs, numbered by first appearance (tile order)
