@@ -644,6 +644,8 @@ def main():
     ap.add_argument("--work", type=int, default=1, help="S:229 work multiplier (FP64-bound probe)")
     ap.add_argument("--flush", default="clean", choices=["clean", "write"],
                     help="L2 flush before each step: write 256 MiB (+ read it back: clean)")
+    ap.add_argument("--tile-form", type=int, default=None, choices=[0, 1],
+                    help="force the TILE layout form (A/B experiments; default: chosen at setup)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-reps", type=int, default=5)
     ap.add_argument("--no-e2e", action="store_true")
@@ -683,7 +685,8 @@ def main():
 
     nl = netgen.named(args.netlist) if args.netlist else netgen.config(args.config)
     cfg = None if args.netlist else args.config
-    ctx = Context.from_netlist(nl, variant=args.variant, rule=args.rule, heavy_degree=args.heavy_degree)
+    ctx = Context.from_netlist(nl, variant=args.variant, rule=args.rule, heavy_degree=args.heavy_degree,
+                               tile_form=args.tile_form)
     if args.work > 1:
         ctx.set_work(args.work)
     clk = ClockSampler(torch.cuda.current_device()).start()
