@@ -291,3 +291,20 @@ def test_abi_struct_sizes_match_binding():
     assert _lib.lib.ees_abi_sizeof(0) == C.sizeof(_lib.ees_desc)
     assert _lib.lib.ees_abi_sizeof(1) == C.sizeof(_lib.ees_stats_t)
     assert _lib.lib.ees_abi_sizeof(7) == 0
+
+
+def test_tile_bank_placement_never_worse():
+    """TILE form 1: the builder's bank-aware lane placement and pair
+    orientation (hill-climbs from the identity placement on its 16-bank-pair
+    model of the evaluation's STS.64) never raise the modelled store
+    wavefronts, and lower them where half-warps collide (the SRAM rows)."""
+    nets = [netgen.config(c, 0.01 if c else 1.0) for c in range(5)]
+    nets += [netgen.full_adder_28t(16), netgen.ring_oscillators(20, 101, fanout=4)]
+    gained = 0
+    for nl in nets:
+        st = _ctx(nl, tile_form=1).stats()
+        assert 0 < st["tile_store_waves"] <= st["tile_store_waves_naive"], nl.name
+        gained += st["tile_store_waves"] < st["tile_store_waves_naive"]
+    assert gained >= 1
+    st = _ctx(netgen.config(2, 0.01), tile_form=0).stats()
+    assert st["tile_store_waves"] == 0 and st["tile_store_waves_naive"] == 0
