@@ -224,6 +224,9 @@ __host__ __device__ constexpr int tile_stages(int form) { return form ? EES_STAG
 #ifndef EES_A_PREFETCH
 #define EES_A_PREFETCH 1               // bulk L2 prefetch of the next tile's CSR block of A
 #endif
+#ifndef EES_TDESC_ASYNC
+#define EES_TDESC_ASYNC 1              // the refill's tdesc entry by a bulk copy into shared memory
+#endif
 #ifndef EES_LATE_GATHER
 #define EES_LATE_GATHER 0
 #endif

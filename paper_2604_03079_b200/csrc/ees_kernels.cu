@@ -1771,6 +1771,9 @@ __device__ __forceinline__ void tile_finish(const TileK &tk, const CallK &P, con
     };                                                                                           \
     auto issue = [&](int32_t tile, int stage) { issue_at(__ldg(tk.tdesc + tile), stage); };     \
     __shared__ double *s_bptr[2 * kTileBases];    /* two tiles (a second slot buffer has no B0) */ \
+    __shared__ __align__(16) uint4 s_rf;          /* the refill's tdesc entry (bulk copy) */        \
+    __shared__ __align__(8) uint64_t s_rf_bar;                                                   \
+    uint32_t rf_phase = 0;                                                                       \
     TileOut out;                                                                                 \
     out.A = P.A;                                                                                 \
     out.Bm = P.b - tk.nnz;                                                                       \
@@ -1779,6 +1782,7 @@ __device__ __forceinline__ void tile_finish(const TileK &tk, const CallK &P, con
     const int32_t t0 = blockIdx.x;                                                               \
     if (tid == 0) {                                                                              \
         for (int k = 0; k < (NSTAGES); k++) mbar_init(&s_bar[k], 1);                             \
+        mbar_init(&s_rf_bar, 1);                                                                 \
         for (int k = 0; k < (NSTAGES); k++)                                                      \
             if (t0 + k * G < tk.n_tiles) issue(t0 + k * G, k);                                   \
     }                                                                                            \
@@ -1857,8 +1861,19 @@ __global__ void __launch_bounds__(kTileThreads, tile_ctas(kForm)) k_tile(TileK t
         // the blob this iteration's refill (at B1) will fetch: its offsets are
         // loaded now, so warp 0 does not wait on global memory after B1
         const int32_t tr = t - G + kStg * G;
+#if EES_TDESC_ASYNC
+        // ... through a bulk copy into shared memory with its own mbarrier:
+        // with a register load the compiler put the first use right behind
+        // it, and warp 0 (hence the CTA, at B1) waited a global-memory latency
+        // per tile (cp.async + wait_all waited for the gathers as well)
+        if (tid == 0 && it > 0 && tr < tk.n_tiles) {
+            mbar_expect_tx(&s_rf_bar, 16);
+            tma_bulk_g2s(&s_rf, tk.tdesc + tr, 16, &s_rf_bar);
+        }
+#else
         uint4 rf = make_uint4(0, 0, 0, 0);
         if (tid == 0 && it > 0 && tr < tk.n_tiles) rf = __ldg(tk.tdesc + tr);
+#endif
         TileOut o = out;
         o.bptr = smem_u32(s_bptr + (it & 1) * kTileBases);
         if (tid < kTileBases) {                 // this tile's destination pointers (read after B1)
@@ -1881,8 +1896,14 @@ __global__ void __launch_bounds__(kTileThreads, tile_ctas(kForm)) k_tile(TileK t
         }
         TILE_TRACE(2 + 2 * it);
         __syncthreads();                                        // B1
-        if (tid == 0 && it > 0 && tr < tk.n_tiles)              // refill the stage of tile t-G
+        if (tid == 0 && it > 0 && tr < tk.n_tiles) {            // refill the stage of tile t-G
+#if EES_TDESC_ASYNC
+            mbar_wait(&s_rf_bar, rf_phase);
+            rf_phase ^= 1u;
+            const uint4 rf = s_rf;
+#endif
             issue_at(rf, stage == 0 ? kStg - 1 : stage - 1);
+        }
         if (kForm == 1) tile_reduce5(blob, sc, tid, o, tk, s_hot);
         else tile_reduce(blob, sc, tid, o, tk, s_hot);
         TILE_TRACE(3 + 2 * it);
